@@ -1,0 +1,347 @@
+"""Benchmark of the FD-apply hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3|4]
+
+One "step" = one fd_apply z = P^{-1} r (Algorithm 1 steps 2-4, PAPER.md 955-964)
+over the whole synthetic workload.  Default workload: BASELINE config 4 (d=3,
+p=6, n_el=128 per direction: 132^3 x 133 = 305,895,744 DOFs, 2.45 GB per vector)
+-- the configuration the metric's "1/2/4/8 B200" is quoted on; it fits one GPU.
+For N > 1 the same global problem is slab-partitioned along time over the ranks
+("scaling": "strong"), the time mode running after an NCCL all-to-all.
+
+Printed (rank 0): ONE JSON line with value = whole-job DOF/s, the roofline of the
+dominant kernel (fd_mode_kernel, FP64 DMMA; peak = 37.0 TF/s measured register-
+only DMMA, profiles/peaks_fp64_r01.json), e2e through fd_apply_host, the oracle
+CPU baseline, secondary PCG solve times, clocks.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 register-only (profiles/peaks_fp64_r01.json)
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA.8x8x4 register-only, 148 SMs (profiles/peaks_fp64_r01.json)"
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload(cfg_id):
+    c = synth.CONFIGS[cfg_id]
+    d, p, n_el = c["d"], c["p"], c["n_el"]
+    n_s, n_t = n_el + p - 2, n_el + p - 1
+    N = n_s ** d * n_t
+    flops = 4.0 * N * (d * n_s + n_t)  # PAPER.md 1071-1072
+    return {"d": d, "p": p, "n_el": n_el, "n_s": n_s, "n_t": n_t, "N": N, "flops": flops}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(cfg_id, seconds_min=10.0, max_reps=8):
+    """The CPU oracle (oracle/fd.py, as it stands) on a bounded sample of the
+    workload: the config's spatial discretisation with the time direction
+    truncated to 8 elements (n_t = 8 + p - 1); returns (DOF/s, sample text, cores)."""
+    from oracle import univariate as uv, fd
+    w = workload(cfg_id)
+    d, p, n_el = w["d"], w["p"], w["n_el"]
+    n_el_t = 8
+    sf, tf = uv.space_factors(n_el, p), uv.time_factors(n_el_t, p)
+    fdd = fd.setup([sf] * d, tf)
+    shape = (tf["Mt"].shape[0],) + (sf["M"].shape[0],) * d
+    r = synth.residual(shape, 0)
+    fd.fd_apply(r, fdd)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while reps < max_reps and (reps == 0 or time.perf_counter() - t0 < seconds_min):
+        fd.fd_apply(r, fdd)
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    N = int(np.prod(shape))
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"oracle fd_apply (numpy tensordot, fp64) on config {cfg_id}'s spatial grid "
+              f"(n_s={sf['M'].shape[0]}, p={p}) with time truncated to n_el_t={n_el_t} "
+              f"(n_t={shape[0]}, N={N}); {reps} reps, {dt:.3f} s each")
+    return N / dt, sample, cores
+
+
+def run_reference(args):
+    """--impl reference: the oracle, as it stands, on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = workload(args.config)
+    from oracle import univariate as uv, fd
+    d, p, n_el = w["d"], w["p"], w["n_el"]
+    sf, tf = uv.space_factors(n_el, p), uv.time_factors(8, p)
+    fdd = fd.setup([sf] * d, tf)
+    shape = (tf["Mt"].shape[0],) + (sf["M"].shape[0],) * d
+    r = synth.residual(shape, 0)
+    for _ in range(args.warmup):
+        fd.fd_apply(r, fdd)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fd.fd_apply(r, fdd)
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    N = int(np.prod(shape))
+    cores = len(os.sched_getaffinity(0))
+    val = N / dt
+    sample = (f"oracle fd_apply on config {args.config}'s spatial grid with time truncated to "
+              f"n_el_t=8 (n_t={shape[0]}, N={N}) per step")
+    line = {"impl": "reference", "metric": "fd_apply DOF/s (fp64)", "value": val, "unit": "DOF/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"config{args.config}-sample",
+                                            "d": d, "p": p, "n_el": n_el, "n_t": shape[0]},
+            "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4])
+    ap.add_argument("--no-extras", action="store_true", help="skip PCG / config-3 / cpu extras")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1809_10026_b200 as ls
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.config)
+    d, p, n_el = w["d"], w["p"], w["n_el"]
+    n_elems = [n_el] * (d + 1)
+    if world > 1:
+        uid = ls.unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = ls.Context(d, p, n_elems, rank=rank, world=world, uid=obj[0])
+    else:
+        ctx = ls.Context(d, p, n_elems)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+
+    # seeded residual, generated globally and scattered by slab (same tensor for every N)
+    r_host = synth.residual(ctx.global_shape, 0)[ctx.t0:ctx.t0 + ctx.nt_local]
+    r = torch.from_numpy(np.ascontiguousarray(r_host)).to("cuda")
+    z = torch.empty_like(r)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ctx.fd_apply(r, z)
+    barrier()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    ctx.profile(True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.fd_apply(r, z)
+        e1.record(stream)
+        barrier()
+    ctx.profile(False)
+    launches = ctx.launches - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    kms, kflops, kn = ctx.profile_read()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = w["N"] / (ms * 1e-3)
+
+    # e2e: the public host-buffer API (H2D of r and D2H of z inside the timed region)
+    pin_r = torch.from_numpy(np.ascontiguousarray(r_host)).pin_memory()
+    pin_z = torch.empty_like(pin_r).pin_memory()
+    ctx.fd_apply_host(pin_r, pin_z)
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.fd_apply_host(pin_r, pin_z)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_bytes = int(pin_r.numel() * 8)
+
+    # roofline of the dominant kernel (fd_mode_kernel): algorithmic flops / device time
+    achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
+    hbm, hbm_src = _hbm_peak()
+    roof = {"kernel": "fd_mode_kernel (all mode products of fd_apply)", "bound": "tensor",
+            "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "peak_source": FP64_PEAK_SOURCE, "kernel_share_of_step": round(kms / (ms * args.steps), 4),
+            "launches_timed": kn, "flops_per_step_algorithmic": w["flops"]}
+
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = run_extras(ls, torch, stream)
+
+    if rank == 0:
+        cpu_val, cpu_sample, cores = (None, "skipped", None)
+        if world == 1 and not args.no_extras:
+            cpu_val, cpu_sample, cores = oracle_sample(args.config)
+        line = {
+            "metric": "fd_apply DOF/s (fp64)",
+            "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config{args.config}", "d": d, "p": p, "n_el": n_el,
+                       "n_s": w["n_s"], "n_t": w["n_t"], "N": w["N"],
+                       "l2": f"inputs larger than L2 ({w['N'] * 8 / 1e9:.2f} GB per vector vs 126 MB)",
+                       "parallelism": f"time-slab x{world}" if world > 1 else "single GPU"},
+            "gflops_algorithmic": w["flops"] / (ms * 1e-3) / 1e9,
+            "fp64_roofline_frac": round(w["flops"] / (ms * 1e-3) / 1e12 / (FP64_PEAK_TFLOPS * world), 4),
+            "roofline": roof,
+            "cpu_baseline": {"value": cpu_val, "unit": "DOF/s", "cores": cores, "kind": "oracle",
+                             "sample": cpu_sample},
+            "e2e": {"value": w["N"] / e2e_s, "unit": "DOF/s", "h2d_bytes_per_step": e2e_bytes,
+                    "d2h_bytes_per_step": e2e_bytes, "api": "fd_apply_host (pinned host buffers)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+        }
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_extras(ls, torch, stream):
+    """Secondary numbers (rank 0, N = 1): config-3 fd_apply (the single-GPU
+    roofline case) and PCG solve times (configs 2 and 5)."""
+    out = {}
+    w = workload(3)
+    ctx = ls.Context(3, 3, [64] * 4)
+    ctx.set_stream(stream)
+    r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
+    z = torch.empty_like(r)
+    for _ in range(3):
+        ctx.fd_apply(r, z)
+    torch.cuda.synchronize()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2
+    tot = 0.0
+    ctx.profile(True)
+    for _ in range(20):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.fd_apply(r, z)
+        b.record(stream)
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    ctx.profile(False)
+    kms, kfl, _ = ctx.profile_read()
+    ms = tot / 20
+    out["config3"] = {"value": w["N"] / (ms * 1e-3), "unit": "DOF/s", "ms_per_step": ms,
+                      "fp64_roofline_frac": round(w["flops"] / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                      "mode_kernel_tflops": round(kfl / (kms * 1e-3) / 1e12, 3),
+                      "l2": "flushed (512 MB write) before every step"}
+    ctx.close()
+    del flush
+    pcg = []
+    for cfg, p, kind in ((2, 3, 0), (5, 2, 1), (5, 4, 1), (5, 8, 1)):
+        n_el = synth.CONFIGS[cfg]["n_el"]
+        d = synth.CONFIGS[cfg]["d"]
+        c = ls.Context(d, p, [n_el] * (d + 1))
+        c.set_stream(stream)
+        b = c.rhs(kind)
+        c.pcg(b, tol=1e-8)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x, st = c.pcg(b, tol=1e-8)
+        torch.cuda.synchronize()
+        pcg.append({"config": cfg, "d": d, "p": p, "n_el": n_el, "N": c.N, "iters": st["iters"],
+                    "solve_ms": (time.perf_counter() - t0) * 1e3, "true_rel_res": st["true_rel_res"]})
+        c.close()
+        del b, x
+    out["pcg"] = pcg
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,178 @@
+/*
+ * ls_api.h -- C-ABI of the B200-native hot path of the space-time
+ * least-squares isogeometric method for the heat equation
+ * (Montardini, Negri, Sangalli, Tani, arXiv 1809.10026; PAPER.md = the paper).
+ *
+ * Problem (PAPER.md 343-353, eq:heat_eq): d_t u - Lap u = f on the
+ * identity-mapped unit hypercube [0,1]^d x [0,T], T = 1 (reading c9),
+ * homogeneous Dirichlet and initial data.  Discretisation: tensor B-splines of
+ * degree p, C^{p-1}, n_el uniform elements per direction (PAPER.md 144-213,
+ * 1111-1112); space basis i_k = 2..m_k-1, time basis i_t = 2..m_t
+ * (eq:basis_par, PAPER.md 266-267), so n_k = n_el,k + p - 2 and
+ * n_t = n_el,t + p - 1 (reading c1).
+ *
+ * VECTOR LAYOUT (all entry points): a vector of N = n_t * n_d * ... * n_1
+ * fp64 values in the colexicographic DOF order of PAPER.md 271-285, i.e. the
+ * row-major tensor [n_t][n_d]...[n_1] with direction 1 contiguous and time
+ * slowest.  Flat index = i_1 + n_1 (i_2 + n_2 (... + n_d i_t)).
+ * For a distributed context (ls_setup_dist) each rank holds the contiguous
+ * time slab [t0, t0 + nt_local) of that tensor (see ls_layout).
+ *
+ * OWNERSHIP: vectors passed to fd_apply / ls_matvec / ls_rhs / pcg_solve are
+ * caller-owned DEVICE memory (cudaMalloc / torch CUDA tensors), 8-byte
+ * aligned, not overlapping partially.  The *_host variants take caller-owned
+ * HOST memory (pinned recommended).  The library owns everything else
+ * (eigenvectors, eigenvalues, banded factors, workspaces); all allocation
+ * happens in ls_setup*, none in the hot calls.
+ *
+ * STREAMS: every device call is enqueued on the stream set by ls_set_stream
+ * (default: the legacy default stream).  fd_apply / ls_matvec / ls_rhs are
+ * asynchronous; pcg_solve and the *_host calls are synchronous.
+ *
+ * ERRORS: every int-returning call returns LS_OK (0) or one of the codes
+ * below; ls_strerror maps a code to a static string.  A failed call leaves
+ * the output unspecified and the context usable unless LS_ECUDA is returned.
+ * Not thread-safe per context; one context per device.
+ */
+#ifndef LS_API_H
+#define LS_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LS_OK 0
+#define LS_EINVAL 1     /* bad argument: d not in {1,2,3}, p < 2, n_el < 1, null/misaligned ptr */
+#define LS_ENOTSPD 2    /* Cholesky failure in the generalized eigensolver (mass matrix not SPD) */
+#define LS_ENOCONV 3    /* PCG did not reach tol within max_iter (stats still filled) */
+#define LS_ENUMERIC 4   /* NaN/Inf in a PCG scalar (alpha, beta) */
+#define LS_ENOMEM 5     /* estimated device memory exceeds the free HBM; refused up front */
+#define LS_ECUDA 6      /* CUDA runtime / cuSOLVER error */
+#define LS_ENCCL 7      /* NCCL error (distributed contexts) */
+#define LS_ENOTSUP 8    /* operation not supported for this context */
+
+typedef struct ls_ctx ls_ctx; /* opaque, library-owned */
+
+typedef struct {
+  int iters;           /* number of A-products performed (reading c7) */
+  double rel_res;      /* final recurrence residual ||r_k|| / ||b|| */
+  double true_rel_res; /* ||b - A x|| / ||b|| recomputed after the loop */
+  int status;          /* LS_OK, LS_ENOCONV or LS_ENUMERIC */
+} ls_pcg_stats;
+
+/*
+ * ls_setup -- build the method's univariate data on the current CUDA device.
+ *   d        : number of space dimensions, 1..3 (PAPER.md 175-178).
+ *   p        : spline degree p_s = p_t >= 2 (Assumption 2, PAPER.md 218-223).
+ *   n_elems  : host array of d+1 element counts; n_elems[k-1] = direction k,
+ *              n_elems[d] = time (PAPER.md 179-180 orders p = (p_s, p_t)).
+ *   out      : receives the new context.
+ * Work (untimed setup): open uniform knots,
+ * Gauss-Legendre assembly of M_k, K_k, J_k (space) and M_t, K_t, W_t (time)
+ * on the host (PAPER.md 686-703, 738-757); generalized eigendecompositions
+ * J_k U_k = M_k U_k Lambda_k, K_t U_t = M_t U_t Lambda_t with U^T M U = I by
+ * cuSOLVER Dsygvd on the device (eq:eig_dec, PAPER.md 939-945); workspace
+ * allocation.  Errors: LS_EINVAL, LS_ENOTSPD, LS_ENOMEM, LS_ECUDA.
+ */
+int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out);
+
+/*
+ * ls_setup_dist -- as ls_setup, for rank `rank` of `world` processes (one
+ * GPU each).  The time axis is split into contiguous slabs (uneven allowed);
+ * fd_apply reshards slab <-> spatial chunk with two NCCL all-to-alls for the
+ * time mode, ls_matvec exchanges p halo time slices with the neighbour ranks,
+ * pcg_solve all-reduces its scalars.  nccl_unique_id: 128 bytes produced by
+ * ls_get_unique_id on rank 0 and broadcast by the caller.
+ * Errors: as ls_setup plus LS_ENCCL.
+ */
+int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int world,
+                  const void* nccl_unique_id, ls_ctx** out);
+int ls_get_unique_id(void* out128);
+
+/*
+ * ls_layout -- sizes: n_t, n_s[0..d-1] (= n_1..n_d), and this rank's time slab
+ * [t0, t0 + nt_local) (t0 = 0, nt_local = n_t for ls_setup).  Any output
+ * pointer may be NULL.
+ */
+int ls_layout(const ls_ctx* ctx, int64_t* n_t, int64_t* n_s, int64_t* t0, int64_t* nt_local);
+
+/* ls_set_stream -- enqueue subsequent work on `cuda_stream` (a cudaStream_t). */
+int ls_set_stream(ls_ctx* ctx, void* cuda_stream);
+
+/*
+ * fd_apply -- z = P^{-1} r, Algorithm 1 steps 2-4 (PAPER.md 955-964):
+ *   s~ = (U_t (x) U_s)^T r ; q~ = (Lambda_t (x) I + I (x) Lambda_s)^{-1} s~ ;
+ *   z = (U_t (x) U_s) q~,
+ * with P = K_t^ (x) M_s^ + M_t^ (x) J_s~ (eq:preconditioner, PAPER.md 733).
+ * r, z: device vectors of this rank's slab (layout above).  z == r (in place)
+ * is allowed.  Asynchronous on the context stream.
+ */
+int fd_apply(ls_ctx* ctx, const double* r, double* z);
+
+/*
+ * ls_matvec -- y = A x, A = K_t (x) M_s + M_t (x) J_s + W_t (x) L_s
+ * (eq:A_kron, PAPER.md 686-703), matrix-free and sum-factorised on the banded
+ * univariate factors (identity map).  x, y: device vectors, y != x.
+ * Asynchronous on the context stream.
+ */
+int ls_matvec(ls_ctx* ctx, const double* x, double* y);
+
+/*
+ * ls_rhs -- b_i = F(B_i) = int int f (d_t B_i - Lap B_i) (PAPER.md 409) for a
+ * built-in separable forcing (reading c11):
+ *   kind 0: f = e^t prod_k sin(pi x_k)                        (BASELINE config 2)
+ *   kind 1: f = prod_k sin(pi x_k) (cos t + d pi^2 sin t)     (cube, PAPER.md 1166)
+ * b: device vector (this rank's slab).  Errors: LS_EINVAL for an unknown kind.
+ */
+int ls_rhs(ls_ctx* ctx, int kind, double* b);
+
+/*
+ * pcg_solve -- preconditioned CG for A x = b with P (PAPER.md 710-712, 1109):
+ * x0 = 0, stop when ||r_k||_2 <= tol ||b||_2 (recurrence residual, reading c7)
+ * or after max_iter A-products.  x is overwritten.  b == 0 returns x = 0 with
+ * 0 iterations.  Synchronous.  Returns LS_OK, LS_ENOCONV or LS_ENUMERIC (st
+ * filled in all three cases; st may be NULL).
+ */
+int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
+              ls_pcg_stats* st);
+
+/*
+ * fd_apply_host -- fd_apply with HOST vectors: copies r host->device, runs
+ * fd_apply, copies z device->host, synchronises.  The end-to-end entry point
+ * of the public API (bench.py "e2e").
+ */
+int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host);
+
+/*
+ * ls_get_factor -- copy a setup quantity to host memory (introspection for
+ * tests).  which: 0 = M_k, 1 = K_k, 2 = J_k (dense n_k x n_k, row-major; dir
+ * = k in 1..d), 3 = M_t^ , 4 = K_t^ (n_t x n_t, dir ignored), 5 = lambda_k
+ * (n_k), 6 = lambda_t (n_t), 7 = U_k (n_k x n_k row-major, column j = j-th
+ * eigenvector), 8 = U_t.  Synchronous.
+ */
+int ls_get_factor(const ls_ctx* ctx, int which, int dir, double* host_out);
+
+/* ls_kernel_launches -- number of kernels the library has launched so far. */
+int64_t ls_kernel_launches(const ls_ctx* ctx);
+
+/*
+ * ls_profile -- enable (1) / disable (0) per-launch CUDA-event timing of the
+ * FD mode-product kernel (the dominant kernel of fd_apply).  Events are
+ * recorded on the context stream around each launch.
+ * ls_profile_read -- synchronise, return the summed device time [ms], the
+ * summed ALGORITHMIC flops (2 n^2 per column per mode product, padding not
+ * counted) and the number of launches recorded since the last read; resets.
+ */
+int ls_profile(ls_ctx* ctx, int enable);
+int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t* launches);
+
+void ls_destroy(ls_ctx* ctx);
+const char* ls_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LS_API_H */

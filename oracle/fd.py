@@ -95,3 +95,26 @@ def dense_P(space, time):
         Js += kron_list([space[l]["J"] if l == k else space[l]["M"]
                          for l in reversed(range(d))])
     return np.kron(time["Kt_hat"], Ms) + np.kron(time["Mt_hat"], Js)
+
+
+def fd_apply_rank1_rows(factors, fdd, rows):
+    """Algorithm 1 on a rank-1 input r = a_t (x) a_d (x) ... (x) a_1
+    (``factors`` = [a_t, a_d, .., a_1], slowest first), returning only the
+    output fibres z[rows[j] + (:,)] along direction 1.  Step 2 is exact on the
+    rank-1 structure (s~ = (U_t^T a_t) (x) ... (x) (U_1^T a_1)); step 3 forms
+    q~ = s~ / (lambda_t + sum_k lambda_k) in full; step 4 is evaluated only for
+    the requested fibres.  Used for full-size (BASELINE config 4) parity."""
+    d = fdd["d"]
+    U = [fdd["U_t"]] + [fdd["U_s"][k - 1] for k in range(d, 0, -1)]  # slowest first
+    sig = [U[a].T @ factors[a] for a in range(d + 1)]
+    q = sig[0]
+    for v in sig[1:]:
+        q = np.multiply.outer(q, v)
+    q = q / divisor(fdd)
+    out = []
+    for idx in rows:  # idx = (i_t, i_d, .., i_2)
+        v = q
+        for a, i in enumerate(idx):
+            v = np.tensordot(U[a][i], v, axes=([0], [0]))
+        out.append(U[d] @ v)
+    return np.array(out)

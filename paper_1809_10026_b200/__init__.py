@@ -1,0 +1,240 @@
+"""B200-native hot path of the space-time least-squares IGA method (arXiv 1809.10026).
+
+Thin ctypes binding over ``libls.so`` (C-ABI declared in ``include/ls_api.h``):
+argument marshalling only -- every step of fd_apply / ls_matvec / pcg_solve runs
+in the library's CUDA kernels.  There is no CPU fallback: importing this module
+without the built library raises, and every call checks that its tensors are
+contiguous fp64 CUDA tensors.
+
+Typical use::
+
+    import torch, paper_1809_10026_b200 as ls
+    ctx = ls.Context(d=3, p=3, n_elems=[64, 64, 64, 64])
+    r = torch.rand(ctx.shape, dtype=torch.float64, device="cuda") * 2 - 1
+    z = ctx.fd_apply(r)                  # z = P^{-1} r   (Algorithm 1)
+    b = ctx.rhs(kind=1)                  # cube forcing (PAPER.md 1166)
+    x, stats = ctx.pcg(b, tol=1e-8)      # PCG with P (PAPER.md 1109)
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libls.so")
+
+LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_ENCCL, LS_ENOTSUP = range(9)
+
+# Every symbol include/ls_api.h declares (checked by tests/test_abi.py).
+EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
+            "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
+            "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror"]
+
+
+class PCGStats(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("rel_res", ctypes.c_double),
+                ("true_rel_res", ctypes.c_double), ("status", ctypes.c_int)]
+
+    def as_dict(self):
+        return {"iters": self.iters, "rel_res": self.rel_res,
+                "true_rel_res": self.true_rel_res, "status": self.status}
+
+
+class LSError(RuntimeError):
+    def __init__(self, code, what):
+        self.code = code
+        super().__init__(f"{what}: {strerror(code)} (code {code})")
+
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load libls.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+    vp, i64p, dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p
+    sig = {
+        "ls_setup": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(vp)]),
+        "ls_setup_dist": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64p, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_char_p, ctypes.POINTER(vp)]),
+        "ls_get_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
+        "ls_layout": (ctypes.c_int, [vp, i64p, i64p, i64p, i64p]),
+        "ls_set_stream": (ctypes.c_int, [vp, vp]),
+        "fd_apply": (ctypes.c_int, [vp, dp, dp]),
+        "ls_matvec": (ctypes.c_int, [vp, dp, dp]),
+        "ls_rhs": (ctypes.c_int, [vp, ctypes.c_int, dp]),
+        "pcg_solve": (ctypes.c_int, [vp, dp, dp, ctypes.c_double, ctypes.c_int, ctypes.POINTER(PCGStats)]),
+        "fd_apply_host": (ctypes.c_int, [vp, dp, dp]),
+        "ls_get_factor": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, dp]),
+        "ls_kernel_launches": (ctypes.c_int64, [vp]),
+        "ls_profile": (ctypes.c_int, [vp, ctypes.c_int]),
+        "ls_profile_read": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double), i64p]),
+        "ls_destroy": (None, [vp]),
+        "ls_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def strerror(code):
+    return load_library().ls_strerror(code).decode()
+
+
+def _check(code, what, ok=(LS_OK,)):
+    if code not in ok:
+        raise LSError(code, what)
+    return code
+
+
+def unique_id():
+    """128-byte NCCL unique id (rank 0), to broadcast before Context(..., world>1)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().ls_get_unique_id(buf), "ls_get_unique_id")
+    return buf.raw
+
+
+def sizes(n_el, p):
+    """(n_s, n_t) for n_el uniform elements (reading c1)."""
+    return n_el + p - 2, n_el + p - 1
+
+
+class Context:
+    """One ls_ctx (one GPU).  ``n_elems``: d+1 element counts, directions 1..d then time."""
+
+    def __init__(self, d, p, n_elems, rank=0, world=1, uid=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1809_10026_b200 needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        lib = load_library()
+        ne = (ctypes.c_int64 * (d + 1))(*[int(v) for v in n_elems])
+        h = ctypes.c_void_p()
+        torch.cuda.init()
+        if world == 1:
+            _check(lib.ls_setup(d, p, ne, ctypes.byref(h)), "ls_setup")
+        else:
+            _check(lib.ls_setup_dist(d, p, ne, rank, world, uid, ctypes.byref(h)), "ls_setup_dist")
+        self._h = h
+        self._lib = lib
+        self.d, self.p = d, p
+        self.n_elems = list(n_elems)
+        nt, t0, ntl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ns = (ctypes.c_int64 * d)()
+        _check(lib.ls_layout(h, ctypes.byref(nt), ns, ctypes.byref(t0), ctypes.byref(ntl)), "ls_layout")
+        self.n_t, self.n_s = nt.value, [ns[k] for k in range(d)]
+        self.t0, self.nt_local = t0.value, ntl.value
+        self.shape = (self.nt_local,) + tuple(reversed(self.n_s))
+        self.global_shape = (self.n_t,) + tuple(reversed(self.n_s))
+        self.N = int(np.prod(self.shape))
+
+    # -- marshalling helpers ------------------------------------------------------------
+    def _dev(self, t, name):
+        torch = self._torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+        if t.numel() != self.N:
+            raise ValueError(f"{name} has {t.numel()} elements, expected {self.N}")
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _new(self):
+        return self._torch.empty(self.shape, dtype=self._torch.float64, device="cuda")
+
+    def set_stream(self, stream):
+        _check(self._lib.ls_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)), "ls_set_stream")
+
+    # -- the boundary ---------------------------------------------------------------------
+    def fd_apply(self, r, z=None):
+        """z = P^{-1} r (Algorithm 1, PAPER.md 955-964)."""
+        z = self._new() if z is None else z
+        _check(self._lib.fd_apply(self._h, self._dev(r, "r"), self._dev(z, "z")), "fd_apply")
+        return z
+
+    def matvec(self, x, y=None):
+        """y = A x (eq:A_kron, PAPER.md 686-703)."""
+        y = self._new() if y is None else y
+        _check(self._lib.ls_matvec(self._h, self._dev(x, "x"), self._dev(y, "y")), "ls_matvec")
+        return y
+
+    def rhs(self, kind, b=None):
+        """b = F(B_i) for forcing `kind` (0: e^t prod sin, 1: cube manufactured)."""
+        b = self._new() if b is None else b
+        _check(self._lib.ls_rhs(self._h, int(kind), self._dev(b, "b")), "ls_rhs")
+        return b
+
+    def pcg(self, b, x=None, tol=1e-8, max_iter=1000, raise_on_noconv=False):
+        """x = A^{-1} b by PCG with P; returns (x, stats dict)."""
+        x = self._new() if x is None else x
+        st = PCGStats()
+        code = self._lib.pcg_solve(self._h, self._dev(b, "b"), self._dev(x, "x"), float(tol),
+                                   int(max_iter), ctypes.byref(st))
+        _check(code, "pcg_solve", ok=(LS_OK,) if raise_on_noconv else (LS_OK, LS_ENOCONV, LS_ENUMERIC))
+        return x, st.as_dict()
+
+    def fd_apply_host(self, r_host, z_host):
+        """fd_apply on host tensors/arrays (pinned recommended); synchronous."""
+        def ptr(a, name):
+            if hasattr(a, "data_ptr"):
+                if a.is_cuda or a.dtype != self._torch.float64 or not a.is_contiguous():
+                    raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
+                return ctypes.c_void_p(a.data_ptr())
+            a = np.ascontiguousarray(a)
+            if a.dtype != np.float64:
+                raise TypeError(f"{name} must be float64")
+            return ctypes.c_void_p(a.ctypes.data)
+        _check(self._lib.fd_apply_host(self._h, ptr(r_host, "r"), ptr(z_host, "z")), "fd_apply_host")
+        return z_host
+
+    def get_factor(self, which, direction=0):
+        """Setup quantities (see ls_get_factor): returns a numpy array."""
+        if which in (0, 1, 2, 7):
+            n = self.n_s[direction - 1]
+            shape = (n, n)
+        elif which in (3, 4, 8):
+            shape = (self.n_t, self.n_t)
+        elif which == 5:
+            shape = (self.n_s[direction - 1],)
+        elif which == 6:
+            shape = (self.n_t,)
+        else:
+            raise ValueError("unknown factor")
+        out = np.empty(shape, dtype=np.float64)
+        _check(self._lib.ls_get_factor(self._h, int(which), int(direction),
+                                       ctypes.c_void_p(out.ctypes.data)), "ls_get_factor")
+        return out
+
+    def profile(self, enable):
+        """Start/stop CUDA-event timing of every FD mode-product launch."""
+        _check(self._lib.ls_profile(self._h, int(bool(enable))), "ls_profile")
+
+    def profile_read(self):
+        """(total_ms, total_algorithmic_flops, launches) since the last read."""
+        ms, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(self._lib.ls_profile_read(self._h, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(n)),
+               "ls_profile_read")
+        return ms.value, fl.value, n.value
+
+    @property
+    def launches(self):
+        return int(self._lib.ls_kernel_launches(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.ls_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,59 @@
+"""Build libls.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared -Xcompiler -fPIC
+Links cuSOLVER (setup only) and the torch-bundled NCCL 2.28 (one libnccl.so.2 per
+process).
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libls.so")
+SOURCES = ["api.cu", "comm.cu", "setup_host.cpp"]
+
+
+def _nccl_dir():
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in spec.submodule_search_locations:
+        d = os.path.join(base, "nccl")
+        if os.path.isdir(os.path.join(d, "include")):
+            return d
+    raise RuntimeError("torch-bundled NCCL not found")
+
+
+def _newest_source_mtime():
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    files.append(os.path.join(ROOT, "include", "ls_api.h"))
+    files.append(os.path.abspath(__file__))
+    return max(os.path.getmtime(f) for f in files)
+
+
+def build(force=False, verbose=False):
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_source_mtime():
+        return LIB
+    nccl = _nccl_dir()
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+           "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nccl, "include"),
+           "-o", LIB + ".tmp"]
+    cmd += [os.path.join(CSRC, s) for s in SOURCES]
+    cmd += ["-lcusolver", "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libls.so")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

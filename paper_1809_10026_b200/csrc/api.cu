@@ -1,0 +1,761 @@
+// C-ABI of libls.so (include/ls_api.h): context setup, fd_apply, ls_matvec,
+// ls_rhs, pcg_solve.  All arithmetic of the hot path runs in the kernels of
+// fd_kernels.cuh / matvec_kernels.cuh / pcg_kernels.cuh; this file is glue.
+#include "ls_api.h"
+
+#include <cusolverDn.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "comm.hpp"
+#include "fd_kernels.cuh"
+#include "matvec_kernels.cuh"
+#include "pcg_kernels.cuh"
+#include "setup_host.hpp"
+
+using namespace ls;
+
+#define LS_CUDA(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t err_ = (x);                                                               \
+    if (err_ != cudaSuccess) {                                                            \
+      std::fprintf(stderr, "[libls] CUDA error %s at %s:%d\n", cudaGetErrorString(err_), \
+                   __FILE__, __LINE__);                                                   \
+      return LS_ECUDA;                                                                    \
+    }                                                                                     \
+  } while (0)
+
+#define LS_CHECK(x)            \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != LS_OK) return rc_; \
+  } while (0)
+
+static constexpr int NMAX_STACK = 256;  // stride of stacked univariate vectors
+static constexpr int N_MAX = 136;       // largest supported univariate size (KS <= 34)
+
+struct ls_ctx {
+  int d = 0, p = 0;
+  int64_t n_el[4] = {0, 0, 0, 0};
+  int n[3] = {1, 1, 1};  // n_1..n_d
+  int nt = 0;
+  int64_t Ns = 0, Ntot = 0;  // global sizes
+  // distributed layout
+  int rank = 0, world = 1;
+  int64_t t0 = 0, ntl = 0, Nl = 0;  // local slab [t0, t0+ntl), Nl = ntl * Ns
+  std::unique_ptr<Comm> comm;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;
+
+  // host copies (introspection)
+  std::vector<double> hM[3], hK[3], hJ[3], hMt, hKt, hlam[4], hU[4];
+
+  // device data
+  double* Wf[4] = {nullptr, nullptr, nullptr, nullptr};  // U^T, n x n row-major (index 3 = time)
+  double* Wb[4] = {nullptr, nullptr, nullptr, nullptr};  // U
+  double* lam[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* lam_s = nullptr;  // Lambda_s per spatial index (N_s)
+  double* bM[3] = {nullptr, nullptr, nullptr};
+  double* bK[3] = {nullptr, nullptr, nullptr};
+  double* bJ[3] = {nullptr, nullptr, nullptr};
+  double* bMt = nullptr;
+  double* bKt = nullptr;
+  double* tmp[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // matvec / fd workspaces
+  double* pr = nullptr;  // pcg vectors
+  double* pz = nullptr;
+  double* pp = nullptr;
+  double* pq = nullptr;
+  double* partials = nullptr;
+  double* scal = nullptr;
+  double* h_scal = nullptr;  // pinned
+  double* rhs_buf = nullptr; // stacked univariate load vectors (device)
+  std::vector<void*> allocs;
+  // profiling of the mode kernel
+  bool prof = false;
+  struct ProfRec { cudaEvent_t a, b; double flops; };
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t get_event() {
+    if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+
+  ~ls_ctx() {
+    for (auto& r : prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (void* a : allocs) cudaFree(a);
+    if (h_scal) cudaFreeHost(h_scal);
+  }
+  int alloc(double** ptr, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(double));
+    if (e != cudaSuccess) return LS_ENOMEM;
+    allocs.push_back(v);
+    *ptr = static_cast<double*>(v);
+    return LS_OK;
+  }
+};
+
+// ------------------------------------------------------------------------------------------
+// mode-product dispatch
+// ------------------------------------------------------------------------------------------
+template <class C>
+static int launch_mode_cfg(ls_ctx* ctx, const ModeArgs& a0) {
+  static int occ = -1;
+  if (occ < 0) {
+    LS_CUDA(cudaFuncSetAttribute(fd_mode_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
+    LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fd_mode_kernel<C>, C::THREADS,
+                                                          C::SMEM));
+    if (occ < 1) occ = 1;
+  }
+  ModeArgs a = a0;
+  a.ntiles = (a.ncols + C::BN - 1) / C::BN;
+  if (a.ntiles == 0) return LS_OK;
+  unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms * occ));
+  ls_ctx::ProfRec rec{};
+  if (ctx->prof) {
+    rec.a = ctx->get_event();
+    rec.b = ctx->get_event();
+    rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
+    cudaEventRecord(rec.a, ctx->stream);
+  }
+  fd_mode_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  ctx->launches++;
+  if (ctx->prof) {
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->prof_recs.push_back(rec);
+  }
+  LS_CUDA(cudaGetLastError());
+  return LS_OK;
+}
+
+template <int KS, int MT, int NT, int WM, int WN>
+static int launch_mode_ks(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
+  if (mode1) return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, true, false, 3>>(ctx, a);
+  if (scale) return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, false, true, 3>>(ctx, a);
+  return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, false, false, 3>>(ctx, a);
+}
+
+// bucket shapes: (MT, NT, WM, WN) chosen so WM*MT*8 >= 4*KS rounded to 8
+#define KS_A(K) case K: return launch_mode_ks<K, 1, 4, 4, 2>(ctx, a, mode1, scale);
+#define KS_B(K) case K: return launch_mode_ks<K, 3, 4, 3, 2>(ctx, a, mode1, scale);
+#define KS_C(K) case K: return launch_mode_ks<K, 2, 4, 7, 1>(ctx, a, mode1, scale);
+#define KS_D(K) case K: return launch_mode_ks<K, 2, 4, 9, 1>(ctx, a, mode1, scale);
+
+static int round_ks(int ks) {
+  static const int list[] = {2, 4, 5, 8, 12, 17, 18, 24, 25, 26, 30, 33, 34};
+  for (int v : list)
+    if (ks <= v) return v;
+  return -1;
+}
+
+static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W, int n, uint64_t P,
+                       uint64_t Q, bool scale, const double* lam_a = nullptr,
+                       const double* lam_c = nullptr) {
+  ModeArgs a{};
+  a.X = X;
+  a.Y = Y;
+  a.W = W;
+  a.lam_a = lam_a;
+  a.lam_c = lam_c;
+  a.n = n;
+  a.P = uint32_t(P);
+  a.Q = uint32_t(Q);
+  a.ncols = uint32_t(P * Q);
+  const bool mode1 = (Q == 1);
+  switch (round_ks((n + 3) / 4)) {
+    KS_A(2) KS_A(4) KS_A(5) KS_A(8)
+    KS_B(12) KS_B(17) KS_B(18)
+    KS_C(24) KS_C(25) KS_C(26)
+    KS_D(30) KS_D(33) KS_D(34)
+    default: return LS_EINVAL;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// setup
+// ------------------------------------------------------------------------------------------
+static int to_band(ls_ctx* ctx, const std::vector<double>& A, int n, int hb, double** out) {
+  const int W = 2 * hb + 1;
+  std::vector<double> band(size_t(n) * W, 0.0);
+  for (int a = 0; a < n; ++a)
+    for (int i = std::max(0, a - hb); i <= std::min(n - 1, a + hb); ++i)
+      band[size_t(a) * W + (i - a + hb)] = A[size_t(a) * n + i];
+  LS_CHECK(ctx->alloc(out, band.size()));
+  LS_CUDA(cudaMemcpy(*out, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
+// generalized eigendecomposition K U = M U Lambda, U^T M U = I (eq:eig_dec) by cuSOLVER Dsygvd
+static int gen_eig(ls_ctx* ctx, cusolverDnHandle_t h, const std::vector<double>& K,
+                   const std::vector<double>& M, int n, std::vector<double>& lam,
+                   std::vector<double>& Urm) {
+  double *dA = nullptr, *dB = nullptr, *dW = nullptr, *work = nullptr;
+  int* info = nullptr;
+  int lwork = 0, hinfo = 0;
+  int rc = LS_OK;
+  LS_CUDA(cudaMalloc(&dA, sizeof(double) * n * n));
+  LS_CUDA(cudaMalloc(&dB, sizeof(double) * n * n));
+  LS_CUDA(cudaMalloc(&dW, sizeof(double) * n));
+  LS_CUDA(cudaMalloc(&info, sizeof(int)));
+  LS_CUDA(cudaMemcpy(dA, K.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  LS_CUDA(cudaMemcpy(dB, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+  if (cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                  CUBLAS_FILL_MODE_LOWER, n, dA, n, dB, n, dW, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    rc = LS_ECUDA;
+  if (rc == LS_OK) LS_CUDA(cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)));
+  if (rc == LS_OK &&
+      cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                       dA, n, dB, n, dW, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    rc = LS_ECUDA;
+  if (rc == LS_OK) {
+    LS_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hinfo > n) rc = LS_ENOTSPD;       // leading minor of M not positive definite
+    else if (hinfo != 0) rc = LS_ECUDA;   // eigensolver did not converge
+  }
+  std::vector<double> Ucm(size_t(n) * n);
+  lam.assign(n, 0.0);
+  if (rc == LS_OK) {
+    LS_CUDA(cudaMemcpy(Ucm.data(), dA, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
+    LS_CUDA(cudaMemcpy(lam.data(), dW, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dW);
+  cudaFree(work);
+  cudaFree(info);
+  if (rc != LS_OK) return rc;
+  // column j of the column-major result is eigenvector j: U[i][j] = Ucm[i + j n]
+  Urm.assign(size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) Urm[size_t(i) * n + j] = Ucm[i + size_t(j) * n];
+  // sanity: U^T M U = I (PAPER.md 945)
+  double err = 0;
+  for (int a = 0; a < n; ++a)
+    for (int b = 0; b < n; ++b) {
+      double s = 0;
+      for (int i = 0; i < n; ++i) {
+        double mu = 0;
+        for (int j = 0; j < n; ++j) mu += M[size_t(i) * n + j] * Urm[size_t(j) * n + b];
+        s += Urm[size_t(i) * n + a] * mu;
+      }
+      err = std::max(err, std::fabs(s - (a == b ? 1.0 : 0.0)));
+    }
+  if (!(err < 1e-8)) return LS_ENOTSPD;
+  (void)ctx;
+  return LS_OK;
+}
+
+static int upload(ls_ctx* ctx, const std::vector<double>& v, double** out) {
+  LS_CHECK(ctx->alloc(out, v.size()));
+  LS_CUDA(cudaMemcpy(*out, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
+static int setup_common(ls_ctx* ctx) {
+  const int d = ctx->d, p = ctx->p;
+  int dev = 0;
+  LS_CUDA(cudaGetDevice(&dev));
+  LS_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  // sizes (reading c1): n_k = n_el + p - 2, n_t = n_el + p - 1
+  ctx->Ns = 1;
+  for (int k = 0; k < d; ++k) {
+    ctx->n[k] = int(ctx->n_el[k] + p - 2);
+    ctx->Ns *= ctx->n[k];
+  }
+  ctx->nt = int(ctx->n_el[d] + p - 1);
+  for (int k = 0; k < d; ++k)
+    if (ctx->n[k] > N_MAX) return LS_EINVAL;
+  if (ctx->nt > N_MAX) return LS_EINVAL;
+  ctx->Ntot = ctx->Ns * ctx->nt;
+  if (ctx->Ns >= (int64_t(1) << 31)) return LS_EINVAL;
+  // slab layout: uneven split of n_t over `world` ranks
+  {
+    const int64_t base = ctx->nt / ctx->world, extra = ctx->nt % ctx->world;
+    ctx->ntl = base + (ctx->rank < extra ? 1 : 0);
+    ctx->t0 = ctx->rank * base + std::min<int64_t>(ctx->rank, extra);
+    ctx->Nl = ctx->ntl * ctx->Ns;
+  }
+  // memory estimate: 6 workspaces + 4 pcg vectors (+ 2 all-to-all buffers when distributed)
+  {
+    size_t fr = 0, tot = 0;
+    LS_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double need = double(ctx->Nl) * 8.0 * (10 + (ctx->world > 1 ? 2 : 0)) + 64e6;
+    if (need > double(fr)) return LS_ENOMEM;
+  }
+
+  // host assembly (PAPER.md 686-703, 738-757)
+  cusolverDnHandle_t h = nullptr;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return LS_ECUDA;
+  int rc = LS_OK;
+  for (int k = 0; k < d && rc == LS_OK; ++k) {
+    Factors f = space_factors(int(ctx->n_el[k]), p);
+    ctx->hM[k] = f.M;
+    ctx->hK[k] = f.K;
+    ctx->hJ[k] = f.J;
+    rc = gen_eig(ctx, h, f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
+  }
+  Factors ft = time_factors(int(ctx->n_el[d]), p);
+  ctx->hMt = ft.M;
+  ctx->hKt = ft.K;
+  if (rc == LS_OK) rc = gen_eig(ctx, h, ft.K, ft.M, ft.n, ctx->hlam[3], ctx->hU[3]);
+  cusolverDnDestroy(h);
+  if (rc != LS_OK) return rc;
+
+  // device copies: W_fwd = U^T, W_bwd = U (row-major), eigenvalues
+  for (int k = 0; k < 4; ++k) {
+    if (k >= d && k != 3) continue;
+    const int n = (k == 3) ? ctx->nt : ctx->n[k];
+    std::vector<double> Ut(size_t(n) * n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) Ut[size_t(j) * n + i] = ctx->hU[k][size_t(i) * n + j];
+    LS_CHECK(upload(ctx, Ut, &ctx->Wf[k]));
+    LS_CHECK(upload(ctx, ctx->hU[k], &ctx->Wb[k]));
+    LS_CHECK(upload(ctx, ctx->hlam[k], &ctx->lam[k]));
+  }
+  LS_CHECK(ctx->alloc(&ctx->lam_s, ctx->Ns));
+  lambda_s_kernel<<<1024, 256, 0, ctx->stream>>>(ctx->lam_s, ctx->lam[0], d >= 2 ? ctx->lam[1] : nullptr,
+                                                 d >= 3 ? ctx->lam[2] : nullptr, ctx->n[0],
+                                                 d >= 2 ? ctx->n[1] : 1, d, uint64_t(ctx->Ns));
+  ctx->launches++;
+  LS_CUDA(cudaGetLastError());
+  // banded factors for A (identity map, T = 1: K_t = K_t^, M_t = M_t^; reading c9)
+  for (int k = 0; k < d; ++k) {
+    LS_CHECK(to_band(ctx, ctx->hM[k], ctx->n[k], p, &ctx->bM[k]));
+    LS_CHECK(to_band(ctx, ctx->hK[k], ctx->n[k], p, &ctx->bK[k]));
+    LS_CHECK(to_band(ctx, ctx->hJ[k], ctx->n[k], p, &ctx->bJ[k]));
+  }
+  LS_CHECK(to_band(ctx, ctx->hMt, ctx->nt, p, &ctx->bMt));
+  LS_CHECK(to_band(ctx, ctx->hKt, ctx->nt, p, &ctx->bKt));
+  // workspaces (halo rows for the distributed matvec: p slices each side)
+  const size_t halo = size_t(2 * p) * ctx->Ns;
+  for (int i = 0; i < 6; ++i) LS_CHECK(ctx->alloc(&ctx->tmp[i], ctx->Nl + halo));
+  LS_CHECK(ctx->alloc(&ctx->pr, ctx->Nl));
+  LS_CHECK(ctx->alloc(&ctx->pz, ctx->Nl));
+  LS_CHECK(ctx->alloc(&ctx->pp, ctx->Nl + halo));
+  LS_CHECK(ctx->alloc(&ctx->pq, ctx->Nl));
+  LS_CHECK(ctx->alloc(&ctx->partials, RED_BLOCKS));
+  LS_CHECK(ctx->alloc(&ctx->scal, S_NSLOT));
+  LS_CHECK(ctx->alloc(&ctx->rhs_buf, 6 * NMAX_STACK));
+  LS_CUDA(cudaMallocHost(&ctx->h_scal, S_NSLOT * sizeof(double)));
+  LS_CUDA(cudaDeviceSynchronize());
+  return LS_OK;
+}
+
+static int validate(int d, int p, const int64_t* n_elems) {
+  if (d < 1 || d > 3 || p < 2 || n_elems == nullptr) return LS_EINVAL;
+  for (int k = 0; k <= d; ++k)
+    if (n_elems[k] < 1 || n_elems[k] > 100000) return LS_EINVAL;
+  return LS_OK;
+}
+
+extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
+  if (!out) return LS_EINVAL;
+  *out = nullptr;
+  LS_CHECK(validate(d, p, n_elems));
+  auto* ctx = new ls_ctx();
+  ctx->d = d;
+  ctx->p = p;
+  for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
+  int rc = setup_common(ctx);
+  if (rc != LS_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return LS_OK;
+}
+
+extern "C" int ls_get_unique_id(void* out128) {
+  if (!out128) return LS_EINVAL;
+  return comm_unique_id(out128);
+}
+
+extern "C" int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int world,
+                             const void* nccl_unique_id, ls_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id))
+    return LS_EINVAL;
+  *out = nullptr;
+  LS_CHECK(validate(d, p, n_elems));
+  auto* ctx = new ls_ctx();
+  ctx->d = d;
+  ctx->p = p;
+  ctx->rank = rank;
+  ctx->world = world;
+  for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
+  // every slab must be at least p time slices thick (halo of the banded time factors)
+  if (world > 1 && (n_elems[d] + p - 1) / world < p) {
+    delete ctx;
+    return LS_EINVAL;
+  }
+  int rc = setup_common(ctx);
+  if (rc == LS_OK && world > 1) {
+    ctx->comm.reset(new Comm());
+    rc = ctx->comm->init(nccl_unique_id, rank, world, ctx->nt, ctx->Ns);
+  }
+  if (rc != LS_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return LS_OK;
+}
+
+extern "C" int ls_layout(const ls_ctx* ctx, int64_t* n_t, int64_t* n_s, int64_t* t0,
+                         int64_t* nt_local) {
+  if (!ctx) return LS_EINVAL;
+  if (n_t) *n_t = ctx->nt;
+  if (n_s)
+    for (int k = 0; k < ctx->d; ++k) n_s[k] = ctx->n[k];
+  if (t0) *t0 = ctx->t0;
+  if (nt_local) *nt_local = ctx->ntl;
+  return LS_OK;
+}
+
+extern "C" int ls_set_stream(ls_ctx* ctx, void* s) {
+  if (!ctx) return LS_EINVAL;
+  ctx->stream = static_cast<cudaStream_t>(s);
+  if (ctx->comm) ctx->comm->stream = ctx->stream;
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// fd_apply: Algorithm 1 steps 2-4
+// ------------------------------------------------------------------------------------------
+static inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
+
+// spatial modes on a [rows][n_d]..[n_1] block (rows = local time slices)
+static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0, double* ws1,
+                         uint64_t rows, bool forward) {
+  const int d = ctx->d;
+  // forward: modes 1..d ; backward: modes d..1.  Ping-pong ws0/ws1, first reads `in`,
+  // last writes `out`.
+  const double* src = in;
+  for (int s = 0; s < d; ++s) {
+    const int k = forward ? s : d - 1 - s;  // 0-based direction
+    uint64_t Q = 1, P = rows;
+    for (int j = 0; j < k; ++j) Q *= ctx->n[j];
+    for (int j = k + 1; j < d; ++j) P *= ctx->n[j];
+    double* dst = (s == d - 1) ? out : ((s % 2 == 0) ? ws0 : ws1);
+    LS_CHECK(launch_mode(ctx, src, dst, forward ? ctx->Wf[k] : ctx->Wb[k], ctx->n[k], P, Q, false));
+    src = dst;
+  }
+  return LS_OK;
+}
+
+extern "C" int fd_apply(ls_ctx* ctx, const double* r, double* z) {
+  if (!ctx || !r || !z || !aligned8(r) || !aligned8(z)) return LS_EINVAL;
+  double* A = ctx->tmp[0];
+  double* B = ctx->tmp[1];
+  double* C = ctx->tmp[2];
+  if (ctx->world == 1) {
+    // F1: forward spatial modes r -> A ; F2: time fwd + scale (A -> B), time bwd (B -> C)
+    LS_CHECK(spatial_modes(ctx, r, A, B, C, ctx->nt, true));
+    LS_CHECK(launch_mode(ctx, A, B, ctx->Wf[3], ctx->nt, 1, ctx->Ns, true, ctx->lam[3], ctx->lam_s));
+    LS_CHECK(launch_mode(ctx, B, C, ctx->Wb[3], ctx->nt, 1, ctx->Ns, false));
+    // F3: backward spatial modes C -> z
+    LS_CHECK(spatial_modes(ctx, C, z, A, B, ctx->nt, false));
+    return LS_OK;
+  }
+  return comm_fd_apply(ctx, r, z);
+}
+
+// distributed fd_apply: slab -> all-to-all -> time mode on spatial chunks -> all-to-all -> slab
+int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
+  Comm& cm = *ctx->comm;
+  double* A = ctx->tmp[0];
+  double* B = ctx->tmp[1];
+  double* C = ctx->tmp[2];
+  LS_CHECK(spatial_modes(ctx, r, A, B, C, ctx->ntl, true));
+  // A: [ntl][Ns] slab -> B: [nt][chunk] (send order = destination chunks)
+  LS_CHECK(cm.slab_to_chunk(A, B, C, ctx->launches));
+  const int64_t chunk = cm.chunk_len[ctx->rank];
+  const int64_t c0 = cm.chunk_off[ctx->rank];
+  if (chunk > 0) {
+    LS_CHECK(launch_mode(ctx, B, C, ctx->Wf[3], ctx->nt, 1, chunk, true, ctx->lam[3], ctx->lam_s + c0));
+    LS_CHECK(launch_mode(ctx, C, B, ctx->Wb[3], ctx->nt, 1, chunk, false));
+  }
+  LS_CHECK(cm.chunk_to_slab(B, A, C, ctx->launches));
+  LS_CHECK(spatial_modes(ctx, A, z, B, C, ctx->ntl, false));
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// ls_matvec
+// ------------------------------------------------------------------------------------------
+static unsigned grid_for(uint64_t total, int threads, int num_sms) {
+  uint64_t g = (total + threads - 1) / threads;
+  return unsigned(std::min<uint64_t>(g, uint64_t(num_sms) * 16));
+}
+
+// y = A x on `rows` time slices starting at x (x, y point at slice 0 of the rows given);
+// spatial part on rows [0, rows), time part on output rows [out0, out0+nout) of that block.
+static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t trow0,
+                        int64_t out0, int64_t nout) {
+  const int d = ctx->d;
+  double* S[3] = {ctx->tmp[0], ctx->tmp[1], ctx->tmp[2]};
+  double* T[3] = {ctx->tmp[3], ctx->tmp[4], ctx->tmp[5]};
+  const uint64_t total = uint64_t(rows) * ctx->Ns;
+  for (int k = 0; k < d; ++k) {
+    BandArgs a{};
+    uint64_t Q = 1;
+    for (int j = 0; j < k; ++j) Q *= ctx->n[j];
+    a.SM = (k == 0) ? x : S[0];
+    a.SK = (k == 0) ? nullptr : S[1];
+    a.SJ = (k == 0) ? nullptr : S[2];
+    a.oM = T[0];
+    a.oK = T[1];
+    a.oJ = T[2];
+    a.bM = ctx->bM[k];
+    a.bK = ctx->bK[k];
+    a.bJ = ctx->bJ[k];
+    a.n = ctx->n[k];
+    a.hb = ctx->p;
+    a.Q = uint32_t(Q);
+    a.total = total;
+    const unsigned g = grid_for(total, 256, ctx->num_sms);
+    if (k == 0)
+      band_triple_kernel<true><<<g, 256, 0, ctx->stream>>>(a);
+    else
+      band_triple_kernel<false><<<g, 256, 0, ctx->stream>>>(a);
+    ctx->launches++;
+    LS_CUDA(cudaGetLastError());
+    std::swap(S, T);
+  }
+  // time: y = K_t S_M + M_t S_J + W_t S_K on output rows [out0, out0 + nout)
+  TimeArgs t{};
+  t.SM = S[0];
+  t.SK = S[1];
+  t.SJ = S[2];
+  t.y = y;
+  t.bKt = ctx->bKt;
+  t.bMt = ctx->bMt;
+  t.nt = ctx->nt;
+  t.hb = ctx->p;
+  t.Ns = uint32_t(ctx->Ns);
+  (void)trow0;
+  (void)out0;
+  t.total = uint64_t(nout) * ctx->Ns;
+  band_time_kernel<<<grid_for(t.total, 256, ctx->num_sms), 256, 0, ctx->stream>>>(t);
+  ctx->launches++;
+  LS_CUDA(cudaGetLastError());
+  return LS_OK;
+}
+
+extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
+  if (!ctx || !x || !y || x == y || !aligned8(x) || !aligned8(y)) return LS_EINVAL;
+  if (ctx->world == 1) return matvec_block(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
+  return LS_ENOTSUP;
+}
+
+// ------------------------------------------------------------------------------------------
+// ls_rhs (PAPER.md 409; reading c11)
+// ------------------------------------------------------------------------------------------
+extern "C" int ls_rhs(ls_ctx* ctx, int kind, double* b) {
+  if (!ctx || !b || !aligned8(b)) return LS_EINVAL;
+  if (kind != 0 && kind != 1) return LS_EINVAL;
+  const int d = ctx->d;
+  std::vector<double> stack(6 * NMAX_STACK, 0.0);  // S0[3], S2[3] ... G0, G1 stacked
+  std::vector<double> i0, i1, i2;
+  for (int k = 0; k < d; ++k) {
+    load_integrals(int(ctx->n_el[k]), ctx->p, true, 0, 0.0, i0, i1, i2);
+    std::copy(i0.begin(), i0.end(), stack.begin() + k * NMAX_STACK);
+    std::copy(i2.begin(), i2.end(), stack.begin() + (3 + k) * NMAX_STACK);
+  }
+  const double pi = 3.14159265358979323846;
+  load_integrals(int(ctx->n_el[d]), ctx->p, false, kind == 0 ? 1 : 2, d * pi * pi, i0, i1, i2);
+  std::vector<double> G(2 * NMAX_STACK, 0.0);
+  std::copy(i0.begin(), i0.end(), G.begin());
+  std::copy(i1.begin(), i1.end(), G.begin() + NMAX_STACK);
+  // device buffer: [S0 x3 | S2 x3] then G0, G1 reuse a second region
+  double* dS = ctx->rhs_buf;
+  LS_CUDA(cudaMemcpyAsync(dS, stack.data(), stack.size() * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  // G0/G1 are staged in the partials buffer tail (RED_BLOCKS >= 2*NMAX_STACK)
+  double* dG = ctx->partials;
+  LS_CUDA(cudaMemcpyAsync(dG, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  const uint64_t total = uint64_t(ctx->Nl);
+  rhs_outer_kernel<<<grid_for(total, 256, ctx->num_sms), 256, 0, ctx->stream>>>(
+      b, dG, dG + NMAX_STACK, dS, dS + 3 * NMAX_STACK, d, ctx->n[0], ctx->n[1], ctx->n[2],
+      uint64_t(ctx->Ns), total, uint64_t(ctx->t0));
+  ctx->launches++;
+  LS_CUDA(cudaGetLastError());
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// PCG
+// ------------------------------------------------------------------------------------------
+static int dot(ls_ctx* ctx, const double* a, const double* b, int slot) {
+  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(a, b, uint64_t(ctx->Nl), ctx->partials);
+  reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, slot);
+  ctx->launches += 2;
+  LS_CUDA(cudaGetLastError());
+  if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + slot));
+  return LS_OK;
+}
+
+static int read_scal(ls_ctx* ctx) {
+  LS_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal, S_NSLOT * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LS_OK;
+}
+
+extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
+                         ls_pcg_stats* st) {
+  if (!ctx || !b || !x || !aligned8(b) || !aligned8(x) || !(tol >= 0) || max_iter < 0)
+    return LS_EINVAL;
+  ls_pcg_stats s{0, 0.0, 0.0, LS_OK};
+  const size_t bytes = size_t(ctx->Nl) * sizeof(double);
+  LS_CUDA(cudaMemsetAsync(x, 0, bytes, ctx->stream));
+  LS_CHECK(dot(ctx, b, b, S_BB));
+  LS_CHECK(read_scal(ctx));
+  const double bnorm = std::sqrt(ctx->h_scal[S_BB]);
+  if (bnorm == 0.0) {
+    if (st) *st = s;
+    return LS_OK;
+  }
+  double *r = ctx->pr, *z = ctx->pz, *p = ctx->pp, *q = ctx->pq;
+  LS_CUDA(cudaMemcpyAsync(r, b, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  LS_CHECK(fd_apply(ctx, r, z));
+  int cur = S_RHO0, nxt = S_RHO1;
+  LS_CHECK(dot(ctx, r, z, cur));
+  LS_CUDA(cudaMemcpyAsync(p, z, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  double rel = 1.0;
+  int k = 0;
+  s.status = LS_ENOCONV;
+  const unsigned g = RED_BLOCKS;
+  while (k < max_iter) {
+    LS_CHECK(ls_matvec(ctx, p, q));
+    LS_CHECK(dot(ctx, p, q, S_PQ));
+    update_xr_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(x, r, p, q, uint64_t(ctx->Nl), ctx->scal, cur,
+                                                         ctx->partials);
+    reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, S_RR);
+    ctx->launches += 2;
+    LS_CUDA(cudaGetLastError());
+    if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + S_RR));
+    LS_CHECK(read_scal(ctx));
+    ++k;
+    const double rr = ctx->h_scal[S_RR], alpha = ctx->h_scal[S_ALPHA];
+    if (!std::isfinite(rr) || !std::isfinite(alpha)) {
+      s.status = LS_ENUMERIC;
+      break;
+    }
+    rel = std::sqrt(rr) / bnorm;
+    if (rel <= tol) {
+      s.status = LS_OK;
+      break;
+    }
+    LS_CHECK(fd_apply(ctx, r, z));
+    LS_CHECK(dot(ctx, r, z, nxt));
+    update_p_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(p, z, uint64_t(ctx->Nl), ctx->scal, nxt, cur);
+    ctx->launches++;
+    LS_CUDA(cudaGetLastError());
+    std::swap(cur, nxt);
+  }
+  s.iters = k;
+  s.rel_res = rel;
+  // true residual ||b - A x|| / ||b||
+  LS_CHECK(ls_matvec(ctx, x, q));
+  sub_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(z, b, q, uint64_t(ctx->Nl));
+  ctx->launches++;
+  LS_CHECK(dot(ctx, z, z, S_RR));
+  LS_CHECK(read_scal(ctx));
+  s.true_rel_res = std::sqrt(ctx->h_scal[S_RR]) / bnorm;
+  if (st) *st = s;
+  return s.status;
+}
+
+// ------------------------------------------------------------------------------------------
+// host-buffer entry point, introspection, teardown
+// ------------------------------------------------------------------------------------------
+extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) {
+  if (!ctx || !r_host || !z_host) return LS_EINVAL;
+  const size_t bytes = size_t(ctx->Nl) * sizeof(double);
+  LS_CUDA(cudaMemcpyAsync(ctx->pr, r_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  LS_CHECK(fd_apply(ctx, ctx->pr, ctx->pz));
+  LS_CUDA(cudaMemcpyAsync(z_host, ctx->pz, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LS_OK;
+}
+
+extern "C" int ls_get_factor(const ls_ctx* ctx, int which, int dir, double* out) {
+  if (!ctx || !out) return LS_EINVAL;
+  const std::vector<double>* v = nullptr;
+  const int k = dir - 1;
+  const bool sp = (k >= 0 && k < ctx->d);
+  switch (which) {
+    case 0: v = sp ? &ctx->hM[k] : nullptr; break;
+    case 1: v = sp ? &ctx->hK[k] : nullptr; break;
+    case 2: v = sp ? &ctx->hJ[k] : nullptr; break;
+    case 3: v = &ctx->hMt; break;
+    case 4: v = &ctx->hKt; break;
+    case 5: v = sp ? &ctx->hlam[k] : nullptr; break;
+    case 6: v = &ctx->hlam[3]; break;
+    case 7: v = sp ? &ctx->hU[k] : nullptr; break;
+    case 8: v = &ctx->hU[3]; break;
+    default: return LS_EINVAL;
+  }
+  if (!v) return LS_EINVAL;
+  std::memcpy(out, v->data(), v->size() * sizeof(double));
+  return LS_OK;
+}
+
+extern "C" int ls_profile(ls_ctx* ctx, int enable) {
+  if (!ctx) return LS_EINVAL;
+  ctx->prof = enable != 0;
+  return LS_OK;
+}
+
+extern "C" int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t* n) {
+  if (!ctx) return LS_EINVAL;
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  double ms = 0, fl = 0;
+  for (auto& r : ctx->prof_recs) {
+    float t = 0;
+    LS_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    fl += r.flops;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  if (total_ms) *total_ms = ms;
+  if (total_flops) *total_flops = fl;
+  if (n) *n = int64_t(ctx->prof_recs.size());
+  ctx->prof_recs.clear();
+  return LS_OK;
+}
+
+extern "C" int64_t ls_kernel_launches(const ls_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+extern "C" void ls_destroy(ls_ctx* ctx) {
+  if (!ctx) return;
+  cudaDeviceSynchronize();
+  delete ctx;
+}
+
+extern "C" const char* ls_strerror(int code) {
+  switch (code) {
+    case LS_OK: return "ok";
+    case LS_EINVAL: return "invalid argument";
+    case LS_ENOTSPD: return "mass matrix not SPD (Cholesky failure in the generalized eigensolver)";
+    case LS_ENOCONV: return "PCG did not converge within max_iter";
+    case LS_ENUMERIC: return "NaN/Inf in a PCG scalar";
+    case LS_ENOMEM: return "not enough device memory";
+    case LS_ECUDA: return "CUDA runtime error";
+    case LS_ENCCL: return "NCCL error";
+    case LS_ENOTSUP: return "operation not supported for this context";
+    default: return "unknown error";
+  }
+}

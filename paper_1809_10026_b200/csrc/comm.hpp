@@ -1,0 +1,56 @@
+// Multi-GPU plumbing for the time-slab partition.
+//
+// Rank g owns time slices [t0_g, t0_g + ntl_g) of the [n_t][N_s] tensor (uneven
+// split).  The spatial modes of fd_apply are local to a slab; the time mode
+// needs every time slice of a column, so fd_apply reshards
+//     slab [ntl][N_s]  --all-to-all-->  spatial chunk [n_t][chunk_h]
+// (rank h owns the contiguous spatial range [c0_h, c0_h + chunk_h)), applies
+// the fused time mode there, and reshards back.  Because slabs are time
+// ordered, the block received from rank g lands contiguously at rows
+// [t0_g, t0_g + ntl_g) of the chunk tensor: only the send side needs a pack.
+// ls_matvec needs p halo time slices from each neighbour (banded time factors);
+// PCG all-reduces its scalar dot products.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+struct ls_ctx;
+
+namespace ls {
+
+struct Comm {
+  void* nccl = nullptr;  // ncclComm_t
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  int64_t nt = 0, Ns = 0;
+  std::vector<int64_t> slab_t0, slab_len;    // per rank, time slabs
+  std::vector<int64_t> chunk_off, chunk_len; // per rank, spatial chunks
+  ~Comm();
+  int init(const void* uid, int rank, int world, int64_t nt, int64_t Ns);
+  // A: local slab [ntl][Ns] -> B: [nt][chunk_me]; tmp: send staging (>= ntl*Ns)
+  int slab_to_chunk(const double* A, double* B, double* tmp, int64_t& launches);
+  // B: [nt][chunk_me] -> A: local slab [ntl][Ns]; tmp: receive staging
+  int chunk_to_slab(const double* B, double* A, double* tmp, int64_t& launches);
+  // x_ext = [p halo | own ntl slices | p halo]: fill the halos from the neighbours
+  int halo_exchange(double* x_ext, int64_t halo_lo, int64_t halo_hi, int64_t& launches);
+  int allreduce_scalar(double* dev_ptr);
+};
+
+int comm_unique_id(void* out128);
+
+// Even split of `total` items over `world` parts (the first total % world parts get one more).
+inline void split_even(int64_t total, int world, std::vector<int64_t>& off, std::vector<int64_t>& len) {
+  off.assign(world, 0);
+  len.assign(world, 0);
+  const int64_t base = total / world, extra = total % world;
+  for (int g = 0; g < world; ++g) {
+    len[g] = base + (g < extra ? 1 : 0);
+    off[g] = g * base + (g < extra ? g : extra);
+  }
+}
+
+} // namespace ls
+
+int comm_fd_apply(ls_ctx* ctx, const double* r, double* z);

@@ -1,0 +1,37 @@
+// Host-side univariate setup: knots, Gauss-Legendre,
+// B-spline evaluation and dense assembly of the univariate factor matrices.
+// Everything here is O(n^2 p) per direction and runs once in ls_setup.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace ls {
+
+// Open uniform knot vector on [0,1] with n_el elements (PAPER.md 144-147, 1111-1112).
+std::vector<double> open_uniform_knots(int n_el, int p);
+
+// q-point Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence).
+void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& w);
+
+// Values and first/second derivatives of all m = len(knots)-p-1 B-splines at x
+// (Cox-de Boor, PAPER.md 148-166; derivative recursion of de Boor).
+void bspline_eval(const std::vector<double>& knots, int p, double x, double* v0, double* v1,
+                  double* v2);
+
+struct Factors {
+  int n = 0;                   // constrained size
+  std::vector<double> M, K, J; // dense n x n row-major; J empty for time
+};
+
+// Space pencil on the Dirichlet-constrained basis (i = 2..m-1): M, K (= int b'b'), J.
+Factors space_factors(int n_el, int p);
+// Time matrices on the initial-condition-constrained basis (i = 2..m): M_t^, K_t^.
+Factors time_factors(int n_el, int p);
+
+// Univariate load integrals for a separable forcing with q = p + 5 Gauss points
+// per element (reading c16).  fn: 0 = sin(pi x), 1 = e^t, 2 = cos t + c sin t.
+// Returns int fn b_i, int fn b_i', int fn b_i'' over the constrained basis.
+void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<double>& i0,
+                    std::vector<double>& i1, std::vector<double>& i2);
+
+} // namespace ls

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Bar (BASELINE.json north_star): relative 2-norm error
+<= 1e-9 in fp64; setup quantities to 1e-10."""
+
+import numpy as np
+import pytest
+
+from oracle import univariate as uv, fd, operator as op, rhs as orhs, pcg as opcg, bspline as bs
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _ctx(d, p, n_elems):
+    import paper_1809_10026_b200 as ls
+    return ls.Context(d, p, n_elems)
+
+
+def _oracle(d, p, n_elems):
+    space = [uv.space_factors(n, p) for n in n_elems[:d]]
+    tf = uv.time_factors(n_elems[d], p)
+    return space, tf, fd.setup(space, tf)
+
+
+def _rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+# (d, p, n_elems) -- BASELINE configs 1-2 plus shapes chosen to hit every kernel
+# bucket (n up to 136), odd/even extents, several tiles and ragged tails.
+FD_CASES = [
+    (1, 2, [16, 16]),          # config 1
+    (1, 5, [40, 31]),
+    (1, 2, [130, 134]),        # n_s = 130, n_t = 135 (largest bucket)
+    (2, 2, [5, 7, 6]),
+    (2, 3, [64, 64, 64]),      # config 2
+    (2, 6, [98, 20, 30]),      # n = 102 bucket
+    (3, 2, [3, 4, 5, 6]),
+    (3, 3, [6, 6, 6, 6]),
+    (3, 4, [8, 9, 10, 11]),
+    (3, 3, [20, 17, 9, 31]),
+]
+
+
+@pytest.mark.parametrize("d,p,n_elems", FD_CASES)
+def test_setup_factors_match_oracle(torch_cuda, d, p, n_elems):
+    ctx = _ctx(d, p, n_elems)
+    space, tf, fdd = _oracle(d, p, n_elems)
+    for k in range(1, d + 1):
+        for which, key in ((0, "M"), (1, "K"), (2, "J")):
+            A = space[k - 1][key]
+            np.testing.assert_allclose(ctx.get_factor(which, k), A, rtol=0, atol=1e-12 * np.abs(A).max())
+        lam = ctx.get_factor(5, k)
+        np.testing.assert_allclose(lam, fdd["lam_s"][k - 1], rtol=1e-10)
+        U = ctx.get_factor(7, k)
+        M, J = space[k - 1]["M"], space[k - 1]["J"]
+        n = M.shape[0]
+        assert np.max(np.abs(U.T @ M @ U - np.eye(n))) < 1e-10
+        assert np.max(np.abs(U.T @ J @ U - np.diag(lam))) < 1e-10 * lam.max()
+    np.testing.assert_allclose(ctx.get_factor(3), tf["Mt_hat"], atol=1e-14)
+    np.testing.assert_allclose(ctx.get_factor(4), tf["Kt_hat"], atol=1e-12 * np.abs(tf["Kt_hat"]).max())
+    np.testing.assert_allclose(ctx.get_factor(6), fdd["lam_t"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("d,p,n_elems", FD_CASES)
+@pytest.mark.parametrize("seed", [0, 1])
+def test_fd_apply_matches_oracle(torch_cuda, d, p, n_elems, seed):
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    _, _, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, seed)
+    z_ref = fd.fd_apply(r, fdd)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert _rel(z, z_ref) <= TOL
+    # element-wise: every entry within 1e-9 of the largest
+    assert np.max(np.abs(z - z_ref)) <= TOL * np.abs(z_ref).max()
+
+
+def test_fd_apply_config1_dense_solve(torch_cuda):
+    """BASELINE config 1: one fd_apply against a dense Kronecker solve of P."""
+    import scipy.linalg
+    torch = torch_cuda
+    ctx = _ctx(1, 2, [16, 16])
+    space, tf, _ = _oracle(1, 2, [16, 16])
+    P = fd.dense_P(space, tf)
+    r = synth.residual(ctx.shape, 0)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy().ravel()
+    z_dense = scipy.linalg.cho_solve(scipy.linalg.cho_factor(P), r.ravel())
+    assert _rel(z, z_dense) <= TOL
+    assert np.linalg.norm(P @ z - r.ravel()) / np.linalg.norm(r) <= TOL
+
+
+def test_fd_apply_in_place_and_zero(torch_cuda):
+    torch = torch_cuda
+    ctx = _ctx(3, 3, [6, 7, 8, 9])
+    _, _, fdd = _oracle(3, 3, [6, 7, 8, 9])
+    r = synth.residual(ctx.shape, 3)
+    t = torch.from_numpy(r).cuda()
+    ctx.fd_apply(t, t)
+    assert _rel(t.cpu().numpy(), fd.fd_apply(r, fdd)) <= TOL
+    zero = torch.zeros(ctx.shape, dtype=torch.float64, device="cuda")
+    assert torch.count_nonzero(ctx.fd_apply(zero)).item() == 0
+
+
+MV_CASES = [
+    (1, 2, [16, 16]),
+    (1, 4, [9, 13]),
+    (2, 2, [5, 7, 6]),
+    (2, 3, [64, 64, 64]),
+    (3, 2, [3, 4, 5, 6]),
+    (3, 5, [7, 6, 9, 8]),
+]
+
+
+@pytest.mark.parametrize("d,p,n_elems", MV_CASES)
+def test_matvec_matches_oracle(torch_cuda, d, p, n_elems):
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    space, tf, _ = _oracle(d, p, n_elems)
+    x = synth.residual(ctx.shape, 5)
+    y_ref = op.apply_A(x, space, tf)
+    y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert _rel(y, y_ref) <= 1e-12
+
+
+def test_matvec_original_form_tiny(torch_cuda):
+    """Against the dense ORIGINAL least-squares form (PAPER.md 406)."""
+    torch = torch_cuda
+    d, p, ne = 2, 3, [3, 2, 3]
+    ctx = _ctx(d, p, ne)
+    A = op.dense_A_original_form([bs.open_uniform_knots(n, p) for n in ne[:d]], p,
+                                 bs.open_uniform_knots(ne[d], p), p)
+    x = synth.residual(ctx.shape, 6)
+    y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy().ravel()
+    assert _rel(y, A @ x.ravel()) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("d,p,n_elems", [(1, 2, [16, 16]), (2, 3, [64, 64, 64]), (3, 4, [8, 9, 10, 11])])
+def test_rhs_matches_oracle(torch_cuda, kind, d, p, n_elems):
+    ctx = _ctx(d, p, n_elems)
+    b_ref = orhs.rhs(kind, [bs.open_uniform_knots(n, p) for n in n_elems[:d]], p,
+                     bs.open_uniform_knots(n_elems[d], p), p)
+    b = ctx.rhs(kind).cpu().numpy()
+    assert _rel(b, b_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n_el", [8, 16])
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_pcg_table1(torch_cuda, n_el, p):
+    """Table 1 (PAPER.md 1187-1189) iteration counts on the GPU, and the
+    solution against the oracle's PCG at the same iteration count."""
+    from conftest import golden
+    ctx = _ctx(3, p, [n_el] * 4)
+    b = ctx.rhs(1)
+    x, st = ctx.pcg(b, tol=1e-8)
+    want = golden("table1_iterations.json")["iterations"][str(n_el)][p - 2]
+    assert st["status"] == 0 and st["iters"] == want
+    assert st["true_rel_res"] <= 1e-7
+    space, tf, fdd = _oracle(3, p, [n_el] * 4)
+    bo = b.cpu().numpy()
+    xo, it, conv, _ = opcg.pcg(lambda v: op.apply_A(v, space, tf), lambda v: fd.fd_apply(v, fdd), bo)
+    assert it == st["iters"]
+    assert _rel(x.cpu().numpy(), xo) <= TOL
+
+
+def test_pcg_config2(torch_cuda):
+    """BASELINE config 2: d=2, p=3, n_el=64, f = sin sin e^t (kind 0)."""
+    ctx = _ctx(2, 3, [64, 64, 64])
+    b = ctx.rhs(0)
+    x, st = ctx.pcg(b, tol=1e-8)
+    space, tf, fdd = _oracle(2, 3, [64, 64, 64])
+    xo, it, conv, _ = opcg.pcg(lambda v: op.apply_A(v, space, tf), lambda v: fd.fd_apply(v, fdd),
+                               b.cpu().numpy())
+    assert st["iters"] == it and st["status"] == 0
+    assert _rel(x.cpu().numpy(), xo) <= TOL
+
+
+def test_pcg_zero_rhs(torch_cuda):
+    torch = torch_cuda
+    ctx = _ctx(2, 2, [4, 4, 4])
+    b = torch.zeros(ctx.shape, dtype=torch.float64, device="cuda")
+    x, st = ctx.pcg(b)
+    assert st["iters"] == 0 and torch.count_nonzero(x).item() == 0
+
+
+def test_fd_apply_host_roundtrip(torch_cuda):
+    ctx = _ctx(2, 3, [12, 10, 9])
+    _, _, fdd = _oracle(2, 3, [12, 10, 9])
+    r = synth.residual(ctx.shape, 2)
+    z = np.empty_like(r)
+    ctx.fd_apply_host(r, z)
+    assert _rel(z, fd.fd_apply(r, fdd)) <= TOL
+
+
+def test_kernels_launched(torch_cuda):
+    """The CUDA path is the one that runs: fd_apply launches 2(d+1) kernels."""
+    torch = torch_cuda
+    ctx = _ctx(3, 3, [6, 6, 6, 6])
+    r = torch.rand(ctx.shape, dtype=torch.float64, device="cuda")
+    n0 = ctx.launches
+    ctx.fd_apply(r)
+    assert ctx.launches - n0 == 8

@@ -115,3 +115,20 @@ def test_mode_apply_kron_vec():
         K = fd.kron_list(mats)
         np.testing.assert_allclose(fd.mode_apply(X, Cs[axis], axis).ravel(), K @ X.ravel(),
                                    rtol=1e-12, atol=1e-12)
+
+
+def test_rank1_rows_match_full_fd():
+    """The sampled rank-1 evaluator equals full Algorithm 1 on the same input."""
+    space, tf = _factors((5, 4, 3), 3, 6)
+    fdd = fd.setup(space, tf)
+    shape = (tf["Mt"].shape[0],) + tuple(f["M"].shape[0] for f in reversed(space))
+    rng = np.random.default_rng(11)
+    facs = [rng.uniform(-1, 1, n) for n in shape]
+    r = facs[0]
+    for v in facs[1:]:
+        r = np.multiply.outer(r, v)
+    z = fd.fd_apply(r, fdd)
+    rows = [(0, 0, 0), (shape[0] - 1, 2, 1), (3, shape[1] - 1, shape[2] - 1)]
+    got = fd.fd_apply_rank1_rows(facs, fdd, rows)
+    for j, idx in enumerate(rows):
+        np.testing.assert_allclose(got[j], z[idx], rtol=1e-12, atol=1e-14 * np.abs(z).max())
