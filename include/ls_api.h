@@ -45,11 +45,11 @@ extern "C" {
 
 #define LS_OK 0
 #define LS_EINVAL 1     /* bad argument: d not in {1,2,3}, p < 2, n_el < 1, null/misaligned ptr */
-#define LS_ENOTSPD 2    /* Cholesky failure in the generalized eigensolver (mass matrix not SPD) */
+#define LS_ENOTSPD 2    /* Cholesky failure of a mass matrix in the generalized eigensolver */
 #define LS_ENOCONV 3    /* PCG did not reach tol within max_iter (stats still filled) */
 #define LS_ENUMERIC 4   /* NaN/Inf in a PCG scalar (alpha, beta) */
 #define LS_ENOMEM 5     /* estimated device memory exceeds the free HBM; refused up front */
-#define LS_ECUDA 6      /* CUDA runtime / cuSOLVER error */
+#define LS_ECUDA 6      /* CUDA runtime error */
 #define LS_ENCCL 7      /* NCCL error (distributed contexts) */
 #define LS_ENOTSUP 8    /* operation not supported for this context */
 
@@ -71,10 +71,13 @@ typedef struct {
  *   out      : receives the new context.
  * Work (untimed setup): open uniform knots,
  * Gauss-Legendre assembly of M_k, K_k, J_k (space) and M_t, K_t, W_t (time)
- * on the host (PAPER.md 686-703, 738-757); generalized eigendecompositions
- * J_k U_k = M_k U_k Lambda_k, K_t U_t = M_t U_t Lambda_t with U^T M U = I by
- * cuSOLVER Dsygvd on the device (eq:eig_dec, PAPER.md 939-945); workspace
- * allocation.  Errors: LS_EINVAL, LS_ENOTSPD, LS_ENOMEM, LS_ECUDA.
+ * on the host in 80-bit extended precision, rounded once to fp64 (PAPER.md
+ * 686-703, 738-757; reading c17); generalized eigendecompositions
+ * J_k U_k = M_k U_k Lambda_k, K_t U_t = M_t U_t Lambda_t with U^T M U = I
+ * (eq:eig_dec, PAPER.md 939-945) by extended-precision Cholesky + cyclic Jacobi
+ * on the host (O(n^3), n <= 136); upload of U, U^T, Lambda; workspace
+ * allocation.  Extents: every n_k and n_t must be <= 136.
+ * Errors: LS_EINVAL, LS_ENOTSPD, LS_ENOMEM, LS_ECUDA.
  */
 int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out);
 

@@ -41,21 +41,22 @@ def _ratio(num, den):
     return num / den
 
 
-def basis_values(knots, p, x):
-    """B[q, i] = b_{i,p}(x_q), i = 0..m-1, by the Cox-de Boor recursion."""
-    knots = np.asarray(knots, dtype=np.float64)
-    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+def basis_values(knots, p, x, dtype=np.float64):
+    """B[q, i] = b_{i,p}(x_q), i = 0..m-1, by the Cox-de Boor recursion
+    (``dtype`` = np.longdouble for the extended-precision assembly, reading c17)."""
+    knots = np.asarray(knots, dtype=dtype)
+    x = np.atleast_1d(np.asarray(x, dtype=dtype))
     n0 = len(knots) - 1  # number of degree-0 functions
-    B = np.zeros((len(x), n0))
+    B = np.zeros((len(x), n0), dtype=dtype)
     for i in range(n0):
-        B[:, i] = ((x >= knots[i]) & (x < knots[i + 1])).astype(np.float64)
+        B[:, i] = ((x >= knots[i]) & (x < knots[i + 1])).astype(dtype)
     # right end point: left limit (last non-empty span closed), see module doc
     last = max(i for i in range(n0) if knots[i] < knots[i + 1])
     at_end = x == knots[-1]
     B[at_end, :] = 0.0
     B[at_end, last] = 1.0
     for q in range(1, p + 1):
-        Bq = np.zeros((len(x), n0 - q))
+        Bq = np.zeros((len(x), n0 - q), dtype=dtype)
         for i in range(n0 - q):
             Bq[:, i] = (_ratio(x - knots[i], knots[i + q] - knots[i]) * B[:, i]
                         + _ratio(knots[i + q + 1] - x, knots[i + q + 1] - knots[i + 1]) * B[:, i + 1])
@@ -63,29 +64,53 @@ def basis_values(knots, p, x):
     return B
 
 
-def basis_derivatives(knots, p, r, x):
+def basis_derivatives(knots, p, r, x, dtype=np.float64):
     """D[q, i] = d^r/deta^r b_{i,p}(x_q) by the derivative recursion of de Boor
     (the paper's reference for B-splines, PAPER.md 147 [DeBoor2001]):
         b'_{i,p} = p/(xi_{i+p} - xi_i) b_{i,p-1} - p/(xi_{i+p+1} - xi_{i+1}) b_{i+1,p-1},
     applied r times, with 0/0 = 0."""
     if r == 0:
-        return basis_values(knots, p, x)
-    knots = np.asarray(knots, dtype=np.float64)
-    D = basis_derivatives(knots, p - 1, r - 1, x)
+        return basis_values(knots, p, x, dtype)
+    knots = np.asarray(knots, dtype=dtype)
+    D = basis_derivatives(knots, p - 1, r - 1, x, dtype)
     n = D.shape[1] - 1
-    out = np.zeros((D.shape[0], n))
+    out = np.zeros((D.shape[0], n), dtype=dtype)
     for i in range(n):
         out[:, i] = p * (_ratio(D[:, i], knots[i + p] - knots[i])
                          - _ratio(D[:, i + 1], knots[i + p + 1] - knots[i + 1]))
     return out
 
 
-def gauss_legendre_rule(knots, q):
+def _leggauss(q, dtype):
+    """Gauss-Legendre nodes/weights on [-1,1]; for extended precision the
+    float64 nodes of numpy's leggauss are polished by Newton steps on the
+    Legendre three-term recurrence in ``dtype``."""
+    t, w = np.polynomial.legendre.leggauss(q)
+    if dtype == np.float64:
+        return t, w
+    t = t.astype(dtype)
+
+    def legendre(x):
+        p0, p1 = np.ones_like(x), x.copy()
+        for k in range(2, q + 1):
+            p0, p1 = p1, ((2 * k - 1) * x * p1 - (k - 1) * p0) / k
+        if q == 1:
+            p0 = np.ones_like(x)
+        return p1, q * (x * p1 - p0) / (x * x - 1)
+
+    for _ in range(3):
+        pq, dp = legendre(t)
+        t = t - pq / dp
+    _, dp = legendre(t)
+    return t, 2 / ((1 - t * t) * dp * dp)
+
+
+def gauss_legendre_rule(knots, q, dtype=np.float64):
     """q-point Gauss-Legendre rule on every non-empty knot span (reading c6:
     the paper does not state its quadrature; with q = p+1 all integrands of the
     factor matrices -- piecewise polynomials of degree <= 2p -- are exact)."""
-    t, w = np.polynomial.legendre.leggauss(q)
-    breaks = np.unique(np.asarray(knots, dtype=np.float64))
+    t, w = _leggauss(q, dtype)
+    breaks = np.unique(np.asarray(knots, dtype=dtype))
     xs, ws = [], []
     for a, b in zip(breaks[:-1], breaks[1:]):
         xs.append(0.5 * (a + b) + 0.5 * (b - a) * t)

@@ -23,18 +23,26 @@ from .bspline import (open_uniform_knots, basis_values, basis_derivatives,
 
 def full_matrices(knots, p, q=None):
     """Unconstrained (m x m) M, K, J, G by Gauss-Legendre with q points per element
-    (default q = p + 1, exact for these degree-<=2p integrands; reading c6)."""
+    (default q = p + 1, exact for these degree-<=2p integrands; reading c6).
+
+    Reading c17: evaluation, quadrature and summation run in 80-bit extended
+    precision (np.longdouble) and the entries are rounded ONCE to fp64.  With
+    plain fp64 assembly the last-ulp rounding of J perturbs the smallest
+    eigenvalue of the pencil (J, M) -- the mode that dominates P^{-1} r -- by up
+    to eps*lambda_max/lambda_min (measured 1e-8 relative at n_el=130, p=2),
+    above the 1e-9 parity bar; correctly rounded entries remove that noise."""
     if q is None:
         q = p + 1
-    x, w = gauss_legendre_rule(knots, q)
-    B0 = basis_values(knots, p, x)
-    B1 = basis_derivatives(knots, p, 1, x)
-    B2 = basis_derivatives(knots, p, 2, x) if p >= 2 else np.zeros_like(B0)
+    ld = np.longdouble
+    x, w = gauss_legendre_rule(knots, q, dtype=ld)
+    B0 = basis_values(knots, p, x, dtype=ld)
+    B1 = basis_derivatives(knots, p, 1, x, dtype=ld)
+    B2 = basis_derivatives(knots, p, 2, x, dtype=ld) if p >= 2 else np.zeros_like(B0)
     M = (B0.T * w) @ B0
     K = (B1.T * w) @ B1
     J = (B2.T * w) @ B2
     G = (B2.T * w) @ B0
-    return M, K, J, G
+    return tuple(A.astype(np.float64) for A in (M, K, J, G))
 
 
 def space_factors(n_el, p, knots=None):

@@ -1,7 +1,7 @@
 """Build libls.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
 
 nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared -Xcompiler -fPIC
-Links cuSOLVER (setup only) and the torch-bundled NCCL 2.28 (one libnccl.so.2 per
+Links the torch-bundled NCCL 2.28 (one libnccl.so.2 per
 process).
 """
 import os
@@ -42,7 +42,7 @@ def build(force=False, verbose=False):
            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", os.path.join(nccl, "include"),
            "-o", LIB + ".tmp"]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
-    cmd += ["-lcusolver", "-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
+    cmd += ["-L", os.path.join(nccl, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

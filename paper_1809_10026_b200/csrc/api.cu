@@ -3,7 +3,6 @@
 // fd_kernels.cuh / matvec_kernels.cuh / pcg_kernels.cuh; this file is glue.
 #include "ls_api.h"
 
-#include <cusolverDn.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -193,50 +192,11 @@ static int to_band(ls_ctx* ctx, const std::vector<double>& A, int n, int hb, dou
   return LS_OK;
 }
 
-// generalized eigendecomposition K U = M U Lambda, U^T M U = I (eq:eig_dec) by cuSOLVER Dsygvd
-static int gen_eig(ls_ctx* ctx, cusolverDnHandle_t h, const std::vector<double>& K,
-                   const std::vector<double>& M, int n, std::vector<double>& lam,
-                   std::vector<double>& Urm) {
-  double *dA = nullptr, *dB = nullptr, *dW = nullptr, *work = nullptr;
-  int* info = nullptr;
-  int lwork = 0, hinfo = 0;
-  int rc = LS_OK;
-  LS_CUDA(cudaMalloc(&dA, sizeof(double) * n * n));
-  LS_CUDA(cudaMalloc(&dB, sizeof(double) * n * n));
-  LS_CUDA(cudaMalloc(&dW, sizeof(double) * n));
-  LS_CUDA(cudaMalloc(&info, sizeof(int)));
-  LS_CUDA(cudaMemcpy(dA, K.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-  LS_CUDA(cudaMemcpy(dB, M.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-  if (cusolverDnDsygvd_bufferSize(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                  CUBLAS_FILL_MODE_LOWER, n, dA, n, dB, n, dW, &lwork) !=
-      CUSOLVER_STATUS_SUCCESS)
-    rc = LS_ECUDA;
-  if (rc == LS_OK) LS_CUDA(cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)));
-  if (rc == LS_OK &&
-      cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                       dA, n, dB, n, dW, work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
-    rc = LS_ECUDA;
-  if (rc == LS_OK) {
-    LS_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
-    if (hinfo > n) rc = LS_ENOTSPD;       // leading minor of M not positive definite
-    else if (hinfo != 0) rc = LS_ECUDA;   // eigensolver did not converge
-  }
-  std::vector<double> Ucm(size_t(n) * n);
-  lam.assign(n, 0.0);
-  if (rc == LS_OK) {
-    LS_CUDA(cudaMemcpy(Ucm.data(), dA, sizeof(double) * n * n, cudaMemcpyDeviceToHost));
-    LS_CUDA(cudaMemcpy(lam.data(), dW, sizeof(double) * n, cudaMemcpyDeviceToHost));
-  }
-  cudaFree(dA);
-  cudaFree(dB);
-  cudaFree(dW);
-  cudaFree(work);
-  cudaFree(info);
-  if (rc != LS_OK) return rc;
-  // column j of the column-major result is eigenvector j: U[i][j] = Ucm[i + j n]
-  Urm.assign(size_t(n) * n, 0.0);
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) Urm[size_t(i) * n + j] = Ucm[i + size_t(j) * n];
+// generalized eigendecomposition K U = M U Lambda, U^T M U = I (eq:eig_dec): host,
+// extended-precision Cholesky + Jacobi (setup_host.cpp; reading c17 in DESIGN.md)
+static int gen_eig(const std::vector<double>& K, const std::vector<double>& M, int n,
+                   std::vector<double>& lam, std::vector<double>& U) {
+  if (generalized_eig(K, M, n, lam, U) != 0) return LS_ENOTSPD;
   // sanity: U^T M U = I (PAPER.md 945)
   double err = 0;
   for (int a = 0; a < n; ++a)
@@ -244,13 +204,12 @@ static int gen_eig(ls_ctx* ctx, cusolverDnHandle_t h, const std::vector<double>&
       double s = 0;
       for (int i = 0; i < n; ++i) {
         double mu = 0;
-        for (int j = 0; j < n; ++j) mu += M[size_t(i) * n + j] * Urm[size_t(j) * n + b];
-        s += Urm[size_t(i) * n + a] * mu;
+        for (int j = std::max(0, i - 16); j < std::min(n, i + 17); ++j) mu += M[size_t(i) * n + j] * U[size_t(j) * n + b];
+        s += U[size_t(i) * n + a] * mu;
       }
       err = std::max(err, std::fabs(s - (a == b ? 1.0 : 0.0)));
     }
   if (!(err < 1e-8)) return LS_ENOTSPD;
-  (void)ctx;
   return LS_OK;
 }
 
@@ -293,21 +252,18 @@ static int setup_common(ls_ctx* ctx) {
   }
 
   // host assembly (PAPER.md 686-703, 738-757)
-  cusolverDnHandle_t h = nullptr;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return LS_ECUDA;
   int rc = LS_OK;
   for (int k = 0; k < d && rc == LS_OK; ++k) {
     Factors f = space_factors(int(ctx->n_el[k]), p);
     ctx->hM[k] = f.M;
     ctx->hK[k] = f.K;
     ctx->hJ[k] = f.J;
-    rc = gen_eig(ctx, h, f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
+    rc = gen_eig(f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
   }
   Factors ft = time_factors(int(ctx->n_el[d]), p);
   ctx->hMt = ft.M;
   ctx->hKt = ft.K;
-  if (rc == LS_OK) rc = gen_eig(ctx, h, ft.K, ft.M, ft.n, ctx->hlam[3], ctx->hU[3]);
-  cusolverDnDestroy(h);
+  if (rc == LS_OK) rc = gen_eig(ft.K, ft.M, ft.n, ctx->hlam[3], ctx->hU[3]);
   if (rc != LS_OK) return rc;
 
   // device copies: W_fwd = U^T, W_bwd = U (row-major), eigenvalues

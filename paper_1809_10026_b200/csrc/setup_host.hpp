@@ -10,13 +10,14 @@ namespace ls {
 // Open uniform knot vector on [0,1] with n_el elements (PAPER.md 144-147, 1111-1112).
 std::vector<double> open_uniform_knots(int n_el, int p);
 
-// q-point Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence).
-void gauss_legendre(int q, std::vector<double>& x, std::vector<double>& w);
+// q-point Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence),
+// in 80-bit extended precision.
+void gauss_legendre(int q, std::vector<long double>& x, std::vector<long double>& w);
 
 // Values and first/second derivatives of all m = len(knots)-p-1 B-splines at x
-// (Cox-de Boor, PAPER.md 148-166; derivative recursion of de Boor).
-void bspline_eval(const std::vector<double>& knots, int p, double x, double* v0, double* v1,
-                  double* v2);
+// (Cox-de Boor, PAPER.md 148-166; derivative recursion of de Boor), extended precision.
+void bspline_eval(const std::vector<double>& knots, int p, long double x, long double* v0,
+                  long double* v1, long double* v2);
 
 struct Factors {
   int n = 0;                   // constrained size
@@ -33,5 +34,10 @@ Factors time_factors(int n_el, int p);
 // Returns int fn b_i, int fn b_i', int fn b_i'' over the constrained basis.
 void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<double>& i0,
                     std::vector<double>& i1, std::vector<double>& i2);
+
+// K U = M U Lambda with U^T M U = I, lambda ascending (extended-precision Cholesky +
+// cyclic Jacobi).  U row-major, column j = eigenvector j.  Returns 1 if M is not SPD.
+int generalized_eig(const std::vector<double>& K, const std::vector<double>& M, int n,
+                    std::vector<double>& lam, std::vector<double>& U);
 
 } // namespace ls
