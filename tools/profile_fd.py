@@ -1,0 +1,33 @@
+"""Minimal driver for ncu: set up BASELINE config C and run fd_apply R times.
+
+    python tools/profile_fd.py --config 4 --reps 2 [--matvec]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+import paper_1809_10026_b200 as ls
+import synth
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--matvec", action="store_true")
+a = ap.parse_args()
+c = synth.CONFIGS[a.config]
+p = c["p"] if isinstance(c["p"], int) else c["p"][0]
+ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
+r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
+z = torch.empty_like(r)
+for _ in range(a.reps):
+    if a.matvec:
+        ctx.matvec(r, z)
+    else:
+        ctx.fd_apply(r, z)
+torch.cuda.synchronize()
+print("ok", ctx.launches, float(z.abs().max()))
