@@ -135,21 +135,21 @@ static int launch_mode_cfg(ls_ctx* ctx, const ModeArgs& a0) {
   return LS_OK;
 }
 
-template <int KS, int MT, int NT, int WM, int WN>
+template <int KS, int NT, int NSTAGE>
 static int launch_mode_ks(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
-  if (mode1) return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, true, false, 3>>(ctx, a);
-  if (scale) return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, false, true, 3>>(ctx, a);
-  return launch_mode_cfg<ModeCfg<MT, NT, WM, WN, KS, false, false, 3>>(ctx, a);
+  if (mode1) return launch_mode_cfg<ModeCfg<KS, NT, true, false, NSTAGE>>(ctx, a);
+  if (scale) return launch_mode_cfg<ModeCfg<KS, NT, false, true, NSTAGE>>(ctx, a);
+  return launch_mode_cfg<ModeCfg<KS, NT, false, false, NSTAGE>>(ctx, a);
 }
 
-// bucket shapes: (MT, NT, WM, WN) chosen so WM*MT*8 >= 4*KS rounded to 8
-#define KS_A(K) case K: return launch_mode_ks<K, 1, 4, 4, 2>(ctx, a, mode1, scale);
-#define KS_B(K) case K: return launch_mode_ks<K, 3, 4, 3, 2>(ctx, a, mode1, scale);
-#define KS_C(K) case K: return launch_mode_ks<K, 2, 4, 7, 1>(ctx, a, mode1, scale);
-#define KS_D(K) case K: return launch_mode_ks<K, 2, 4, 9, 1>(ctx, a, mode1, scale);
+// buckets by k-steps (KS = ceil(n/4)): (NT, NSTAGE) sized for <= 227 KB of shared memory
+#define KS_A(K) case K: return launch_mode_ks<K, 4, 3>(ctx, a, mode1, scale);
+#define KS_B(K) case K: return launch_mode_ks<K, 2, 3>(ctx, a, mode1, scale);
+#define KS_C(K) case K: return launch_mode_ks<K, 2, 2>(ctx, a, mode1, scale);
+#define KS_D(K) case K: return launch_mode_ks<K, 1, 2>(ctx, a, mode1, scale);
 
 static int round_ks(int ks) {
-  static const int list[] = {2, 4, 5, 8, 12, 17, 18, 24, 25, 26, 30, 33, 34};
+  static const int list[] = {2, 4, 5, 8, 12, 16, 17, 18, 24, 25, 26, 30, 33, 34};
   for (int v : list)
     if (ks <= v) return v;
   return -1;
@@ -159,6 +159,7 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
                        uint64_t Q, bool scale, const double* lam_a = nullptr,
                        const double* lam_c = nullptr) {
   ModeArgs a{};
+  a.y16 = (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
   a.X = X;
   a.Y = Y;
   a.W = W;
@@ -171,7 +172,7 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   const bool mode1 = (Q == 1);
   switch (round_ks((n + 3) / 4)) {
     KS_A(2) KS_A(4) KS_A(5) KS_A(8)
-    KS_B(12) KS_B(17) KS_B(18)
+    KS_B(12) KS_B(16) KS_B(17) KS_B(18)
     KS_C(24) KS_C(25) KS_C(26)
     KS_D(30) KS_D(33) KS_D(34)
     default: return LS_EINVAL;

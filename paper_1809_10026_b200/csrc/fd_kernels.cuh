@@ -1,28 +1,39 @@
-// FD mode-k product kernels (Algorithm 1 steps 2-4, PAPER.md 959-962) for sm_100a.
+// FD mode-k product kernel (Algorithm 1 steps 2-4, PAPER.md 959-962) for sm_100a.
 //
 // A d+1-mode tensor in colex layout is viewed, for the mode being applied, as
 // X[P][n][Q] (row-major; n = the mode's extent, Q = product of the faster
 // extents, P = product of the slower ones).  The mode-k product with a dense
 // n x n matrix W is, for every column c = (p, q) of the (n x P*Q) unfolding,
 //     Y[p][a][q] = sum_i W[a][i] X[p][i][q],
-// i.e. a GEMM  Y_(k) = W X_(k)  with M = n, K = n, N = P*Q (the mode-k
-// unfolding of Kolda-Bader; eq:kron_vec, PAPER.md 646).
+// i.e. a GEMM  Y_(k) = W X_(k)  with M = n, K = n, N = P*Q (mode-k unfolding;
+// eq:kron_vec, PAPER.md 646).
 //
 // FP64 on B200 has no tcgen05 kind, so the contraction runs on
-// the FP64 tensor path: mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4, 37.0 TF/s
-// measured (profiles/peaks_fp64_r01.json).  Design:
-//   * W (U^T or U, <= 136 x 136) is WEIGHT-STATIONARY IN REGISTERS: warp-row
-//     wm owns m-tiles [wm*MT, wm*MT+MT) for all K, loaded once per CTA.
-//   * The streamed operand X is staged in shared memory tile by tile
-//     (BN columns x Kp rows) with cp.async, NSTAGE-deep ring, persistent CTAs.
-//   * Shared-memory row strides are = 4 (mod 16) doubles so the m8n8k4
-//     B-fragment reads (lane -> row lane%4, col lane/4) are bank-conflict free.
+// the FP64 tensor path: mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4.  Measured
+// (profiles/peaks_fp64_r01.json, tools/fp64_mix.cu): 37.0 TF/s chip peak,
+// DMMA and DFMA share the FP64 datapath, one warp with >= 2 independent
+// accumulators saturates its SM sub-partition (dependent latency ~27 cycles,
+// issue interval 16 cycles).  Design ("v2", balanced per sub-partition):
+//   * 8 warps per CTA (two per SMSP, so one warp's LDS / epilogue / loader
+//     instructions overlap the other's DMMAs), persistent CTAs (one per SM).
+//   * W (U^T or U, <= 136 x 136) lives in shared memory in m8n8k4 A-fragment
+//     order (32 consecutive doubles per (m-tile, k-step): conflict-free LDS.64).
+//   * Warp w owns the NT n-tiles (8 columns each) of group w%4 and the m-tile
+//     half w/4 ([0, ceil(MT/2)) or [ceil(MT/2), MT)); the two warps of an SMSP
+//     (w, w+4) together cover all m-tiles of one n-tile group, so every SMSP
+//     does exactly the same number of DMMAs per tile (n = 132/133 has 17
+//     m-tiles: a split of rows over 4 sub-partitions cannot balance).
+//   * The streamed operand X is staged tile by tile (BN columns x Kp rows)
+//     with cp.async (16-byte when aligned, else 8-byte) in an NSTAGE ring.
+//     Row strides are = 4 (mod 16) doubles: the B-fragment reads
+//     (lane -> k = lane%4, column = lane/4) are bank-conflict free.
+//   * A/B fragments are double-buffered in registers one k-step ahead.
 //   * Ragged extents: K padded to Kp = 4*ceil(n/4) (zero rows in smem, zero
-//     columns in W), M to 8*ceil(n/8) (zero W rows; never stored), N tail
+//     columns in W), M to 8*ceil(n/8) (zero W rows; never stored), tail
 //     columns skipped at the store.
-//   * Optional epilogue (the time mode, the last forward mode): Algorithm 1
-//     step 3, Y[a][c] /= (lambda_t[a] + Lambda_s[c]) (reading c3), with the
-//     reciprocal from rcp.approx + 2 Newton steps (rel. err ~1e-16).
+//   * Optional epilogue (time mode, the last forward mode): Algorithm 1 step 3,
+//     Y[a][c] /= (lambda_t[a] + Lambda_s[c]) (reading c3), reciprocal by
+//     rcp.approx + 2 Newton steps (relative error ~1e-16).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -38,6 +49,10 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -56,19 +71,24 @@ constexpr int pad4mod16(int v) {  // smallest s >= v with s % 16 == 4
   return v + ((4 - v % 16) + 16) % 16;
 }
 
-template <int MT_, int NT_, int WM_, int WN_, int KS_, bool MODE1_, bool SCALE_, int NSTAGE_>
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, int NSTAGE_>
 struct ModeCfg {
-  static constexpr int MT = MT_, NT = NT_, WM = WM_, WN = WN_, KS = KS_, NSTAGE = NSTAGE_;
+  static constexpr int KS = KS_, NT = NT_, NSTAGE = NSTAGE_;
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_;
-  static constexpr int THREADS = 32 * WM * WN;
-  static constexpr int BN = 8 * NT * WN;  // columns per tile
-  static constexpr int KP = 4 * KS;       // padded K
-  // non-MODE1 tile: [KP][SN]; MODE1 tile: [BN][SK]
-  static constexpr int SN = pad4mod16(BN);
-  static constexpr int SK = pad4mod16(KP);
+  static constexpr int NWARPS = 8;
+  static constexpr int THREADS = 32 * NWARPS;
+  static constexpr int MTILES = (KS + 1) / 2;   // ceil(n/8) for n in (4KS-4, 4KS]
+  static constexpr int MTH = (MTILES + 1) / 2;  // m-tiles per warp (low half; high half may be one less)
+  static constexpr int BN = 8 * NT * 4;         // columns per tile (4 n-tile groups)
+  static constexpr int KP = 4 * KS;             // padded K
+  static constexpr int SN = pad4mod16(BN);      // non-MODE1 tile [KP][SN]
+  static constexpr int SK = pad4mod16(KP);      // MODE1 tile [BN][SK]
   static constexpr int TILE = MODE1 ? BN * SK : KP * SN;  // doubles
-  static constexpr size_t SMEM = size_t(TILE) * NSTAGE * sizeof(double);
-  static_assert(THREADS % BN == 0 || MODE1, "loader needs THREADS % BN == 0");
+  static constexpr int WFRAG = MTILES * KS * 32;          // doubles
+  static constexpr size_t SMEM = size_t(WFRAG + TILE * NSTAGE) * sizeof(double);
+  static_assert(MODE1 || THREADS % (BN / 2) == 0, "loader: THREADS % (BN/2) == 0");
+  static_assert(MODE1 || (BN / 2) <= THREADS, "loader: one column pair per thread");
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 struct ModeArgs {
@@ -81,71 +101,93 @@ struct ModeArgs {
   uint32_t P, Q;
   uint32_t ncols;   // P * Q
   uint32_t ntiles;  // ceil(ncols / BN)
+  bool y16;         // Y is 16-byte aligned (vector stores allowed)
 };
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
   extern __shared__ __align__(16) double smem[];
+  double* wsm = smem;                 // W fragments
+  double* tiles = smem + C::WFRAG;    // NSTAGE x TILE
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const int wm = warp % C::WM;  // warp-row: output rows
-  const int wn = warp / C::WM;  // warp-col: columns
+  const int grp = warp & 3;                       // n-tile group (= SMSP)
+  const int mbase = (warp >> 2) ? C::MTH : 0;     // m-tile half
+  const int mcount = (warp >> 2) ? (C::MTILES - C::MTH) : C::MTH;
   const int n = args.n;
   const uint32_t Q = args.Q;
   const uint32_t ncols = args.ncols;
-  const int mtiles = (n + 7) >> 3;
 
-  // ---- weights: W fragments for this warp's m-tiles, all k-steps (registers)
-  double wreg[C::MT][C::KS];
-#pragma unroll
-  for (int mt = 0; mt < C::MT; ++mt) {
-    const int a = (wm * C::MT + mt) * 8 + (lane >> 2);
-#pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      const int i = ks * 4 + (lane & 3);
-      wreg[mt][ks] = (a < n && i < n) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
-    }
+  // ---- W -> shared memory in A-fragment order: wsm[(mt*KS + ks)*32 + lane]
+  for (int e = tid; e < C::WFRAG; e += C::THREADS) {
+    const int l = e & 31, ks = (e >> 5) % C::KS, mt = (e >> 5) / C::KS;
+    const int a = mt * 8 + (l >> 2), i = ks * 4 + (l & 3);
+    wsm[e] = (a < n && i < n) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
   }
-
   // ---- zero the K padding of every stage once (never written by the loader)
   for (int s = 0; s < C::NSTAGE; ++s) {
-    double* t = smem + s * C::TILE;
+    double* t = tiles + s * C::TILE;
     if (C::MODE1) {
-      for (int e = tid; e < C::BN * (C::SK - n); e += C::THREADS) {
-        int r = e / (C::SK - n), cidx = n + e % (C::SK - n);
-        t[r * C::SK + cidx] = 0.0;
-      }
+      const int padw = C::SK - n;
+      for (int e = tid; e < C::BN * padw; e += C::THREADS) t[(e / padw) * C::SK + n + e % padw] = 0.0;
     } else {
       for (int e = tid; e < (C::KP - n) * C::SN; e += C::THREADS) t[n * C::SN + e] = 0.0;
     }
   }
 
-  // ---- loader: tile -> stage
+  // ---- loader: tile -> stage (cp.async; 16 B where both sides are aligned)
   auto load_tile = [&](uint32_t tile, int stage) {
-    double* t = smem + stage * C::TILE;
+    double* t = tiles + stage * C::TILE;
     const uint32_t c0 = tile * C::BN;
     if (C::MODE1) {
-      // columns are rows of length n, contiguous: chunk X[c0*n, (c0+BN)*n)
+      // the tile is the contiguous chunk X[c0*n, (c0+BN)*n): element e -> (c = e/n, i = e%n)
       const uint32_t cend = min(c0 + (uint32_t)C::BN, ncols);
       const uint32_t total = (cend - c0) * (uint32_t)n;
       const double* src = args.X + size_t(c0) * n;
-      uint32_t cc = tid / n, i = tid % n;
-      const uint32_t dq = C::THREADS / n, dr = C::THREADS % n;
-      for (uint32_t e = tid; e < total; e += C::THREADS) {
-        cp_async8(t + cc * C::SK + i, src + e);
-        cc += dq;
-        i += dr;
-        if (i >= (uint32_t)n) { i -= n; ++cc; }
+      if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+        // even n: pairs (e, e+1) with e even never straddle a row; 16-byte copies
+        const uint32_t half = total >> 1, hn = n >> 1;
+        for (uint32_t h = tid; h < half; h += C::THREADS) {
+          const uint32_t cc = h / hn, i = 2 * (h - cc * hn);
+          cp_async16(t + cc * C::SK + i, src + 2 * h);
+        }
+      } else {
+        uint32_t cc = tid / n, i = tid % n;
+        const uint32_t dq = C::THREADS / n, dr = C::THREADS % n;
+        for (uint32_t e = tid; e < total; e += C::THREADS) {
+          cp_async8(t + cc * C::SK + i, src + e);
+          cc += dq;
+          i += dr;
+          if (i >= (uint32_t)n) { i -= n; ++cc; }
+        }
       }
     } else {
-      const int cc = tid % C::BN;
+      // column pairs (cc, cc+1): one 16-byte copy when adjacent and aligned
+      constexpr int PAIRS = C::BN / 2;
+      const int pr = tid % PAIRS;
+      const int cc = 2 * pr;
       const uint32_t c = c0 + cc;
       if (c < ncols) {
         const uint32_t p = c / Q, q = c - p * Q;
         const double* src = args.X + (size_t(p) * n) * Q + q;
-        for (int i = tid / C::BN; i < n; i += C::THREADS / C::BN)
-          cp_async8(t + i * C::SN + cc, src + size_t(i) * Q);
+        const bool second = (c + 1 < ncols);
+        const bool vec = second && (q + 1 < Q) && ((Q & 1) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+        const double* src2 = nullptr;
+        if (second && !vec) {
+          const uint32_t c2 = c + 1, p2 = c2 / Q, q2 = c2 - p2 * Q;
+          src2 = args.X + (size_t(p2) * n) * Q + q2;
+        }
+        for (int i = tid / PAIRS; i < n; i += C::THREADS / PAIRS) {
+          double* dst = t + i * C::SN + cc;
+          if (vec) {
+            cp_async16(dst, src + size_t(i) * Q);
+          } else {
+            cp_async8(dst, src + size_t(i) * Q);
+            if (second) cp_async8(dst + 1, src2 + size_t(i) * Q);
+          }
+        }
       }
     }
   };
@@ -159,6 +201,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
     cp_async_commit();
   }
 
+  const double* wl = wsm + lane;
+  // SCALE: this lane's output rows' lambda_t, loaded once
+  double lam_row[C::SCALE ? C::MTH : 1];
+#pragma unroll
+  for (int mt = 0; mt < (C::SCALE ? C::MTH : 1); ++mt) {
+    const int a = (mbase + mt) * 8 + (lane >> 2);
+    lam_row[mt] = (C::SCALE && mt < mcount && a < n) ? __ldg(args.lam_a + a) : 0.0;
+  }
 #pragma unroll 1
   for (int j = 0; tile < args.ntiles; ++j, tile += stride) {
     cp_async_wait<C::NSTAGE - 2>();
@@ -168,57 +218,90 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
       if (tn < args.ntiles) load_tile(tn, (j + C::NSTAGE - 1) % C::NSTAGE);
       cp_async_commit();
     }
-    const double* t = smem + (j % C::NSTAGE) * C::TILE;
-
-    double acc[C::MT][C::NT][2];
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-
-    const int colbase = wn * C::NT * 8 + (lane >> 2);
-#pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      double xf[C::NT];
-      const int krow = ks * 4 + (lane & 3);
+    const double* t = tiles + (j % C::NSTAGE) * C::TILE;
+    const uint32_t c0 = tile * C::BN;
+    // SCALE: this lane's columns' Lambda_s, prefetched before the k-loop
+    double lam_col[C::SCALE ? C::NT : 1][2];
+    if (C::SCALE) {
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt) {
-        const int col = colbase + nt * 8;
-        xf[nt] = C::MODE1 ? t[col * C::SK + krow] : t[krow * C::SN + col];
-      }
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) {
-        if (wm * C::MT + mt < mtiles) {
-#pragma unroll
-          for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], wreg[mt][ks], xf[nt]);
-        }
+        const uint32_t c = c0 + grp * C::NT * 8 + nt * 8 + 2 * (lane & 3);
+        lam_col[nt][0] = c < ncols ? __ldg(args.lam_c + c) : 0.0;
+        lam_col[nt][1] = c + 1 < ncols ? __ldg(args.lam_c + c + 1) : 0.0;
       }
     }
 
+    double acc[C::MTH][C::NT][2];
+#pragma unroll
+    for (int mt = 0; mt < C::MTH; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+    // B-fragment base: column = warp's n-tile group, k-row = lane%4
+    const int col0 = grp * C::NT * 8 + (lane >> 2);
+    const double* tb = C::MODE1 ? (t + col0 * C::SK + (lane & 3)) : (t + (lane & 3) * C::SN + col0);
+    auto bfrag = [&](int ks, int nt) -> double {
+      return C::MODE1 ? tb[nt * 8 * C::SK + ks * 4] : tb[ks * 4 * C::SN + nt * 8];
+    };
+
+    double af[2][C::MTH], bf[2][C::NT];
+#pragma unroll
+    for (int mt = 0; mt < C::MTH; ++mt) af[0][mt] = wl[((mbase + mt) * C::KS) * 32];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) bf[0][nt] = bfrag(0, nt);
+#pragma unroll
+    for (int ks = 0; ks < C::KS; ++ks) {
+      const int cur = ks & 1, nxt = cur ^ 1;
+      if (ks + 1 < C::KS) {
+#pragma unroll
+        for (int mt = 0; mt < C::MTH; ++mt)
+          if (mt < mcount) af[nxt][mt] = wl[((mbase + mt) * C::KS + ks + 1) * 32];
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) bf[nxt][nt] = bfrag(ks + 1, nt);
+      }
+#pragma unroll
+      for (int mt = 0; mt < C::MTH; ++mt)
+        if (mt < mcount) {
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt], bf[cur][nt]);
+        }
+    }
+
     // ---- epilogue: registers -> global (optionally scaled, Alg. 1 step 3)
-    const uint32_t c0 = tile * C::BN;
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt) {
-#pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const uint32_t c = c0 + wn * C::NT * 8 + nt * 8 + 2 * (lane & 3) + jj;
-        if (c >= ncols) continue;
-        size_t base;
-        if (C::MODE1) {
-          base = size_t(c) * n;
-        } else {
-          const uint32_t p = c / Q, q = c - p * Q;
-          base = size_t(p) * n * Q + q;
+      const uint32_t c = c0 + grp * C::NT * 8 + nt * 8 + 2 * (lane & 3);  // even; lane owns c, c+1
+      if (c >= ncols) continue;
+      const bool two = (c + 1 < ncols);
+      size_t base, base2 = 0;
+      bool vec = false;
+      if (C::MODE1) {
+        base = size_t(c) * n;
+        base2 = base + n;
+      } else {
+        const uint32_t p = c / Q, q = c - p * Q;
+        base = size_t(p) * n * Q + q;
+        vec = args.y16 && two && (q + 1 < Q) && ((Q & 1) == 0) && ((base & 1) == 0);
+        if (two && !vec) {
+          const uint32_t c2 = c + 1, p2 = c2 / Q, q2 = c2 - p2 * Q;
+          base2 = size_t(p2) * n * Q + q2;
         }
-        double lc = 0.0;
-        if (C::SCALE) lc = __ldg(args.lam_c + c);
+      }
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          const int a = (wm * C::MT + mt) * 8 + (lane >> 2);
-          if (a < n) {
-            double v = acc[mt][nt][jj];
-            if (C::SCALE) v *= fast_rcp(__ldg(args.lam_a + a) + lc);
-            args.Y[base + (C::MODE1 ? size_t(a) : size_t(a) * Q)] = v;
+      for (int mt = 0; mt < C::MTH; ++mt) {
+        const int a = (mbase + mt) * 8 + (lane >> 2);
+        if (mt < mcount && a < n) {
+          double v0 = acc[mt][nt][0], v1 = acc[mt][nt][1];
+          if (C::SCALE) {
+            v0 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lam_col[C::SCALE ? nt : 0][0]);
+            v1 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lam_col[C::SCALE ? nt : 0][1]);
+          }
+          const size_t off = C::MODE1 ? size_t(a) : size_t(a) * Q;
+          if (vec) {
+            *reinterpret_cast<double2*>(args.Y + base + off) = make_double2(v0, v1);
+          } else {
+            args.Y[base + off] = v0;
+            if (two) args.Y[base2 + off] = v1;
           }
         }
       }

@@ -1,0 +1,78 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (one ls_setup per config, fd_apply on the whole tensor).
+
+* config 3 (d=3, p=3, n_el=64; 18.1M DOFs): element-by-element against the
+  full oracle fd_apply on the same seeded uniform residual.
+* config 4 (d=3, p=6, n_el=128; 306M DOFs): the oracle cannot redo the whole
+  transform in seconds, so (a) a rank-1 seeded input whose exact image the
+  oracle samples fibre by fibre (oracle.fd.fd_apply_rank1_rows), and (b) the
+  seeded uniform residual checked through properties that hold at any size:
+  linearity fd(a r1 + b r2) = a fd(r1) + b fd(r2) and symmetry
+  <r2, P^{-1} r1> = <r1, P^{-1} r2> (P is SPD), both evaluated on the GPU
+  results with fp64 host reductions.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import univariate as uv, fd
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def _ctx(cfg):
+    import paper_1809_10026_b200 as ls
+    c = synth.CONFIGS[cfg]
+    return ls.Context(c["d"], c["p"], [c["n_el"]] * (c["d"] + 1))
+
+
+def _fdd(cfg):
+    c = synth.CONFIGS[cfg]
+    sf = uv.space_factors(c["n_el"], c["p"])
+    tf = uv.time_factors(c["n_el"], c["p"])
+    return fd.setup([sf] * c["d"], tf)
+
+
+def test_config3_full_against_oracle():
+    import torch
+    ctx = _ctx(3)
+    r = synth.residual(ctx.shape, 0)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    z_ref = fd.fd_apply(r, _fdd(3))
+    assert np.linalg.norm(z - z_ref) / np.linalg.norm(z_ref) <= TOL
+    assert np.max(np.abs(z - z_ref)) <= TOL * np.abs(z_ref).max()
+
+
+def test_config4_rank1_sampled_fibres():
+    import torch
+    ctx = _ctx(4)
+    facs = synth.rank1_factors(ctx.shape, 7)
+    r = torch.from_numpy(synth.rank1_tensor(facs)).cuda()
+    z = ctx.fd_apply(r)
+    nt, n3, n2, _ = ctx.shape
+    rows = [(0, 0, 0), (nt - 1, n3 - 1, n2 - 1), (nt // 2, 5, n2 - 3), (1, n3 // 2, 0),
+            (nt - 2, 0, n2 // 2), (66, 66, 66)]
+    ref = fd.fd_apply_rank1_rows(facs, _fdd(4), rows)
+    zc = z.cpu().numpy()
+    scale = np.abs(zc).max()
+    for j, idx in enumerate(rows):
+        got = zc[idx]
+        assert np.linalg.norm(got - ref[j]) <= TOL * max(np.linalg.norm(ref[j]), 1e-300) + 1e-12 * scale
+
+
+def test_config4_uniform_linearity_symmetry():
+    import torch
+    ctx = _ctx(4)
+    r1 = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
+    r2 = torch.from_numpy(synth.residual(ctx.shape, 1)).cuda()
+    z1, z2 = ctx.fd_apply(r1), ctx.fd_apply(r2)
+    s12 = float(torch.dot(r2.view(-1), z1.view(-1)))
+    s21 = float(torch.dot(r1.view(-1), z2.view(-1)))
+    assert abs(s12 - s21) <= 1e-10 * np.sqrt(abs(float(torch.dot(r1.view(-1), z1.view(-1))) *
+                                                float(torch.dot(r2.view(-1), z2.view(-1)))))
+    comb = ctx.fd_apply(2.0 * r1 - 3.0 * r2)
+    err = torch.linalg.norm(comb - (2.0 * z1 - 3.0 * z2)) / torch.linalg.norm(comb)
+    assert float(err) <= 1e-12
+    assert torch.isfinite(z1).all()
