@@ -84,7 +84,8 @@ struct ModeCfg {
   static constexpr int SN = pad4mod16(BN);      // non-MODE1 tile [KP][SN]
   static constexpr int SK = pad4mod16(KP);      // MODE1 tile [BN][SK]
   static constexpr int TILE = MODE1 ? BN * SK : KP * SN;  // doubles
-  static constexpr int WFRAG = MTILES * KS * 32;          // doubles
+  static constexpr int KSP = (KS + 1) / 2;                 // k-step pairs
+  static constexpr int WFRAG = MTILES * KSP * 64;         // doubles (A fragments, k-step pairs)
   static constexpr size_t SMEM = size_t(WFRAG + TILE * NSTAGE) * sizeof(double);
   static_assert(MODE1 || THREADS % (BN / 2) == 0, "loader: THREADS % (BN/2) == 0");
   static_assert(MODE1 || (BN / 2) <= THREADS, "loader: one column pair per thread");
@@ -104,6 +105,59 @@ struct ModeArgs {
   bool y16;         // Y is 16-byte aligned (vector stores allowed)
 };
 
+// One warp's share of one tile: MC m-tiles (compile time: no predicates, so no
+// re-convergence around mma.sync) x NT n-tiles, all k-steps.  A fragments come
+// two k-steps per LDS.128 and are double-buffered one k-step pair ahead.
+template <class C, int MC>
+__device__ __forceinline__ void compute_tile(double (&acc)[C::MTH][C::NT][2], const double* wl,
+                                             const double* t, int grp, int lane) {
+#pragma unroll
+  for (int mt = 0; mt < C::MTH; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  if (MC == 0) return;
+  const int col0 = grp * C::NT * 8 + (lane >> 2);
+  const double* tb = C::MODE1 ? (t + col0 * C::SK + (lane & 3)) : (t + (lane & 3) * C::SN + col0);
+  auto bfrag = [&](int ks, int nt) -> double {
+    return C::MODE1 ? tb[nt * 8 * C::SK + ks * 4] : tb[ks * 4 * C::SN + nt * 8];
+  };
+  auto apair = [&](int mt, int ksp) -> double2 {
+    return *reinterpret_cast<const double2*>(wl + (mt * C::KSP + ksp) * 64);
+  };
+  double2 af[2][MC > 0 ? MC : 1];
+  double bf[2][2][C::NT];
+#pragma unroll
+  for (int mt = 0; mt < MC; ++mt) af[0][mt] = apair(mt, 0);
+#pragma unroll
+  for (int nt = 0; nt < C::NT; ++nt) {
+    bf[0][0][nt] = bfrag(0, nt);
+    bf[0][1][nt] = (1 < C::KS) ? bfrag(1, nt) : 0.0;
+  }
+#pragma unroll
+  for (int ksp = 0; ksp < C::KSP; ++ksp) {
+    const int cur = ksp & 1, nxt = cur ^ 1;
+    if (ksp + 1 < C::KSP) {
+#pragma unroll
+      for (int mt = 0; mt < MC; ++mt) af[nxt][mt] = apair(mt, ksp + 1);
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) {
+        bf[nxt][0][nt] = bfrag(2 * ksp + 2, nt);
+        bf[nxt][1][nt] = (2 * ksp + 3 < C::KS) ? bfrag(2 * ksp + 3, nt) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MC; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].x, bf[cur][0][nt]);
+    if (2 * ksp + 1 < C::KS) {
+#pragma unroll
+      for (int mt = 0; mt < MC; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].y, bf[cur][1][nt]);
+    }
+  }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
   extern __shared__ __align__(16) double smem[];
@@ -119,11 +173,13 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
   const uint32_t Q = args.Q;
   const uint32_t ncols = args.ncols;
 
-  // ---- W -> shared memory in A-fragment order: wsm[(mt*KS + ks)*32 + lane]
+  // ---- W -> shared memory in A-fragment order, two k-steps per lane-slot so one
+  //      LDS.128 fetches both: wsm[((mt*KSP + ks/2)*32 + lane)*2 + ks%2]
   for (int e = tid; e < C::WFRAG; e += C::THREADS) {
-    const int l = e & 31, ks = (e >> 5) % C::KS, mt = (e >> 5) / C::KS;
+    const int h = e & 1, l = (e >> 1) & 31, ksp = (e >> 6) % C::KSP, mt = (e >> 6) / C::KSP;
+    const int ks = 2 * ksp + h;
     const int a = mt * 8 + (l >> 2), i = ks * 4 + (l & 3);
-    wsm[e] = (a < n && i < n) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
+    wsm[e] = (a < n && i < n && ks < C::KS) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
   }
   // ---- zero the K padding of every stage once (never written by the loader)
   for (int s = 0; s < C::NSTAGE; ++s) {
@@ -201,7 +257,6 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
     cp_async_commit();
   }
 
-  const double* wl = wsm + lane;
   // SCALE: this lane's output rows' lambda_t, loaded once
   double lam_row[C::SCALE ? C::MTH : 1];
 #pragma unroll
@@ -232,40 +287,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
     }
 
     double acc[C::MTH][C::NT][2];
-#pragma unroll
-    for (int mt = 0; mt < C::MTH; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-
-    // B-fragment base: column = warp's n-tile group, k-row = lane%4
-    const int col0 = grp * C::NT * 8 + (lane >> 2);
-    const double* tb = C::MODE1 ? (t + col0 * C::SK + (lane & 3)) : (t + (lane & 3) * C::SN + col0);
-    auto bfrag = [&](int ks, int nt) -> double {
-      return C::MODE1 ? tb[nt * 8 * C::SK + ks * 4] : tb[ks * 4 * C::SN + nt * 8];
-    };
-
-    double af[2][C::MTH], bf[2][C::NT];
-#pragma unroll
-    for (int mt = 0; mt < C::MTH; ++mt) af[0][mt] = wl[((mbase + mt) * C::KS) * 32];
-#pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) bf[0][nt] = bfrag(0, nt);
-#pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      const int cur = ks & 1, nxt = cur ^ 1;
-      if (ks + 1 < C::KS) {
-#pragma unroll
-        for (int mt = 0; mt < C::MTH; ++mt)
-          if (mt < mcount) af[nxt][mt] = wl[((mbase + mt) * C::KS + ks + 1) * 32];
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) bf[nxt][nt] = bfrag(ks + 1, nt);
-      }
-#pragma unroll
-      for (int mt = 0; mt < C::MTH; ++mt)
-        if (mt < mcount) {
-#pragma unroll
-          for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt], bf[cur][nt]);
-        }
-    }
+    if (warp >> 2)
+      compute_tile<C, C::MTILES - C::MTH>(acc, wsm + (C::MTH * C::KSP * 32 + lane) * 2, t, grp, lane);
+    else
+      compute_tile<C, C::MTH>(acc, wsm + lane * 2, t, grp, lane);
 
     // ---- epilogue: registers -> global (optionally scaled, Alg. 1 step 3)
 #pragma unroll
