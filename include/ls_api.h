@@ -157,6 +157,30 @@ int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host);
  */
 int ls_get_factor(const ls_ctx* ctx, int which, int dir, double* host_out);
 
+/*
+ * Host-only plan queries of the time-slab decomposition; no GPU
+ * and no context needed.  They are the exact functions the NCCL plumbing uses,
+ * exported so the multi-rank logic can be tested on CPU.
+ * ls_partition -- even split of `total` items over `world` parts (first
+ *   total % world parts one larger): part `part` is [*off, *off + *len).
+ *   Time slabs: total = n_t; spatial chunks of the time mode: total = N_s.
+ * ls_a2a_plan -- slab -> chunk all-to-all of `rank` (counts in doubles), arrays
+ *   of length world indexed by peer h: send [send_off[h], +send_cnt[h]) of the
+ *   packed send buffer; receive [recv_off[h], +recv_cnt[h]) of the [n_t][chunk]
+ *   tensor.  chunk -> slab is the transpose (send<->recv).
+ * ls_pack_map -- pos[e] = packed send-buffer position of element e of an
+ *   [ntl][N_s] slab (pos must hold ntl*N_s entries).
+ * ls_halo_plan -- ls_matvec halo of `rank`: slab [*t0, *t0 + *ntl), halo rows
+ *   *lo below (from rank-1) and *hi above (from rank+1), each = p or 0.
+ *   LS_EINVAL if a slab is thinner than p.
+ */
+int ls_partition(int64_t total, int world, int part, int64_t* off, int64_t* len);
+int ls_a2a_plan(int64_t n_t, int64_t N_s, int world, int rank, int64_t* send_off,
+                int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt);
+int ls_pack_map(int64_t ntl, int64_t N_s, int world, int64_t* pos);
+int ls_halo_plan(int64_t n_t, int world, int rank, int p, int64_t* t0, int64_t* ntl,
+                 int64_t* lo, int64_t* hi);
+
 /* ls_kernel_launches -- number of kernels the library has launched so far. */
 int64_t ls_kernel_launches(const ls_ctx* ctx);
 

@@ -29,7 +29,8 @@ LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_E
 # Every symbol include/ls_api.h declares (checked by tests/test_abi.py).
 EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
             "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
-            "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror"]
+            "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
+            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan"]
 
 
 class PCGStats(ctypes.Structure):
@@ -77,6 +78,12 @@ def load_library(path=LIB_PATH):
         "ls_profile_read": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), i64p]),
         "ls_destroy": (None, [vp]),
+        "ls_partition": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
+        "ls_a2a_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                       i64p, i64p, i64p, i64p]),
+        "ls_pack_map": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, i64p]),
+        "ls_halo_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        i64p, i64p, i64p, i64p]),
         "ls_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -102,6 +109,38 @@ def unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(load_library().ls_get_unique_id(buf), "ls_get_unique_id")
     return buf.raw
+
+
+def partition(total, world, part):
+    """(offset, length) of part `part` of the even split (host only, no GPU)."""
+    off, ln = ctypes.c_int64(), ctypes.c_int64()
+    _check(load_library().ls_partition(int(total), int(world), int(part), ctypes.byref(off),
+                                       ctypes.byref(ln)), "ls_partition")
+    return off.value, ln.value
+
+
+def a2a_plan(n_t, N_s, world, rank):
+    """slab -> chunk all-to-all plan of `rank`: dict of numpy arrays (host only)."""
+    arrs = [np.zeros(world, dtype=np.int64) for _ in range(4)]
+    ptrs = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) for a in arrs]
+    _check(load_library().ls_a2a_plan(int(n_t), int(N_s), int(world), int(rank), *ptrs), "ls_a2a_plan")
+    return dict(zip(("send_off", "send_cnt", "recv_off", "recv_cnt"), arrs))
+
+
+def pack_map(ntl, N_s, world):
+    """Packed send position of every slab element (host only)."""
+    pos = np.zeros(int(ntl) * int(N_s), dtype=np.int64)
+    _check(load_library().ls_pack_map(int(ntl), int(N_s), int(world),
+                                      pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "ls_pack_map")
+    return pos
+
+
+def halo_plan(n_t, world, rank, p):
+    """(t0, ntl, lo, hi) of the ls_matvec halo of `rank` (host only)."""
+    v = [ctypes.c_int64() for _ in range(4)]
+    _check(load_library().ls_halo_plan(int(n_t), int(world), int(rank), int(p), *[ctypes.byref(x) for x in v]),
+           "ls_halo_plan")
+    return tuple(x.value for x in v)
 
 
 def sizes(n_el, p):

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "comm.hpp"
+#include "plan.hpp"
 #include "fd_kernels.cuh"
 #include "matvec_kernels.cuh"
 #include "pcg_kernels.cuh"
@@ -238,12 +239,8 @@ static int setup_common(ls_ctx* ctx) {
   ctx->Ntot = ctx->Ns * ctx->nt;
   if (ctx->Ns >= (int64_t(1) << 31)) return LS_EINVAL;
   // slab layout: uneven split of n_t over `world` ranks
-  {
-    const int64_t base = ctx->nt / ctx->world, extra = ctx->nt % ctx->world;
-    ctx->ntl = base + (ctx->rank < extra ? 1 : 0);
-    ctx->t0 = ctx->rank * base + std::min<int64_t>(ctx->rank, extra);
-    ctx->Nl = ctx->ntl * ctx->Ns;
-  }
+  split_part(ctx->nt, ctx->world, ctx->rank, &ctx->t0, &ctx->ntl);
+  ctx->Nl = ctx->ntl * ctx->Ns;
   // memory estimate: 6 workspaces + 4 pcg vectors (+ 2 all-to-all buffers when distributed)
   {
     size_t fr = 0, tot = 0;
@@ -349,7 +346,7 @@ extern "C" int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int
   ctx->world = world;
   for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
   // every slab must be at least p time slices thick (halo of the banded time factors)
-  if (world > 1 && (n_elems[d] + p - 1) / world < p) {
+  if (world > 1 && (n_elems[d] + p - 1) / world < p) {  // slab thinner than the time halo
     delete ctx;
     return LS_EINVAL;
   }
@@ -453,10 +450,11 @@ static unsigned grid_for(uint64_t total, int threads, int num_sms) {
   return unsigned(std::min<uint64_t>(g, uint64_t(num_sms) * 16));
 }
 
-// y = A x on `rows` time slices starting at x (x, y point at slice 0 of the rows given);
-// spatial part on rows [0, rows), time part on output rows [out0, out0+nout) of that block.
-static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t trow0,
-                        int64_t out0, int64_t nout) {
+// y = A x: spatial sum-factorisation on the `rows` time slices of x (global rows
+// [s_first, s_first + rows), halo included), time part on global output rows
+// [t_first, t_first + nout) written to y.
+static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
+                        int64_t t_first, int64_t nout) {
   const int d = ctx->d;
   double* S[3] = {ctx->tmp[0], ctx->tmp[1], ctx->tmp[2]};
   double* T[3] = {ctx->tmp[3], ctx->tmp[4], ctx->tmp[5]};
@@ -498,8 +496,8 @@ static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, i
   t.nt = ctx->nt;
   t.hb = ctx->p;
   t.Ns = uint32_t(ctx->Ns);
-  (void)trow0;
-  (void)out0;
+  t.t_first = int(t_first);
+  t.s_first = int(s_first);
   t.total = uint64_t(nout) * ctx->Ns;
   band_time_kernel<<<grid_for(t.total, 256, ctx->num_sms), 256, 0, ctx->stream>>>(t);
   ctx->launches++;
@@ -507,10 +505,22 @@ static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, i
   return LS_OK;
 }
 
+// extended-slab geometry of this rank (halo rows of the time factors)
+static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
+  int64_t t0, ntl;
+  halo_plan(ctx->nt, ctx->world, ctx->rank, ctx->p, &t0, &ntl, lo, hi);
+}
+
 extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y || !aligned8(x) || !aligned8(y)) return LS_EINVAL;
   if (ctx->world == 1) return matvec_block(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
-  return LS_ENOTSUP;
+  int64_t lo, hi;
+  ext_geom(ctx, &lo, &hi);
+  double* own = ctx->pp + lo * ctx->Ns;  // extended buffer [lo | own | hi]
+  if (x != own)
+    LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->p));
+  return matvec_block(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -583,7 +593,10 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
     if (st) *st = s;
     return LS_OK;
   }
-  double *r = ctx->pr, *z = ctx->pz, *p = ctx->pp, *q = ctx->pq;
+  int64_t lo = 0, hi = 0;
+  if (ctx->world > 1) ext_geom(ctx, &lo, &hi);
+  // p lives inside the halo-extended buffer so ls_matvec needs no copy
+  double *r = ctx->pr, *z = ctx->pz, *p = ctx->pp + lo * ctx->Ns, *q = ctx->pq;
   LS_CUDA(cudaMemcpyAsync(r, b, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   LS_CHECK(fd_apply(ctx, r, z));
   int cur = S_RHO0, nxt = S_RHO1;
@@ -691,6 +704,36 @@ extern "C" int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flop
   if (total_flops) *total_flops = fl;
   if (n) *n = int64_t(ctx->prof_recs.size());
   ctx->prof_recs.clear();
+  return LS_OK;
+}
+
+// ---- host-only plan queries (no GPU needed; used by the CPU multi-rank tests) -------------
+extern "C" int ls_partition(int64_t total, int world, int part, int64_t* off, int64_t* len) {
+  if (world < 1 || part < 0 || part >= world || total < 0 || !off || !len) return LS_EINVAL;
+  split_part(total, world, part, off, len);
+  return LS_OK;
+}
+
+extern "C" int ls_a2a_plan(int64_t nt, int64_t Ns, int world, int rank, int64_t* send_off,
+                           int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt) {
+  if (world < 1 || rank < 0 || rank >= world || !send_off || !send_cnt || !recv_off || !recv_cnt)
+    return LS_EINVAL;
+  for (int h = 0; h < world; ++h)
+    a2a_plan(nt, Ns, world, rank, h, send_off + h, send_cnt + h, recv_off + h, recv_cnt + h);
+  return LS_OK;
+}
+
+extern "C" int ls_pack_map(int64_t ntl, int64_t Ns, int world, int64_t* pos) {
+  if (world < 1 || ntl < 0 || Ns < 0 || !pos) return LS_EINVAL;
+  for (int64_t e = 0; e < ntl * Ns; ++e) pos[e] = pack_pos(e, ntl, Ns, world);
+  return LS_OK;
+}
+
+extern "C" int ls_halo_plan(int64_t nt, int world, int rank, int p, int64_t* t0, int64_t* ntl,
+                            int64_t* lo, int64_t* hi) {
+  if (world < 1 || rank < 0 || rank >= world || p < 0 || !t0 || !ntl || !lo || !hi) return LS_EINVAL;
+  halo_plan(nt, world, rank, p, t0, ntl, lo, hi);
+  if (world > 1 && nt / world < p) return LS_EINVAL;  // a slab thinner than the halo
   return LS_OK;
 }
 

@@ -49,24 +49,14 @@ int Comm::init(const void* uid, int rank_, int world_, int64_t nt_, int64_t Ns_)
   return LS_OK;
 }
 
-// owner chunk of spatial index s for the even split (first `extra` chunks have base+1)
-__device__ __forceinline__ int owner(int64_t s, int64_t base, int64_t extra) {
-  const int64_t big = extra * (base + 1);
-  return s < big ? int(s / (base + 1)) : int(extra + (s - big) / base);
-}
-
-// pack: A[t][s] (ntl x Ns) -> tmp[ntl*c0_h + t*len_h + (s - c0_h)]
+// pack (PACK) / unpack: slab element e <-> packed all-to-all position (plan.hpp pack_pos)
 template <bool PACK>
 __global__ void pack_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t ntl,
-                            int64_t Ns, int64_t base, int64_t extra) {
+                            int64_t Ns, int world) {
   const int64_t total = ntl * Ns;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = e / Ns, s = e - t * Ns;
-    const int h = owner(s, base, extra);
-    const int64_t len = base + (h < extra ? 1 : 0);
-    const int64_t c0 = h * base + (h < extra ? h : extra);
-    const int64_t pe = ntl * c0 + t * len + (s - c0);
+    const int64_t pe = pack_pos(e, ntl, Ns, world);
     if (PACK)
       dst[pe] = src[e];
     else
@@ -76,15 +66,15 @@ __global__ void pack_kernel(const double* __restrict__ src, double* __restrict__
 
 int Comm::slab_to_chunk(const double* A, double* B, double* tmp, int64_t& launches) {
   const int64_t ntl = slab_len[rank];
-  const int64_t base = Ns / world, extra = Ns % world;
-  pack_kernel<true><<<1184, 256, 0, stream>>>(A, tmp, ntl, Ns, base, extra);
+  pack_kernel<true><<<1184, 256, 0, stream>>>(A, tmp, ntl, Ns, world);
   ++launches;
   if (cudaGetLastError() != cudaSuccess) return LS_ECUDA;
-  const int64_t me = chunk_len[rank];
   NCCL_OK(ncclGroupStart());
   for (int h = 0; h < world; ++h) {
-    NCCL_OK(ncclSend(tmp + ntl * chunk_off[h], size_t(ntl * chunk_len[h]), ncclDouble, h, C(nccl), stream));
-    NCCL_OK(ncclRecv(B + slab_t0[h] * me, size_t(slab_len[h] * me), ncclDouble, h, C(nccl), stream));
+    int64_t so, sc, ro, rc;
+    a2a_plan(nt, Ns, world, rank, h, &so, &sc, &ro, &rc);
+    NCCL_OK(ncclSend(tmp + so, size_t(sc), ncclDouble, h, C(nccl), stream));
+    NCCL_OK(ncclRecv(B + ro, size_t(rc), ncclDouble, h, C(nccl), stream));
   }
   NCCL_OK(ncclGroupEnd());
   return LS_OK;
@@ -92,34 +82,32 @@ int Comm::slab_to_chunk(const double* A, double* B, double* tmp, int64_t& launch
 
 int Comm::chunk_to_slab(const double* B, double* A, double* tmp, int64_t& launches) {
   const int64_t ntl = slab_len[rank];
-  const int64_t me = chunk_len[rank];
   NCCL_OK(ncclGroupStart());
   for (int h = 0; h < world; ++h) {
-    NCCL_OK(ncclSend(B + slab_t0[h] * me, size_t(slab_len[h] * me), ncclDouble, h, C(nccl), stream));
-    NCCL_OK(ncclRecv(tmp + ntl * chunk_off[h], size_t(ntl * chunk_len[h]), ncclDouble, h, C(nccl), stream));
+    int64_t so, sc, ro, rc;
+    a2a_plan(nt, Ns, world, rank, h, &so, &sc, &ro, &rc);  // transpose of slab -> chunk
+    NCCL_OK(ncclSend(B + ro, size_t(rc), ncclDouble, h, C(nccl), stream));
+    NCCL_OK(ncclRecv(tmp + so, size_t(sc), ncclDouble, h, C(nccl), stream));
   }
   NCCL_OK(ncclGroupEnd());
-  const int64_t base = Ns / world, extra = Ns % world;
-  pack_kernel<false><<<1184, 256, 0, stream>>>(tmp, A, ntl, Ns, base, extra);
+  pack_kernel<false><<<1184, 256, 0, stream>>>(tmp, A, ntl, Ns, world);
   ++launches;
   if (cudaGetLastError() != cudaSuccess) return LS_ECUDA;
   return LS_OK;
 }
 
-int Comm::halo_exchange(double* x_ext, int64_t halo, int64_t /*unused*/, int64_t& launches) {
-  // x_ext = [halo rows | own ntl rows | halo rows]; slabs are >= halo thick (checked at setup)
-  (void)launches;
-  const int64_t ntl = slab_len[rank];
-  double* own = x_ext + halo * Ns;
-  const size_t cnt = size_t(halo * Ns);
+int Comm::halo_exchange(double* x_ext, int p) {
+  int64_t t0, ntl, lo, hi;
+  halo_plan(nt, world, rank, p, &t0, &ntl, &lo, &hi);
+  double* own = x_ext + lo * Ns;
   NCCL_OK(ncclGroupStart());
-  if (rank > 0) {
-    NCCL_OK(ncclRecv(own - halo * Ns, cnt, ncclDouble, rank - 1, C(nccl), stream));
-    NCCL_OK(ncclSend(own, cnt, ncclDouble, rank - 1, C(nccl), stream));
+  if (lo > 0) {
+    NCCL_OK(ncclRecv(x_ext, size_t(lo * Ns), ncclDouble, rank - 1, C(nccl), stream));
+    NCCL_OK(ncclSend(own, size_t(lo * Ns), ncclDouble, rank - 1, C(nccl), stream));
   }
-  if (rank + 1 < world) {
-    NCCL_OK(ncclRecv(own + ntl * Ns, cnt, ncclDouble, rank + 1, C(nccl), stream));
-    NCCL_OK(ncclSend(own + (ntl - halo) * Ns, cnt, ncclDouble, rank + 1, C(nccl), stream));
+  if (hi > 0) {
+    NCCL_OK(ncclRecv(own + ntl * Ns, size_t(hi * Ns), ncclDouble, rank + 1, C(nccl), stream));
+    NCCL_OK(ncclSend(own + (ntl - hi) * Ns, size_t(hi * Ns), ncclDouble, rank + 1, C(nccl), stream));
   }
   NCCL_OK(ncclGroupEnd());
   return LS_OK;

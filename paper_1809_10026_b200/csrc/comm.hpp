@@ -16,6 +16,8 @@
 
 #include <cuda_runtime.h>
 
+#include "plan.hpp"
+
 struct ls_ctx;
 
 namespace ls {
@@ -33,22 +35,18 @@ struct Comm {
   int slab_to_chunk(const double* A, double* B, double* tmp, int64_t& launches);
   // B: [nt][chunk_me] -> A: local slab [ntl][Ns]; tmp: receive staging
   int chunk_to_slab(const double* B, double* A, double* tmp, int64_t& launches);
-  // x_ext = [p halo | own ntl slices | p halo]: fill the halos from the neighbours
-  int halo_exchange(double* x_ext, int64_t halo_lo, int64_t halo_hi, int64_t& launches);
+  // x_ext = [lo halo | own ntl slices | hi halo] (plan.hpp halo_plan): fill the halos
+  int halo_exchange(double* x_ext, int p);
   int allreduce_scalar(double* dev_ptr);
 };
 
 int comm_unique_id(void* out128);
 
-// Even split of `total` items over `world` parts (the first total % world parts get one more).
+// Even split of `total` items over `world` parts (plan.hpp split_part for every part).
 inline void split_even(int64_t total, int world, std::vector<int64_t>& off, std::vector<int64_t>& len) {
   off.assign(world, 0);
   len.assign(world, 0);
-  const int64_t base = total / world, extra = total % world;
-  for (int g = 0; g < world; ++g) {
-    len[g] = base + (g < extra ? 1 : 0);
-    off[g] = g * base + (g < extra ? g : extra);
-  }
+  for (int g = 0; g < world; ++g) split_part(total, world, g, &off[g], &len[g]);
 }
 
 } // namespace ls

@@ -80,26 +80,30 @@ struct TimeArgs {
   const double* bKt;  // bands of K_t, M_t
   const double* bMt;
   int nt, hb;
+  int t_first;   // global time index of output row 0
+  int s_first;   // global time index of S row 0 (extended slab incl. halo)
   uint32_t Ns;
-  uint64_t total;
+  uint64_t total;  // output rows * Ns
 };
 
 // y[t][s] = sum_i K_t[t][i] S_M[i][s] + M_t[t][i] S_J[i][s] + [t == n_t-1] S_K[t][s]
+// (t, i global time indices; S rows are stored from global row s_first)
 __global__ void __launch_bounds__(256) band_time_kernel(TimeArgs a) {
   const int W = 2 * a.hb + 1;
   for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < a.total;
        e += uint64_t(gridDim.x) * blockDim.x) {
-    const int t = int(e / a.Ns);
-    const uint32_t s = uint32_t(e - uint64_t(t) * a.Ns);
+    const int tl = int(e / a.Ns);
+    const uint32_t s = uint32_t(e - uint64_t(tl) * a.Ns);
+    const int t = a.t_first + tl;
     const int lo = max(0, t - a.hb), hi = min(a.nt - 1, t + a.hb);
     const double* bk = a.bKt + size_t(t) * W - t + a.hb;
     const double* bm = a.bMt + size_t(t) * W - t + a.hb;
     double y = 0;
     for (int i = lo; i <= hi; ++i) {
-      const uint64_t off = uint64_t(i) * a.Ns + s;
+      const uint64_t off = uint64_t(i - a.s_first) * a.Ns + s;
       y = fma(__ldg(bk + i), __ldg(a.SM + off), fma(__ldg(bm + i), __ldg(a.SJ + off), y));
     }
-    if (t == a.nt - 1) y += __ldg(a.SK + e);
+    if (t == a.nt - 1) y += __ldg(a.SK + uint64_t(t - a.s_first) * a.Ns + s);
     a.y[e] = y;
   }
 }

@@ -1,0 +1,193 @@
+"""Multi-rank (N > 1) path on CPU: world_size 2 and 3 over torch.distributed/gloo.
+
+The GPU kernels cannot run here, so each rank executes the distributed SCHEDULE
+of libls (time slabs, pack map, all-to-all plan, halo plan -- queried from the
+library's host-only C-ABI, i.e. the exact functions comm.cu uses) with the
+oracle's per-mode arithmetic, exchanges data over gloo exactly as comm.cu does
+over NCCL, and compares the gathered result with the single-process oracle.
+"""
+
+import os
+import socket
+import traceback
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import univariate as uv, fd, operator as op
+import synth
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _setup(d, p, ne):
+    space = [uv.space_factors(n, p) for n in ne[:d]]
+    tf = uv.time_factors(ne[d], p)
+    return space, tf, fd.setup(space, tf)
+
+
+def _fd_rank(rank, world, d, p, ne):
+    import paper_1809_10026_b200 as ls
+    space, tf, fdd = _setup(d, p, ne)
+    nt = tf["Mt"].shape[0]
+    gshape = (nt,) + tuple(f["M"].shape[0] for f in reversed(space))
+    Ns = int(np.prod(gshape[1:]))
+    r = synth.residual(gshape, 0)
+    t0, ntl = ls.partition(nt, world, rank)
+    x = r[t0:t0 + ntl].copy()
+    for k in range(1, d + 1):                      # F1 (local)
+        x = fd.mode_apply(x, fdd["U_s"][k - 1].T, d + 1 - k)
+    pos = ls.pack_map(ntl, Ns, world)              # pack (comm.cu pack_kernel<true>)
+    send = np.empty(ntl * Ns)
+    send[pos] = x.ravel()
+    plan = ls.a2a_plan(nt, Ns, world, rank)
+    assert np.all(plan["send_off"] == np.concatenate([[0], np.cumsum(plan["send_cnt"])[:-1]]))
+    assert np.all(plan["recv_off"] == np.concatenate([[0], np.cumsum(plan["recv_cnt"])[:-1]]))
+    c0, clen = ls.partition(Ns, world, rank)
+    recv = torch.empty(nt * clen, dtype=torch.float64)
+    dist.all_to_all_single(recv, torch.from_numpy(send), output_split_sizes=plan["recv_cnt"].tolist(),
+                           input_split_sizes=plan["send_cnt"].tolist())
+    chunk = recv.numpy().reshape(nt, clen)         # [n_t][chunk]: time mode is local now
+    lam_s = (fd.divisor(fdd) - fdd["lam_t"].reshape((-1,) + (1,) * d))[0].ravel()
+    y = fdd["U_t"].T @ chunk
+    y = y / (fdd["lam_t"][:, None] + lam_s[None, c0:c0 + clen])
+    y = fdd["U_t"] @ y
+    back = torch.empty(ntl * Ns, dtype=torch.float64)  # chunk -> slab: transpose plan
+    dist.all_to_all_single(back, torch.from_numpy(np.ascontiguousarray(y).ravel()),
+                           output_split_sizes=plan["send_cnt"].tolist(),
+                           input_split_sizes=plan["recv_cnt"].tolist())
+    z = back.numpy()[pos].reshape((ntl,) + gshape[1:])  # unpack (pack_kernel<false>)
+    for k in range(d, 0, -1):                      # F3 (local)
+        z = fd.mode_apply(z, fdd["U_s"][k - 1], d + 1 - k)
+    ref = fd.fd_apply(r, fdd)[t0:t0 + ntl]
+    return float(np.linalg.norm(z - ref) / np.linalg.norm(ref))
+
+
+def _matvec_rank(rank, world, d, p, ne):
+    import paper_1809_10026_b200 as ls
+    space, tf, _ = _setup(d, p, ne)
+    nt = tf["Mt"].shape[0]
+    gshape = (nt,) + tuple(f["M"].shape[0] for f in reversed(space))
+    x = synth.residual(gshape, 1)
+    t0, ntl, lo, hi = ls.halo_plan(nt, world, rank, p)
+    own = x[t0:t0 + ntl].copy()
+    ext = np.zeros((lo + ntl + hi,) + gshape[1:])
+    ext[lo:lo + ntl] = own
+    reqs = []  # comm.cu halo_exchange, over gloo point-to-point
+    if lo > 0:
+        lo_buf = torch.empty(ext[:lo].shape, dtype=torch.float64)
+        reqs.append(dist.irecv(lo_buf, src=rank - 1))
+        reqs.append(dist.isend(torch.from_numpy(own[:lo].copy()), dst=rank - 1))
+    if hi > 0:
+        hi_buf = torch.empty(ext[lo + ntl:].shape, dtype=torch.float64)
+        reqs.append(dist.irecv(hi_buf, src=rank + 1))
+        reqs.append(dist.isend(torch.from_numpy(own[ntl - hi:].copy()), dst=rank + 1))
+    for q in reqs:
+        q.wait()
+    if lo > 0:
+        ext[:lo] = lo_buf.numpy()
+    if hi > 0:
+        ext[lo + ntl:] = hi_buf.numpy()
+    # spatial part of each Kronecker term on the extended slab, time band on own rows
+    s_first = t0 - lo
+    M = [f["M"] for f in space]
+    SM = op.apply_kron(ext, None, M)
+    SJ = 0.0
+    SL = 0.0
+    for k in range(d):
+        mats = list(M)
+        mats[k] = space[k]["J"]
+        SJ = SJ + op.apply_kron(ext, None, mats)
+        for l in range(d):
+            if l != k:
+                mats = list(M)
+                mats[k], mats[l] = space[k]["G"], space[l]["G"].T
+                SJ = SJ + op.apply_kron(ext, None, mats)
+        mats = list(M)
+        mats[k] = space[k]["K"]
+        SL = SL + op.apply_kron(ext, None, mats)
+    y = np.zeros_like(own)
+    for tl in range(ntl):
+        t = t0 + tl
+        for i in range(max(0, t - p), min(nt - 1, t + p) + 1):
+            y[tl] += tf["Kt"][t, i] * SM[i - s_first] + tf["Mt"][t, i] * SJ[i - s_first]
+        y[tl] += tf["Wt"][t, t] * SL[t - s_first] if t == nt - 1 else 0.0
+    ref = op.apply_A(x, space, tf)[t0:t0 + ntl]
+    return float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+
+
+def _worker(rank, world, port, fn_name, args, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        err = globals()[fn_name](rank, world, *args)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, err, None))
+    except Exception:
+        q.put((rank, None, traceback.format_exc()))
+
+
+def _run(world, fn_name, args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn_name, args, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+    for rank, err, tb in res:
+        assert tb is None, tb
+    return [err for _, err, _ in sorted(res)]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("d,p,ne", [(2, 2, [5, 4, 7]), (3, 3, [3, 4, 2, 9])])
+def test_distributed_fd_schedule(world, d, p, ne):
+    errs = _run(world, "_fd_rank", (d, p, ne))
+    assert max(errs) <= 1e-12, errs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("d,p,ne", [(1, 2, [6, 9]), (2, 3, [3, 4, 12])])
+def test_distributed_matvec_halo(world, d, p, ne):
+    errs = _run(world, "_matvec_rank", (d, p, ne))
+    assert max(errs) <= 1e-12, errs
+
+
+def test_plans_cover_everything():
+    """Slabs and chunks tile their ranges; the pack map is a permutation; the
+    a2a plans of all ranks are mutually consistent (what r sends to h is what h
+    receives from r)."""
+    import paper_1809_10026_b200 as ls
+    nt, Ns = 133, 132 ** 3 // 1000
+    for world in (1, 2, 3, 8):
+        offs = [ls.partition(nt, world, g) for g in range(world)]
+        assert offs[0][0] == 0 and sum(l for _, l in offs) == nt
+        assert all(offs[g][0] + offs[g][1] == offs[g + 1][0] for g in range(world - 1))
+        plans = [ls.a2a_plan(nt, Ns, world, r) for r in range(world)]
+        for r in range(world):
+            for h in range(world):
+                assert plans[r]["send_cnt"][h] == plans[h]["recv_cnt"][r]
+            assert plans[r]["send_cnt"].sum() == ls.partition(nt, world, r)[1] * Ns
+            assert plans[r]["recv_cnt"].sum() == nt * ls.partition(Ns, world, r)[1]
+        ntl = ls.partition(nt, world, world - 1)[1]
+        pos = ls.pack_map(ntl, Ns, world)
+        assert np.array_equal(np.sort(pos), np.arange(ntl * Ns))
+    t0, ntl, lo, hi = ls.halo_plan(133, 8, 0, 6)
+    assert (t0, ntl, lo, hi) == (0, 17, 0, 6)
+    assert ls.halo_plan(133, 8, 7, 6) == (117, 16, 6, 0)
+    with pytest.raises(ls.LSError):
+        ls.halo_plan(10, 8, 0, 6)   # slabs of 1-2 rows are thinner than the halo

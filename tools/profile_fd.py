@@ -18,13 +18,20 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--matvec", action="store_true")
+ap.add_argument("--pcg", action="store_true")
+ap.add_argument("--p", type=int, default=None)
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
-p = c["p"] if isinstance(c["p"], int) else c["p"][0]
+p = a.p if a.p is not None else (c["p"] if isinstance(c["p"], int) else c["p"][0])
 ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
 r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 z = torch.empty_like(r)
-for _ in range(a.reps):
+if a.pcg:
+    b = ctx.rhs(1)
+    for _ in range(a.reps):
+        x, st = ctx.pcg(b, tol=1e-8)
+    print(st)
+for _ in range(0 if a.pcg else a.reps):
     if a.matvec:
         ctx.matvec(r, z)
     else:
