@@ -450,6 +450,74 @@ static unsigned grid_for(uint64_t total, int threads, int num_sms) {
   return unsigned(std::min<uint64_t>(g, uint64_t(num_sms) * 16));
 }
 
+// ---- banded kernels (matvec_kernels.cuh): dispatch on p (template P) and row blocks RB
+template <class Kern>
+static int prepare_kernel(Kern k, size_t smem, int* occ, int threads = 256) {
+  LS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  LS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, threads, smem));
+  if (*occ < 1) *occ = 1;
+  return LS_OK;
+}
+
+template <int P, int RB, int KIND, int NWARPS>
+static int launch_tile(ls_ctx* ctx, BandArgs a) {
+  using C = BandCfg<P, RB, KIND, 3, NWARPS>;
+  static int occ = -1;
+  if (occ < 0) LS_CHECK(prepare_kernel(band_tile_kernel<P, RB, KIND, 3, NWARPS>, C::SMEM, &occ, C::THREADS));
+  a.ntiles = (a.ncols + C::BN - 1) / C::BN;
+  if (a.ntiles == 0) return LS_OK;
+  const unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms * occ));
+  band_tile_kernel<P, RB, KIND, 3, NWARPS><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  ctx->launches++;
+  LS_CUDA(cudaGetLastError());
+  return LS_OK;
+}
+
+template <int P, int NMAX>
+static int launch_first(ls_ctx* ctx, BandArgs a) {
+  using C = FirstCfg<P, NMAX, 2>;
+  static int occ = -1;
+  if (occ < 0) LS_CHECK(prepare_kernel(band_first_kernel<P, NMAX, 2>, C::SMEM, &occ));
+  a.ntiles = (a.ncols + C::BN - 1) / C::BN;
+  if (a.ntiles == 0) return LS_OK;
+  const unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms * occ));
+  band_first_kernel<P, NMAX, 2><<<grid, 256, C::SMEM, ctx->stream>>>(a);
+  ctx->launches++;
+  LS_CUDA(cudaGetLastError());
+  return LS_OK;
+}
+
+// kind 0: direction 1 ; kind 1: directions >= 2 ; kind 2: time.  rows = output rows.
+template <int P>
+static int launch_band_p(ls_ctx* ctx, const BandArgs& a, int kind, int rows) {
+  if (kind == 0) {
+    if (a.n <= 32) return launch_first<P, 32>(ctx, a);
+    if (a.n <= 72) return launch_first<P, 72>(ctx, a);
+    if (a.n <= 104) return launch_first<P, 104>(ctx, a);
+    return launch_first<P, 136>(ctx, a);
+  }
+  // (RB rows per warp, warps): rows covered = RB * NW >= rows; <= ~48 doubles of
+  // accumulators + window per thread
+#define LS_RB(R, NW)                                                                          \
+  if (rows <= R * NW) return kind == 1 ? launch_tile<P, R, 1, NW>(ctx, a) : launch_tile<P, R, 2, NW>(ctx, a);
+  LS_RB(2, 8) LS_RB(4, 8) LS_RB(8, 8) LS_RB(9, 8) LS_RB(13, 8) LS_RB(17, 8)
+#undef LS_RB
+  return LS_EINVAL;
+}
+
+static int launch_band(ls_ctx* ctx, const BandArgs& a, int kind, int rows) {
+  switch (ctx->p) {
+    case 2: return launch_band_p<2>(ctx, a, kind, rows);
+    case 3: return launch_band_p<3>(ctx, a, kind, rows);
+    case 4: return launch_band_p<4>(ctx, a, kind, rows);
+    case 5: return launch_band_p<5>(ctx, a, kind, rows);
+    case 6: return launch_band_p<6>(ctx, a, kind, rows);
+    case 7: return launch_band_p<7>(ctx, a, kind, rows);
+    case 8: return launch_band_p<8>(ctx, a, kind, rows);
+    default: return LS_ENOTSUP;  // ls_matvec supports p <= 8 (BASELINE configs: p <= 8)
+  }
+}
+
 // y = A x: spatial sum-factorisation on the `rows` time slices of x (global rows
 // [s_first, s_first + rows), halo included), time part on global output rows
 // [t_first, t_first + nout) written to y.
@@ -463,46 +531,36 @@ static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, i
     BandArgs a{};
     uint64_t Q = 1;
     for (int j = 0; j < k; ++j) Q *= ctx->n[j];
-    a.SM = (k == 0) ? x : S[0];
-    a.SK = (k == 0) ? nullptr : S[1];
-    a.SJ = (k == 0) ? nullptr : S[2];
-    a.oM = T[0];
-    a.oK = T[1];
-    a.oJ = T[2];
-    a.bM = ctx->bM[k];
-    a.bK = ctx->bK[k];
-    a.bJ = ctx->bJ[k];
+    a.in[0] = (k == 0) ? x : S[0];
+    a.in[1] = (k == 0) ? nullptr : S[1];
+    a.in[2] = (k == 0) ? nullptr : S[2];
+    for (int m = 0; m < 3; ++m) a.out[m] = T[m];
+    a.band[0] = ctx->bM[k];
+    a.band[1] = ctx->bK[k];
+    a.band[2] = ctx->bJ[k];
     a.n = ctx->n[k];
-    a.hb = ctx->p;
     a.Q = uint32_t(Q);
-    a.total = total;
-    const unsigned g = grid_for(total, 256, ctx->num_sms);
-    if (k == 0)
-      band_triple_kernel<true><<<g, 256, 0, ctx->stream>>>(a);
-    else
-      band_triple_kernel<false><<<g, 256, 0, ctx->stream>>>(a);
-    ctx->launches++;
-    LS_CUDA(cudaGetLastError());
+    a.ncols = uint32_t(total / ctx->n[k]);
+    LS_CHECK(launch_band(ctx, a, k == 0 ? 0 : 1, ctx->n[k]));
     std::swap(S, T);
   }
-  // time: y = K_t S_M + M_t S_J + W_t S_K on output rows [out0, out0 + nout)
-  TimeArgs t{};
-  t.SM = S[0];
-  t.SK = S[1];
-  t.SJ = S[2];
-  t.y = y;
-  t.bKt = ctx->bKt;
-  t.bMt = ctx->bMt;
-  t.nt = ctx->nt;
-  t.hb = ctx->p;
-  t.Ns = uint32_t(ctx->Ns);
+  // time: y = K_t S_M + M_t S_J + W_t S_K on global output rows [t_first, t_first + nout)
+  BandArgs t{};
+  t.in[0] = S[0];
+  t.in[1] = S[2];
+  t.in[2] = S[1];
+  t.out[0] = y;
+  t.band[0] = ctx->bMt;
+  t.band[1] = ctx->bKt;
+  t.band[2] = nullptr;
+  t.n = ctx->nt;
+  t.Q = uint32_t(ctx->Ns);
+  t.ncols = uint32_t(ctx->Ns);
   t.t_first = int(t_first);
   t.s_first = int(s_first);
-  t.total = uint64_t(nout) * ctx->Ns;
-  band_time_kernel<<<grid_for(t.total, 256, ctx->num_sms), 256, 0, ctx->stream>>>(t);
-  ctx->launches++;
-  LS_CUDA(cudaGetLastError());
-  return LS_OK;
+  t.s_rows = int(rows);
+  t.nout = int(nout);
+  return launch_band(ctx, t, 2, int(nout));
 }
 
 // extended-slab geometry of this rank (halo rows of the time factors)
