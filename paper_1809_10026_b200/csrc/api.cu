@@ -170,7 +170,7 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   a.P = uint32_t(P);
   a.Q = uint32_t(Q);
   a.ncols = uint32_t(P * Q);
-  const bool mode1 = (Q == 1);
+  const bool mode1 = (Q == 1) && !scale;  // the scaled (time) mode always uses the strided variant
   switch (round_ks((n + 3) / 4)) {
     KS_A(2) KS_A(4) KS_A(5) KS_A(8)
     KS_B(12) KS_B(16) KS_B(17) KS_B(18)

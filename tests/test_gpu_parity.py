@@ -210,3 +210,58 @@ def test_kernels_launched(torch_cuda):
     n0 = ctx.launches
     ctx.fd_apply(r)
     assert ctx.launches - n0 == 8
+
+
+EDGE_CASES = [
+    (1, 2, [1, 1]),            # n_s = 1, n_t = 2 (smallest space-time grid)
+    (2, 2, [1, 3, 1]),         # single-function directions
+    (3, 2, [1, 1, 1, 1]),      # N = 2
+    (3, 2, [2, 1, 40, 2]),     # extreme aspect ratio
+    (1, 8, [128, 127]),        # n = 134 / n_t = 134 (near the 136 cap), p = 8
+    (2, 4, [134, 1, 5]),       # n_1 = 136 (the cap)
+]
+
+
+@pytest.mark.parametrize("d,p,n_elems", EDGE_CASES)
+def test_fd_apply_edge_shapes(torch_cuda, d, p, n_elems):
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    _, _, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 4)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    z_ref = fd.fd_apply(r, fdd)
+    assert _rel(z, z_ref) <= TOL
+
+
+@pytest.mark.parametrize("d,p,n_elems", EDGE_CASES[:4] + [(2, 8, [20, 3, 25])])
+def test_matvec_edge_shapes(torch_cuda, d, p, n_elems):
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    space, tf, _ = _oracle(d, p, n_elems)
+    x = synth.residual(ctx.shape, 8)
+    y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert _rel(y, op.apply_A(x, space, tf)) <= 1e-12
+
+
+def test_setup_rejects_too_large_extent(torch_cuda):
+    import paper_1809_10026_b200 as ls
+    with pytest.raises(ls.LSError) as e:
+        ls.Context(1, 4, [10, 134])   # n_t = 137 > 136
+    assert e.value.code == ls.LS_EINVAL
+
+
+def test_matvec_rejects_aliasing(torch_cuda):
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    ctx = _ctx(2, 2, [4, 4, 4])
+    x = torch.zeros(ctx.shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(ls.LSError):
+        ctx.matvec(x, x)
+
+
+def test_pcg_nonconvergence_status(torch_cuda):
+    """max_iter too small -> LS_ENOCONV with stats filled (SPEC.md 405)."""
+    import paper_1809_10026_b200 as ls
+    ctx = _ctx(3, 3, [8, 8, 8, 8])
+    x, st = ctx.pcg(ctx.rhs(1), tol=1e-12, max_iter=3)
+    assert st["status"] == ls.LS_ENOCONV and st["iters"] == 3 and st["rel_res"] > 1e-12
