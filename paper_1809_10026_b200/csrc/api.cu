@@ -136,18 +136,57 @@ static int launch_mode_cfg(ls_ctx* ctx, const ModeArgs& a0) {
   return LS_OK;
 }
 
-template <int KS, int NT, int NSTAGE>
+template <class C>
+static int launch_mode_pp(ls_ctx* ctx, const ModeArgs& a0) {
+  static int ready = 0;
+  if (!ready) {
+    LS_CUDA(cudaFuncSetAttribute(fd_mode_pp_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(C::SMEM)));
+    ready = 1;
+  }
+  ModeArgs a = a0;
+  a.ntiles = (a.ncols + C::BN - 1) / C::BN;
+  if (a.ntiles == 0) return LS_OK;
+  unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms));
+  ls_ctx::ProfRec rec{};
+  if (ctx->prof) {
+    rec.a = ctx->get_event();
+    rec.b = ctx->get_event();
+    rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
+    cudaEventRecord(rec.a, ctx->stream);
+  }
+  fd_mode_pp_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  ctx->launches++;
+  if (ctx->prof) {
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->prof_recs.push_back(rec);
+  }
+  LS_CUDA(cudaGetLastError());
+  return LS_OK;
+}
+
+// ping-pong kernel: SPS stages per warp set (buckets A-C)
+template <int KS, int NT, int SPS>
 static int launch_mode_ks(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
+  if (mode1) return launch_mode_pp<PPCfg<KS, NT, true, false, SPS>>(ctx, a);
+  if (scale) return launch_mode_pp<PPCfg<KS, NT, false, true, SPS>>(ctx, a);
+  return launch_mode_pp<PPCfg<KS, NT, false, false, SPS>>(ctx, a);
+}
+
+// balanced m-half kernel (bucket D, n <= 136: W fills 148 KB of shared memory, one tile
+// in flight per stage; measured faster than ping-pong there)
+template <int KS, int NT, int NSTAGE>
+static int launch_mode_half(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
   if (mode1) return launch_mode_cfg<ModeCfg<KS, NT, true, false, NSTAGE>>(ctx, a);
   if (scale) return launch_mode_cfg<ModeCfg<KS, NT, false, true, NSTAGE>>(ctx, a);
   return launch_mode_cfg<ModeCfg<KS, NT, false, false, NSTAGE>>(ctx, a);
 }
 
 // buckets by k-steps (KS = ceil(n/4)): (NT, NSTAGE) sized for <= 227 KB of shared memory
-#define KS_A(K) case K: return launch_mode_ks<K, 4, 3>(ctx, a, mode1, scale);
-#define KS_B(K) case K: return launch_mode_ks<K, 2, 3>(ctx, a, mode1, scale);
-#define KS_C(K) case K: return launch_mode_ks<K, 2, 2>(ctx, a, mode1, scale);
-#define KS_D(K) case K: return launch_mode_ks<K, 1, 2>(ctx, a, mode1, scale);
+#define KS_A(K) case K: return launch_mode_ks<K, 4, 2>(ctx, a, mode1, scale);
+#define KS_B(K) case K: return launch_mode_ks<K, 2, 2>(ctx, a, mode1, scale);
+#define KS_C(K) case K: return launch_mode_ks<K, 2, 1>(ctx, a, mode1, scale);
+#define KS_D(K) case K: return launch_mode_half<K, 1, 2>(ctx, a, mode1, scale);
 
 static int round_ks(int ks) {
   static const int list[] = {2, 4, 5, 8, 12, 16, 17, 18, 24, 25, 26, 30, 33, 34};

@@ -108,11 +108,11 @@ struct ModeArgs {
 // One warp's share of one tile: MC m-tiles (compile time: no predicates, so no
 // re-convergence around mma.sync) x NT n-tiles, all k-steps.  A fragments come
 // two k-steps per LDS.128 and are double-buffered one k-step pair ahead.
-template <class C, int MC>
-__device__ __forceinline__ void compute_tile(double (&acc)[C::MTH][C::NT][2], const double* wl,
+template <class C, int MC, int MA>
+__device__ __forceinline__ void compute_tile(double (&acc)[MA][C::NT][2], const double* wl,
                                              const double* t, int grp, int lane) {
 #pragma unroll
-  for (int mt = 0; mt < C::MTH; ++mt)
+  for (int mt = 0; mt < MA; ++mt)
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   if (MC == 0) return;
@@ -288,9 +288,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
 
     double acc[C::MTH][C::NT][2];
     if (warp >> 2)
-      compute_tile<C, C::MTILES - C::MTH>(acc, wsm + (C::MTH * C::KSP * 32 + lane) * 2, t, grp, lane);
+      compute_tile<C, C::MTILES - C::MTH, C::MTH>(acc, wsm + (C::MTH * C::KSP * 32 + lane) * 2, t, grp, lane);
     else
-      compute_tile<C, C::MTH>(acc, wsm + lane * 2, t, grp, lane);
+      compute_tile<C, C::MTH, C::MTH>(acc, wsm + lane * 2, t, grp, lane);
 
     // ---- epilogue: registers -> global (optionally scaled, Alg. 1 step 3)
 #pragma unroll
@@ -320,6 +320,221 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
           if (C::SCALE) {
             v0 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lam_col[C::SCALE ? nt : 0][0]);
             v1 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lam_col[C::SCALE ? nt : 0][1]);
+          }
+          const size_t off = C::MODE1 ? size_t(a) : size_t(a) * Q;
+          if (vec) {
+            *reinterpret_cast<double2*>(args.Y + base + off) = make_double2(v0, v1);
+          } else {
+            args.Y[base + off] = v0;
+            if (two) args.Y[base2 + off] = v1;
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// =====================================================================================
+// Ping-pong variant (the production kernel).  Two warp sets of 4 warps (one warp per
+// SMSP each) work on alternate tiles of the CTA's tile sequence; their DMMA phases are
+// serialised by a pair of named barriers (set 0 MMA -> set 1 MMA -> set 0 MMA ...), so
+// while one set runs its k-loop at the full DMMA rate of every SMSP the other set
+// stores its previous tile and loads its next one.  Each warp owns all m-tiles of NT
+// n-tiles (acc[MTILES][NT]); a set's 4 warps cover the tile's 4 n-tile groups.
+// Stage s of the ring belongs to set s % 2 (SPS stages per set).
+// =====================================================================================
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, int SPS_>
+struct PPCfg {
+  static constexpr int KS = KS_, NT = NT_, SPS = SPS_;
+  static constexpr bool MODE1 = MODE1_, SCALE = SCALE_;
+  static constexpr int THREADS = 256, SET_THREADS = 128;
+  static constexpr int NSTAGE = 2 * SPS;
+  static constexpr int MTILES = (KS + 1) / 2;
+  static constexpr int MTH = MTILES;
+  static constexpr int BN = 8 * NT * 4;
+  static constexpr int KP = 4 * KS;
+  static constexpr int SN = pad4mod16(BN);
+  static constexpr int SK = pad4mod16(KP);
+  static constexpr int TILE = MODE1 ? BN * SK : KP * SN;
+  static constexpr int KSP = (KS + 1) / 2;
+  static constexpr int WFRAG = MTILES * KSP * 64;
+  static constexpr size_t SMEM = size_t(WFRAG + TILE * NSTAGE) * sizeof(double);
+  static_assert(MODE1 || SET_THREADS % (BN / 2) == 0, "loader: SET_THREADS % (BN/2) == 0");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// cp.async loader of one tile by LT threads (thread index lt)
+template <class C, int LT>
+__device__ __forceinline__ void load_tile_dev(const ModeArgs& args, double* t, uint32_t tile, int lt) {
+  const int n = args.n;
+  const uint32_t Q = args.Q, ncols = args.ncols;
+  const uint32_t c0 = tile * C::BN;
+  if (C::MODE1) {
+    const uint32_t cend = min(c0 + (uint32_t)C::BN, ncols);
+    const uint32_t total = (cend - c0) * (uint32_t)n;
+    const double* src = args.X + size_t(c0) * n;
+    if ((n & 1) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      const uint32_t half = total >> 1, hn = n >> 1;
+      for (uint32_t h = lt; h < half; h += LT) {
+        const uint32_t cc = h / hn, i = 2 * (h - cc * hn);
+        cp_async16(t + cc * C::SK + i, src + 2 * h);
+      }
+    } else {
+      uint32_t cc = lt / n, i = lt % n;
+      const uint32_t dq = LT / n, dr = LT % n;
+      for (uint32_t e = lt; e < total; e += LT) {
+        cp_async8(t + cc * C::SK + i, src + e);
+        cc += dq;
+        i += dr;
+        if (i >= (uint32_t)n) { i -= n; ++cc; }
+      }
+    }
+  } else {
+    constexpr int PAIRS = C::BN / 2;
+    const int cc = 2 * (lt % PAIRS);
+    const uint32_t c = c0 + cc;
+    if (c < ncols) {
+      const uint32_t p = c / Q, q = c - p * Q;
+      const double* src = args.X + (size_t(p) * n) * Q + q;
+      const bool second = (c + 1 < ncols);
+      const bool vec = second && (q + 1 < Q) && ((Q & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+      const double* src2 = src;
+      if (second && !vec) {
+        const uint32_t c2 = c + 1, p2 = c2 / Q, q2 = c2 - p2 * Q;
+        src2 = args.X + (size_t(p2) * n) * Q + q2;
+      }
+      const size_t rstep = size_t(LT / PAIRS) * Q;
+      int i = lt / PAIRS;
+      const double* s1 = src + size_t(i) * Q;
+      const double* s2 = src2 + size_t(i) * Q;
+      double* dst = t + i * C::SN + cc;
+      for (; i < n; i += LT / PAIRS) {
+        if (vec) {
+          cp_async16(dst, s1);
+        } else {
+          cp_async8(dst, s1);
+          if (second) cp_async8(dst + 1, s2);
+        }
+        s1 += rstep;
+        s2 += rstep;
+        dst += (LT / PAIRS) * C::SN;
+      }
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
+  extern __shared__ __align__(16) double smem[];
+  double* wsm = smem;
+  double* tiles = smem + C::WFRAG;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int set = warp >> 2;       // warp set (ping / pong)
+  const int grp = warp & 3;        // n-tile group (= SMSP)
+  const int stid = tid & 127;      // thread index within the set
+  const int n = args.n;
+  const uint32_t Q = args.Q;
+  const uint32_t ncols = args.ncols;
+
+  for (int e = tid; e < C::WFRAG; e += C::THREADS) {
+    const int h = e & 1, l = (e >> 1) & 31, ksp = (e >> 6) % C::KSP, mt = (e >> 6) / C::KSP;
+    const int ks = 2 * ksp + h;
+    const int a = mt * 8 + (l >> 2), i = ks * 4 + (l & 3);
+    wsm[e] = (a < n && i < n && ks < C::KS) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
+  }
+  for (int s = 0; s < C::NSTAGE; ++s) {
+    double* t = tiles + s * C::TILE;
+    if (C::MODE1) {
+      const int padw = C::SK - n;
+      for (int e = tid; e < C::BN * padw; e += C::THREADS) t[(e / padw) * C::SK + n + e % padw] = 0.0;
+    } else {
+      for (int e = tid; e < (C::KP - n) * C::SN; e += C::THREADS) t[n * C::SN + e] = 0.0;
+    }
+  }
+  double lam_row[C::SCALE ? C::MTILES : 1];
+#pragma unroll
+  for (int mt = 0; mt < (C::SCALE ? C::MTILES : 1); ++mt) {
+    const int a = mt * 8 + (lane >> 2);
+    lam_row[mt] = (C::SCALE && a < n) ? __ldg(args.lam_a + a) : 0.0;
+  }
+  __syncthreads();
+
+  // CTA tile sequence: local k -> blockIdx.x + k*gridDim.x; set s takes k = s, s+2, ...
+  const uint32_t stride = gridDim.x;
+  const uint32_t my_tiles = (args.ntiles > blockIdx.x) ? (args.ntiles - blockIdx.x + stride - 1) / stride : 0;
+  const uint32_t n0 = (my_tiles + 1) / 2, n1 = my_tiles / 2;  // tiles of set 0 / set 1
+  const uint32_t mine = set ? n1 : n0, other = set ? n0 : n1;
+  auto tile_of = [&](uint32_t j) { return blockIdx.x + (set + 2 * j) * stride; };
+  auto stage_of = [&](uint32_t j) { return set + 2 * int(j % C::SPS); };
+#pragma unroll 1
+  for (int j = 0; j < C::SPS; ++j) {
+    if (uint32_t(j) < mine) load_tile_dev<C, 128>(args, tiles + stage_of(j) * C::TILE, tile_of(j), stid);
+    cp_async_commit();
+  }
+  const int BAR_SET = 1 + set;                       // set-local barrier
+  const int BAR_MY_TURN = 3 + set, BAR_OTHER_TURN = 3 + (set ^ 1);
+
+#pragma unroll 1
+  for (uint32_t j = 0; j < mine; ++j) {
+    cp_async_wait<C::SPS - 1>();
+    named_sync(BAR_SET, 128);                        // my stage is loaded for all 128 threads
+    // DMMA phase, serialised with the other set: set 0 starts, then alternate
+    if (set == 1 || j > 0) named_sync(BAR_MY_TURN, 256);
+    const double* t = tiles + stage_of(j) * C::TILE;
+    double acc[C::MTILES][C::NT][2];
+    compute_tile<C, C::MTILES, C::MTILES>(acc, wsm + lane * 2, t, grp, lane);
+    // hand the tensor pipes to the other set if it has a tile for this turn
+    if ((set == 0 && j < other) || (set == 1 && j + 1 < other)) named_arrive(BAR_OTHER_TURN, 256);
+    named_sync(BAR_SET, 128);                        // all 4 warps done reading the stage
+    {
+      const uint32_t jn = j + C::SPS;
+      if (jn < mine) load_tile_dev<C, 128>(args, tiles + stage_of(jn) * C::TILE, tile_of(jn), stid);
+      cp_async_commit();
+    }
+    // ---- epilogue (overlaps the other set's DMMA phase)
+    const uint32_t c0 = tile_of(j) * C::BN;
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      const uint32_t c = c0 + grp * C::NT * 8 + nt * 8 + 2 * (lane & 3);
+      if (c >= ncols) continue;
+      const bool two = (c + 1 < ncols);
+      size_t base, base2 = 0;
+      bool vec = false;
+      if (C::MODE1) {
+        base = size_t(c) * n;
+        base2 = base + n;
+      } else {
+        const uint32_t p = c / Q, q = c - p * Q;
+        base = size_t(p) * n * Q + q;
+        vec = args.y16 && two && (q + 1 < Q) && ((Q & 1) == 0) && ((base & 1) == 0);
+        if (two && !vec) {
+          const uint32_t c2 = c + 1, p2 = c2 / Q, q2 = c2 - p2 * Q;
+          base2 = size_t(p2) * n * Q + q2;
+        }
+      }
+      double lc0 = 0.0, lc1 = 0.0;
+      if (C::SCALE) {
+        lc0 = __ldg(args.lam_c + c);
+        lc1 = two ? __ldg(args.lam_c + c + 1) : 0.0;
+      }
+#pragma unroll
+      for (int mt = 0; mt < C::MTILES; ++mt) {
+        const int a = mt * 8 + (lane >> 2);
+        if (a < n) {
+          double v0 = acc[mt][nt][0], v1 = acc[mt][nt][1];
+          if (C::SCALE) {
+            v0 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lc0);
+            v1 *= fast_rcp(lam_row[C::SCALE ? mt : 0] + lc1);
           }
           const size_t off = C::MODE1 ? size_t(a) : size_t(a) * Q;
           if (vec) {
