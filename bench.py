@@ -42,6 +42,17 @@ def _hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _traffic(cfg_id):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per fd_mode_kernel launch, from the
+    committed --set full capture summary (tools/traffic_from_ncu.py -> profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[f"config{cfg_id}"]
+        return t["bytes_per_launch"], t["source"]
+    except Exception:
+        return None, None
+
+
 def workload(cfg_id):
     c = synth.CONFIGS[cfg_id]
     d, p, n_el = c["d"], c["p"], c["n_el"]
@@ -65,6 +76,23 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        try:  # NVML: ~1 ms per sample, so even a sub-second timed region gets many samples
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.rows.append([str(sm), str(mx), str(pw)] +
+                                 ["Active" if rs & b else "Not Active" for b in bits])
+                self._stop.wait(0.02)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
@@ -249,9 +277,12 @@ def main():
     # roofline of the dominant kernel (fd_mode_kernel): algorithmic flops / device time
     achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
     hbm, hbm_src = _hbm_peak()
+    traffic, traffic_src = _traffic(args.config)
     roof = {"kernel": "fd_mode_kernel (all mode products of fd_apply)", "bound": "tensor",
             "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
+            "traffic_unit": "bytes per launch (mean over the captured launches)", "traffic_source": traffic_src,
+            "algorithmic_bytes_per_launch": 16 * w["N"],
             "peak_source": FP64_PEAK_SOURCE, "kernel_share_of_step": round(kms / (ms * args.steps), 4),
             "launches_timed": kn, "flops_per_step_algorithmic": w["flops"]}
 

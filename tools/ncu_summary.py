@@ -12,9 +12,10 @@ def f(v):
 
 
 def summarise(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1])) if len(rows) > 1 else {}
     out = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
@@ -23,10 +24,12 @@ def summarise(rep):
                      and k.endswith("per_issue_active.ratio")), key=lambda kv: -kv[1])
         out.append({
             "kernel": d.get("Kernel Name", "")[:70],
-            "time_ms": f(d.get("gpu__time_duration.sum")),
+            "time": f(d.get("gpu__time_duration.sum")),
             "dmma_pipe_pct": f(d.get("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active")),
-            "dram_read_GB": f(d.get("dram__bytes_read.sum")),
-            "dram_write_GB": f(d.get("dram__bytes_write.sum")),
+            "dram_read": f(d.get("dram__bytes_read.sum")),
+            "dram_write": f(d.get("dram__bytes_write.sum")),
+            "dram_unit": units.get("dram__bytes_read.sum"),
+            "time_unit": units.get("gpu__time_duration.sum"),
             "dram_pct": f(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
             "issue_pct": f(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active")),
             "regs": d.get("launch__registers_per_thread"),
