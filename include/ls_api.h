@@ -195,6 +195,21 @@ int64_t ls_kernel_launches(const ls_ctx* ctx);
 int ls_profile(ls_ctx* ctx, int enable);
 int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t* launches);
 
+/*
+ * ls_tune -- select among equivalent implementations (same results up to
+ * rounding order, c13); for benchmarking.  Knobs:
+ *   LS_TUNE_FD_KERNEL: 0 = automatic per mode extent (default),
+ *                      1 = shared-memory-staged DMMA mode kernels,
+ *                      2 = register-direct DMMA mode kernel.
+ *   LS_TUNE_MATVEC:    0 = automatic per degree (default),
+ *                      1 = four banded passes, 152 B/DOF,
+ *                      2 = three fused banded passes (Toeplitz stencils), 96 B/DOF.
+ * Errors: LS_EINVAL for an unknown knob or value.
+ */
+#define LS_TUNE_FD_KERNEL 1
+#define LS_TUNE_MATVEC 2
+int ls_tune(ls_ctx* ctx, int knob, int value);
+
 void ls_destroy(ls_ctx* ctx);
 const char* ls_strerror(int code);
 

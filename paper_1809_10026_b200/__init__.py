@@ -30,7 +30,7 @@ LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_E
 EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
             "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
-            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan"]
+            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune"]
 
 
 class PCGStats(ctypes.Structure):
@@ -78,6 +78,7 @@ def load_library(path=LIB_PATH):
         "ls_profile_read": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), i64p]),
         "ls_destroy": (None, [vp]),
+        "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "ls_partition": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
         "ls_a2a_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                        i64p, i64p, i64p, i64p]),
@@ -251,6 +252,11 @@ class Context:
         _check(self._lib.ls_get_factor(self._h, int(which), int(direction),
                                        ctypes.c_void_p(out.ctypes.data)), "ls_get_factor")
         return out
+
+    def tune(self, knob, value):
+        """ls_tune: select an equivalent implementation (knob 1 = FD mode kernel:
+        0 auto, 1 shared-memory staged, 2 register-direct)."""
+        _check(self._lib.ls_tune(self._h, int(knob), int(value)), "ls_tune")
 
     def profile(self, enable):
         """Start/stop CUDA-event timing of every FD mode-product launch."""

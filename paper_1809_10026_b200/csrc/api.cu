@@ -14,7 +14,9 @@
 #include "comm.hpp"
 #include "plan.hpp"
 #include "fd_kernels.cuh"
+#include "fd_rd_launch.cuh"
 #include "matvec_kernels.cuh"
+#include "matvec2_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 
@@ -52,6 +54,18 @@ struct ls_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int64_t launches = 0;
+  int fd_variant = 0;  // ls_tune knob LS_TUNE_FD_KERNEL: 0 auto, 1 smem-staged (v2/pp), 2 register-direct
+  int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
+  // matvec v2: Toeplitz stencil + boundary corrections per band matrix (matvec2_kernels.cuh)
+  struct Split {
+    std::vector<double> s;  // 2p+1
+    double* E = nullptr;     // device [nb][2p+1]
+  };
+  struct DirSplit {
+    Split M, K, J, K2;  // space: M, K, J, 2K ; time: M = M_t, K = K_t
+    int lo = 0, hi = 0;
+  };
+  DirSplit dsplit[3], tsplit;
 
   // host copies (introspection)
   std::vector<double> hM[3], hK[3], hJ[3], hMt, hKt, hlam[4], hU[4];
@@ -195,6 +209,32 @@ static int round_ks(int ks) {
   return -1;
 }
 
+// register-direct kernel (fd_rd_kernel.cuh), one explicit instantiation per k-step bucket
+static int launch_mode_rd(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
+  if (a.ncols == 0) return LS_OK;
+  ls_ctx::ProfRec rec{};
+  if (ctx->prof) {
+    rec.a = ctx->get_event();
+    rec.b = ctx->get_event();
+    rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
+    cudaEventRecord(rec.a, ctx->stream);
+  }
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (round_ks((a.n + 3) / 4)) {
+#define LS_RD_CASE(K) case K: e = rd_launch<K>(a, mode1, scale, ctx->stream, ctx->num_sms); break;
+    LS_RD_BUCKETS(LS_RD_CASE)
+#undef LS_RD_CASE
+    default: return LS_EINVAL;
+  }
+  ctx->launches++;
+  if (ctx->prof) {
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->prof_recs.push_back(rec);
+  }
+  LS_CUDA(e);
+  return LS_OK;
+}
+
 static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W, int n, uint64_t P,
                        uint64_t Q, bool scale, const double* lam_a = nullptr,
                        const double* lam_c = nullptr) {
@@ -210,6 +250,9 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   a.Q = uint32_t(Q);
   a.ncols = uint32_t(P * Q);
   const bool mode1 = (Q == 1) && !scale;  // the scaled (time) mode always uses the strided variant
+  // auto (measured, tools/fd_variants.py): register-direct for n > 116 (config 4: 75% -> 86% of
+  // the FP64 peak), smem-staged ping-pong / m-half kernels below (config 3: 56% vs 37%)
+  if (ctx->fd_variant == 2 || (ctx->fd_variant == 0 && (n + 3) / 4 >= 30)) return launch_mode_rd(ctx, a, mode1, scale);
   switch (round_ks((n + 3) / 4)) {
     KS_A(2) KS_A(4) KS_A(5) KS_A(8)
     KS_B(12) KS_B(16) KS_B(17) KS_B(18)
@@ -257,6 +300,64 @@ static int gen_eig(const std::vector<double>& K, const std::vector<double>& M, i
 static int upload(ls_ctx* ctx, const std::vector<double>& v, double** out) {
   LS_CHECK(ctx->alloc(out, v.size()));
   LS_CUDA(cudaMemcpy(*out, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
+// Toeplitz split B = T + E of the band matrices of one direction (matvec2_kernels.cuh):
+// stencil s = the middle row; zone [lo, hi) = the maximal run of rows around the middle
+// whose band equals s to 64 ulps (relative to max|s|) in every matrix of the set; E =
+// B - T on the other rows.  n < 2p + 1: empty zone, s = 0, E = B.
+static int make_split(ls_ctx* ctx, const std::vector<double>* const* mats, int nm, int n, int p,
+                      ls_ctx::DirSplit& out, bool space) {
+  const int W = 2 * p + 1;
+  const int c = n / 2;
+  const bool has_mid = (n >= W) && (c - p >= 0) && (c + p < n);
+  std::vector<std::vector<double>> st(nm, std::vector<double>(W, 0.0));
+  if (has_mid)
+    for (int m = 0; m < nm; ++m)
+      for (int j = 0; j < W; ++j) st[m][j] = (*mats[m])[size_t(c) * n + (c - p + j)];
+  auto interior = [&](int i) {
+    if (!has_mid || i - p < 0 || i + p >= n) return false;
+    for (int m = 0; m < nm; ++m) {
+      double mx = 0;
+      for (int j = 0; j < W; ++j) mx = std::max(mx, std::fabs(st[m][j]));
+      for (int j = 0; j < W; ++j)
+        if (std::fabs((*mats[m])[size_t(i) * n + (i - p + j)] - st[m][j]) > 64 * 2.220446049250313e-16 * mx)
+          return false;
+    }
+    return true;
+  };
+  int lo = n, hi = n;
+  if (has_mid && interior(c)) {
+    lo = c;
+    hi = c + 1;
+    while (lo - 1 >= 0 && interior(lo - 1)) --lo;
+    while (hi < n && interior(hi)) ++hi;
+  }
+  out.lo = lo;
+  out.hi = hi;
+  const int nb = lo + (n - hi);
+  auto fill = [&](int m, double scale, ls_ctx::Split& sp) -> int {
+    sp.s.assign(W, 0.0);
+    for (int j = 0; j < W; ++j) sp.s[j] = scale * st[m][j];
+    std::vector<double> E(size_t(std::max(nb, 1)) * W, 0.0);
+    for (int i = 0; i < n; ++i) {
+      if (i >= lo && i < hi) continue;
+      const int e = (i < lo) ? i : lo + (i - hi);
+      for (int j = 0; j < W; ++j) {
+        const int col = i - p + j;
+        E[size_t(e) * W + j] = (col >= 0 && col < n) ? scale * ((*mats[m])[size_t(i) * n + col] - st[m][j]) : 0.0;
+      }
+    }
+    return upload(ctx, E, &sp.E);
+  };
+  // space: mats = {M, K, J}; time: mats = {M_t, K_t}
+  LS_CHECK(fill(0, 1.0, out.M));
+  LS_CHECK(fill(1, 1.0, out.K));
+  if (space) {
+    LS_CHECK(fill(2, 1.0, out.J));
+    LS_CHECK(fill(1, 2.0, out.K2));
+  }
   return LS_OK;
 }
 
@@ -328,6 +429,15 @@ static int setup_common(ls_ctx* ctx) {
   }
   LS_CHECK(to_band(ctx, ctx->hMt, ctx->nt, p, &ctx->bMt));
   LS_CHECK(to_band(ctx, ctx->hKt, ctx->nt, p, &ctx->bKt));
+  // matvec v2 stencil splits (reading c18)
+  for (int k = 0; k < d; ++k) {
+    const std::vector<double>* mats[3] = {&ctx->hM[k], &ctx->hK[k], &ctx->hJ[k]};
+    LS_CHECK(make_split(ctx, mats, 3, ctx->n[k], p, ctx->dsplit[k], true));
+  }
+  {
+    const std::vector<double>* mats[2] = {&ctx->hMt, &ctx->hKt};
+    LS_CHECK(make_split(ctx, mats, 2, ctx->nt, p, ctx->tsplit, false));
+  }
   // workspaces (halo rows for the distributed matvec: p slices each side)
   const size_t halo = size_t(2 * p) * ctx->Ns;
   for (int i = 0; i < 6; ++i) LS_CHECK(ctx->alloc(&ctx->tmp[i], ctx->Nl + halo));
@@ -602,6 +712,118 @@ static int matvec_block(ls_ctx* ctx, const double* x, double* y, int64_t rows, i
   return launch_band(ctx, t, 2, int(nout));
 }
 
+// ---- matvec v2 (matvec2_kernels.cuh) ---------------------------------------------------
+static void mv_set(MVArgs& a, int slot, const ls_ctx::Split& sp) {
+  for (int j = 0; j < MV_MAXW; ++j) a.st[slot][j] = j < int(sp.s.size()) ? sp.s[j] : 0.0;
+  a.E[slot] = sp.E;
+}
+
+static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
+                      int64_t t_first, int64_t nout) {
+  const int d = ctx->d, P = ctx->p;
+  if (P < 2 || P > 8) return LS_ENOTSUP;  // ls_matvec supports p <= 8 (BASELINE configs: p <= 8)
+  double* Kx = ctx->tmp[0];
+  double* Mx = ctx->tmp[1];
+  double* A = ctx->tmp[2];
+  double* B = ctx->tmp[3];
+  double* C = ctx->tmp[4];
+  MV2Plan pl{};
+  pl.d = d;
+  pl.stream = ctx->stream;
+  pl.num_sms = ctx->num_sms;
+  // time pass on all N_s columns
+  {
+    MVArgs& a = pl.time;
+    mv_set(a, 0, ctx->tsplit.K);
+    mv_set(a, 1, ctx->tsplit.M);
+    a.r_lo = ctx->tsplit.lo;
+    a.r_hi = ctx->tsplit.hi;
+    a.in[0] = x;
+    a.out[0] = Kx;
+    a.out[1] = Mx;
+    a.n = ctx->nt;
+    a.ncols = uint32_t(ctx->Ns);
+    a.t_first = int(t_first);
+    a.s_first = int(s_first);
+    a.s_rows = int(rows);
+    a.nout = int(nout);
+    pl.grid_time = nout > 0 ? unsigned((ctx->Ns + 31) / 32) : 0;
+  }
+  // direction d on [nout][n_d][Q]
+  const int kd = d - 1;
+  uint64_t Q = 1;
+  for (int j = 0; j < kd; ++j) Q *= ctx->n[j];
+  {
+    MVArgs& a = pl.dir;
+    const auto& sp = ctx->dsplit[kd];
+    mv_set(a, 0, sp.M);
+    mv_set(a, 1, sp.J);
+    mv_set(a, 2, sp.K);
+    mv_set(a, 3, sp.K2);
+    a.r_lo = sp.lo;
+    a.r_hi = sp.hi;
+    a.in[0] = Kx;
+    a.in[1] = Mx;
+    a.out[0] = (d == 1) ? y : A;
+    a.out[1] = B;
+    a.out[2] = C;
+    const int64_t tT = (ctx->nt - 1) - t_first;  // local output index of the last time slice
+    const bool own_last = tT >= 0 && tT < nout;
+    a.tT = own_last ? int(tT) : -1;
+    a.xT = own_last ? x + (ctx->nt - 1 - s_first) * ctx->Ns : nullptr;
+    a.n = ctx->n[kd];
+    a.Q = uint32_t(Q);
+    a.ncols = uint32_t(uint64_t(nout) * Q);
+    pl.grid_dir = unsigned((a.ncols + 31) / 32);
+  }
+  // plane pass: directions d-1 .. 1
+  if (d >= 2) {
+    MVArgs& a = pl.plane;
+    const auto& s1 = ctx->dsplit[0];
+    mv_set(a, 4, s1.M);
+    mv_set(a, 5, s1.J);
+    mv_set(a, 6, s1.K);
+    a.r_lo1 = s1.lo;
+    a.r_hi1 = s1.hi;
+    a.n1 = ctx->n[0];
+    a.in[0] = A;
+    a.in[1] = B;
+    a.in[2] = C;
+    a.out[0] = y;
+    uint64_t items;
+    if (d == 3) {
+      const auto& s2 = ctx->dsplit[1];
+      mv_set(a, 0, s2.M);
+      mv_set(a, 1, s2.J);
+      mv_set(a, 2, s2.K);
+      mv_set(a, 3, s2.K2);
+      a.r_lo = s2.lo;
+      a.r_hi = s2.hi;
+      a.n = ctx->n[1];
+      a.ncols = uint32_t(nout * ctx->n[2]);  // planes
+      items = uint64_t(a.ncols) * ((ctx->n[1] + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS);
+    } else {
+      a.n = 1;
+      a.ncols = uint32_t(nout * ctx->n[1]);  // rows of [rows][n1]
+      items = (uint64_t(a.ncols) + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS;
+    }
+    pl.smem_plane = size_t(3) * MV_PLANE_ROWS * mv_plane_pitch(ctx->n[0], P) * sizeof(double);
+    const int per_sm = (pl.smem_plane <= 113 * 1024) ? 2 : 1;  // register-bound at 2
+    pl.grid_plane = unsigned(std::min<uint64_t>(items, uint64_t(ctx->num_sms) * per_sm));
+  }
+  LS_CUDA(mv2_run(P, pl, &ctx->launches));
+  return LS_OK;
+}
+
+static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
+                      int64_t t_first, int64_t nout) {
+  // auto (measured, tools/mv_variants.py, r01): v2 wins at p = 2 only (config 5 p=2: 2.74 vs
+  // 3.07 ms); at p >= 3 its passes are latency-bound and v1 is faster (config 4: 16.3 vs 19.5 ms)
+  const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2);
+  if (!v2) return matvec_block(ctx, x, y, rows, s_first, t_first, nout);
+  return mv2_launch(ctx, x, y, rows, s_first, t_first, nout);
+}
+
 // extended-slab geometry of this rank (halo rows of the time factors)
 static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
   int64_t t0, ntl;
@@ -610,14 +832,14 @@ static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
 
 extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y || !aligned8(x) || !aligned8(y)) return LS_EINVAL;
-  if (ctx->world == 1) return matvec_block(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
+  if (ctx->world == 1) return matvec_any(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
   int64_t lo, hi;
   ext_geom(ctx, &lo, &hi);
   double* own = ctx->pp + lo * ctx->Ns;  // extended buffer [lo | own | hi]
   if (x != own)
     LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->p));
-  return matvec_block(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
+  return matvec_any(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -835,6 +1057,21 @@ extern "C" int ls_halo_plan(int64_t nt, int world, int rank, int p, int64_t* t0,
 }
 
 extern "C" int64_t ls_kernel_launches(const ls_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
+  if (!ctx) return LS_EINVAL;
+  switch (knob) {
+    case LS_TUNE_FD_KERNEL:
+      if (value < 0 || value > 2) return LS_EINVAL;
+      ctx->fd_variant = value;
+      return LS_OK;
+    case LS_TUNE_MATVEC:
+      if (value < 0 || value > 2) return LS_EINVAL;
+      ctx->mv_variant = value;
+      return LS_OK;
+    default: return LS_EINVAL;
+  }
+}
 
 extern "C" void ls_destroy(ls_ctx* ctx) {
   if (!ctx) return;

@@ -1,0 +1,56 @@
+// Launcher of fd_mode_rd_kernel for one k-step bucket KS (explicitly
+// instantiated per bucket in rd_ks*.cu so the buckets compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fd_rd_kernel.cuh"
+
+namespace ls {
+
+// NT (columns per n-tile group) and the prefetch window D per bucket: NT = 2 keeps
+// acc[MT][2] + the window under ~200 registers for MT >= 10; small MT takes NT = 4.
+template <int KS>
+struct RDBucket {
+  static constexpr int MT = (KS + 1) / 2;
+  static constexpr int NT = MT >= 10 ? 2 : 4;
+  static constexpr int D = 4;
+};
+
+template <class C>
+static cudaError_t rd_launch_cfg(const ModeArgs& a, cudaStream_t s, int num_sms) {
+  static bool ready = false;
+  if (!ready) {
+    cudaError_t e = cudaFuncSetAttribute(fd_mode_rd_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    ready = true;
+  }
+  const uint32_t ntw = (a.ncols + C::TW - 1) / C::TW;
+  if (ntw == 0) return cudaSuccess;
+  const unsigned grid = std::min<unsigned>((ntw + C::WARPS - 1) / C::WARPS, unsigned(num_sms));
+  fd_mode_rd_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+// mode1: contiguous mode (Q == 1); scale: fused Algorithm-1 step 3 (time mode, P == 1)
+template <int KS>
+cudaError_t rd_launch(const ModeArgs& a, bool mode1, bool scale, cudaStream_t s, int num_sms) {
+  using B = RDBucket<KS>;
+  constexpr int NT = B::NT, D = B::D;
+  if (mode1) return rd_launch_cfg<RDCfg<KS, NT, true, false, false, D>>(a, s, num_sms);
+  const bool fast = (a.Q % (2 * NT) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
+  if (scale) {
+    if (fast) return rd_launch_cfg<RDCfg<KS, NT, false, true, true, D>>(a, s, num_sms);
+    return rd_launch_cfg<RDCfg<KS, NT, false, true, false, D>>(a, s, num_sms);
+  }
+  if (fast) return rd_launch_cfg<RDCfg<KS, NT, false, false, true, D>>(a, s, num_sms);
+  return rd_launch_cfg<RDCfg<KS, NT, false, false, false, D>>(a, s, num_sms);
+}
+
+#define LS_RD_BUCKETS(X) X(2) X(4) X(5) X(8) X(12) X(16) X(17) X(18) X(24) X(25) X(26) X(30) X(33) X(34)
+#define LS_RD_DECL(K) extern template cudaError_t rd_launch<K>(const ModeArgs&, bool, bool, cudaStream_t, int);
+LS_RD_BUCKETS(LS_RD_DECL)
+#undef LS_RD_DECL
+
+}  // namespace ls

@@ -1,0 +1,338 @@
+// Matrix-free y = A x on the identity map (eq:A_kron, PAPER.md 686-703), v2:
+// three fused banded passes, 96 B/DOF of HBM traffic (v1, matvec_kernels.cuh:
+// four passes, 152 B/DOF).
+//
+// Algebra.  With M_s = (x)_k M_k, L_s = sum_k K_(k) and
+// J_s = sum_k J_(k) + sum_{k != l} K_(k) K_(l) (integration by parts on the
+// Dirichlet basis), expand A direction by direction starting from
+// time with a triple (A, B, C):
+//     A0 = K_t x,   B0 = M_t x,   C0 = W_t x        (W_t = e_{n_t} e_{n_t}^T)
+//     direction k:  A <- M_k A + J_k B + K_k C
+//                   B <- M_k B
+//                   C <- 2 K_k B + M_k C
+// and after the last direction y = A.  (Induction: after directions d..k the
+// triple holds the time/space terms whose remaining factors are M, J and K
+// respectively; every ordered pair k != l of the K K cross terms appears once in
+// each order, hence the 2.)  Passes:
+//   mv_time_kernel  (time):          x -> Kx = K_t x, Mx = M_t x            8 + 16 B/DOF
+//   mv_dir_kernel   (direction d):   Kx, Mx (+ x at t = n_t - 1) -> A, B, C  16 + 24 B/DOF
+//   mv_plane_kernel (directions d-1 .. 1, i.e. 2 and 1 fused per plane for
+//                    d = 3, 1 for d = 2):  A, B, C -> y                      24 + 8 B/DOF
+// (d = 1: mv_dir_kernel in A-only mode writes y.)
+//
+// Banded products.  The univariate matrices of uniform open knots are Toeplitz
+// away from the boundary (translation invariance of the interior B-splines).
+// Each band matrix B (half-bandwidth P) is split as B = T + E: T applies ONE
+// stencil s[0..2P] on every row (inputs outside [0, n) are zero), and E holds the
+// per-row corrections of the boundary rows [0, r_lo) and [r_hi, n) (interior
+// rows agree with s to rounding, reading c18).  The stencils are
+// kernel parameters (__grid_constant__): the DFMAs take them as constant-bank
+// operands, so the hot loops issue only data loads and DFMAs.
+// Thread mapping: lane = column of the banded direction (coalesced rows), each
+// thread sweeps its column in chunks of R rows with a window of R + 2P values;
+// the boundary chunks add the E rows (warp-uniform broadcast loads).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ls {
+
+constexpr int MV_MAXW = 17;  // 2P + 1 for P <= 8
+constexpr int MV_NST = 7;    // stencils per pass (plane pass: M2 J2 K2 2K2 M1 J1 K1)
+
+struct MVArgs {
+  double st[MV_NST][MV_MAXW];  // Toeplitz stencils (constant-bank operands)
+  const double* E[MV_NST];     // boundary corrections [nb][2P+1]: rows [0, r_lo) then [r_hi, n)
+  int r_lo, r_hi;              // interior zone of the pass direction (plane: direction 2)
+  int r_lo1, r_hi1;            // plane pass: interior zone of direction 1
+  const double* in[3];
+  double* out[3];
+  const double* xT;   // mv_dir: x rows of the last time slice [n][Q] (nullptr if not owned)
+  int n;              // extent of the banded direction (time: n_t; dir: n_d; plane: n_2)
+  int n1;             // plane pass: extent of direction 1
+  uint32_t Q;         // dir pass: product of the faster extents
+  uint32_t ncols;     // dir / time: columns; plane: number of planes (or rows when d = 2)
+  int t_first, s_first, s_rows, nout;  // time pass: global output rows / stored input rows
+  int tT;             // dir pass: local time index of global t = n_t - 1 (or -1)
+};
+
+__device__ __forceinline__ double mv_ld(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+// acc[i] += sum_j s[j] w[i + j] (Toeplitz part; s is a compile-time-indexed parameter)
+template <int P, int R>
+__device__ __forceinline__ void mv_stencil(double (&acc)[R], const double (&w)[R + 2 * P], const double* s) {
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < 2 * P + 1; ++j) acc[i] = fma(s[j], w[i + j], acc[i]);
+}
+
+// boundary corrections for rows r0 .. r0+R-1 of a band direction with zone [lo, hi)
+template <int P, int R>
+__device__ __forceinline__ void mv_correct(double (&acc)[R], const double (&w)[R + 2 * P], const double* E,
+                                           int r0, int n, int lo, int hi) {
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int r = r0 + i;
+    if (r < n && (r < lo || r >= hi)) {
+      const double* e = E + (r < lo ? r : lo + (r - hi)) * (2 * P + 1);
+#pragma unroll
+      for (int j = 0; j < 2 * P + 1; ++j) acc[i] = fma(__ldg(e + j), w[i + j], acc[i]);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// time pass: Kx = K_t x, Mx = M_t x on every spatial column (Q = N_s columns)
+// --------------------------------------------------------------------------------------
+// block (32, MV_CY): x = column, y = chunk of R output rows; one chunk per thread, the
+// halo rows of neighbouring chunks hit L1
+constexpr int MV_CY = 8;
+
+template <int P, int R>
+__global__ void __launch_bounds__(32 * MV_CY) mv_time_kernel(const __grid_constant__ MVArgs a) {
+  const uint32_t c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = (blockIdx.y * MV_CY + threadIdx.y) * R;  // local output row of acc[0]
+  if (c >= a.ncols || r0 >= a.nout) return;
+  const size_t Q = a.ncols;
+  const int n = a.n;
+  const double* x = a.in[0];
+  const int g0 = a.t_first + r0;  // global output row of acc[0]
+  double w[R + 2 * P];
+#pragma unroll
+  for (int j = 0; j < R + 2 * P; ++j) {
+    const int g = g0 - P + j;
+    const bool ok = g >= 0 && g < n && g >= a.s_first && g < a.s_first + a.s_rows;
+    w[j] = ok ? mv_ld(x + size_t(g - a.s_first) * Q + c) : 0.0;
+  }
+  const bool corr = g0 < a.r_lo || g0 + R > a.r_hi;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {  // m = 0: Kx (stencil 0), m = 1: Mx (stencil 1)
+    double acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = 0.0;
+    mv_stencil<P, R>(acc, w, a.st[m]);
+    if (corr) mv_correct<P, R>(acc, w, a.E[m], g0, n, a.r_lo, a.r_hi);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (r0 + i < a.nout) a.out[m][size_t(r0 + i) * Q + c] = acc[i];
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// direction-d pass on [P_t][n][Q] (P_t = local time slices): stencils 0 M, 1 J, 2 K, 3 2K
+//   A = M Kx + J Mx (+ K xT),  B = M Mx,  C = 2K Mx (+ M xT)     (xT only at t = tT)
+// AONLY (d = 1): only A, written to out[0] (= y).
+// --------------------------------------------------------------------------------------
+template <int P, int R, bool AONLY>
+__global__ void __launch_bounds__(32 * MV_CY) mv_dir_kernel(const __grid_constant__ MVArgs a) {
+  const uint32_t c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = (blockIdx.y * MV_CY + threadIdx.y) * R;
+  const int n = a.n;
+  if (c >= a.ncols || r0 >= n) return;
+  const uint32_t Q = a.Q;
+  const uint32_t pt = c / Q, q = c - pt * Q;
+  const size_t base = size_t(pt) * n * Q + q;
+  const bool last = int(pt) == a.tT;
+  const bool corr = r0 < a.r_lo || r0 + R > a.r_hi;
+  double acc[R], w[R + 2 * P];
+  auto window = [&](const double* src) {
+#pragma unroll
+    for (int j = 0; j < R + 2 * P; ++j) {
+      const int r = r0 - P + j;
+      w[j] = (r >= 0 && r < n) ? mv_ld(src + size_t(r) * Q) : 0.0;
+    }
+  };
+  auto zero = [&]() {
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = 0.0;
+  };
+  auto apply = [&](int m) {
+    mv_stencil<P, R>(acc, w, a.st[m]);
+    if (corr) mv_correct<P, R>(acc, w, a.E[m], r0, n, a.r_lo, a.r_hi);
+  };
+  auto put = [&](int o) {
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (r0 + i < n) a.out[o][base + size_t(r0 + i) * Q] = acc[i];
+  };
+  // A = M Kx + J Mx (+ K xT)
+  zero();
+  window(a.in[0] + base);
+  apply(0);
+  window(a.in[1] + base);
+  apply(1);
+  if (last) {
+    window(a.xT + q);
+    apply(2);
+  }
+  put(0);
+  if (AONLY) return;
+  // C = (M xT) + 2K Mx
+  zero();
+  if (last) apply(0);  // w holds the xT window
+  window(a.in[1] + base);
+  apply(3);
+  put(2);
+  // B = M Mx (w holds the Mx window)
+  zero();
+  apply(0);
+  put(1);
+}
+
+// --------------------------------------------------------------------------------------
+// plane pass.  PHASE1 (d = 3): a work item = up to 32 consecutive rows i2 of one
+// (t, i3) plane [n2][n1]; phase 1 applies direction 2 (stencils 0 M2, 1 J2, 2 K2,
+// 3 2K2) from global memory into shared rows
+//     A2 = M2 A + J2 B + K2 C,  B2 = M2 B,  C2 = 2K2 B + M2 C,
+// phase 2 applies direction 1 (stencils 4 M1, 5 J1, 6 K1) along the shared rows
+//     y = M1 A2 + J1 B2 + K1 C2
+// with lane = row and warp = segment of direction-1 outputs (warp-uniform output
+// positions, so boundary corrections are broadcasts), and the outputs are staged
+// back through shared memory for coalesced stores.  !PHASE1 (d = 2): the work item
+// is 32 consecutive rows of [rows][n1], phase 1 only copies A, B, C into shared.
+// --------------------------------------------------------------------------------------
+constexpr int MV_PLANE_THREADS = 288;  // 9 warps
+constexpr int MV_PLANE_ROWS = 16;      // rows per work item
+
+__host__ __device__ inline int mv_plane_pitch(int n1, int P) {
+  const int w = n1 + 2 * P;
+  return (w & 1) ? w : w + 1;  // odd pitch: lane = row reads are conflict-free
+}
+
+template <int P, int R, bool PHASE1>
+__global__ void __launch_bounds__(MV_PLANE_THREADS, 2) mv_plane_kernel(const __grid_constant__ MVArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  const int n1 = a.n1, n2 = a.n;
+  const int pitch = mv_plane_pitch(n1, P);
+  const int slab = MV_PLANE_ROWS * pitch;
+  double* S0 = sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // zero the P-column borders once (never written afterwards)
+  for (int e = tid; e < 3 * MV_PLANE_ROWS * 2 * P; e += MV_PLANE_THREADS) {
+    const int m = e / (MV_PLANE_ROWS * 2 * P), rem = e % (MV_PLANE_ROWS * 2 * P);
+    const int r = rem / (2 * P), j = rem % (2 * P);
+    S0[m * slab + r * pitch + (j < P ? j : P + n1 + (j - P))] = 0.0;
+  }
+  const int bpp = PHASE1 ? (n2 + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS : 1;  // blocks per plane
+  const uint32_t nitems = PHASE1 ? a.ncols * uint32_t(bpp) : (a.ncols + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS;
+  // phase 2: thread = (row, segment of R direction-1 outputs)
+  const int prow = lane & (MV_PLANE_ROWS - 1);
+  const int nseg = (n1 + R - 1) / R;
+  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    size_t row0;  // global row (of the [rows][n1] view) of local row 0
+    int nr, i2_0 = 0;
+    uint32_t plane = 0;
+    if (PHASE1) {
+      plane = it / bpp;
+      const int b = it - plane * bpp;
+      i2_0 = (b * n2) / bpp;
+      nr = ((b + 1) * n2) / bpp - i2_0;  // balanced blocks (<= 16 rows)
+      row0 = size_t(plane) * n2 + i2_0;
+    } else {
+      row0 = size_t(it) * MV_PLANE_ROWS;
+      nr = int(min(size_t(MV_PLANE_ROWS), size_t(a.ncols) - row0));
+    }
+    __syncthreads();  // previous item's shared rows fully consumed
+    if (PHASE1) {
+      // ---- phase 1: direction 2, thread = (column i1, chunk of R rows)
+      const int nch = (nr + R - 1) / R;
+      for (int job = tid; job < nch * n1; job += MV_PLANE_THREADS) {
+        const int i1 = job % n1, lr = (job / n1) * R;
+        const size_t cbase = size_t(plane) * n2 * n1 + i1;
+        const int r0 = i2_0 + lr;  // row of the direction-2 band
+        const bool corr = r0 < a.r_lo || r0 + R > a.r_hi;
+        double acc[R], w[R + 2 * P];
+        auto window = [&](const double* src) {
+#pragma unroll
+          for (int j = 0; j < R + 2 * P; ++j) {
+            const int r = r0 - P + j;
+            w[j] = (r >= 0 && r < n2) ? mv_ld(src + cbase + size_t(r) * n1) : 0.0;
+          }
+        };
+        auto zero = [&]() {
+#pragma unroll
+          for (int i = 0; i < R; ++i) acc[i] = 0.0;
+        };
+        auto apply = [&](int m) {
+          mv_stencil<P, R>(acc, w, a.st[m]);
+          if (corr) mv_correct<P, R>(acc, w, a.E[m], r0, n2, a.r_lo, a.r_hi);
+        };
+        auto put = [&](int m) {
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+            if (lr + i < nr) S0[m * slab + (lr + i) * pitch + P + i1] = acc[i];
+        };
+        // A2 = M2 A + J2 B + K2 C
+        zero();
+        window(a.in[0]);
+        apply(0);
+        window(a.in[1]);
+        apply(1);
+        window(a.in[2]);
+        apply(2);
+        put(0);
+        // C2 = M2 C + 2K2 B  (w holds the C window)
+        zero();
+        apply(0);
+        window(a.in[1]);
+        apply(3);
+        put(2);
+        // B2 = M2 B  (w holds the B window)
+        zero();
+        apply(0);
+        put(1);
+      }
+    } else {
+      for (int e = tid; e < nr * n1; e += MV_PLANE_THREADS) {
+        const int r = e / n1, i1 = e - r * n1;
+        const size_t g = (row0 + r) * n1 + i1;
+        const int o = r * pitch + P + i1;
+        S0[o] = mv_ld(a.in[0] + g);
+        S0[slab + o] = mv_ld(a.in[1] + g);
+        S0[2 * slab + o] = mv_ld(a.in[2] + g);
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: direction 1 along the shared rows; thread = (row, segment); outputs go
+    //      straight to global memory (a thread's R outputs are contiguous)
+    for (int seg = warp * 2 + (lane >> 4); seg < nseg; seg += 2 * (MV_PLANE_THREADS / 32)) {
+      if (prow >= nr) continue;
+      const int c0 = seg * R;
+      const bool corr = c0 < a.r_lo1 || c0 + R > a.r_hi1;
+      double acc[R], w[R + 2 * P];
+#pragma unroll
+      for (int i = 0; i < R; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const double* row = S0 + m * slab + prow * pitch + c0;  // staged column c0 - P
+#pragma unroll
+        for (int j = 0; j < R + 2 * P; ++j) w[j] = (c0 - P + j < n1 + P) ? row[j] : 0.0;
+        mv_stencil<P, R>(acc, w, a.st[4 + m]);
+        if (corr) mv_correct<P, R>(acc, w, a.E[4 + m], c0, n1, a.r_lo1, a.r_hi1);
+      }
+      double* yrow = a.out[0] + (row0 + prow) * n1;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (c0 + i < n1) yrow[c0 + i] = acc[i];
+    }
+  }
+}
+
+// launch plan built by the host (api.cu) and executed by mv2.cu (own translation unit)
+struct MV2Plan {
+  MVArgs time, dir, plane;
+  int d;
+  unsigned grid_time, grid_dir, grid_plane;
+  size_t smem_plane;
+  cudaStream_t stream;
+  int num_sms;
+};
+// returns the CUDA error of the launches; *launches += number of kernels launched
+cudaError_t mv2_run(int p, const MV2Plan& plan, int64_t* launches);
+
+}  // namespace ls

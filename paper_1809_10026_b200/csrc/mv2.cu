@@ -1,0 +1,52 @@
+// ls_matvec v2 launches (matvec2_kernels.cuh), one translation unit of their own.
+#include "matvec2_kernels.cuh"
+
+namespace ls {
+
+template <int P>
+static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
+  constexpr int R = 8;
+  cudaError_t e;
+  if (pl.grid_time) {
+    mv_time_kernel<P, R><<<dim3(pl.grid_time, (pl.time.nout + R * MV_CY - 1) / (R * MV_CY)), dim3(32, MV_CY), 0, pl.stream>>>(pl.time);
+    ++*launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (pl.grid_dir) {
+    const dim3 g(pl.grid_dir, (pl.dir.n + R * MV_CY - 1) / (R * MV_CY));
+    if (pl.d == 1) mv_dir_kernel<P, R, true><<<g, dim3(32, MV_CY), 0, pl.stream>>>(pl.dir);
+    else mv_dir_kernel<P, R, false><<<g, dim3(32, MV_CY), 0, pl.stream>>>(pl.dir);
+    ++*launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (pl.d >= 2 && pl.grid_plane) {
+    static bool attr[2] = {false, false};
+    const int ph = pl.d == 3;
+    if (!attr[ph]) {
+      e = ph ? cudaFuncSetAttribute(mv_plane_kernel<P, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)
+             : cudaFuncSetAttribute(mv_plane_kernel<P, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      if (e != cudaSuccess) return e;
+      attr[ph] = true;
+    }
+    if (ph) mv_plane_kernel<P, R, true><<<pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream>>>(pl.plane);
+    else mv_plane_kernel<P, R, false><<<pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream>>>(pl.plane);
+    ++*launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t mv2_run(int p, const MV2Plan& plan, int64_t* launches) {
+  switch (p) {
+    case 2: return run_p<2>(plan, launches);
+    case 3: return run_p<3>(plan, launches);
+    case 4: return run_p<4>(plan, launches);
+    case 5: return run_p<5>(plan, launches);
+    case 6: return run_p<6>(plan, launches);
+    case 7: return run_p<7>(plan, launches);
+    case 8: return run_p<8>(plan, launches);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ls

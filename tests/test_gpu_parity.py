@@ -85,6 +85,30 @@ def test_fd_apply_matches_oracle(torch_cuda, d, p, n_elems, seed):
     assert np.max(np.abs(z - z_ref)) <= TOL * np.abs(z_ref).max()
 
 
+VARIANT_CASES = FD_CASES + [
+    (3, 6, [9, 7, 12, 10]),     # Q = 13 odd, n_t = 15
+    (2, 2, [130, 7, 129]),      # n_1 = 130 (register-direct bucket), odd Q, n_t = 130
+    (3, 2, [128, 3, 2, 131]),   # n_1 = 128, n_t = 132: FAST strided time mode (Q % 4 == 0)
+    (1, 3, [130, 131]),         # d = 1, n = 131 / 133
+]
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("d,p,n_elems", VARIANT_CASES)
+def test_fd_apply_kernel_variants(torch_cuda, variant, d, p, n_elems):
+    """Both FD mode-kernel families (ls_tune knob 1: 1 = smem-staged, 2 = register-
+    direct) against the oracle, whatever the automatic dispatch picks."""
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    ctx.tune(1, variant)
+    _, _, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 11)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    z_ref = fd.fd_apply(r, fdd)
+    assert _rel(z, z_ref) <= TOL
+    assert np.max(np.abs(z - z_ref)) <= TOL * np.abs(z_ref).max()
+
+
 def test_fd_apply_config1_dense_solve(torch_cuda):
     """BASELINE config 1: one fd_apply against a dense Kronecker solve of P."""
     import scipy.linalg
@@ -119,6 +143,30 @@ MV_CASES = [
     (3, 2, [3, 4, 5, 6]),
     (3, 5, [7, 6, 9, 8]),
 ]
+
+
+MV_VARIANT_CASES = MV_CASES + [
+    (3, 6, [20, 11, 9, 14]),     # interior Toeplitz zones in every direction, p = 6
+    (3, 8, [3, 40, 2, 33]),      # n < 2p + 1 in two directions (no interior zone)
+    (2, 5, [60, 1, 37]),         # n_2 = 4
+    (3, 3, [64, 5, 6, 7]),       # n_1 = 65
+    (3, 2, [128, 3, 31, 2]),     # n_1 = 128, n_t = 3 < 2p + 1
+]
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("d,p,n_elems", MV_VARIANT_CASES)
+def test_matvec_variants_match_oracle(torch_cuda, variant, d, p, n_elems):
+    """Both ls_matvec implementations (ls_tune knob 2: 1 = four banded passes,
+    2 = three fused passes with Toeplitz stencils + boundary corrections)."""
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    ctx.tune(2, variant)
+    space, tf, _ = _oracle(d, p, n_elems)
+    x = synth.residual(ctx.shape, 9)
+    y_ref = op.apply_A(x, space, tf)
+    y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert _rel(y, y_ref) <= 1e-12
 
 
 @pytest.mark.parametrize("d,p,n_elems", MV_CASES)
