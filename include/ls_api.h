@@ -203,7 +203,8 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  *                      2 = register-direct DMMA mode kernel.
  *   LS_TUNE_MATVEC:    0 = automatic per degree (default),
  *                      1 = four banded passes, 152 B/DOF,
- *                      2 = three fused banded passes (Toeplitz stencils), 96 B/DOF.
+ *                      2 = three fused banded passes (Toeplitz stencils), 96 B/DOF,
+ *                      3 = four banded passes on the FP64 tensor pipe (DMMA).
  * Errors: LS_EINVAL for an unknown knob or value.
  */
 #define LS_TUNE_FD_KERNEL 1

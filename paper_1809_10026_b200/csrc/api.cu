@@ -17,6 +17,7 @@
 #include "fd_rd_launch.cuh"
 #include "matvec_kernels.cuh"
 #include "matvec2_kernels.cuh"
+#include "matvec3_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 
@@ -66,6 +67,9 @@ struct ls_ctx {
     int lo = 0, hi = 0;
   };
   DirSplit dsplit[3], tsplit;
+  // matvec v3: band blocks in DMMA A-fragment order per direction (matvec3_kernels.cuh)
+  double* frag_dir[3] = {nullptr, nullptr, nullptr};  // mats M, J, K, 2K
+  double* frag_time = nullptr;                        // mats K_t, M_t
 
   // host copies (introspection)
   std::vector<double> hM[3], hK[3], hJ[3], hMt, hKt, hlam[4], hU[4];
@@ -361,6 +365,23 @@ static int make_split(ls_ctx* ctx, const std::vector<double>* const* mats, int n
   return LS_OK;
 }
 
+// band blocks of `nm` matrices in m8n8k4 A-fragment order for matvec v3:
+// out[((m*MT + mt)*NKB + j)*32 + l] = scale[m] * W_m[8mt + l/4][4(2mt - OFF + j) + l%4]
+static int make_frags(ls_ctx* ctx, const std::vector<double>* const* mats, const double* scale, int nm,
+                      int n, int p, double** out) {
+  const int MT = (n + 7) / 8, NKB = mv3_nkb(p), OFF = mv3_off(p);
+  std::vector<double> f(size_t(nm) * MT * NKB * 32, 0.0);
+  for (int m = 0; m < nm; ++m)
+    for (int mt = 0; mt < MT; ++mt)
+      for (int j = 0; j < NKB; ++j)
+        for (int l = 0; l < 32; ++l) {
+          const int row = 8 * mt + l / 4, col = 4 * (2 * mt - OFF + j) + l % 4;
+          if (row < n && col >= 0 && col < n && std::abs(row - col) <= p)
+            f[((size_t(m) * MT + mt) * NKB + j) * 32 + l] = scale[m] * (*mats[m])[size_t(row) * n + col];
+        }
+  return upload(ctx, f, out);
+}
+
 static int setup_common(ls_ctx* ctx) {
   const int d = ctx->d, p = ctx->p;
   int dev = 0;
@@ -437,6 +458,17 @@ static int setup_common(ls_ctx* ctx) {
   {
     const std::vector<double>* mats[2] = {&ctx->hMt, &ctx->hKt};
     LS_CHECK(make_split(ctx, mats, 2, ctx->nt, p, ctx->tsplit, false));
+  }
+  // matvec v3 band fragments
+  for (int k = 0; k < d; ++k) {
+    const std::vector<double>* mats[4] = {&ctx->hM[k], &ctx->hJ[k], &ctx->hK[k], &ctx->hK[k]};
+    const double scale[4] = {1.0, 1.0, 1.0, 2.0};
+    LS_CHECK(make_frags(ctx, mats, scale, 4, ctx->n[k], p, &ctx->frag_dir[k]));
+  }
+  {
+    const std::vector<double>* mats[2] = {&ctx->hKt, &ctx->hMt};
+    const double scale[2] = {1.0, 1.0};
+    LS_CHECK(make_frags(ctx, mats, scale, 2, ctx->nt, p, &ctx->frag_time));
   }
   // workspaces (halo rows for the distributed matvec: p slices each side)
   const size_t halo = size_t(2 * p) * ctx->Ns;
@@ -815,10 +847,117 @@ static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   return LS_OK;
 }
 
+// ---- matvec v3 (matvec3_kernels.cuh): DMMA band passes time -> d -> ... -> 1 ----------
+static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
+                      int64_t t_first, int64_t nout) {
+  const int d = ctx->d, P = ctx->p;
+  if (P < 2 || P > 8) return LS_ENOTSUP;
+  double* Kx = ctx->tmp[0];
+  double* Mx = ctx->tmp[1];
+  double* A = ctx->tmp[2];
+  double* B = ctx->tmp[3];
+  double* C = ctx->tmp[4];
+  MV3Pass ps[4];
+  int np = 0;
+  {  // time
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = MV3_TIME;
+    q.mode1 = false;
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_time;
+    a.in[0] = x;
+    a.out[0] = Kx;
+    a.out[1] = Mx;
+    a.n = ctx->nt;
+    a.mt = (ctx->nt + 7) / 8;
+    a.Q = uint32_t(ctx->Ns);
+    a.ncols = uint32_t(ctx->Ns);
+    a.s_first = int(s_first);
+    a.s_rows = int(rows);
+    a.t_first = int(t_first);
+    a.nout = int(nout);
+    a.mt0 = int(t_first / 8);
+    a.mt1 = int((t_first + nout + 7) / 8);
+  }
+  const int kd = d - 1;
+  uint64_t Q = 1;
+  for (int j = 0; j < kd; ++j) Q *= ctx->n[j];
+  {  // direction d
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = (d == 1) ? MV3_DIR_A : MV3_DIR;
+    q.mode1 = (d == 1);
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_dir[kd];
+    a.in[0] = Kx;
+    a.in[1] = Mx;
+    a.out[0] = (d == 1) ? y : A;
+    a.out[1] = B;
+    a.out[2] = C;
+    const int64_t tT = (ctx->nt - 1) - t_first;
+    const bool own_last = tT >= 0 && tT < nout;
+    a.tT = own_last ? int(tT) : -1;
+    a.xT = own_last ? x + (ctx->nt - 1 - s_first) * ctx->Ns : nullptr;
+    a.n = ctx->n[kd];
+    a.mt = (a.n + 7) / 8;
+    a.Q = uint32_t(Q);
+    a.ncols = uint32_t(uint64_t(nout) * Q);
+    a.mt0 = 0;
+    a.mt1 = a.mt;
+  }
+  const double* cur[3] = {A, B, C};
+  if (d == 3) {  // direction 2: (A, B, C) -> (A2, B2, C2) in Kx, Mx, tmp[5]
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = MV3_MID;
+    q.mode1 = false;
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_dir[1];
+    for (int m = 0; m < 3; ++m) a.in[m] = cur[m];
+    a.out[0] = Kx;
+    a.out[1] = Mx;
+    a.out[2] = ctx->tmp[5];
+    a.n = ctx->n[1];
+    a.mt = (a.n + 7) / 8;
+    a.Q = uint32_t(ctx->n[0]);
+    a.ncols = uint32_t(uint64_t(nout) * ctx->n[2] * ctx->n[0]);
+    a.tT = -1;
+    a.mt0 = 0;
+    a.mt1 = a.mt;
+    cur[0] = Kx;
+    cur[1] = Mx;
+    cur[2] = ctx->tmp[5];
+  }
+  if (d >= 2) {  // direction 1: y = M A + J B + K C
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = MV3_LAST;
+    q.mode1 = true;
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_dir[0];
+    for (int m = 0; m < 3; ++m) a.in[m] = cur[m];
+    a.out[0] = y;
+    a.n = ctx->n[0];
+    a.mt = (a.n + 7) / 8;
+    a.Q = 1;
+    a.ncols = uint32_t(uint64_t(nout) * (ctx->Ns / ctx->n[0]));
+    a.tT = -1;
+    a.mt0 = 0;
+    a.mt1 = a.mt;
+  }
+  LS_CUDA(mv3_run(P, ps, np, ctx->num_sms, ctx->stream, &ctx->launches));
+  return LS_OK;
+}
+
 static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
                       int64_t t_first, int64_t nout) {
-  // auto (measured, tools/mv_variants.py, r01): v2 wins at p = 2 only (config 5 p=2: 2.74 vs
-  // 3.07 ms); at p >= 3 its passes are latency-bound and v1 is faster (config 4: 16.3 vs 19.5 ms)
+  // auto (measured, tools/mv_variants.py, r01):
+  //   p = 2:  v2 (config 5 p=2: 2.74 ms vs v1 3.07, v3 3.30)
+  //   p = 3, 4: v1 (config 3: 0.81 ms vs v3 1.06, v2 1.16)
+  //   p >= 5: v3, DMMA band passes (config 4: 12.8 ms vs v1 16.4; config 5 p=8: 5.28 vs 6.49)
+  if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 5))
+    return mv3_launch(ctx, x, y, rows, s_first, t_first, nout);
   const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2);
   if (!v2) return matvec_block(ctx, x, y, rows, s_first, t_first, nout);
   return mv2_launch(ctx, x, y, rows, s_first, t_first, nout);
@@ -1066,7 +1205,7 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       ctx->fd_variant = value;
       return LS_OK;
     case LS_TUNE_MATVEC:
-      if (value < 0 || value > 2) return LS_EINVAL;
+      if (value < 0 || value > 3) return LS_EINVAL;
       ctx->mv_variant = value;
       return LS_OK;
     default: return LS_EINVAL;

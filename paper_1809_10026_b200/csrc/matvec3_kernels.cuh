@@ -1,0 +1,283 @@
+// Matrix-free y = A x (eq:A_kron, PAPER.md 686-703), v3: the banded univariate
+// products on the FP64 tensor pipe (DMMA.8x8x4), one streaming pass per direction.
+//
+// Order of the passes (the triple recursion of matvec2_kernels.cuh):
+//     time:         Kx = K_t x,  Mx = M_t x
+//     direction d:  A = M Kx + J Mx (+ K xT),  B = M Mx,  C = 2K Mx (+ M xT)
+//                   (xT = x on the last time slice: the W_t = e e^T term)
+//     directions d-1 .. 2:  A <- M A + J B + K C,  B <- M B,  C <- 2K B + M C
+//     direction 1:  y = M A + J B + K C
+// (d = 1: the direction-d pass writes y = A.)
+//
+// Band product as DMMA.  A pass computes Y = W X along its direction for band
+// matrices W of half-bandwidth P: the 8 output rows of m-tile mt need input rows
+// [8mt - P, 8mt + 7 + P], i.e. the NKB k-steps 2mt - OFF .. 2mt - OFF + NKB - 1
+// (OFF = 1, NKB = 4 for P <= 4; OFF = 2, NKB = 6 for P <= 8).  The band blocks are
+// precomputed on the host in m8n8k4 A-fragment order ([mat][mt][j][lane]) and
+// staged in shared memory once per CTA.  A warp owns a strip of 8*NT columns and
+// sweeps it top to bottom: B fragments (4 rows x 8 columns per k-step) come from
+// global memory into a register ring of RING = NKB + 4 k-steps, refilled two
+// m-tiles ahead (the m-tile loop is unrolled by RING/2 so ring slots are static);
+// each m-tile's accumulators are complete after its NKB k-steps and are stored
+// at once, so only one m-tile of accumulators is live.  Column permutation as in
+// fd_rd_kernel.cuh: lane l holds columns NT*(l/4) .. +NT-1 for its B loads
+// (LDG.128 when FAST) and columns 2NT*(l%4) .. +2NT-1 for its stores.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fd_kernels.cuh"  // dmma_8x8x4
+
+namespace ls {
+
+enum MV3Kind { MV3_TIME = 0, MV3_DIR = 1, MV3_DIR_A = 2, MV3_MID = 3, MV3_LAST = 4 };
+
+struct MV3Args {
+  const double* frag;  // [nmat][MT][NKB][32] band A-fragments of this pass' direction
+  const double* in[3];
+  double* out[3];
+  const double* xT;    // MV3_DIR*: x of the last time slice, same [n][Q] layout as one slice
+  int n;               // extent of the pass direction (band rows)
+  int mt;              // m-tiles = ceil(n / 8)
+  int nmat;
+  uint32_t Q;          // row stride (product of the faster extents; 1 = contiguous mode)
+  uint32_t ncols;      // columns = P_slow * Q
+  int tT;              // MV3_DIR*: index of the last time slice among the P_slow slices (or -1)
+  // time pass with a halo-extended input: input rows [s_first, s_first + s_rows) of the
+  // band, output rows [t_first, t_first + nout)
+  int s_first, s_rows, t_first, nout;
+  int mt0, mt1;        // m-tile range swept (time pass: the tiles covering the output rows)
+};
+
+template <int KIND>
+struct MV3IO {
+  // ring inputs (the xT input of the direction-d pass is loaded without the ring: only
+  // the warps holding last-slice columns need it)
+  static constexpr int NIN = (KIND == MV3_TIME) ? 1 : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? 2 : 3;
+  static constexpr int NOUT = (KIND == MV3_TIME) ? 2 : (KIND == MV3_DIR || KIND == MV3_MID) ? 3 : 1;
+  static constexpr int NMAT = (KIND == MV3_TIME) ? 2 : (KIND == MV3_LAST) ? 3 : 4;
+};
+
+template <int P, int KIND>
+struct MV3Geom {
+  static constexpr int OFF = P <= 4 ? 1 : 2;
+  static constexpr int NKB = P <= 4 ? 4 : 6;
+  // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 3 for 2, 2 for 3
+  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : MV3IO<KIND>::NIN == 2 ? 3 : 2;
+  static constexpr int RING = NKB + 2 * AHEAD;
+  static constexpr int G = RING / 2;  // m-tiles per unrolled group
+};
+
+__device__ __forceinline__ double mv3_ld(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 mv3_ld2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+template <int P, int NT, int KIND, bool MODE1, bool FAST>
+__global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant__ MV3Args a) {
+  using Gm = MV3Geom<P, KIND>;
+  using IO = MV3IO<KIND>;
+  constexpr int NKB = Gm::NKB, OFF = Gm::OFF, RING = Gm::RING, G = Gm::G;
+  constexpr int NIN = IO::NIN, NOUT = IO::NOUT;
+  constexpr int TW = 8 * NT;
+  extern __shared__ __align__(16) double fsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, nq = lane >> 2;
+  const int MT = a.mt;
+  const int nfrag = IO::NMAT * MT * NKB * 32;
+  for (int e = tid; e < nfrag; e += 256) fsm[e] = __ldg(a.frag + e);
+  __syncthreads();
+  const int n = a.n;
+  const uint32_t Q = a.Q, ncols = a.ncols;
+  const uint32_t nstrips = (ncols + TW - 1) / TW;
+  // time pass: band row of stored input row 0 / of output row 0
+  const int gin0 = (KIND == MV3_TIME) ? a.s_first : 0;
+  const int in_rows = (KIND == MV3_TIME) ? a.s_rows : n;
+  const int gout0 = (KIND == MV3_TIME) ? a.t_first : 0;
+  const int nout = (KIND == MV3_TIME) ? a.nout : n;
+  const size_t rstride = MODE1 ? 1 : size_t(Q);
+
+  for (uint32_t strip = blockIdx.x * 8 + warp; strip < nstrips; strip += gridDim.x * 8) {
+    // ---- this lane's B columns (NT) and store columns (2NT)
+    const uint32_t cb = strip * TW + NT * nq;  // first B column
+    uint32_t boff[NT];  // element offset of (row 0, column) per B column
+    uint32_t bmask = 0;
+    bool is_last = false;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const uint32_t c = cb + j;
+      boff[j] = 0;
+      if (c < ncols) {
+        bmask |= 1u << j;
+        const uint32_t pt = c / Q, q = c - pt * Q;
+        boff[j] = MODE1 ? c * uint32_t(n) : pt * uint32_t(in_rows) * Q + q;
+        if (KIND == MV3_DIR || KIND == MV3_DIR_A) is_last |= int(pt) == a.tT;
+      }
+    }
+    // W_t term: only warps holding a column of the last time slice do the xT products
+    const bool warp_last = (KIND == MV3_DIR || KIND == MV3_DIR_A) && __any_sync(0xffffffffu, is_last);
+    // B fragment of input m, k-step ks (rows 4ks + kq) -> v[NT]
+    auto loadB = [&](double (&v)[NT], int m, int ks) {
+      const int row = 4 * ks + kq;           // band row
+      const int sr = row - gin0;              // stored row
+      const bool rok = row >= 0 && row < n && sr >= 0 && sr < in_rows;
+      const double* src = (m == 2 && (KIND == MV3_DIR || KIND == MV3_DIR_A)) ? a.xT : a.in[m];
+      if (FAST) {
+        const bool ok = rok && bmask && (m != 2 || (KIND != MV3_DIR && KIND != MV3_DIR_A) || is_last);
+        const size_t off = (m == 2 && (KIND == MV3_DIR || KIND == MV3_DIR_A))
+                               ? size_t(boff[0] % Q)  // xT is one slice: (row, q)
+                               : size_t(boff[0]);
+#pragma unroll
+        for (int j = 0; j < NT; j += 2) {
+          double2 t = make_double2(0.0, 0.0);
+          if (ok) t = mv3_ld2(src + off + size_t(sr) * rstride + j);
+          v[j] = t.x;
+          v[j + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          bool ok = rok && ((bmask >> j) & 1u);
+          size_t off = boff[j];
+          if (m == 2 && (KIND == MV3_DIR || KIND == MV3_DIR_A)) {
+            const uint32_t c = cb + j;
+            const uint32_t pt = c / Q;
+            ok = ok && int(pt) == a.tT;
+            off = c - pt * Q;
+          }
+          v[j] = ok ? mv3_ld(src + off + size_t(sr) * rstride) : 0.0;
+        }
+      }
+    };
+    double ring[NIN][RING][NT];
+    // prologue: k-steps 2 mt0 - OFF + s into slots s = 0 .. RING-1
+    const int mt0 = a.mt0, mt1 = a.mt1;
+#pragma unroll
+    for (int m = 0; m < NIN; ++m)
+#pragma unroll
+      for (int s = 0; s < RING; ++s) loadB(ring[m][s], m, 2 * mt0 - OFF + s);
+
+    const uint32_t cs = strip * TW + 2 * NT * kq;  // first store column
+    for (int g0 = mt0; g0 < mt1; g0 += G) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int mt = g0 + u;
+        if (mt < mt1) {
+          double acc[NOUT][NT][2];
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[o][j][0] = acc[o][j][1] = 0.0;
+          // sum over the NKB band k-steps: acc[o] += W_mat * ring[in]
+#pragma unroll
+          for (int jk = 0; jk < NKB; ++jk) {
+            const int slot = (2 * u + jk) % RING;
+            auto fr = [&](int mat) { return fsm[((mat * MT + mt) * NKB + jk) * 32 + lane]; };
+            auto mma = [&](int o, int mat, int in) {
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[o][j], fr(mat), ring[in][slot][j]);
+            };
+            if (KIND == MV3_TIME) {          // mats: 0 K_t, 1 M_t
+              mma(0, 0, 0);
+              mma(1, 1, 0);
+            } else if (KIND == MV3_DIR || KIND == MV3_DIR_A) {  // mats: 0 M, 1 J, 2 K, 3 2K; in: Kx, Mx
+              mma(0, 0, 0);
+              mma(0, 1, 1);
+              if (KIND == MV3_DIR) {
+                mma(1, 0, 1);
+                mma(2, 3, 1);
+              }
+              if (warp_last) {  // W_t term: xT fragments loaded directly (rare warps)
+                double xv[NT];
+                loadB(xv, 2, 2 * mt - OFF + jk);
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[0][j], fr(2), xv[j]);
+                if (KIND == MV3_DIR) {
+#pragma unroll
+                  for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[2][j], fr(0), xv[j]);
+                }
+              }
+            } else if (KIND == MV3_MID) {    // mats: 0 M, 1 J, 2 K, 3 2K; in: A, B, C
+              mma(0, 0, 0);
+              mma(0, 1, 1);
+              mma(0, 2, 2);
+              mma(1, 0, 1);
+              mma(2, 3, 1);
+              mma(2, 0, 2);
+            } else {                         // MV3_LAST, mats: 0 M, 1 J, 2 K
+              mma(0, 0, 0);
+              mma(0, 1, 1);
+              mma(0, 2, 2);
+            }
+          }
+          // refill the two consumed slots with k-steps two m-tiles ahead
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int slot = (2 * u + h) % RING;
+            const int ks = 2 * (mt - mt0) - OFF + h + RING + 2 * mt0;
+#pragma unroll
+            for (int m = 0; m < NIN; ++m) loadB(ring[m][slot], m, ks);
+          }
+          // ---- store m-tile mt: rows 8mt + nq, columns cs .. cs + 2NT - 1
+          const int lrow = 8 * mt + nq - gout0;  // local output row (time pass: slab rows)
+          const int brow = 8 * mt + nq;
+          if (brow < n && lrow >= 0 && lrow < nout) {
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) {
+              double* Y = a.out[o];
+              if (FAST) {
+                if (cs < ncols) {
+                  const uint32_t pt = cs / Q, q = cs - pt * Q;
+                  double* dst = Y + (size_t(pt) * nout + lrow) * Q + q;
+                  // accumulator column 2kq + h of n-tile j = physical column cs + NT*h + j
+#pragma unroll
+                  for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int j = 0; j < NT; j += 2)
+                      *reinterpret_cast<double2*>(dst + NT * h + j) = make_double2(acc[o][j][h], acc[o][j + 1][h]);
+                }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                  for (int j = 0; j < NT; ++j) {
+                    const uint32_t c = cs + NT * h + j;
+                    if (c < ncols) {
+                      size_t o_off;
+                      if (MODE1) {
+                        o_off = size_t(c) * n + lrow;
+                      } else {
+                        const uint32_t pt = c / Q, q = c - pt * Q;
+                        o_off = (size_t(pt) * nout + lrow) * Q + q;
+                      }
+                      Y[o_off] = acc[o][j][h];
+                    }
+                  }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// host-side launch (mv3.cu)
+struct MV3Pass {
+  MV3Args args;
+  int kind;
+  bool mode1;
+};
+// p: spline degree; returns the CUDA error; *launches += kernels launched
+cudaError_t mv3_run(int p, const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
+size_t mv3_frag_count(int p, int n, int nmat);  // doubles of one direction's fragment array
+int mv3_nkb(int p);
+int mv3_off(int p);
+
+}  // namespace ls

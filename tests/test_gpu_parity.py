@@ -154,7 +154,7 @@ MV_VARIANT_CASES = MV_CASES + [
 ]
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 @pytest.mark.parametrize("d,p,n_elems", MV_VARIANT_CASES)
 def test_matvec_variants_match_oracle(torch_cuda, variant, d, p, n_elems):
     """Both ls_matvec implementations (ls_tune knob 2: 1 = four banded passes,

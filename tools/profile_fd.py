@@ -20,10 +20,14 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--matvec", action="store_true")
 ap.add_argument("--pcg", action="store_true")
 ap.add_argument("--p", type=int, default=None)
+ap.add_argument("--mv", type=int, default=0, help="ls_tune matvec variant")
+ap.add_argument("--fdk", type=int, default=0, help="ls_tune FD kernel variant")
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = a.p if a.p is not None else (c["p"] if isinstance(c["p"], int) else c["p"][0])
 ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
+ctx.tune(2, a.mv)
+ctx.tune(1, a.fdk)
 r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 z = torch.empty_like(r)
 if a.pcg:
