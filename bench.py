@@ -355,7 +355,7 @@ def run_extras(ls, torch, stream):
     ctx.close()
     del flush
     pcg = []
-    for cfg, p, kind in ((2, 3, 0), (5, 2, 1), (5, 4, 1), (5, 8, 1)):
+    for cfg, p, kind in ((2, 3, 0), (5, 2, 1), (5, 4, 1), (5, 8, 1), (4, 6, 1)):
         n_el = synth.CONFIGS[cfg]["n_el"]
         d = synth.CONFIGS[cfg]["d"]
         c = ls.Context(d, p, [n_el] * (d + 1))
@@ -366,8 +366,21 @@ def run_extras(ls, torch, stream):
         t0 = time.perf_counter()
         x, st = c.pcg(b, tol=1e-8)
         torch.cuda.synchronize()
+        solve_ms = (time.perf_counter() - t0) * 1e3
+        # per-iteration split: one fd_apply and one matvec timed with CUDA events
+        z = torch.empty_like(b)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        c.fd_apply(b, z)
+        ev[1].record(stream)
+        c.matvec(b, z)
+        ev[2].record(stream)
+        ev[2].synchronize()
         pcg.append({"config": cfg, "d": d, "p": p, "n_el": n_el, "N": c.N, "iters": st["iters"],
-                    "solve_ms": (time.perf_counter() - t0) * 1e3, "true_rel_res": st["true_rel_res"]})
+                    "solve_ms": solve_ms, "true_rel_res": st["true_rel_res"],
+                    "fd_apply_ms": ev[0].elapsed_time(ev[1]), "matvec_ms": ev[1].elapsed_time(ev[2]),
+                    "rhs": "kind %d (DESIGN.md reading c11)" % kind})
+        del z
         c.close()
         del b, x
     out["pcg"] = pcg

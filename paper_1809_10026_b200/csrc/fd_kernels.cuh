@@ -58,9 +58,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// 1/d for d > 0 (the FD divisor lambda_t + Lambda_s, >= 2.4): FP32 MUFU.RCP seed
+// (~2^-22 relative) + two Newton steps in FP64 (~2^-44, then below fp64 rounding).
+// The FP64 seed (rcp.approx.f64 -> MUFU.RCP64H) measured ~30% slower for the whole
+// scaled time-mode launch (profiles/r01 launch list: 3.25 vs 2.52 ms unscaled).
 __device__ __forceinline__ double fast_rcp(double d) {
-  double x;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(x) : "d"(d));
+  float xf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(xf) : "f"(__double2float_rn(d)));
+  double x = double(xf);
   double e = fma(-d, x, 1.0);
   x = fma(x, e, x);
   e = fma(-d, x, 1.0);

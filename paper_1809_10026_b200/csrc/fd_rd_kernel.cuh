@@ -45,7 +45,8 @@ struct RDCfg {
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int TW = 8 * NT;  // columns per warp tile
   static constexpr int WFRAG = MT * KSP * 64;
-  static constexpr size_t SMEM = size_t(WFRAG) * sizeof(double);
+  static constexpr int LAMA = SCALE ? 8 * MT : 0;  // lambda_t per output row (SCALE)
+  static constexpr size_t SMEM = size_t(WFRAG + LAMA) * sizeof(double);
   static_assert(!(MODE1 && FAST), "FAST is a strided-mode path");
   static_assert(NT % 2 == 0, "NT even (LDG.128 pairs)");
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -147,6 +148,9 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
     const int a = mt * 8 + (l >> 2), i = ks * 4 + (l & 3);
     wsm[e] = (a < n && i < n && ks < C::KS) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
   }
+  double* lam_a_s = wsm + C::WFRAG;  // SCALE: lambda_t of the output rows, staged once
+  if (C::SCALE)
+    for (int e = tid; e < C::LAMA; e += C::THREADS) lam_a_s[e] = e < n ? __ldg(args.lam_a + e) : 0.0;
   __syncthreads();
 
   const uint32_t ntw = (ncols + C::TW - 1) / C::TW;
@@ -166,6 +170,13 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
 #pragma unroll 1
   for (; tile < ntw; tile += wstride) {
     const RDIn<C::NT> nxt = rd_make_in<C>(args, tile + wstride, lane);
+    // SCALE: this lane's Lambda_s columns, loaded before the k-loop (latency hidden)
+    const uint32_t cg = tile * C::TW + 2 * C::NT * kq;
+    double lc[C::SCALE ? 2 * C::NT : 1];
+    if (C::SCALE) {
+#pragma unroll
+      for (int e = 0; e < 2 * C::NT; ++e) lc[e] = (cg + e < ncols) ? __ldg(args.lam_c + cg + e) : 0.0;
+    }
     double acc[C::MT][C::NT][2];
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
@@ -204,12 +215,6 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
     }
 
     // ---- epilogue: lane's columns cg .. cg + 2NT - 1, rows mt*8 + nq
-    const uint32_t cg = tile * C::TW + 2 * C::NT * kq;
-    double lc[C::SCALE ? 2 * C::NT : 1];
-    if (C::SCALE) {
-#pragma unroll
-      for (int e = 0; e < 2 * C::NT; ++e) lc[e] = (cg + e < ncols) ? __ldg(args.lam_c + cg + e) : 0.0;
-    }
     if (C::FAST) {
       if (cg < ncols) {
         const uint32_t p = cg / Q, q = cg - p * Q;
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
 #pragma unroll
               for (int j = 0; j < C::NT; ++j) v[h * C::NT + j] = acc[mt][j][h];
             if (C::SCALE) {
-              const double la = __ldg(args.lam_a + a);
+              const double la = lam_a_s[a];
 #pragma unroll
               for (int e = 0; e < 2 * C::NT; ++e) v[e] *= fast_rcp(la + lc[C::SCALE ? e : 0]);
             }
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
         const int a = mt * 8 + nq;
         if (a < n) {
           double la = 0.0;
-          if (C::SCALE) la = __ldg(args.lam_a + a);
+          if (C::SCALE) la = lam_a_s[a];
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
