@@ -115,12 +115,35 @@ int ls_set_stream(ls_ctx* ctx, void* cuda_stream);
 int fd_apply(ls_ctx* ctx, const double* r, double* z);
 
 /*
+ * fd_apply_stage -- one stage of fd_apply on a caller-chosen piece, i.e. what every rank
+ * of ls_setup_dist runs between its all-to-alls (for custom decompositions):
+ *   stage 0: forward spatial modes  X x_1 U_1^T .. x_d U_d^T  on a = #time slices of
+ *            in/out ([a][N_s], 1 <= a <= slab length);  stage 2: backward (U_d .. U_1);
+ *   stage 1: time mode of a spatial chunk [n_t][b] whose first spatial index is a:
+ *            U_t^T, divide by lambda_t[i_t] + Lambda_s[a + j] (Alg. 1 step 3), U_t.
+ * in and out must not overlap.  Asynchronous.  Errors: LS_EINVAL.
+ */
+int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* out, int64_t a, int64_t b);
+
+/*
  * ls_matvec -- y = A x, A = K_t (x) M_s + M_t (x) J_s + W_t (x) L_s
  * (eq:A_kron, PAPER.md 686-703), matrix-free and sum-factorised on the banded
  * univariate factors (identity map).  x, y: device vectors, y != x.
  * Asynchronous on the context stream.
  */
 int ls_matvec(ls_ctx* ctx, const double* x, double* y);
+
+/*
+ * ls_matvec_slab -- the slab-local kernel of ls_matvec (the part every rank runs after
+ * its halo exchange), exposed so a caller can drive its own time decomposition:
+ * y = rows [t_first, t_first + nout) of A x, given the rows [s_first, s_first + s_rows)
+ * of x in x_ext ([s_rows][N_s], device).  The stored rows must include the time band
+ * of the outputs, [max(0, t_first - p), min(n_t, t_first + nout + p)); nout must not
+ * exceed this context's slab length and s_rows its slab length + 2p.  y: [nout][N_s]
+ * device.  Asynchronous.  Errors: LS_EINVAL (geometry), LS_ENOTSUP (p > 8).
+ */
+int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows, double* y,
+                   int64_t t_first, int64_t nout);
 
 /*
  * ls_rhs -- b_i = F(B_i) = int int f (d_t B_i - Lap B_i) (PAPER.md 409) for a

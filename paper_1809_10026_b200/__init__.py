@@ -30,7 +30,8 @@ LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_E
 EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
             "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
-            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune"]
+            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
+            "ls_matvec_slab", "fd_apply_stage"]
 
 
 class PCGStats(ctypes.Structure):
@@ -79,6 +80,9 @@ def load_library(path=LIB_PATH):
                                            ctypes.POINTER(ctypes.c_double), i64p]),
         "ls_destroy": (None, [vp]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
+        "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
+        "ls_matvec_slab": (ctypes.c_int, [vp, dp, ctypes.c_int64, ctypes.c_int64, dp, ctypes.c_int64,
+                                          ctypes.c_int64]),
         "ls_partition": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
         "ls_a2a_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                        i64p, i64p, i64p, i64p]),
@@ -204,6 +208,30 @@ class Context:
         """y = A x (eq:A_kron, PAPER.md 686-703)."""
         y = self._new() if y is None else y
         _check(self._lib.ls_matvec(self._h, self._dev(x, "x"), self._dev(y, "y")), "ls_matvec")
+        return y
+
+    def fd_stage(self, stage, inp, out, a, b=0):
+        """fd_apply_stage: 0/2 = forward/backward spatial modes on `a` time slices,
+        1 = time mode of a spatial chunk [n_t][b] at spatial offset a."""
+        torch = self._torch
+        for t, nm in ((inp, "in"), (out, "out")):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise TypeError(f"{nm} must be a contiguous float64 CUDA tensor")
+        _check(self._lib.fd_apply_stage(self._h, int(stage), ctypes.c_void_p(inp.data_ptr()),
+                                        ctypes.c_void_p(out.data_ptr()), int(a), int(b)), "fd_apply_stage")
+        return out
+
+    def matvec_slab(self, x_ext, s_first, t_first, nout, y=None):
+        """Rows [t_first, t_first + nout) of A x from the stored rows [s_first, s_first +
+        x_ext.shape[0]) of x (ls_matvec_slab)."""
+        torch = self._torch
+        if not (x_ext.is_cuda and x_ext.dtype == torch.float64 and x_ext.is_contiguous()):
+            raise TypeError("x_ext must be a contiguous float64 CUDA tensor")
+        s_rows = x_ext.shape[0]
+        if y is None:
+            y = torch.empty((nout,) + tuple(self.shape[1:]), dtype=torch.float64, device="cuda")
+        _check(self._lib.ls_matvec_slab(self._h, ctypes.c_void_p(x_ext.data_ptr()), int(s_first), int(s_rows),
+                                        ctypes.c_void_p(y.data_ptr()), int(t_first), int(nout)), "ls_matvec_slab")
         return y
 
     def rhs(self, kind, b=None):

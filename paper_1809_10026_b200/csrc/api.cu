@@ -603,6 +603,26 @@ extern "C" int fd_apply(ls_ctx* ctx, const double* r, double* z) {
   return comm_fd_apply(ctx, r, z);
 }
 
+// the three stages of fd_apply on caller-chosen pieces (what each rank of the distributed
+// path runs between its all-to-alls; exposed for custom decompositions and for testing)
+extern "C" int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* out, int64_t a, int64_t b) {
+  if (!ctx || !in || !out || in == out || !aligned8(in) || !aligned8(out)) return LS_EINVAL;
+  switch (stage) {
+    case 0:
+    case 2: {  // spatial modes (forward / backward) on `a` time slices [a][N_s]
+      if (a < 1 || a > ctx->ntl) return LS_EINVAL;
+      return spatial_modes(ctx, in, out, ctx->tmp[3], ctx->tmp[4], uint64_t(a), stage == 0);
+    }
+    case 1: {  // time mode U_t^T, /(lambda_t + Lambda_s), U_t on a chunk [n_t][b] at spatial offset a
+      if (a < 0 || b < 1 || a + b > ctx->Ns || int64_t(ctx->nt) * b > (ctx->Nl + 2 * ctx->p * ctx->Ns)) return LS_EINVAL;
+      double* mid = ctx->tmp[3];
+      LS_CHECK(launch_mode(ctx, in, mid, ctx->Wf[3], ctx->nt, 1, uint64_t(b), true, ctx->lam[3], ctx->lam_s + a));
+      return launch_mode(ctx, mid, out, ctx->Wb[3], ctx->nt, 1, uint64_t(b), false);
+    }
+    default: return LS_EINVAL;
+  }
+}
+
 // distributed fd_apply: slab -> all-to-all -> time mode on spatial chunks -> all-to-all -> slab
 int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
   Comm& cm = *ctx->comm;
@@ -979,6 +999,20 @@ extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
     LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->p));
   return matvec_any(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
+}
+
+extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows,
+                              double* y, int64_t t_first, int64_t nout) {
+  if (!ctx || !x_ext || !y || !aligned8(x_ext) || !aligned8(y)) return LS_EINVAL;
+  const int64_t nt = ctx->nt, p = ctx->p;
+  if (nout < 0 || t_first < 0 || t_first + nout > nt || s_rows < 0) return LS_EINVAL;
+  if (nout > ctx->ntl) return LS_EINVAL;  // workspaces hold ntl (+ halo) slices
+  // the stored rows must cover the time band of every output row (clipped to [0, n_t))
+  const int64_t need_lo = std::max<int64_t>(0, t_first - p), need_hi = std::min<int64_t>(nt, t_first + nout + p);
+  if (nout > 0 && (s_first > need_lo || s_first + s_rows < need_hi)) return LS_EINVAL;
+  if (s_rows > ctx->ntl + 2 * p) return LS_EINVAL;
+  if (nout == 0) return LS_OK;
+  return matvec_any(ctx, x_ext, y, s_rows, s_first, t_first, nout);
 }
 
 // ------------------------------------------------------------------------------------------

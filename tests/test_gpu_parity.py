@@ -313,3 +313,70 @@ def test_pcg_nonconvergence_status(torch_cuda):
     ctx = _ctx(3, 3, [8, 8, 8, 8])
     x, st = ctx.pcg(ctx.rhs(1), tol=1e-12, max_iter=3)
     assert st["status"] == ls.LS_ENOCONV and st["iters"] == 3 and st["rel_res"] > 1e-12
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("d,p,n_elems,world", [(3, 6, [9, 8, 7, 40], 4), (3, 2, [6, 5, 7, 29], 3),
+                                                (2, 8, [20, 12, 37], 2), (1, 3, [30, 50], 5),
+                                                (3, 3, [12, 10, 8, 61], 8)])
+def test_matvec_slab_decomposition(torch_cuda, variant, d, p, n_elems, world):
+    """The per-rank kernel of the distributed ls_matvec (ls_matvec_slab, time slab plus
+    p halo slices each side, exactly what ls_matvec runs after its NCCL halo exchange),
+    for every rank of a `world`-way split, against the oracle's full A x."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    ctx.tune(2, variant)
+    space, tf, _ = _oracle(d, p, n_elems)
+    x = synth.residual(ctx.shape, 13)
+    y_ref = op.apply_A(x, space, tf)
+    xg = torch.from_numpy(x).cuda()
+    nt = ctx.shape[0]
+    for r in range(world):
+        t0, ntl, lo, hi = ls.halo_plan(nt, world, r, p)
+        x_ext = xg[t0 - lo:t0 + ntl + hi].contiguous()
+        y = ctx.matvec_slab(x_ext, t0 - lo, t0, ntl).cpu().numpy()
+        assert _rel(y, y_ref[t0:t0 + ntl]) <= 1e-12, (r, t0, ntl)
+
+
+@pytest.mark.parametrize("fdk", [1, 2])
+@pytest.mark.parametrize("d,p,n_elems,world", [(3, 3, [8, 7, 6, 21], 4), (2, 6, [30, 25, 40], 3),
+                                                (1, 2, [40, 17], 8), (3, 6, [30, 3, 2, 9], 2)])
+def test_fd_apply_slab_chunk_decomposition(torch_cuda, fdk, d, p, n_elems, world):
+    """The distributed fd_apply of ls_setup_dist emulated rank by rank on one GPU: forward
+    spatial modes on every time slab (stage 0), the slab -> chunk all-to-all done here
+    with the library's own plan (ls_a2a_plan), the fused time mode on every spatial chunk
+    with its Lambda_s offset (stage 1), the transpose all-to-all, backward spatial modes
+    (stage 2); against the oracle's fd_apply of the whole tensor."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    ctx.tune(1, fdk)
+    _, _, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 17)
+    nt = ctx.shape[0]
+    Ns = int(np.prod(ctx.shape[1:]))
+    rg = torch.from_numpy(r).cuda().reshape(nt, Ns)
+    slabs = [ls.partition(nt, world, g) for g in range(world)]
+    chunks = [ls.partition(Ns, world, h) for h in range(world)]
+    fwd = []
+    for (t0, ntl) in slabs:
+        out = torch.empty(ntl, Ns, dtype=torch.float64, device="cuda")
+        ctx.fd_stage(0, rg[t0:t0 + ntl].contiguous(), out, ntl)
+        fwd.append(out)
+    full = torch.cat(fwd)  # the all-to-all, by hand: chunk h = columns [c0, c0 + len) of every slab
+    back = torch.empty_like(full)
+    for (c0, ln) in chunks:
+        if ln == 0:
+            continue
+        ch = full[:, c0:c0 + ln].contiguous()
+        res = torch.empty_like(ch)
+        ctx.fd_stage(1, ch, res, c0, ln)
+        back[:, c0:c0 + ln] = res
+    z = torch.empty_like(back)
+    for (t0, ntl) in slabs:
+        out = torch.empty(ntl, Ns, dtype=torch.float64, device="cuda")
+        ctx.fd_stage(2, back[t0:t0 + ntl].contiguous(), out, ntl)
+        z[t0:t0 + ntl] = out
+    z_ref = fd.fd_apply(r, fdd)
+    assert _rel(z.cpu().numpy().reshape(r.shape), z_ref) <= TOL
