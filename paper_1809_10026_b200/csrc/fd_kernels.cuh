@@ -58,18 +58,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// 1/d for d > 0 (the FD divisor lambda_t + Lambda_s, >= 2.4): FP32 MUFU.RCP seed
-// (~2^-22 relative) + two Newton steps in FP64 (~2^-44, then below fp64 rounding).
-// The FP64 seed (rcp.approx.f64 -> MUFU.RCP64H) measured ~30% slower for the whole
-// scaled time-mode launch (profiles/r01 launch list: 3.25 vs 2.52 ms unscaled).
+// 1/d for d > 0 (the FD divisor lambda_t + Lambda_s >= 2.4): FP32 MUFU.RCP seed (relative
+// error <= 2^-22) and ONE Newton step in FP64, which squares the error to <= 2^-44 ~ 6e-14
+// (c13: rounding-level, far below the 1e-9 parity bar).  Each FP64 op here competes with
+// the DMMAs for the FP64 pipe, so the second Newton step (and the MUFU.RCP64H seed) are
+// not taken.
 __device__ __forceinline__ double fast_rcp(double d) {
   float xf;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(xf) : "f"(__double2float_rn(d)));
-  double x = double(xf);
-  double e = fma(-d, x, 1.0);
-  x = fma(x, e, x);
-  e = fma(-d, x, 1.0);
-  return fma(x, e, x);
+  const double x = double(xf);
+  return fma(x, fma(-d, x, 1.0), x);
 }
 
 constexpr int pad4mod16(int v) {  // smallest s >= v with s % 16 == 4
@@ -496,6 +494,17 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
     // DMMA phase, serialised with the other set: set 0 starts, then alternate
     if (set == 1 || j > 0) named_sync(BAR_MY_TURN, 256);
     const double* t = tiles + stage_of(j) * C::TILE;
+    // SCALE: this lane's Lambda_s columns, loaded before the k-loop (latency hidden)
+    double lcp[C::SCALE ? C::NT : 1][2];
+    if (C::SCALE) {
+      const uint32_t cb = tile_of(j) * C::BN + grp * C::NT * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) {
+        const uint32_t c = cb + nt * 8;
+        lcp[nt][0] = c < ncols ? __ldg(args.lam_c + c) : 0.0;
+        lcp[nt][1] = c + 1 < ncols ? __ldg(args.lam_c + c + 1) : 0.0;
+      }
+    }
     double acc[C::MTILES][C::NT][2];
     compute_tile<C, C::MTILES, C::MTILES>(acc, wsm + lane * 2, t, grp, lane);
     // hand the tensor pipes to the other set if it has a tile for this turn
@@ -529,8 +538,8 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
       }
       double lc0 = 0.0, lc1 = 0.0;
       if (C::SCALE) {
-        lc0 = __ldg(args.lam_c + c);
-        lc1 = two ? __ldg(args.lam_c + c + 1) : 0.0;
+        lc0 = lcp[C::SCALE ? nt : 0][0];
+        lc1 = lcp[C::SCALE ? nt : 0][1];
       }
 #pragma unroll
       for (int mt = 0; mt < C::MTILES; ++mt) {

@@ -7,13 +7,14 @@
 
 namespace ls {
 
-// NT (columns per n-tile group) and the prefetch window D per bucket: NT = 2 keeps
-// acc[MT][2] + the window under ~200 registers for MT >= 10; small MT takes NT = 4.
+// NT (n-tiles per warp) and the prefetch window D per k-step bucket.
 template <int KS>
 struct RDBucket {
   static constexpr int MT = (KS + 1) / 2;
-  static constexpr int NT = MT >= 10 ? 2 : 4;
-  static constexpr int D = 4;
+  static constexpr int NT = 2;
+  // prefetch window (k-steps): a tile's DMMA time shrinks with MT, so small extents need a
+  // deeper window to keep enough bytes in flight
+  static constexpr int D = MT >= 15 ? 4 : MT >= 10 ? 8 : 12;
 };
 
 template <class C>
