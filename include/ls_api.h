@@ -232,6 +232,7 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  */
 #define LS_TUNE_FD_KERNEL 1
 #define LS_TUNE_MATVEC 2
+#define LS_TUNE_MV3_PAD 3  /* v3 matvec: direction-1 row granularity of its intermediates: 1, 8, 16 */
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

@@ -70,6 +70,8 @@ struct ls_ctx {
   // matvec v3: band blocks in DMMA A-fragment order per direction (matvec3_kernels.cuh)
   double* frag_dir[3] = {nullptr, nullptr, nullptr};  // mats M, J, K, 2K
   double* frag_time = nullptr;                        // mats K_t, M_t
+  int n1p = 0;                 // padded direction-1 row of the v3 intermediates
+  double* xT_pad = nullptr;    // v3: the last time slice of x in the padded layout
 
   // host copies (introspection)
   std::vector<double> hM[3], hK[3], hJ[3], hMt, hKt, hlam[4], hU[4];
@@ -472,7 +474,14 @@ static int setup_common(ls_ctx* ctx) {
   }
   // workspaces (halo rows for the distributed matvec: p slices each side)
   const size_t halo = size_t(2 * p) * ctx->Ns;
-  for (int i = 0; i < 6; ++i) LS_CHECK(ctx->alloc(&ctx->tmp[i], ctx->Nl + halo));
+  // v3 matvec intermediates use 64-byte rows along direction 1 (d >= 2, n_1 >= 64):
+  // unaligned 132-double rows made the strided and contiguous passes re-read ~50 %
+  ctx->n1p = (d >= 2 && ctx->n[0] >= 64) ? (ctx->n[0] + 7) / 8 * 8 : ctx->n[0];
+  // buffers sized for the widest padding ls_tune may select (16 doubles = 128-byte rows)
+  const size_t nsp = size_t(ctx->Ns / ctx->n[0]) * ((ctx->n[0] + 15) / 16 * 16);
+  const size_t tmp_sz = std::max(size_t(ctx->Nl) + halo, size_t(ctx->ntl) * nsp);
+  for (int i = 0; i < 6; ++i) LS_CHECK(ctx->alloc(&ctx->tmp[i], tmp_sz));
+  LS_CHECK(ctx->alloc(&ctx->xT_pad, nsp));
   LS_CHECK(ctx->alloc(&ctx->pr, ctx->Nl));
   LS_CHECK(ctx->alloc(&ctx->pz, ctx->Nl));
   LS_CHECK(ctx->alloc(&ctx->pp, ctx->Nl + halo));
@@ -879,6 +888,12 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   double* C = ctx->tmp[4];
   MV3Pass ps[4];
   int np = 0;
+  const int n1 = ctx->n[0], n1p = ctx->n1p;
+  const int64_t Nsp = (ctx->Ns / n1) * n1p;  // padded slice
+  const bool own_last_t = (ctx->nt - 1) - t_first >= 0 && (ctx->nt - 1) - t_first < nout;
+  if (own_last_t && d >= 2)  // W_t term input in the padded layout
+    LS_CUDA(mv3_pad_slice(x + (ctx->nt - 1 - s_first) * ctx->Ns, ctx->xT_pad, Nsp, n1, n1p, ctx->stream,
+                          &ctx->launches));
   {  // time
     MV3Pass& q = ps[np++];
     q = MV3Pass{};
@@ -892,7 +907,12 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.n = ctx->nt;
     a.mt = (ctx->nt + 7) / 8;
     a.Q = uint32_t(ctx->Ns);
-    a.ncols = uint32_t(ctx->Ns);
+    a.Qout = uint32_t(Nsp);
+    a.ncols = uint32_t(Nsp);
+    if (n1p != n1 && d >= 2) {
+      a.map_n1 = n1;
+      a.map_n1p = n1p;
+    }
     a.s_first = int(s_first);
     a.s_rows = int(rows);
     a.t_first = int(t_first);
@@ -902,7 +922,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   }
   const int kd = d - 1;
   uint64_t Q = 1;
-  for (int j = 0; j < kd; ++j) Q *= ctx->n[j];
+  for (int j = 0; j < kd; ++j) Q *= (j == 0 ? n1p : ctx->n[j]);
   {  // direction d
     MV3Pass& q = ps[np++];
     q = MV3Pass{};
@@ -918,13 +938,14 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     const int64_t tT = (ctx->nt - 1) - t_first;
     const bool own_last = tT >= 0 && tT < nout;
     a.tT = own_last ? int(tT) : -1;
-    a.xT = own_last ? x + (ctx->nt - 1 - s_first) * ctx->Ns : nullptr;
+    a.xT = own_last ? (d >= 2 ? ctx->xT_pad : x + (ctx->nt - 1 - s_first) * ctx->Ns) : nullptr;
     a.n = ctx->n[kd];
     a.mt = (a.n + 7) / 8;
     a.Q = uint32_t(Q);
     a.ncols = uint32_t(uint64_t(nout) * Q);
     a.mt0 = 0;
     a.mt1 = a.mt;
+    a.in_fiber = a.out_fiber = a.n;  // d = 1 (contiguous, unpadded)
   }
   const double* cur[3] = {A, B, C};
   if (d == 3) {  // direction 2: (A, B, C) -> (A2, B2, C2) in Kx, Mx, tmp[5]
@@ -940,8 +961,8 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.out[2] = ctx->tmp[5];
     a.n = ctx->n[1];
     a.mt = (a.n + 7) / 8;
-    a.Q = uint32_t(ctx->n[0]);
-    a.ncols = uint32_t(uint64_t(nout) * ctx->n[2] * ctx->n[0]);
+    a.Q = uint32_t(n1p);
+    a.ncols = uint32_t(uint64_t(nout) * ctx->n[2] * n1p);
     a.tT = -1;
     a.mt0 = 0;
     a.mt1 = a.mt;
@@ -962,6 +983,8 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.mt = (a.n + 7) / 8;
     a.Q = 1;
     a.ncols = uint32_t(uint64_t(nout) * (ctx->Ns / ctx->n[0]));
+    a.in_fiber = n1p;   // padded intermediates
+    a.out_fiber = n1;   // y in the caller's layout
     a.tT = -1;
     a.mt0 = 0;
     a.mt1 = a.mt;
@@ -974,9 +997,10 @@ static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
                       int64_t t_first, int64_t nout) {
   // auto (measured, tools/mv_variants.py, r01):
   //   p = 2:  v2 (config 5 p=2: 2.74 ms vs v1 3.07, v3 3.30)
-  //   p = 3, 4: v1 (config 3: 0.81 ms vs v3 1.06, v2 1.16)
-  //   p >= 5: v3, DMMA band passes (config 4: 12.8 ms vs v1 16.4; config 5 p=8: 5.28 vs 6.49)
-  if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 5))
+  //   p = 3: v1 (config 3: 0.81 ms vs v3 1.06, v2 1.16)
+  //   p >= 4: v3, DMMA band passes (config 4: 12.0 ms vs v1 16.4; config 5 p=8: 5.04 vs 6.49,
+  //           p=4: 3.96 vs 4.08)
+  if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 4))
     return mv3_launch(ctx, x, y, rows, s_first, t_first, nout);
   const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2);
   if (!v2) return matvec_block(ctx, x, y, rows, s_first, t_first, nout);
@@ -1241,6 +1265,11 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_MATVEC:
       if (value < 0 || value > 3) return LS_EINVAL;
       ctx->mv_variant = value;
+      return LS_OK;
+    case LS_TUNE_MV3_PAD:  // row granularity of the v3 intermediates along direction 1
+      if (value != 1 && value != 8 && value != 16) return LS_EINVAL;
+      if (ctx->d < 2) return LS_OK;
+      ctx->n1p = (ctx->n[0] + value - 1) / value * value;
       return LS_OK;
     default: return LS_EINVAL;
   }

@@ -47,6 +47,10 @@ struct MV3Args {
   // band, output rows [t_first, t_first + nout)
   int s_first, s_rows, t_first, nout;
   int mt0, mt1;        // m-tile range swept (time pass: the tiles covering the output rows)
+  // layouts: the intermediates use rows of n1p >= n1 doubles (n1p % 8 == 0: 64-byte rows)
+  uint32_t Qout;       // output row stride of strided passes (0: = Q)
+  int map_n1, map_n1p; // time pass: padded column c' -> input column (c'/n1p)*n1 + c'%n1p (0: identity)
+  int in_fiber, out_fiber;  // contiguous (MODE1) passes: fibre strides of input / output
 };
 
 template <int KIND>
@@ -62,8 +66,9 @@ template <int P, int KIND>
 struct MV3Geom {
   static constexpr int OFF = P <= 4 ? 1 : 2;
   static constexpr int NKB = P <= 4 ? 4 : 6;
-  // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 3 for 2, 2 for 3
-  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : MV3IO<KIND>::NIN == 2 ? 3 : 2;
+  // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 2 for 2 or 3
+  // (the 2-input pass runs 2 CTAs per SM within 128 registers)
+  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : 2;
   static constexpr int RING = NKB + 2 * AHEAD;
   static constexpr int G = RING / 2;  // m-tiles per unrolled group
 };
@@ -79,8 +84,14 @@ __device__ __forceinline__ double2 mv3_ld2(const double* p) {
   return v;
 }
 
+// two CTAs per SM for the one- and two-input passes (latency hiding; <= 128 registers)
+template <int KIND>
+struct MV3Occ {
+  static constexpr int CTAS = (KIND == MV3_TIME || KIND == MV3_DIR || KIND == MV3_DIR_A) ? 2 : 1;
+};
+
 template <int P, int NT, int KIND, bool MODE1, bool FAST>
-__global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant__ MV3Args a) {
+__global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const __grid_constant__ MV3Args a) {
   using Gm = MV3Geom<P, KIND>;
   using IO = MV3IO<KIND>;
   constexpr int NKB = Gm::NKB, OFF = Gm::OFF, RING = Gm::RING, G = Gm::G;
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant_
   __syncthreads();
   const int n = a.n;
   const uint32_t Q = a.Q, ncols = a.ncols;
+  const uint32_t Qo = a.Qout ? a.Qout : a.Q;
   const uint32_t nstrips = (ncols + TW - 1) / TW;
   // time pass: band row of stored input row 0 / of output row 0
   const int gin0 = (KIND == MV3_TIME) ? a.s_first : 0;
@@ -116,7 +128,15 @@ __global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant_
       if (c < ncols) {
         bmask |= 1u << j;
         const uint32_t pt = c / Q, q = c - pt * Q;
-        boff[j] = MODE1 ? c * uint32_t(n) : pt * uint32_t(in_rows) * Q + q;
+        if (MODE1) {
+          boff[j] = c * uint32_t(a.in_fiber);
+        } else if (KIND == MV3_TIME && a.map_n1) {  // padded column -> unpadded input column
+          const uint32_t r = q % uint32_t(a.map_n1p);
+          boff[j] = (q / uint32_t(a.map_n1p)) * uint32_t(a.map_n1) + r;
+          if (r >= uint32_t(a.map_n1)) bmask &= ~(1u << j);
+        } else {
+          boff[j] = pt * uint32_t(in_rows) * Q + q;
+        }
         if (KIND == MV3_DIR || KIND == MV3_DIR_A) is_last |= int(pt) == a.tT;
       }
     }
@@ -233,8 +253,8 @@ __global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant_
               double* Y = a.out[o];
               if (FAST) {
                 if (cs < ncols) {
-                  const uint32_t pt = cs / Q, q = cs - pt * Q;
-                  double* dst = Y + (size_t(pt) * nout + lrow) * Q + q;
+                  const uint32_t pt = cs / Qo, q = cs - pt * Qo;
+                  double* dst = Y + (size_t(pt) * nout + lrow) * Qo + q;
                   // accumulator column 2kq + h of n-tile j = physical column cs + NT*h + j
 #pragma unroll
                   for (int h = 0; h < 2; ++h)
@@ -251,10 +271,10 @@ __global__ void __launch_bounds__(256, 1) mv3_band_kernel(const __grid_constant_
                     if (c < ncols) {
                       size_t o_off;
                       if (MODE1) {
-                        o_off = size_t(c) * n + lrow;
+                        o_off = size_t(c) * a.out_fiber + lrow;
                       } else {
-                        const uint32_t pt = c / Q, q = c - pt * Q;
-                        o_off = (size_t(pt) * nout + lrow) * Q + q;
+                        const uint32_t pt = c / Qo, q = c - pt * Qo;
+                        o_off = (size_t(pt) * nout + lrow) * Qo + q;
                       }
                       Y[o_off] = acc[o][j][h];
                     }
@@ -276,6 +296,9 @@ struct MV3Pass {
 };
 // p: spline degree; returns the CUDA error; *launches += kernels launched
 cudaError_t mv3_run(int p, const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
+// dst[c'] = src[(c'/n1p)*n1 + c'%n1p] (0 in the padding) for one slice of Nsp padded columns
+cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, int n1p, cudaStream_t s,
+                          int64_t* launches);
 size_t mv3_frag_count(int p, int n, int nmat);  // doubles of one direction's fragment array
 int mv3_nkb(int p);
 int mv3_off(int p);

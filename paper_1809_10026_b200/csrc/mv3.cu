@@ -21,7 +21,7 @@ static cudaError_t launch(const MV3Args& a, int num_sms, cudaStream_t s) {
   }
   const size_t smem = size_t(MV3IO<KIND>::NMAT) * a.mt * MV3Geom<P, KIND>::NKB * 32 * sizeof(double);
   const uint32_t nstrips = (a.ncols + 8 * NT - 1) / (8 * NT);
-  const unsigned grid = std::min<unsigned>((nstrips + 7) / 8, unsigned(num_sms));
+  const unsigned grid = std::min<unsigned>((nstrips + 7) / 8, unsigned(num_sms * MV3Occ<KIND>::CTAS));
   if (grid == 0 || a.mt1 <= a.mt0) return cudaSuccess;
   mv3_band_kernel<P, NT, KIND, MODE1, FAST><<<grid, 256, smem, s>>>(a);
   return cudaGetLastError();
@@ -30,7 +30,10 @@ static cudaError_t launch(const MV3Args& a, int num_sms, cudaStream_t s) {
 template <int P>
 static cudaError_t run_pass(const MV3Pass& ps, int num_sms, cudaStream_t s) {
   const MV3Args& a = ps.args;
-  const bool fast = !ps.mode1 && (a.Q % 4 == 0);  // NT = 2: Q % 2NT
+  // NT = 2: 2-column loads / 4-column stores stay inside one row and 16-byte aligned
+  const uint32_t qo = a.Qout ? a.Qout : a.Q;
+  const bool fast = !ps.mode1 && (a.Q % 4 == 0) && (qo % 4 == 0) &&
+                    (a.map_n1 == 0 || (a.map_n1 % 2 == 0 && a.map_n1p % 4 == 0));
   switch (ps.kind) {
     case MV3_TIME: return fast ? launch<P, MV3_TIME, false, true>(a, num_sms, s) : launch<P, MV3_TIME, false, false>(a, num_sms, s);
     case MV3_DIR: return fast ? launch<P, MV3_DIR, false, true>(a, num_sms, s) : launch<P, MV3_DIR, false, false>(a, num_sms, s);
@@ -39,6 +42,21 @@ static cudaError_t run_pass(const MV3Pass& ps, int num_sms, cudaStream_t s) {
     case MV3_LAST: return launch<P, MV3_LAST, true, false>(a, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+__global__ void mv3_pad_slice_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t nsp,
+                                     int n1, int n1p) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nsp; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = e / n1p, r = e - row * n1p;
+    dst[e] = r < n1 ? src[row * n1 + r] : 0.0;
+  }
+}
+
+cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, int n1p, cudaStream_t s,
+                          int64_t* launches) {
+  mv3_pad_slice_kernel<<<unsigned(std::min<int64_t>((nsp + 255) / 256, 148 * 8)), 256, 0, s>>>(src, dst, nsp, n1, n1p);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 cudaError_t mv3_run(int p, const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches) {

@@ -19,6 +19,7 @@ ap.add_argument("--configs", nargs="+", default=["4", "3", "5:8", "5:2"])
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--variants", nargs="+", type=int, default=[1, 2])
 ap.add_argument("--pcg", action="store_true")
+ap.add_argument("--pad", type=int, default=0, help="ls_tune knob 3 (v3 row padding), 0 = default")
 a = ap.parse_args()
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
 for cs in a.configs:
@@ -31,6 +32,8 @@ for cs in a.configs:
     ctx.set_stream(s)
     x = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
     outs = {}
+    if a.pad:
+        ctx.tune(3, a.pad)
     for v in a.variants:
         ctx.tune(2, v)
         y = torch.empty_like(x)

@@ -22,12 +22,15 @@ ap.add_argument("--pcg", action="store_true")
 ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--mv", type=int, default=0, help="ls_tune matvec variant")
 ap.add_argument("--fdk", type=int, default=0, help="ls_tune FD kernel variant")
+ap.add_argument("--pad", type=int, default=0, help="ls_tune v3 matvec padding")
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = a.p if a.p is not None else (c["p"] if isinstance(c["p"], int) else c["p"][0])
 ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
 ctx.tune(2, a.mv)
 ctx.tune(1, a.fdk)
+if a.pad:
+    ctx.tune(3, a.pad)
 r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 z = torch.empty_like(r)
 if a.pcg:
