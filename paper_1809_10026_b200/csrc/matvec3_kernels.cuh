@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
       boff[j] = 0;
       if (c < ncols) {
         bmask |= 1u << j;
-        const uint32_t pt = c / Q, q = c - pt * Q;
+        // the time pass has one column per (padded) spatial index: no slow index
+        const uint32_t pt = (KIND == MV3_TIME) ? 0u : c / Q, q = c - pt * Q;
         if (MODE1) {
           boff[j] = c * uint32_t(a.in_fiber);
         } else if (KIND == MV3_TIME && a.map_n1) {  // padded column -> unpadded input column

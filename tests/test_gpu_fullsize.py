@@ -76,3 +76,20 @@ def test_config4_uniform_linearity_symmetry():
     err = torch.linalg.norm(comb - (2.0 * z1 - 3.0 * z2)) / torch.linalg.norm(comb)
     assert float(err) <= 1e-12
     assert torch.isfinite(z1).all()
+
+
+@pytest.mark.parametrize("cfg,p", [(5, 8), (4, 6)])
+def test_pcg_fullsize(cfg, p):
+    """A full-size PCG solve in the configuration bench.py times (the automatic kernel
+    choice: register-direct FD kernel, DMMA band matvec): the cube manufactured forcing of
+    PAPER.md 1166, tol 1e-8.  Pins: convergence, the recomputed true residual, and the
+    iteration count of Table 1's finest rows (13 at n_el = 64 and 128, PAPER.md 1193-1195;
+    h- and p-robust by Thm spec_est, PAPER.md 905-911), with +-2 of slack for p beyond the
+    table."""
+    import paper_1809_10026_b200 as ls
+    c = synth.CONFIGS[cfg]
+    ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
+    x, st = ctx.pcg(ctx.rhs(1), tol=1e-8)
+    assert st["status"] == 0, st
+    assert 11 <= st["iters"] <= 15, st
+    assert st["rel_res"] <= 1e-8 and st["true_rel_res"] <= 1e-7, st
