@@ -126,6 +126,22 @@ int fd_apply(ls_ctx* ctx, const double* r, double* z);
 int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* out, int64_t a, int64_t b);
 
 /*
+ * fd_apply_scatter -- the two fused-all-to-all stages of the distributed fd_apply for rank
+ * `me` of `world`, with caller-given destination buffers (dst_host: host array of `world`
+ * device pointers; the same stores a multi-GPU run makes into peer memory):
+ *   stage 0: forward spatial modes of rank me's slab `in` ([a][N_s], a = its slab length
+ *            under ls_partition(n_t, world)); the last mode writes element (t, s) into
+ *            dst[h][(t0_me + t) * ld_h + s - c0_h], h = owner of s, ld_h = 4*ceil(len_h/4);
+ *   stage 1: time mode of rank me's chunk `in` ([n_t][ld_me], a = c0_me, b = len_me under
+ *            ls_partition(N_s, world)); the backward time mode writes element (t, j) into
+ *            dst[g][(t - t0_g) * N_s + c0_me + j], g = owner of t.
+ * Asynchronous.  Errors: LS_EINVAL (geometry), LS_ENOTSUP (d = 1 or a mode stride not a
+ * multiple of 4).
+ */
+int fd_apply_scatter(ls_ctx* ctx, int stage, const double* in, int64_t a, int64_t b, int world, int me,
+                     double* const* dst_host);
+
+/*
  * ls_matvec -- y = A x, A = K_t (x) M_s + M_t (x) J_s + W_t (x) L_s
  * (eq:A_kron, PAPER.md 686-703), matrix-free and sum-factorised on the banded
  * univariate factors (identity map).  x, y: device vectors, y != x.
@@ -203,6 +219,14 @@ int ls_a2a_plan(int64_t n_t, int64_t N_s, int world, int rank, int64_t* send_off
 int ls_pack_map(int64_t ntl, int64_t N_s, int world, int64_t* pos);
 int ls_halo_plan(int64_t n_t, int world, int rank, int p, int64_t* t0, int64_t* ntl,
                  int64_t* lo, int64_t* hi);
+/* ls_a2a_dest -- destination of one element in the fused all-to-all (the addressing of
+ * the peer-memory epilogues, LS_TUNE_A2A / fd_apply_scatter): dir 0 (slab -> chunk):
+ * element (i = local time slice, j = spatial index) of rank `rank`'s slab; dir 1 (chunk ->
+ * slab): element (i = time slice, j = local spatial index) of its chunk.  Returns the
+ * destination rank and element offset in that rank's receive buffer ([n_t][4*ceil(len/4)]
+ * chunk, resp. [ntl][N_s] slab). */
+int ls_a2a_dest(int64_t n_t, int64_t N_s, int world, int rank, int dir, int64_t i, int64_t j, int* peer,
+                int64_t* off);
 
 /* ls_kernel_launches -- number of kernels the library has launched so far. */
 int64_t ls_kernel_launches(const ls_ctx* ctx);
@@ -233,6 +257,12 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
 #define LS_TUNE_FD_KERNEL 1
 #define LS_TUNE_MATVEC 2
 #define LS_TUNE_MV3_PAD 3  /* v3 matvec: direction-1 row granularity of its intermediates: 1, 8, 16 */
+/* LS_TUNE_A2A (distributed contexts, d >= 2, N_1*..*N_{d-1} % 4 == 0): 0 = NCCL all-to-all
+ * (default), 1 = fused all-to-all: the last forward spatial mode and the backward time mode
+ * store their outputs straight into the owners' receive buffers in peer memory (CUDA IPC
+ * over NVLink), each followed by a cross-GPU flag barrier.  Enabling is collective (every
+ * rank calls it).  Not yet validated on a multi-GPU box. */
+#define LS_TUNE_A2A 4
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

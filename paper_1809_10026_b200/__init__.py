@@ -31,7 +31,7 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
-            "ls_matvec_slab", "fd_apply_stage"]
+            "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest"]
 
 
 class PCGStats(ctypes.Structure):
@@ -81,6 +81,8 @@ def load_library(path=LIB_PATH):
         "ls_destroy": (None, [vp]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
+        "fd_apply_scatter": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                            ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
         "ls_matvec_slab": (ctypes.c_int, [vp, dp, ctypes.c_int64, ctypes.c_int64, dp, ctypes.c_int64,
                                           ctypes.c_int64]),
         "ls_partition": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
@@ -90,6 +92,8 @@ def load_library(path=LIB_PATH):
         "ls_halo_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         i64p, i64p, i64p, i64p]),
         "ls_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+        "ls_a2a_dest": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int), i64p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -138,6 +142,14 @@ def pack_map(ntl, N_s, world):
     _check(load_library().ls_pack_map(int(ntl), int(N_s), int(world),
                                       pos.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))), "ls_pack_map")
     return pos
+
+
+def a2a_dest(n_t, N_s, world, rank, direction, i, j):
+    """(peer, offset) of one element in the fused all-to-all (host only)."""
+    peer, off = ctypes.c_int(), ctypes.c_int64()
+    _check(load_library().ls_a2a_dest(int(n_t), int(N_s), int(world), int(rank), int(direction), int(i), int(j),
+                                      ctypes.byref(peer), ctypes.byref(off)), "ls_a2a_dest")
+    return peer.value, off.value
 
 
 def halo_plan(n_t, world, rank, p):
@@ -220,6 +232,14 @@ class Context:
         _check(self._lib.fd_apply_stage(self._h, int(stage), ctypes.c_void_p(inp.data_ptr()),
                                         ctypes.c_void_p(out.data_ptr()), int(a), int(b)), "fd_apply_stage")
         return out
+
+    def fd_scatter(self, stage, inp, a, b, world, me, dsts):
+        """fd_apply_scatter: stage 0 = forward spatial modes of rank `me`'s slab scattered into
+        the chunk buffers `dsts`; stage 1 = time mode of its chunk scattered into the slab
+        buffers `dsts` (lists of `world` CUDA tensors)."""
+        arr = (ctypes.c_void_p * world)(*[t.data_ptr() for t in dsts])
+        _check(self._lib.fd_apply_scatter(self._h, int(stage), ctypes.c_void_p(inp.data_ptr()), int(a), int(b),
+                                          int(world), int(me), arr), "fd_apply_scatter")
 
     def matvec_slab(self, x_ext, s_first, t_first, nout, y=None):
         """Rows [t_first, t_first + nout) of A x from the stored rows [s_first, s_first +

@@ -71,6 +71,8 @@ struct ls_ctx {
   double* frag_dir[3] = {nullptr, nullptr, nullptr};  // mats M, J, K, 2K
   double* frag_time = nullptr;                        // mats K_t, M_t
   int n1p = 0;                 // padded direction-1 row of the v3 intermediates
+  double** scatter_tab = nullptr;  // fd_apply_scatter: device copy of the caller's table
+  double** scatter_stage = nullptr;  // pinned host staging of that table
   double* xT_pad = nullptr;    // v3: the last time slice of x in the padded layout
 
   // host copies (introspection)
@@ -111,6 +113,7 @@ struct ls_ctx {
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (void* a : allocs) cudaFree(a);
     if (h_scal) cudaFreeHost(h_scal);
+    if (scatter_stage) cudaFreeHost(scatter_stage);
   }
   int alloc(double** ptr, size_t count) {
     void* v = nullptr;
@@ -632,12 +635,125 @@ extern "C" int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* 
   }
 }
 
+// ---- fused all-to-all pieces (register-direct kernel with peer-memory epilogues) ----------
+// forward spatial modes 1..d-1 on `rows` slab slices, then mode d scattering its output
+// straight into the owners' chunk buffers (plan.hpp a2a_fwd_dest).  Workspaces tmp[3], tmp[4].
+static int spatial_fwd_scatter(ls_ctx* ctx, const double* in, uint64_t rows, double* const* peer, int world,
+                               int me) {
+  const int d = ctx->d;
+  if (d < 2) return LS_ENOTSUP;
+  const double* src = in;
+  double* ws[2] = {ctx->tmp[3], ctx->tmp[4]};
+  for (int k = 0; k < d - 1; ++k) {
+    uint64_t Q = 1, P = rows;
+    for (int j = 0; j < k; ++j) Q *= ctx->n[j];
+    for (int j = k + 1; j < d; ++j) P *= ctx->n[j];
+    LS_CHECK(launch_mode(ctx, src, ws[k % 2], ctx->Wf[k], ctx->n[k], P, Q, false));
+    src = ws[k % 2];
+  }
+  const int k = d - 1;
+  uint64_t Q = 1;
+  for (int j = 0; j < k; ++j) Q *= ctx->n[j];
+  ModeArgs a{};
+  a.X = src;
+  a.Y = ctx->tmp[5];  // unused by the scattering epilogue (alignment probe only)
+  a.W = ctx->Wf[k];
+  a.n = ctx->n[k];
+  a.P = uint32_t(rows);
+  a.Q = uint32_t(Q);
+  a.ncols = uint32_t(rows * Q);
+  a.y16 = true;
+  a.remote = 1;
+  a.peer = peer;
+  a.world = world;
+  a.me = me;
+  a.nt_g = ctx->nt;
+  a.Ns_g = ctx->Ns;
+  return launch_mode_rd(ctx, a, false, false);
+}
+
+// time mode of this rank's spatial chunk [n_t][chunk_ld(len)] (spatial offset c0): forward +
+// scale locally into `mid`, backward scattering into the owners' slab buffers (a2a_bwd_dest)
+static int time_chunk_scatter(ls_ctx* ctx, const double* chunk, int64_t c0, int64_t len, double* mid,
+                              double* const* peer, int world, int me) {
+  const int64_t ld = chunk_ld(len);
+  ModeArgs a{};
+  a.X = chunk;
+  a.Y = mid;
+  a.W = ctx->Wf[3];
+  a.lam_a = ctx->lam[3];
+  a.lam_c = ctx->lam_s + c0;
+  a.n = ctx->nt;
+  a.P = 1;
+  a.Q = uint32_t(ld);
+  a.ncols = uint32_t(len);
+  a.y16 = (reinterpret_cast<uintptr_t>(mid) & 15) == 0;
+  LS_CHECK(launch_mode_rd(ctx, a, false, true));
+  ModeArgs b{};
+  b.X = mid;
+  b.Y = ctx->tmp[5];
+  b.W = ctx->Wb[3];
+  b.n = ctx->nt;
+  b.P = 1;
+  b.Q = uint32_t(ld);
+  b.ncols = uint32_t(len);
+  b.y16 = true;
+  b.remote = 2;
+  b.peer = peer;
+  b.world = world;
+  b.me = me;
+  b.nt_g = ctx->nt;
+  b.Ns_g = ctx->Ns;
+  return launch_mode_rd(ctx, b, false, false);
+}
+
+extern "C" int fd_apply_scatter(ls_ctx* ctx, int stage, const double* in, int64_t a, int64_t b, int world, int me,
+                                double* const* dst_host) {
+  if (!ctx || !in || !dst_host || world < 1 || world > 64 || me < 0 || me >= world || !aligned8(in)) return LS_EINVAL;
+  if (ctx->d < 2) return LS_ENOTSUP;
+  if (!ctx->scatter_tab) {
+    LS_CHECK(ctx->alloc(reinterpret_cast<double**>(&ctx->scatter_tab), 64));
+    LS_CUDA(cudaMallocHost(&ctx->scatter_stage, 64 * sizeof(double*)));
+  }
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer is free
+  for (int h = 0; h < world; ++h) {
+    if (!dst_host[h]) return LS_EINVAL;
+    ctx->scatter_stage[h] = dst_host[h];
+  }
+  LS_CUDA(cudaMemcpyAsync(ctx->scatter_tab, ctx->scatter_stage, world * sizeof(double*), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  int64_t off, len;
+  if (stage == 0) {
+    split_part(ctx->nt, world, me, &off, &len);
+    if (a != len || len < 1 || len > ctx->ntl) return LS_EINVAL;
+    return spatial_fwd_scatter(ctx, in, uint64_t(a), ctx->scatter_tab, world, me);
+  }
+  if (stage == 1) {
+    split_part(ctx->Ns, world, me, &off, &len);
+    if (a != off || b != len || len < 1) return LS_EINVAL;
+    return time_chunk_scatter(ctx, in, a, b, ctx->tmp[3], ctx->scatter_tab, world, me);
+  }
+  return LS_EINVAL;
+}
+
 // distributed fd_apply: slab -> all-to-all -> time mode on spatial chunks -> all-to-all -> slab
 int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
   Comm& cm = *ctx->comm;
   double* A = ctx->tmp[0];
   double* B = ctx->tmp[1];
   double* C = ctx->tmp[2];
+  if (cm.fused) {
+    // fused path: the all-to-alls are the epilogues of the last forward spatial mode and of
+    // the backward time mode (stores into peer memory), each followed by a cross-GPU
+    // barrier.  Receive buffers: B = tmp[1] (chunk), A = tmp[0] (slab); every workspace
+    // written locally after a barrier (tmp[2..4]) is never a peer's destination.
+    const int64_t c0 = cm.chunk_off[ctx->rank], len = cm.chunk_len[ctx->rank];
+    LS_CHECK(spatial_fwd_scatter(ctx, r, uint64_t(ctx->ntl), cm.d_peer_chunk, ctx->world, ctx->rank));
+    LS_CHECK(cm.barrier());
+    if (len > 0) LS_CHECK(time_chunk_scatter(ctx, B, c0, len, C, cm.d_peer_slab, ctx->world, ctx->rank));
+    LS_CHECK(cm.barrier());
+    return spatial_modes(ctx, A, z, C, ctx->tmp[3], ctx->ntl, false);
+  }
   LS_CHECK(spatial_modes(ctx, r, A, B, C, ctx->ntl, true));
   // A: [ntl][Ns] slab -> B: [nt][chunk] (send order = destination chunks)
   LS_CHECK(cm.slab_to_chunk(A, B, C, ctx->launches));
@@ -1245,6 +1361,14 @@ extern "C" int ls_pack_map(int64_t ntl, int64_t Ns, int world, int64_t* pos) {
   return LS_OK;
 }
 
+extern "C" int ls_a2a_dest(int64_t nt, int64_t Ns, int world, int rank, int dir, int64_t i, int64_t j, int* peer,
+                           int64_t* off) {
+  if (world < 1 || rank < 0 || rank >= world || !peer || !off || (dir != 0 && dir != 1)) return LS_EINVAL;
+  if (dir == 0) a2a_fwd_dest(i, j, nt, Ns, world, rank, peer, off);
+  else a2a_bwd_dest(i, j, nt, Ns, world, rank, peer, off);
+  return LS_OK;
+}
+
 extern "C" int ls_halo_plan(int64_t nt, int world, int rank, int p, int64_t* t0, int64_t* ntl,
                             int64_t* lo, int64_t* hi) {
   if (world < 1 || rank < 0 || rank >= world || p < 0 || !t0 || !ntl || !lo || !hi) return LS_EINVAL;
@@ -1266,6 +1390,17 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       if (value < 0 || value > 3) return LS_EINVAL;
       ctx->mv_variant = value;
       return LS_OK;
+    case LS_TUNE_A2A: {  // collective when enabling: every rank calls it
+      if (value == 0) {
+        if (ctx->comm) ctx->comm->fused = false;
+        return LS_OK;
+      }
+      if (value != 1 || !ctx->comm || ctx->d < 2) return LS_EINVAL;
+      uint64_t Q = 1;
+      for (int j = 0; j < ctx->d - 1; ++j) Q *= ctx->n[j];
+      if (Q % 4 != 0) return LS_ENOTSUP;  // the scattering epilogue is a FAST-path variant
+      return ctx->comm->setup_fused(ctx->tmp[1], ctx->tmp[0]);
+    }
     case LS_TUNE_MV3_PAD:  // row granularity of the v3 intermediates along direction 1
       if (value != 1 && value != 8 && value != 16) return LS_EINVAL;
       if (ctx->d < 2) return LS_OK;

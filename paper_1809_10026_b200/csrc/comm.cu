@@ -31,7 +31,92 @@ int comm_unique_id(void* out128) {
 }
 
 Comm::~Comm() {
+  for (void* q : opened) cudaIpcCloseMemHandle(q);
+  for (void* q : owned) cudaFree(q);
   if (nccl) ncclCommDestroy(C(nccl));
+}
+
+// system-scope release store / acquire load (PTX memory model) for the cross-GPU barrier
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void a2a_barrier_kernel(int* const* peer_flags, const int* my_flags, int me, int world, int epoch) {
+  const int h = threadIdx.x;
+  __threadfence_system();
+  if (h < world) st_release_sys(peer_flags[h] + me, epoch);
+  if (h < world)
+    while (ld_acquire_sys(my_flags + h) < epoch) {
+    }
+}
+
+int Comm::setup_fused(double* chunk_buf, double* slab_buf) {
+  if (fused) return LS_OK;
+  if (world < 2 || world > 32) return LS_EINVAL;
+  void* v = nullptr;
+  if (cudaMalloc(&v, sizeof(int) * world) != cudaSuccess) return LS_ENOMEM;
+  owned.push_back(v);
+  flags = static_cast<int*>(v);
+  if (cudaMemset(flags, 0, sizeof(int) * world) != cudaSuccess) return LS_ECUDA;
+  cudaIpcMemHandle_t hs[3];
+  if (cudaIpcGetMemHandle(&hs[0], chunk_buf) != cudaSuccess || cudaIpcGetMemHandle(&hs[1], slab_buf) != cudaSuccess ||
+      cudaIpcGetMemHandle(&hs[2], flags) != cudaSuccess)
+    return LS_ECUDA;
+  const size_t hb = sizeof(hs);
+  char* dev = nullptr;
+  if (cudaMalloc(&dev, hb * (world + 1)) != cudaSuccess) return LS_ENOMEM;
+  std::vector<char> all(hb * world);
+  int rc = LS_OK;
+  if (cudaMemcpy(dev + hb * world, hs, hb, cudaMemcpyHostToDevice) != cudaSuccess) rc = LS_ECUDA;
+  if (rc == LS_OK && ncclAllGather(dev + hb * world, dev, hb, ncclChar, C(nccl), stream) != ncclSuccess) rc = LS_ENCCL;
+  if (rc == LS_OK && cudaStreamSynchronize(stream) != cudaSuccess) rc = LS_ECUDA;
+  if (rc == LS_OK && cudaMemcpy(all.data(), dev, hb * world, cudaMemcpyDeviceToHost) != cudaSuccess) rc = LS_ECUDA;
+  cudaFree(dev);
+  if (rc != LS_OK) return rc;
+  std::vector<double*> pc(world), ps(world);
+  std::vector<int*> pf(world);
+  for (int h = 0; h < world; ++h) {
+    if (h == rank) {
+      pc[h] = chunk_buf;
+      ps[h] = slab_buf;
+      pf[h] = flags;
+      continue;
+    }
+    const cudaIpcMemHandle_t* hh = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * h);
+    void* q[3];
+    for (int k = 0; k < 3; ++k) {
+      if (cudaIpcOpenMemHandle(&q[k], hh[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return LS_ECUDA;
+      opened.push_back(q[k]);
+    }
+    pc[h] = static_cast<double*>(q[0]);
+    ps[h] = static_cast<double*>(q[1]);
+    pf[h] = static_cast<int*>(q[2]);
+  }
+  void* t[3];
+  for (int k = 0; k < 3; ++k) {
+    if (cudaMalloc(&t[k], sizeof(void*) * world) != cudaSuccess) return LS_ENOMEM;
+    owned.push_back(t[k]);
+  }
+  d_peer_chunk = static_cast<double**>(t[0]);
+  d_peer_slab = static_cast<double**>(t[1]);
+  d_peer_flags = static_cast<int**>(t[2]);
+  if (cudaMemcpy(d_peer_chunk, pc.data(), sizeof(void*) * world, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(d_peer_slab, ps.data(), sizeof(void*) * world, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(d_peer_flags, pf.data(), sizeof(void*) * world, cudaMemcpyHostToDevice) != cudaSuccess)
+    return LS_ECUDA;
+  fused = true;
+  return LS_OK;
+}
+
+int Comm::barrier() {
+  ++epoch;
+  a2a_barrier_kernel<<<1, 32, 0, stream>>>(d_peer_flags, flags, rank, world, epoch);
+  return cudaGetLastError() == cudaSuccess ? LS_OK : LS_ECUDA;
 }
 
 int Comm::init(const void* uid, int rank_, int world_, int64_t nt_, int64_t Ns_) {

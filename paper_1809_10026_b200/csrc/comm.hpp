@@ -38,6 +38,25 @@ struct Comm {
   // x_ext = [lo halo | own ntl slices | hi halo] (plan.hpp halo_plan): fill the halos
   int halo_exchange(double* x_ext, int p);
   int allreduce_scalar(double* dev_ptr);
+
+  // ---- fused all-to-all over peer memory (ls_tune LS_TUNE_A2A = 1) -----------------
+  // chunk_buf: this rank's [n_t][chunk_ld(len)] receive buffer of the forward exchange,
+  // slab_buf: its [ntl][N_s] receive buffer of the backward exchange (both the base of a
+  // cudaMalloc allocation).  Collective: every rank calls it.  IPC handles are exchanged
+  // with ncclAllGather and opened with peer access (NVLink / NVSwitch).
+  int setup_fused(double* chunk_buf, double* slab_buf);
+  // cross-GPU barrier on the stream: signal every peer, then wait for every peer's signal
+  // (system-scope release / acquire on flags in peer memory); orders the epilogue stores
+  // of the previous kernel before the next kernel reads the receive buffer.
+  int barrier();
+  bool fused = false;
+  double** d_peer_chunk = nullptr;  // device tables [world]
+  double** d_peer_slab = nullptr;
+  int** d_peer_flags = nullptr;
+  int* flags = nullptr;             // this rank's [world] flags (written by the peers)
+  int epoch = 0;
+  std::vector<void*> opened;        // IPC mappings to close
+  std::vector<void*> owned;         // device allocations of this object
 };
 
 int comm_unique_id(void* out128);

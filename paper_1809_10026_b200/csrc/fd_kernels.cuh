@@ -38,6 +38,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "plan.hpp"
+
 namespace ls {
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
@@ -106,6 +108,15 @@ struct ModeArgs {
   uint32_t ncols;   // P * Q
   uint32_t ntiles;  // ceil(ncols / BN)
   bool y16;         // Y is 16-byte aligned (vector stores allowed)
+  // fused all-to-all epilogue (register-direct kernel only): 0 = store to Y;
+  // 1 = forward (this launch is the last forward spatial mode of a time slab: element
+  //     (t_local, a, q) -> spatial s = a*Q + q -> peer chunk buffer, plan.hpp a2a_fwd_dest);
+  // 2 = backward (this launch is the backward time mode of a spatial chunk: element
+  //     (t = a, q) -> peer slab buffer, a2a_bwd_dest)
+  int remote;
+  double* const* peer;  // device table [world] of destination buffers
+  int world, me;
+  int64_t nt_g, Ns_g;   // global n_t, N_s
 };
 
 // One warp's share of one tile: MC m-tiles (compile time: no predicates, so no

@@ -20,7 +20,8 @@
 //     contiguous doubles (LDG.128) for strided modes, and its accumulators
 //     (C-fragment columns 2(l%4), 2(l%4)+1 of every n-tile) are the 2*NT
 //     contiguous physical columns 2*NT*(l%4) .. +2*NT-1 (vector stores);
-//   * K padding: the last k-step loads rows >= n as 0 (predicated), W's padded
+//   * K padding: rows >= n are never loaded (predicated to 0: a bucket's KS can exceed
+//     ceil(n/4), and those rows would lie past the end of the column), W's padded
 //     columns are 0; M padding rows are never stored;
 //   * SCALE (forward time mode): Algorithm 1 step 3 in the epilogue,
 //     Y[a][c] /= (lambda_t[a] + Lambda_s[c]) (reading c3).
@@ -35,9 +36,10 @@
 
 namespace ls {
 
-template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_>
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_, int REMOTE_ = 0>
 struct RDCfg {
   static constexpr int KS = KS_, NT = NT_, D = D_;
+  static constexpr int REMOTE = REMOTE_;  // fused all-to-all epilogue (ModeArgs::remote)
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_, FAST = FAST_;
   static constexpr int MT = (KS + 1) / 2;  // ceil(n/8) for n in (4KS-4, 4KS]
   static constexpr int KSP = (KS + 1) / 2;  // k-step pairs
@@ -48,6 +50,7 @@ struct RDCfg {
   static constexpr int LAMA = SCALE ? 8 * MT : 0;  // lambda_t per output row (SCALE)
   static constexpr size_t SMEM = size_t(WFRAG + LAMA) * sizeof(double);
   static_assert(!(MODE1 && FAST), "FAST is a strided-mode path");
+  static_assert(REMOTE == 0 || (FAST && !SCALE), "fused all-to-all epilogues: unscaled FAST launches");
   static_assert(NT % 2 == 0, "NT even (LDG.128 pairs)");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -158,14 +161,17 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
   uint32_t tile = blockIdx.x * C::WARPS + warp;
   if (tile >= ntw) return;
   const size_t kstep = C::MODE1 ? size_t(4) : size_t(4) * Q;
-  const bool last_ok = kq < n - 4 * (C::KS - 1);  // row of the last k-step inside [0, n)
+  // rows 4*kk + kq >= n are never loaded (zero B fragment): the bucket's KS may exceed
+  // ceil(n/4) by a few k-steps, and those rows lie past the end of the column
+  // (the k-step buckets exceed ceil(n/4) by at most 5, so only the last 6 k-steps test)
+  auto row_ok = [&](int kk) { return 4 * kk + kq < n; };
   const double* wl = wsm + lane * 2;
 
   RDIn<C::NT> cur = rd_make_in<C>(args, tile, lane);
   double bw[C::D][C::NT];
 #pragma unroll
   for (int s = 0; s < C::D; ++s)
-    if (s < C::KS) rd_load<C>(bw[s], args.X, cur, s, kstep, s < C::KS - 1 || last_ok, n);
+    if (s < C::KS) rd_load<C>(bw[s], args.X, cur, s, kstep, row_ok(s), n);
 
 #pragma unroll 1
   for (; tile < ntw; tile += wstride) {
@@ -206,16 +212,53 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
         if (k >= C::KSE) continue;
         const int kk = k + C::D;
         if (kk < C::KS) {
-          rd_load<C>(bw[k % C::D], args.X, cur, kk, kstep, kk < C::KS - 1 || last_ok, n);
+          rd_load<C>(bw[k % C::D], args.X, cur, kk, kstep, row_ok(kk), n);
         } else if (kk >= C::KSE) {
           const int s = kk - C::KSE;  // next tile's k-step, same slot (KSE % D == 0)
-          if (s < C::KS) rd_load<C>(bw[k % C::D], args.X, nxt, s, kstep, s < C::KS - 1 || last_ok, n);
+          if (s < C::KS) rd_load<C>(bw[k % C::D], args.X, nxt, s, kstep, row_ok(s), n);
         }
       }
     }
 
     // ---- epilogue: lane's columns cg .. cg + 2NT - 1, rows mt*8 + nq
-    if (C::FAST) {
+    if (C::REMOTE) {
+      // fused all-to-all: every output element goes straight to its owner's receive buffer
+      // (peer memory over NVLink in a multi-GPU run); pairs that stay contiguous and
+      // 16-byte aligned in the destination are stored as one double2
+      if (cg < ncols) {
+        const uint32_t p = cg / Q, q = cg - p * Q;
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) {
+          const int a = mt * 8 + nq;
+          if (a < n) {
+#pragma unroll
+            for (int e = 0; e < 2 * C::NT; e += 2) {
+              if (cg + e >= ncols) continue;
+              const double v0 = acc[mt][e % C::NT][e / C::NT];
+              const double v1 = acc[mt][(e + 1) % C::NT][(e + 1) / C::NT];
+              int r0, r1;
+              int64_t o0, o1;
+              if (C::REMOTE == 1) {
+                const int64_t s0 = int64_t(a) * Q + q + e;
+                a2a_fwd_dest(int64_t(p), s0, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
+                a2a_fwd_dest(int64_t(p), s0 + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
+              } else {
+                a2a_bwd_dest(int64_t(a), int64_t(q) + e, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
+                a2a_bwd_dest(int64_t(a), int64_t(q) + e + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
+              }
+              const bool second = cg + e + 1 < ncols;
+              double* d0 = args.peer[r0] + o0;
+              if (second && r1 == r0 && o1 == o0 + 1 && ((reinterpret_cast<uintptr_t>(d0) & 15) == 0)) {
+                *reinterpret_cast<double2*>(d0) = make_double2(v0, v1);
+              } else {
+                *d0 = v0;
+                if (second) args.peer[r1][o1] = v1;
+              }
+            }
+          }
+        }
+      }
+    } else if (C::FAST) {
       if (cg < ncols) {
         const uint32_t p = cg / Q, q = cg - p * Q;
         double* ob = args.Y + size_t(p) * n * Q + q;

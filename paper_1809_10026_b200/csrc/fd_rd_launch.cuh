@@ -38,9 +38,14 @@ template <int KS>
 cudaError_t rd_launch(const ModeArgs& a, bool mode1, bool scale, cudaStream_t s, int num_sms) {
   using B = RDBucket<KS>;
   constexpr int NT = B::NT, D = B::D;
-  if (mode1) return rd_launch_cfg<RDCfg<KS, NT, true, false, false, D>>(a, s, num_sms);
+  if (mode1) return a.remote ? cudaErrorInvalidValue : rd_launch_cfg<RDCfg<KS, NT, true, false, false, D>>(a, s, num_sms);
   const bool fast = (a.Q % (2 * NT) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
                     ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
+  if (a.remote) {  // fused all-to-all epilogues exist for unscaled FAST launches only
+    if (!fast || scale) return cudaErrorInvalidValue;
+    if (a.remote == 1) return rd_launch_cfg<RDCfg<KS, NT, false, false, true, D, 1>>(a, s, num_sms);
+    return rd_launch_cfg<RDCfg<KS, NT, false, false, true, D, 2>>(a, s, num_sms);
+  }
   if (scale) {
     if (fast) return rd_launch_cfg<RDCfg<KS, NT, false, true, true, D>>(a, s, num_sms);
     return rd_launch_cfg<RDCfg<KS, NT, false, true, false, D>>(a, s, num_sms);

@@ -54,6 +54,36 @@ LS_HD void a2a_plan(int64_t nt, int64_t Ns, int world, int r, int h, int64_t* se
   *recv_cnt = ntlh * lenr;
 }
 
+// ---- fused all-to-all (peer-memory epilogues, comm.cu / fd_rd_kernel.cuh) ---------------
+// Receive layouts: rank h's chunk buffer is [n_t][ld_h] with ld_h = chunk_ld(len_h) (rows
+// padded to 4 doubles so the time-mode kernel's 2-column loads and 4-column stores stay
+// aligned); rank g's slab buffer is [ntl_g][N_s].
+LS_HD int64_t chunk_ld(int64_t len) { return (len + 3) / 4 * 4; }
+
+// forward (slab -> chunk): element (t_local, s) of rank r's slab -> rank *h, element offset
+// *off of its chunk buffer.  Same data movement as pack_pos + a2a_plan.
+LS_HD void a2a_fwd_dest(int64_t t_local, int64_t s, int64_t nt, int64_t Ns, int world, int r, int* h,
+                        int64_t* off) {
+  int64_t t0, ntl, c0, len;
+  split_part(nt, world, r, &t0, &ntl);
+  const int hh = split_owner(Ns, world, s);
+  split_part(Ns, world, hh, &c0, &len);
+  *h = hh;
+  *off = (t0 + t_local) * chunk_ld(len) + (s - c0);
+}
+
+// backward (chunk -> slab): element (t, s_local) of rank r's chunk -> rank *g, element
+// offset *off of its slab buffer.
+LS_HD void a2a_bwd_dest(int64_t t, int64_t s_local, int64_t nt, int64_t Ns, int world, int r, int* g,
+                        int64_t* off) {
+  int64_t c0, len, t0, ntl;
+  split_part(Ns, world, r, &c0, &len);
+  const int gg = split_owner(nt, world, t);
+  split_part(nt, world, gg, &t0, &ntl);
+  *g = gg;
+  *off = (t - t0) * Ns + c0 + s_local;
+}
+
 // Halo of the banded time factors (half-bandwidth p) for ls_matvec on rank r.
 // Extended slab = [lo halo rows | ntl own rows | hi halo rows], first row global t0 - lo.
 // Rows (not doubles):  recv from r-1 into ext [0, lo), send own [0, lo) to r-1;

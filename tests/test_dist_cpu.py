@@ -191,3 +191,35 @@ def test_plans_cover_everything():
     assert ls.halo_plan(133, 8, 7, 6) == (117, 16, 6, 0)
     with pytest.raises(ls.LSError):
         ls.halo_plan(10, 8, 0, 6)   # slabs of 1-2 rows are thinner than the halo
+
+
+@pytest.mark.parametrize("nt,Ns,world", [(13, 30, 2), (17, 45, 3), (9, 23, 4), (20, 7, 8), (5, 64, 5)])
+def test_fused_a2a_dest_equals_nccl_plan(nt, Ns, world):
+    """The fused all-to-all's per-element destinations (ls_a2a_dest = the addressing of the
+    peer-memory epilogues) move every element exactly where the NCCL path (pack map +
+    all-to-all plan + receive layout) puts it, forward (slab -> chunk, padded rows of
+    4*ceil(len/4)) and backward (chunk -> slab)."""
+    import paper_1809_10026_b200 as ls
+    rng = np.random.default_rng(nt * 100 + Ns)
+    g = rng.standard_normal((nt, Ns))
+    chunks = [ls.partition(Ns, world, h) for h in range(world)]
+    slabs = [ls.partition(nt, world, r) for r in range(world)]
+    # NCCL path: receiver h holds [n_t][len_h] = the columns of its chunk for every time
+    ref_chunk = [g[:, c0:c0 + ln] for (c0, ln) in chunks]
+    fused = [np.full((nt, max(4 * ((ln + 3) // 4), 1)), np.nan) for (_, ln) in chunks]
+    for r, (t0, ntl) in enumerate(slabs):
+        for t in range(ntl):
+            for s in range(Ns):
+                h, off = ls.a2a_dest(nt, Ns, world, r, 0, t, s)
+                fused[h].ravel()[off] = g[t0 + t, s]
+    for h, (c0, ln) in enumerate(chunks):
+        np.testing.assert_array_equal(fused[h][:, :ln], ref_chunk[h])
+    # backward: every chunk element back into the owner's slab
+    slab_bufs = [np.full((ntl, Ns), np.nan) for (_, ntl) in slabs]
+    for h, (c0, ln) in enumerate(chunks):
+        for t in range(nt):
+            for j in range(ln):
+                r, off = ls.a2a_dest(nt, Ns, world, h, 1, t, j)
+                slab_bufs[r].ravel()[off] = g[t, c0 + j]
+    for r, (t0, ntl) in enumerate(slabs):
+        np.testing.assert_array_equal(slab_bufs[r], g[t0:t0 + ntl])

@@ -86,6 +86,8 @@ def test_fd_apply_matches_oracle(torch_cuda, d, p, n_elems, seed):
 
 
 VARIANT_CASES = FD_CASES + [
+    (1, 2, [121, 125]),         # n = 121 / 126: k-step buckets wider than ceil(n/4) (33 vs 31, 32)
+    (2, 3, [118, 5, 120]),      # n_1 = 119, n_t = 122
     (3, 6, [9, 7, 12, 10]),     # Q = 13 odd, n_t = 15
     (2, 2, [130, 7, 129]),      # n_1 = 130 (register-direct bucket), odd Q, n_t = 130
     (3, 2, [128, 3, 2, 131]),   # n_1 = 128, n_t = 132: FAST strided time mode (Q % 4 == 0)
@@ -377,6 +379,40 @@ def test_fd_apply_slab_chunk_decomposition(torch_cuda, fdk, d, p, n_elems, world
     for (t0, ntl) in slabs:
         out = torch.empty(ntl, Ns, dtype=torch.float64, device="cuda")
         ctx.fd_stage(2, back[t0:t0 + ntl].contiguous(), out, ntl)
+        z[t0:t0 + ntl] = out
+    z_ref = fd.fd_apply(r, fdd)
+    assert _rel(z.cpu().numpy().reshape(r.shape), z_ref) <= TOL
+
+
+# the scattering epilogue is a FAST-path variant: n_1 ... n_{d-1} multiple of 4
+@pytest.mark.parametrize("d,p,n_elems,world", [(3, 3, [5, 9, 6, 21], 4), (2, 2, [12, 25, 40], 3),
+                                                (3, 6, [130, 2, 3, 9], 2), (2, 4, [6, 30, 17], 8)])
+def test_fd_apply_fused_a2a_emulated(torch_cuda, d, p, n_elems, world):
+    """The fused all-to-all path of the distributed fd_apply (LS_TUNE_A2A = 1), emulated rank
+    by rank on one GPU: the scattering epilogues (fd_apply_scatter) write into per-rank
+    receive buffers exactly as they write into peer memory in a multi-GPU run; the
+    barriers are replaced by running the ranks one after the other.  Against the oracle."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    _, _, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 19)
+    nt = ctx.shape[0]
+    Ns = int(np.prod(ctx.shape[1:]))
+    rg = torch.from_numpy(r).cuda().reshape(nt, Ns)
+    slabs = [ls.partition(nt, world, g) for g in range(world)]
+    chunks = [ls.partition(Ns, world, h) for h in range(world)]
+    nan = float("nan")
+    chunk_bufs = [torch.full((nt, 4 * ((ln + 3) // 4)), nan, dtype=torch.float64, device="cuda") for (_, ln) in chunks]
+    for g, (t0, ntl) in enumerate(slabs):
+        ctx.fd_scatter(0, rg[t0:t0 + ntl].contiguous(), ntl, 0, world, g, chunk_bufs)
+    slab_bufs = [torch.full((ntl, Ns), nan, dtype=torch.float64, device="cuda") for (_, ntl) in slabs]
+    for h, (c0, ln) in enumerate(chunks):
+        ctx.fd_scatter(1, chunk_bufs[h], c0, ln, world, h, slab_bufs)
+    z = torch.empty(nt, Ns, dtype=torch.float64, device="cuda")
+    for g, (t0, ntl) in enumerate(slabs):
+        out = torch.empty(ntl, Ns, dtype=torch.float64, device="cuda")
+        ctx.fd_stage(2, slab_bufs[g], out, ntl)
         z[t0:t0 + ntl] = out
     z_ref = fd.fd_apply(r, fdd)
     assert _rel(z.cpu().numpy().reshape(r.shape), z_ref) <= TOL
