@@ -194,6 +194,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4])
     ap.add_argument("--no-extras", action="store_true", help="skip PCG / config-3 / cpu extras")
+    ap.add_argument("--a2a", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL all-to-all (default) or the fused peer-memory epilogues (LS_TUNE_A2A)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -221,6 +223,8 @@ def main():
         ctx = ls.Context(d, p, n_elems)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
+    if world > 1 and args.a2a == "fused":
+        ctx.tune(4, 1)  # collective: every rank enables it
 
     # seeded residual, generated globally and scattered by slab (same tensor for every N)
     r_host = synth.residual(ctx.global_shape, 0)[ctx.t0:ctx.t0 + ctx.nt_local]
@@ -302,7 +306,8 @@ def main():
             "config": {"workload": f"config{args.config}", "d": d, "p": p, "n_el": n_el,
                        "n_s": w["n_s"], "n_t": w["n_t"], "N": w["N"],
                        "l2": f"inputs larger than L2 ({w['N'] * 8 / 1e9:.2f} GB per vector vs 126 MB)",
-                       "parallelism": f"time-slab x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"time-slab x{world}" if world > 1 else "single GPU",
+                       "all_to_all": args.a2a if world > 1 else None},
             "gflops_algorithmic": w["flops"] / (ms * 1e-3) / 1e9,
             "fp64_roofline_frac": round(w["flops"] / (ms * 1e-3) / 1e12 / (FP64_PEAK_TFLOPS * world), 4),
             "roofline": roof,

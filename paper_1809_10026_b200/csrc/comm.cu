@@ -50,9 +50,12 @@ __global__ void a2a_barrier_kernel(int* const* peer_flags, const int* my_flags, 
   const int h = threadIdx.x;
   __threadfence_system();
   if (h < world) st_release_sys(peer_flags[h] + me, epoch);
-  if (h < world)
-    while (ld_acquire_sys(my_flags + h) < epoch) {
-    }
+  if (h < world) {
+    // bounded spin (~9 s): a peer that never arrives fails the launch instead of hanging the GPU
+    const long long t0 = clock64();
+    while (ld_acquire_sys(my_flags + h) < epoch)
+      if (clock64() - t0 > (1LL << 34)) __trap();
+  }
 }
 
 int Comm::setup_fused(double* chunk_buf, double* slab_buf) {
