@@ -183,7 +183,9 @@ int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
 /*
  * fd_apply_host -- fd_apply with HOST vectors: copies r host->device, runs
  * fd_apply, copies z device->host, synchronises.  The end-to-end entry point
- * of the public API (bench.py "e2e").
+ * of the public API (bench.py "e2e").  Single-GPU contexts pipeline the copies
+ * over 8 time-slice chunks on a second stream (the copies overlap the spatial
+ * modes); pinned host memory is needed for the overlap.
  */
 int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host);
 

@@ -72,6 +72,9 @@ struct ls_ctx {
   double* frag_time = nullptr;                        // mats K_t, M_t
   int n1p = 0;                 // padded direction-1 row of the v3 intermediates
   double** scatter_tab = nullptr;  // fd_apply_scatter: device copy of the caller's table
+  // fd_apply_host pipeline: copy stream + events (H2D / D2H per time-slice chunk)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t hev[17] = {};
   double** scatter_stage = nullptr;  // pinned host staging of that table
   double* xT_pad = nullptr;    // v3: the last time slice of x in the padded layout
 
@@ -114,6 +117,9 @@ struct ls_ctx {
     for (void* a : allocs) cudaFree(a);
     if (h_scal) cudaFreeHost(h_scal);
     if (scatter_stage) cudaFreeHost(scatter_stage);
+    for (auto e : hev)
+      if (e) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
   int alloc(double** ptr, size_t count) {
     void* v = nullptr;
@@ -1285,6 +1291,43 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
 extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) {
   if (!ctx || !r_host || !z_host) return LS_EINVAL;
   const size_t bytes = size_t(ctx->Nl) * sizeof(double);
+  constexpr int NCH = 8;
+  if (ctx->world == 1 && ctx->ntl >= NCH) {
+    // pipelined over NCH time-slice chunks (the spatial modes act slice by slice): the
+    // H2D copy of chunk k+1 overlaps the forward spatial modes of chunk k, the D2H copy of
+    // chunk k overlaps the backward spatial modes of chunk k+1; the time mode needs all.
+    if (!ctx->copy_stream) {
+      LS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->hev) LS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t Ns = ctx->Ns;
+    double *A = ctx->tmp[0], *B = ctx->tmp[1], *C = ctx->tmp[2], *R = ctx->pr, *Z = ctx->pz;
+    LS_CUDA(cudaEventRecord(ctx->hev[16], ctx->stream));  // earlier work on the context stream
+    LS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[16], 0));
+    for (int k = 0; k < NCH; ++k) {
+      int64_t off, rows;
+      split_part(ctx->ntl, NCH, k, &off, &rows);
+      LS_CUDA(cudaMemcpyAsync(R + off * Ns, r_host + off * Ns, size_t(rows * Ns) * sizeof(double),
+                              cudaMemcpyHostToDevice, ctx->copy_stream));
+      LS_CUDA(cudaEventRecord(ctx->hev[k], ctx->copy_stream));
+      LS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->hev[k], 0));
+      LS_CHECK(spatial_modes(ctx, R + off * Ns, A + off * Ns, B + off * Ns, C + off * Ns, uint64_t(rows), true));
+    }
+    LS_CHECK(launch_mode(ctx, A, B, ctx->Wf[3], ctx->nt, 1, Ns, true, ctx->lam[3], ctx->lam_s));
+    LS_CHECK(launch_mode(ctx, B, C, ctx->Wb[3], ctx->nt, 1, Ns, false));
+    for (int k = 0; k < NCH; ++k) {
+      int64_t off, rows;
+      split_part(ctx->ntl, NCH, k, &off, &rows);
+      LS_CHECK(spatial_modes(ctx, C + off * Ns, Z + off * Ns, A + off * Ns, B + off * Ns, uint64_t(rows), false));
+      LS_CUDA(cudaEventRecord(ctx->hev[NCH + k], ctx->stream));
+      LS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->hev[NCH + k], 0));
+      LS_CUDA(cudaMemcpyAsync(z_host + off * Ns, Z + off * Ns, size_t(rows * Ns) * sizeof(double),
+                              cudaMemcpyDeviceToHost, ctx->copy_stream));
+    }
+    LS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    LS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LS_OK;
+  }
   LS_CUDA(cudaMemcpyAsync(ctx->pr, r_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
   LS_CHECK(fd_apply(ctx, ctx->pr, ctx->pz));
   LS_CUDA(cudaMemcpyAsync(z_host, ctx->pz, bytes, cudaMemcpyDeviceToHost, ctx->stream));

@@ -243,9 +243,13 @@ def test_pcg_zero_rhs(torch_cuda):
     assert st["iters"] == 0 and torch.count_nonzero(x).item() == 0
 
 
-def test_fd_apply_host_roundtrip(torch_cuda):
-    ctx = _ctx(2, 3, [12, 10, 9])
-    _, _, fdd = _oracle(2, 3, [12, 10, 9])
+@pytest.mark.parametrize("d,p,n_elems", [(2, 3, [12, 10, 9]),      # n_t = 11: pipelined copies
+                                         (3, 2, [5, 6, 7, 4]),       # n_t = 5 < 8 chunks: plain path
+                                         (1, 4, [30, 60])])
+def test_fd_apply_host_roundtrip(torch_cuda, d, p, n_elems):
+    """fd_apply_host (host buffers; chunked H2D / compute / D2H pipeline when n_t >= 8)."""
+    ctx = _ctx(d, p, n_elems)
+    _, _, fdd = _oracle(d, p, n_elems)
     r = synth.residual(ctx.shape, 2)
     z = np.empty_like(r)
     ctx.fd_apply_host(r, z)
