@@ -68,7 +68,13 @@ struct MV3Geom {
   static constexpr int NKB = P <= 4 ? 4 : 6;
   // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 2 for 2 or 3
   // (the 2-input pass runs 2 CTAs per SM within 128 registers)
-  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : 2;
+#ifndef MV3_AHEAD2
+#define MV3_AHEAD2 2
+#endif
+#ifndef MV3_AHEAD3
+#define MV3_AHEAD3 2
+#endif
+  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : MV3IO<KIND>::NIN == 2 ? MV3_AHEAD2 : MV3_AHEAD3;
   static constexpr int RING = NKB + 2 * AHEAD;
   static constexpr int G = RING / 2;  // m-tiles per unrolled group
 };
@@ -87,7 +93,10 @@ __device__ __forceinline__ double2 mv3_ld2(const double* p) {
 // two CTAs per SM for the one- and two-input passes (latency hiding; <= 128 registers)
 template <int KIND>
 struct MV3Occ {
-  static constexpr int CTAS = (KIND == MV3_TIME || KIND == MV3_DIR || KIND == MV3_DIR_A) ? 2 : 1;
+#ifndef MV3_DIR_CTAS
+#define MV3_DIR_CTAS 2
+#endif
+  static constexpr int CTAS = (KIND == MV3_TIME) ? 2 : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? MV3_DIR_CTAS : 1;
 };
 
 template <int P, int NT, int KIND, bool MODE1, bool FAST>

@@ -11,7 +11,10 @@ size_t mv3_frag_count(int p, int n, int nmat) { return size_t(nmat) * ((n + 7) /
 
 template <int P, int KIND, bool MODE1, bool FAST>
 static cudaError_t launch(const MV3Args& a, int num_sms, cudaStream_t s) {
-  constexpr int NT = 2;
+#ifndef MV3_NT
+#define MV3_NT 2
+#endif
+  constexpr int NT = MV3_NT;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(mv3_band_kernel<P, NT, KIND, MODE1, FAST>,
@@ -32,7 +35,7 @@ static cudaError_t run_pass(const MV3Pass& ps, int num_sms, cudaStream_t s) {
   const MV3Args& a = ps.args;
   // NT = 2: 2-column loads / 4-column stores stay inside one row and 16-byte aligned
   const uint32_t qo = a.Qout ? a.Qout : a.Q;
-  const bool fast = !ps.mode1 && (a.Q % 4 == 0) && (qo % 4 == 0) &&
+  const bool fast = !ps.mode1 && (a.Q % (2 * MV3_NT) == 0) && (qo % (2 * MV3_NT) == 0) &&
                     (a.map_n1 == 0 || (a.map_n1 % 2 == 0 && a.map_n1p % 4 == 0));
   switch (ps.kind) {
     case MV3_TIME: return fast ? launch<P, MV3_TIME, false, true>(a, num_sms, s) : launch<P, MV3_TIME, false, false>(a, num_sms, s);
