@@ -125,6 +125,106 @@ def _matvec_rank(rank, world, d, p, ne):
     return float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
 
 
+def _dist_fd(r_slab, rank, world, fdd, d, gshape):
+    """One rank's share of the distributed fd_apply (comm_fd_apply's NCCL schedule, over gloo)."""
+    import paper_1809_10026_b200 as ls
+    nt = gshape[0]
+    Ns = int(np.prod(gshape[1:]))
+    t0, ntl = ls.partition(nt, world, rank)
+    x = r_slab.copy()
+    for k in range(1, d + 1):
+        x = fd.mode_apply(x, fdd["U_s"][k - 1].T, d + 1 - k)
+    pos = ls.pack_map(ntl, Ns, world)
+    send = np.empty(ntl * Ns)
+    send[pos] = x.ravel()
+    plan = ls.a2a_plan(nt, Ns, world, rank)
+    c0, clen = ls.partition(Ns, world, rank)
+    recv = torch.empty(nt * clen, dtype=torch.float64)
+    dist.all_to_all_single(recv, torch.from_numpy(send), output_split_sizes=plan["recv_cnt"].tolist(),
+                           input_split_sizes=plan["send_cnt"].tolist())
+    chunk = recv.numpy().reshape(nt, clen)
+    lam_s = (fd.divisor(fdd) - fdd["lam_t"].reshape((-1,) + (1,) * d))[0].ravel()
+    y = fdd["U_t"] @ ((fdd["U_t"].T @ chunk) / (fdd["lam_t"][:, None] + lam_s[None, c0:c0 + clen]))
+    back = torch.empty(ntl * Ns, dtype=torch.float64)
+    dist.all_to_all_single(back, torch.from_numpy(np.ascontiguousarray(y).ravel()),
+                           output_split_sizes=plan["send_cnt"].tolist(), input_split_sizes=plan["recv_cnt"].tolist())
+    z = back.numpy()[pos].reshape((ntl,) + gshape[1:])
+    for k in range(d, 0, -1):
+        z = fd.mode_apply(z, fdd["U_s"][k - 1], d + 1 - k)
+    return z
+
+
+def _dist_matvec(x_slab, rank, world, space, tf, p, gshape):
+    """One rank's share of the distributed ls_matvec: halo exchange (comm.cu halo_exchange,
+    over gloo) then the slab-local operator on the extended slab."""
+    import paper_1809_10026_b200 as ls
+    nt = gshape[0]
+    t0, ntl, lo, hi = ls.halo_plan(nt, world, rank, p)
+    ext = np.zeros((lo + ntl + hi,) + gshape[1:])
+    ext[lo:lo + ntl] = x_slab
+    reqs, lo_buf, hi_buf = [], None, None
+    if lo > 0:
+        lo_buf = torch.empty(ext[:lo].shape, dtype=torch.float64)
+        reqs += [dist.irecv(lo_buf, src=rank - 1), dist.isend(torch.from_numpy(x_slab[:lo].copy()), dst=rank - 1)]
+    if hi > 0:
+        hi_buf = torch.empty(ext[lo + ntl:].shape, dtype=torch.float64)
+        reqs += [dist.irecv(hi_buf, src=rank + 1), dist.isend(torch.from_numpy(x_slab[ntl - hi:].copy()), dst=rank + 1)]
+    for q in reqs:
+        q.wait()
+    if lo > 0:
+        ext[:lo] = lo_buf.numpy()
+    if hi > 0:
+        ext[lo + ntl:] = hi_buf.numpy()
+    # the oracle's A on a zero-padded global tensor holding only the extended slab: exact on
+    # the own rows (the time band reaches at most p slices, all present)
+    g = np.zeros(gshape)
+    g[t0 - lo:t0 + ntl + hi] = ext
+    return op.apply_A(g, space, tf)[t0:t0 + ntl]
+
+
+def _pcg_rank(rank, world, d, p, ne):
+    """The distributed pcg_solve schedule: slab vectors, the two distributed operators above,
+    every dot product all-reduced (comm.cu allreduce_scalar), stopping test on the global
+    recurrence residual; against the single-process oracle PCG."""
+    import paper_1809_10026_b200 as ls
+    from oracle import rhs as orhs, pcg as opcg, bspline as bs
+    space, tf, fdd = _setup(d, p, ne)
+    nt = tf["Mt"].shape[0]
+    gshape = (nt,) + tuple(f["M"].shape[0] for f in reversed(space))
+    b = orhs.rhs(1, [bs.open_uniform_knots(n, p) for n in ne[:d]], p, bs.open_uniform_knots(ne[d], p), p)
+    t0, ntl = ls.partition(nt, world, rank)
+
+    def allsum(v):
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    bs_ = b[t0:t0 + ntl].copy()
+    bnorm = np.sqrt(allsum(np.vdot(bs_, bs_)))
+    x = np.zeros_like(bs_)
+    r = bs_.copy()
+    z = _dist_fd(r, rank, world, fdd, d, gshape)
+    pv = z.copy()
+    rho = allsum(np.vdot(r, z))
+    it = 0
+    while it < 100:
+        q = _dist_matvec(pv, rank, world, space, tf, p, gshape)
+        alpha = rho / allsum(np.vdot(pv, q))
+        x += alpha * pv
+        r -= alpha * q
+        it += 1
+        if np.sqrt(allsum(np.vdot(r, r))) <= 1e-8 * bnorm:
+            break
+        z = _dist_fd(r, rank, world, fdd, d, gshape)
+        rho_new = allsum(np.vdot(r, z))
+        pv = z + (rho_new / rho) * pv
+        rho = rho_new
+    xo, it_o, _, _ = opcg.pcg(lambda v: op.apply_A(v, space, tf), lambda v: fd.fd_apply(v, fdd), b)
+    assert it == it_o, (it, it_o)
+    ref = xo[t0:t0 + ntl]
+    return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
 def _worker(rank, world, port, fn_name, args, q):
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -165,6 +265,15 @@ def test_distributed_fd_schedule(world, d, p, ne):
 def test_distributed_matvec_halo(world, d, p, ne):
     errs = _run(world, "_matvec_rank", (d, p, ne))
     assert max(errs) <= 1e-12, errs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("d,p,ne", [(2, 2, [4, 5, 8]), (3, 2, [3, 3, 3, 8])])
+def test_distributed_pcg(world, d, p, ne):
+    """pcg_solve's distributed schedule (slab fd_apply with two all-to-alls, halo matvec,
+    all-reduced dots) reaches the single-process oracle's iterate at the same iteration."""
+    errs = _run(world, "_pcg_rank", (d, p, ne))
+    assert max(errs) <= 1e-10, errs
 
 
 def test_plans_cover_everything():
