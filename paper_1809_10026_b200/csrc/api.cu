@@ -377,17 +377,17 @@ static int make_split(ls_ctx* ctx, const std::vector<double>* const* mats, int n
 }
 
 // band blocks of `nm` matrices in m8n8k4 A-fragment order for matvec v3:
-// out[((m*MT + mt)*NKB + j)*32 + l] = scale[m] * W_m[8mt + l/4][4(2mt - OFF + j) + l%4]
+// out[((m*MT + mt)*NKB + j)*32 + l] = scale[m] * W_m[8mt + S0 + l/4][4(2mt - OFF + j) + l%4]
 static int make_frags(ls_ctx* ctx, const std::vector<double>* const* mats, const double* scale, int nm,
                       int n, int p, double** out) {
-  const int MT = (n + 7) / 8, NKB = mv3_nkb(p), OFF = mv3_off(p);
+  const int MT = mv3_mt(p, n), NKB = mv3_nkb(p), OFF = mv3_off(p), S0 = mv3_s0(p);
   std::vector<double> f(size_t(nm) * MT * NKB * 32, 0.0);
   for (int m = 0; m < nm; ++m)
     for (int mt = 0; mt < MT; ++mt)
       for (int j = 0; j < NKB; ++j)
         for (int l = 0; l < 32; ++l) {
-          const int row = 8 * mt + l / 4, col = 4 * (2 * mt - OFF + j) + l % 4;
-          if (row < n && col >= 0 && col < n && std::abs(row - col) <= p)
+          const int row = 8 * mt + S0 + l / 4, col = 4 * (2 * mt - OFF + j) + l % 4;
+          if (row >= 0 && row < n && col >= 0 && col < n && std::abs(row - col) <= p)
             f[((size_t(m) * MT + mt) * NKB + j) * 32 + l] = scale[m] * (*mats[m])[size_t(row) * n + col];
         }
   return upload(ctx, f, out);
@@ -1027,7 +1027,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.out[0] = Kx;
     a.out[1] = Mx;
     a.n = ctx->nt;
-    a.mt = (ctx->nt + 7) / 8;
+    a.mt = mv3_mt(P, ctx->nt);
     a.Q = uint32_t(ctx->Ns);
     a.Qout = uint32_t(Nsp);
     a.ncols = uint32_t(Nsp);
@@ -1039,8 +1039,9 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.s_rows = int(rows);
     a.t_first = int(t_first);
     a.nout = int(nout);
-    a.mt0 = int(t_first / 8);
-    a.mt1 = int((t_first + nout + 7) / 8);
+    const int S0 = mv3_s0(P);  // m-tiles covering the output band rows [t_first, t_first + nout)
+    a.mt0 = int((t_first - S0) / 8);
+    a.mt1 = int((t_first + nout - S0 + 7) / 8);
   }
   const int kd = d - 1;
   uint64_t Q = 1;
@@ -1062,7 +1063,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.tT = own_last ? int(tT) : -1;
     a.xT = own_last ? (d >= 2 ? ctx->xT_pad : x + (ctx->nt - 1 - s_first) * ctx->Ns) : nullptr;
     a.n = ctx->n[kd];
-    a.mt = (a.n + 7) / 8;
+    a.mt = mv3_mt(P, a.n);
     a.Q = uint32_t(Q);
     a.ncols = uint32_t(uint64_t(nout) * Q);
     a.mt0 = 0;
@@ -1082,7 +1083,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.out[1] = Mx;
     a.out[2] = ctx->tmp[5];
     a.n = ctx->n[1];
-    a.mt = (a.n + 7) / 8;
+    a.mt = mv3_mt(P, a.n);
     a.Q = uint32_t(n1p);
     a.ncols = uint32_t(uint64_t(nout) * ctx->n[2] * n1p);
     a.tT = -1;
@@ -1102,7 +1103,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     for (int m = 0; m < 3; ++m) a.in[m] = cur[m];
     a.out[0] = y;
     a.n = ctx->n[0];
-    a.mt = (a.n + 7) / 8;
+    a.mt = mv3_mt(P, a.n);
     a.Q = 1;
     a.ncols = uint32_t(uint64_t(nout) * (ctx->Ns / ctx->n[0]));
     a.in_fiber = n1p;   // padded intermediates

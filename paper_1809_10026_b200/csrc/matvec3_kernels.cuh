@@ -11,8 +11,8 @@
 //
 // Band product as DMMA.  A pass computes Y = W X along its direction for band
 // matrices W of half-bandwidth P: the 8 output rows of m-tile mt need input rows
-// [8mt - P, 8mt + 7 + P], i.e. the NKB k-steps 2mt - OFF .. 2mt - OFF + NKB - 1
-// (OFF = 1, NKB = 4 for P <= 4; OFF = 2, NKB = 6 for P <= 8).  The band blocks are
+// [8mt + S0 - P, 8mt + S0 + 7 + P] (S0 = (P mod 4) - 8 or 0 aligns that band on a
+// k-step), i.e. the NKB = 2 + ceil(P/2) k-steps 2mt - OFF .. 2mt - OFF + NKB - 1.  The band blocks are
 // precomputed on the host in m8n8k4 A-fragment order ([mat][mt][j][lane]) and
 // staged in shared memory once per CTA.  A warp owns a strip of 8*NT columns and
 // sweeps it top to bottom: B fragments (4 rows x 8 columns per k-step) come from
@@ -64,8 +64,12 @@ struct MV3IO {
 
 template <int P, int KIND>
 struct MV3Geom {
-  static constexpr int OFF = P <= 4 ? 1 : 2;
-  static constexpr int NKB = P <= 4 ? 4 : 6;
+  // m-tile mt covers output rows [8mt + S0, 8mt + S0 + 8) with S0 = (P mod 4) - 8 (or 0):
+  // its input band [8mt + S0 - P, 8mt + S0 + 7 + P] then starts on a k-step boundary, so
+  // it spans NKB = 2 + ceil(P/2) k-steps (p = 6: 5 instead of 6 for tiles at 8mt)
+  static constexpr int S0 = (P % 4) ? (P % 4) - 8 : 0;
+  static constexpr int OFF = (P - S0) / 4;  // first k-step of m-tile mt: 2mt - OFF
+  static constexpr int NKB = 2 + (P + 1) / 2;
   // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 2 for 2 or 3
   // (the 2-input pass runs 2 CTAs per SM within 128 registers)
 #ifndef MV3_AHEAD2
@@ -75,7 +79,7 @@ struct MV3Geom {
 #define MV3_AHEAD3 2
 #endif
   static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : MV3IO<KIND>::NIN == 2 ? MV3_AHEAD2 : MV3_AHEAD3;
-  static constexpr int RING = NKB + 2 * AHEAD;
+  static constexpr int RING = NKB + 2 * AHEAD + (NKB & 1);  // even: static slots per RING/2 m-tiles
   static constexpr int G = RING / 2;  // m-tiles per unrolled group
 };
 
@@ -255,8 +259,8 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
             for (int m = 0; m < NIN; ++m) loadB(ring[m][slot], m, ks);
           }
           // ---- store m-tile mt: rows 8mt + nq, columns cs .. cs + 2NT - 1
-          const int lrow = 8 * mt + nq - gout0;  // local output row (time pass: slab rows)
-          const int brow = 8 * mt + nq;
+          const int brow = 8 * mt + Gm::S0 + nq;  // band row
+          const int lrow = brow - gout0;          // local output row (time pass: slab rows)
           if (brow < n && lrow >= 0 && lrow < nout) {
 #pragma unroll
             for (int o = 0; o < NOUT; ++o) {
@@ -312,5 +316,7 @@ cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, i
 size_t mv3_frag_count(int p, int n, int nmat);  // doubles of one direction's fragment array
 int mv3_nkb(int p);
 int mv3_off(int p);
+int mv3_s0(int p);          // band row of the first m-tile's row 0 (<= 0)
+int mv3_mt(int p, int n);   // m-tiles covering [0, n)
 
 }  // namespace ls

@@ -5,9 +5,11 @@
 
 namespace ls {
 
-int mv3_nkb(int p) { return p <= 4 ? 4 : 6; }
-int mv3_off(int p) { return p <= 4 ? 1 : 2; }
-size_t mv3_frag_count(int p, int n, int nmat) { return size_t(nmat) * ((n + 7) / 8) * mv3_nkb(p) * 32; }
+int mv3_s0(int p) { return (p % 4) ? (p % 4) - 8 : 0; }
+int mv3_nkb(int p) { return 2 + (p + 1) / 2; }
+int mv3_off(int p) { return (p - mv3_s0(p)) / 4; }
+int mv3_mt(int p, int n) { return (n - mv3_s0(p) + 7) / 8; }
+size_t mv3_frag_count(int p, int n, int nmat) { return size_t(nmat) * mv3_mt(p, n) * mv3_nkb(p) * 32; }
 
 template <int P, int KIND, bool MODE1, bool FAST>
 static cudaError_t launch(const MV3Args& a, int num_sms, cudaStream_t s) {
