@@ -420,3 +420,47 @@ def test_fd_apply_fused_a2a_emulated(torch_cuda, d, p, n_elems, world):
         z[t0:t0 + ntl] = out
     z_ref = fd.fd_apply(r, fdd)
     assert _rel(z.cpu().numpy().reshape(r.shape), z_ref) <= TOL
+
+
+GUARD_CASES = [(3, 3, [6, 7, 5, 9]), (2, 6, [29, 3, 11]), (1, 2, [121, 125]), (3, 2, [3, 4, 2, 6]),
+               (2, 8, [130, 1, 14]), (3, 6, [128, 2, 3, 11])]
+
+
+def _guarded(torch, shape, fill, pad=4096):
+    """A tensor of `shape` inside a larger allocation whose other entries are `fill`
+    (compute-sanitizer is closed on this pool: NaN guards catch out-of-range reads that
+    reach a result, canaries catch out-of-range writes)."""
+    n = int(np.prod(shape))
+    big = torch.full((n + 2 * pad,), fill, dtype=torch.float64, device="cuda")
+    return big, big[pad:pad + n].view(shape), pad
+
+
+@pytest.mark.parametrize("d,p,n_elems", GUARD_CASES)
+def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
+    """Inputs embedded in NaN-filled allocations, outputs inside canary-filled ones, for
+    every FD kernel family and every matvec implementation: results match the oracle
+    (no NaN leaked in from outside the input) and the canaries are untouched."""
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    space, tf, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 23)
+    z_ref = fd.fd_apply(r, fdd)
+    y_ref = op.apply_A(r, space, tf)
+    canary = 1.2345e300
+    for fdk in (1, 2):
+        ctx.tune(1, fdk)
+        _, rin, _ = _guarded(torch, ctx.shape, float("nan"))
+        rin.copy_(torch.from_numpy(r))
+        obig, zout, pad = _guarded(torch, ctx.shape, canary)
+        ctx.fd_apply(rin, zout)
+        assert _rel(zout.cpu().numpy(), z_ref) <= TOL, fdk
+        assert bool((obig[:pad] == canary).all()) and bool((obig[pad + zout.numel():] == canary).all()), fdk
+    ctx.tune(1, 0)
+    for mv in (1, 2, 3):
+        ctx.tune(2, mv)
+        _, xin, _ = _guarded(torch, ctx.shape, float("nan"))
+        xin.copy_(torch.from_numpy(r))
+        obig, yout, pad = _guarded(torch, ctx.shape, canary)
+        ctx.matvec(xin, yout)
+        assert _rel(yout.cpu().numpy(), y_ref) <= 1e-12, mv
+        assert bool((obig[:pad] == canary).all()) and bool((obig[pad + yout.numel():] == canary).all()), mv
