@@ -53,6 +53,16 @@ def _traffic(cfg_id):
         return None, None
 
 
+def _config_dict(cfg_id, world, a2a="nccl"):
+    """The `config` object of the JSON line (identical for both arms)."""
+    w = workload(cfg_id)
+    return {"workload": f"config{cfg_id}", "d": w["d"], "p": w["p"], "n_el": w["n_el"],
+            "n_s": w["n_s"], "n_t": w["n_t"], "N": w["N"],
+            "l2": f"inputs larger than L2 ({w['N'] * 8 / 1e9:.2f} GB per vector vs 126 MB)",
+            "parallelism": f"time-slab x{world}" if world > 1 else "single GPU",
+            "all_to_all": a2a if world > 1 else None}
+
+
 def workload(cfg_id):
     c = synth.CONFIGS[cfg_id]
     d, p, n_el = c["d"], c["p"], c["n_el"]
@@ -172,13 +182,12 @@ def run_reference(args):
     N = int(np.prod(shape))
     cores = len(os.sched_getaffinity(0))
     val = N / dt
-    sample = (f"oracle fd_apply on config {args.config}'s spatial grid with time truncated to "
-              f"n_el_t=8 (n_t={shape[0]}, N={N}) per step")
+    sample = (f"oracle fd_apply (numpy tensordot, fp64) on config {args.config}'s spatial grid with the "
+              f"time direction truncated to n_el_t=8 (n_t={shape[0]}, N={N}) per step; DOF/s of that sample")
     line = {"impl": "reference", "metric": "fd_apply DOF/s (fp64)", "value": val, "unit": "DOF/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"config{args.config}-sample",
-                                            "d": d, "p": p, "n_el": n_el, "n_t": shape[0]},
+            "data": "synthetic", "config": _config_dict(args.config, args.gpus),
             "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -303,11 +312,7 @@ def main():
             "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config{args.config}", "d": d, "p": p, "n_el": n_el,
-                       "n_s": w["n_s"], "n_t": w["n_t"], "N": w["N"],
-                       "l2": f"inputs larger than L2 ({w['N'] * 8 / 1e9:.2f} GB per vector vs 126 MB)",
-                       "parallelism": f"time-slab x{world}" if world > 1 else "single GPU",
-                       "all_to_all": args.a2a if world > 1 else None},
+            "config": _config_dict(args.config, world, args.a2a),
             "gflops_algorithmic": w["flops"] / (ms * 1e-3) / 1e9,
             "fp64_roofline_frac": round(w["flops"] / (ms * 1e-3) / 1e12 / (FP64_PEAK_TFLOPS * world), 4),
             "roofline": roof,
