@@ -82,6 +82,14 @@ typedef struct {
 int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out);
 
 /*
+ * ls_setup_deg -- as ls_setup with separate degrees in space and time, p = (p_s, p_t)
+ * (PAPER.md 179-180; e.g. p_s = p_t + 1 as in Fig. 2b, PAPER.md 1132): p_s >= 2
+ * (Assumption 2), 1 <= p_t; n_k = n_el,k + p_s - 2, n_t = n_el,t + p_t - 1.  ls_matvec
+ * supports p_s, p_t <= 8.  ls_setup(d, p, ...) is ls_setup_deg(d, p, p, ...).
+ */
+int ls_setup_deg(int d, int p_s, int p_t, const int64_t* n_elems, ls_ctx** out);
+
+/*
  * ls_setup_dist -- as ls_setup, for rank `rank` of `world` processes (one
  * GPU each).  The time axis is split into contiguous slabs (uneven allowed);
  * fd_apply reshards slab <-> spatial chunk with two NCCL all-to-alls for the
@@ -92,6 +100,8 @@ int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out);
  */
 int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int world,
                   const void* nccl_unique_id, ls_ctx** out);
+int ls_setup_dist_deg(int d, int p_s, int p_t, const int64_t* n_elems, int rank, int world,
+                      const void* nccl_unique_id, ls_ctx** out);
 int ls_get_unique_id(void* out128);
 
 /*

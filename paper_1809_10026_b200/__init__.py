@@ -31,7 +31,8 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
-            "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest"]
+            "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
+            "ls_setup_dist_deg"]
 
 
 class PCGStats(ctypes.Structure):
@@ -63,6 +64,9 @@ def load_library(path=LIB_PATH):
     vp, i64p, dp = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p
     sig = {
         "ls_setup": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(vp)]),
+        "ls_setup_deg": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(vp)]),
+        "ls_setup_dist_deg": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, ctypes.c_int,
+                                             ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(vp)]),
         "ls_setup_dist": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i64p, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_char_p, ctypes.POINTER(vp)]),
         "ls_get_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
@@ -166,7 +170,8 @@ def sizes(n_el, p):
 
 
 class Context:
-    """One ls_ctx (one GPU).  ``n_elems``: d+1 element counts, directions 1..d then time."""
+    """One ls_ctx (one GPU).  ``p``: the degree, or (p_s, p_t) (ls_setup_deg); ``n_elems``:
+    d+1 element counts, directions 1..d then time."""
 
     def __init__(self, d, p, n_elems, rank=0, world=1, uid=None):
         import torch
@@ -177,13 +182,14 @@ class Context:
         ne = (ctypes.c_int64 * (d + 1))(*[int(v) for v in n_elems])
         h = ctypes.c_void_p()
         torch.cuda.init()
+        ps, pt = (p, p) if isinstance(p, int) else (int(p[0]), int(p[1]))
         if world == 1:
-            _check(lib.ls_setup(d, p, ne, ctypes.byref(h)), "ls_setup")
+            _check(lib.ls_setup_deg(d, ps, pt, ne, ctypes.byref(h)), "ls_setup_deg")
         else:
-            _check(lib.ls_setup_dist(d, p, ne, rank, world, uid, ctypes.byref(h)), "ls_setup_dist")
+            _check(lib.ls_setup_dist_deg(d, ps, pt, ne, rank, world, uid, ctypes.byref(h)), "ls_setup_dist_deg")
         self._h = h
         self._lib = lib
-        self.d, self.p = d, p
+        self.d, self.p, self.p_s, self.p_t = d, p, ps, pt
         self.n_elems = list(n_elems)
         nt, t0, ntl = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         ns = (ctypes.c_int64 * d)()

@@ -43,7 +43,8 @@ static constexpr int NMAX_STACK = 256;  // stride of stacked univariate vectors
 static constexpr int N_MAX = 136;       // largest supported univariate size (KS <= 34)
 
 struct ls_ctx {
-  int d = 0, p = 0;
+  int d = 0, p = 0;  // p: space degree p_s
+  int pt = 0;        // time degree p_t (PAPER.md 179-180: p = (p_s, p_t))
   int64_t n_el[4] = {0, 0, 0, 0};
   int n[3] = {1, 1, 1};  // n_1..n_d
   int nt = 0;
@@ -394,7 +395,7 @@ static int make_frags(ls_ctx* ctx, const std::vector<double>* const* mats, const
 }
 
 static int setup_common(ls_ctx* ctx) {
-  const int d = ctx->d, p = ctx->p;
+  const int d = ctx->d, p = ctx->p, pt = ctx->pt;
   int dev = 0;
   LS_CUDA(cudaGetDevice(&dev));
   LS_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -404,7 +405,7 @@ static int setup_common(ls_ctx* ctx) {
     ctx->n[k] = int(ctx->n_el[k] + p - 2);
     ctx->Ns *= ctx->n[k];
   }
-  ctx->nt = int(ctx->n_el[d] + p - 1);
+  ctx->nt = int(ctx->n_el[d] + pt - 1);
   for (int k = 0; k < d; ++k)
     if (ctx->n[k] > N_MAX) return LS_EINVAL;
   if (ctx->nt > N_MAX) return LS_EINVAL;
@@ -430,7 +431,7 @@ static int setup_common(ls_ctx* ctx) {
     ctx->hJ[k] = f.J;
     rc = gen_eig(f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
   }
-  Factors ft = time_factors(int(ctx->n_el[d]), p);
+  Factors ft = time_factors(int(ctx->n_el[d]), pt);
   ctx->hMt = ft.M;
   ctx->hKt = ft.K;
   if (rc == LS_OK) rc = gen_eig(ft.K, ft.M, ft.n, ctx->hlam[3], ctx->hU[3]);
@@ -459,8 +460,8 @@ static int setup_common(ls_ctx* ctx) {
     LS_CHECK(to_band(ctx, ctx->hK[k], ctx->n[k], p, &ctx->bK[k]));
     LS_CHECK(to_band(ctx, ctx->hJ[k], ctx->n[k], p, &ctx->bJ[k]));
   }
-  LS_CHECK(to_band(ctx, ctx->hMt, ctx->nt, p, &ctx->bMt));
-  LS_CHECK(to_band(ctx, ctx->hKt, ctx->nt, p, &ctx->bKt));
+  LS_CHECK(to_band(ctx, ctx->hMt, ctx->nt, pt, &ctx->bMt));
+  LS_CHECK(to_band(ctx, ctx->hKt, ctx->nt, pt, &ctx->bKt));
   // matvec v2 stencil splits (reading c18)
   for (int k = 0; k < d; ++k) {
     const std::vector<double>* mats[3] = {&ctx->hM[k], &ctx->hK[k], &ctx->hJ[k]};
@@ -468,7 +469,7 @@ static int setup_common(ls_ctx* ctx) {
   }
   {
     const std::vector<double>* mats[2] = {&ctx->hMt, &ctx->hKt};
-    LS_CHECK(make_split(ctx, mats, 2, ctx->nt, p, ctx->tsplit, false));
+    LS_CHECK(make_split(ctx, mats, 2, ctx->nt, pt, ctx->tsplit, false));
   }
   // matvec v3 band fragments
   for (int k = 0; k < d; ++k) {
@@ -479,10 +480,10 @@ static int setup_common(ls_ctx* ctx) {
   {
     const std::vector<double>* mats[2] = {&ctx->hKt, &ctx->hMt};
     const double scale[2] = {1.0, 1.0};
-    LS_CHECK(make_frags(ctx, mats, scale, 2, ctx->nt, p, &ctx->frag_time));
+    LS_CHECK(make_frags(ctx, mats, scale, 2, ctx->nt, pt, &ctx->frag_time));
   }
   // workspaces (halo rows for the distributed matvec: p slices each side)
-  const size_t halo = size_t(2 * p) * ctx->Ns;
+  const size_t halo = size_t(2 * pt) * ctx->Ns;  // time halo of the banded time factors
   // v3 matvec intermediates use 64-byte rows along direction 1 (d >= 2, n_1 >= 64):
   // unaligned 132-double rows made the strided and contiguous passes re-read ~50 %
   ctx->n1p = (d >= 2 && ctx->n[0] >= 64) ? (ctx->n[0] + 7) / 8 * 8 : ctx->n[0];
@@ -503,20 +504,22 @@ static int setup_common(ls_ctx* ctx) {
   return LS_OK;
 }
 
-static int validate(int d, int p, const int64_t* n_elems) {
-  if (d < 1 || d > 3 || p < 2 || n_elems == nullptr) return LS_EINVAL;
+static int validate(int d, int p, int pt, const int64_t* n_elems) {
+  // p_s >= 2 (Assumption 2, PAPER.md 218-223: C^1 in space); p_t >= 1
+  if (d < 1 || d > 3 || p < 2 || pt < 1 || n_elems == nullptr) return LS_EINVAL;
   for (int k = 0; k <= d; ++k)
     if (n_elems[k] < 1 || n_elems[k] > 100000) return LS_EINVAL;
   return LS_OK;
 }
 
-extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
+extern "C" int ls_setup_deg(int d, int p_s, int p_t, const int64_t* n_elems, ls_ctx** out) {
   if (!out) return LS_EINVAL;
   *out = nullptr;
-  LS_CHECK(validate(d, p, n_elems));
+  LS_CHECK(validate(d, p_s, p_t, n_elems));
   auto* ctx = new ls_ctx();
   ctx->d = d;
-  ctx->p = p;
+  ctx->p = p_s;
+  ctx->pt = p_t;
   for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
   int rc = setup_common(ctx);
   if (rc != LS_OK) {
@@ -527,25 +530,30 @@ extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
   return LS_OK;
 }
 
+extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
+  return ls_setup_deg(d, p, p, n_elems, out);
+}
+
 extern "C" int ls_get_unique_id(void* out128) {
   if (!out128) return LS_EINVAL;
   return comm_unique_id(out128);
 }
 
-extern "C" int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int world,
-                             const void* nccl_unique_id, ls_ctx** out) {
+extern "C" int ls_setup_dist_deg(int d, int p_s, int p_t, const int64_t* n_elems, int rank, int world,
+                                 const void* nccl_unique_id, ls_ctx** out) {
   if (!out || world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id))
     return LS_EINVAL;
   *out = nullptr;
-  LS_CHECK(validate(d, p, n_elems));
+  LS_CHECK(validate(d, p_s, p_t, n_elems));
   auto* ctx = new ls_ctx();
   ctx->d = d;
-  ctx->p = p;
+  ctx->p = p_s;
+  ctx->pt = p_t;
   ctx->rank = rank;
   ctx->world = world;
   for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
-  // every slab must be at least p time slices thick (halo of the banded time factors)
-  if (world > 1 && (n_elems[d] + p - 1) / world < p) {  // slab thinner than the time halo
+  // every slab must be at least p_t time slices thick (halo of the banded time factors)
+  if (world > 1 && (n_elems[d] + p_t - 1) / world < p_t) {
     delete ctx;
     return LS_EINVAL;
   }
@@ -560,6 +568,11 @@ extern "C" int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int
   }
   *out = ctx;
   return LS_OK;
+}
+
+extern "C" int ls_setup_dist(int d, int p, const int64_t* n_elems, int rank, int world,
+                             const void* nccl_unique_id, ls_ctx** out) {
+  return ls_setup_dist_deg(d, p, p, n_elems, rank, world, nccl_unique_id, out);
 }
 
 extern "C" int ls_layout(const ls_ctx* ctx, int64_t* n_t, int64_t* n_s, int64_t* t0,
@@ -632,7 +645,7 @@ extern "C" int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* 
       return spatial_modes(ctx, in, out, ctx->tmp[3], ctx->tmp[4], uint64_t(a), stage == 0);
     }
     case 1: {  // time mode U_t^T, /(lambda_t + Lambda_s), U_t on a chunk [n_t][b] at spatial offset a
-      if (a < 0 || b < 1 || a + b > ctx->Ns || int64_t(ctx->nt) * b > (ctx->Nl + 2 * ctx->p * ctx->Ns)) return LS_EINVAL;
+      if (a < 0 || b < 1 || a + b > ctx->Ns || int64_t(ctx->nt) * b > (ctx->Nl + 2 * ctx->pt * ctx->Ns)) return LS_EINVAL;
       double* mid = ctx->tmp[3];
       LS_CHECK(launch_mode(ctx, in, mid, ctx->Wf[3], ctx->nt, 1, uint64_t(b), true, ctx->lam[3], ctx->lam_s + a));
       return launch_mode(ctx, mid, out, ctx->Wb[3], ctx->nt, 1, uint64_t(b), false);
@@ -838,7 +851,8 @@ static int launch_band_p(ls_ctx* ctx, const BandArgs& a, int kind, int rows) {
 }
 
 static int launch_band(ls_ctx* ctx, const BandArgs& a, int kind, int rows) {
-  switch (ctx->p) {
+  switch (kind == 2 ? ctx->pt : ctx->p) {  // time kernel: p_t; direction kernels: p_s
+    case 1: return kind == 2 ? launch_band_p<1>(ctx, a, kind, rows) : LS_ENOTSUP;
     case 2: return launch_band_p<2>(ctx, a, kind, rows);
     case 3: return launch_band_p<3>(ctx, a, kind, rows);
     case 4: return launch_band_p<4>(ctx, a, kind, rows);
@@ -904,7 +918,7 @@ static void mv_set(MVArgs& a, int slot, const ls_ctx::Split& sp) {
 static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
                       int64_t t_first, int64_t nout) {
   const int d = ctx->d, P = ctx->p;
-  if (P < 2 || P > 8) return LS_ENOTSUP;  // ls_matvec supports p <= 8 (BASELINE configs: p <= 8)
+  if (P < 2 || P > 8 || ctx->pt < 2 || ctx->pt > 8) return LS_ENOTSUP;  // ls_matvec supports p <= 8 (BASELINE configs: p <= 8)
   double* Kx = ctx->tmp[0];
   double* Mx = ctx->tmp[1];
   double* A = ctx->tmp[2];
@@ -994,15 +1008,15 @@ static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     const int per_sm = (pl.smem_plane <= 113 * 1024) ? 2 : 1;  // register-bound at 2
     pl.grid_plane = unsigned(std::min<uint64_t>(items, uint64_t(ctx->num_sms) * per_sm));
   }
-  LS_CUDA(mv2_run(P, pl, &ctx->launches));
+  LS_CUDA(mv2_run(P, ctx->pt, pl, &ctx->launches));
   return LS_OK;
 }
 
 // ---- matvec v3 (matvec3_kernels.cuh): DMMA band passes time -> d -> ... -> 1 ----------
 static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
                       int64_t t_first, int64_t nout) {
-  const int d = ctx->d, P = ctx->p;
-  if (P < 2 || P > 8) return LS_ENOTSUP;
+  const int d = ctx->d, P = ctx->p, PT = ctx->pt;
+  if (P < 2 || P > 8 || PT < 2 || PT > 8) return LS_ENOTSUP;
   double* Kx = ctx->tmp[0];
   double* Mx = ctx->tmp[1];
   double* A = ctx->tmp[2];
@@ -1027,7 +1041,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.out[0] = Kx;
     a.out[1] = Mx;
     a.n = ctx->nt;
-    a.mt = mv3_mt(P, ctx->nt);
+    a.mt = mv3_mt(PT, ctx->nt);
     a.Q = uint32_t(ctx->Ns);
     a.Qout = uint32_t(Nsp);
     a.ncols = uint32_t(Nsp);
@@ -1039,7 +1053,7 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.s_rows = int(rows);
     a.t_first = int(t_first);
     a.nout = int(nout);
-    const int S0 = mv3_s0(P);  // m-tiles covering the output band rows [t_first, t_first + nout)
+    const int S0 = mv3_s0(PT);  // m-tiles covering the output band rows [t_first, t_first + nout)
     a.mt0 = int((t_first - S0) / 8);
     a.mt1 = int((t_first + nout - S0 + 7) / 8);
   }
@@ -1112,7 +1126,8 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.mt0 = 0;
     a.mt1 = a.mt;
   }
-  LS_CUDA(mv3_run(P, ps, np, ctx->num_sms, ctx->stream, &ctx->launches));
+  for (int i = 0; i < np; ++i) ps[i].p = (ps[i].kind == MV3_TIME) ? PT : P;
+  LS_CUDA(mv3_run(ps, np, ctx->num_sms, ctx->stream, &ctx->launches));
   return LS_OK;
 }
 
@@ -1123,9 +1138,10 @@ static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   //   p = 3: v1 (config 3: 0.81 ms vs v3 1.06, v2 1.16)
   //   p >= 4: v3, DMMA band passes (config 4: 12.0 ms vs v1 16.4; config 5 p=8: 5.04 vs 6.49,
   //           p=4: 3.96 vs 4.08)
-  if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 4))
+  //   (v2 / v3 have time passes for p_t >= 2 only; p_t = 1 runs v1)
+  if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 4 && ctx->pt >= 2))
     return mv3_launch(ctx, x, y, rows, s_first, t_first, nout);
-  const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2);
+  const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2 && ctx->pt >= 2);
   if (!v2) return matvec_block(ctx, x, y, rows, s_first, t_first, nout);
   return mv2_launch(ctx, x, y, rows, s_first, t_first, nout);
 }
@@ -1133,7 +1149,7 @@ static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
 // extended-slab geometry of this rank (halo rows of the time factors)
 static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
   int64_t t0, ntl;
-  halo_plan(ctx->nt, ctx->world, ctx->rank, ctx->p, &t0, &ntl, lo, hi);
+  halo_plan(ctx->nt, ctx->world, ctx->rank, ctx->pt, &t0, &ntl, lo, hi);
 }
 
 extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
@@ -1144,14 +1160,14 @@ extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   double* own = ctx->pp + lo * ctx->Ns;  // extended buffer [lo | own | hi]
   if (x != own)
     LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
-  LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->p));
+  LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->pt));
   return matvec_any(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
 }
 
 extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows,
                               double* y, int64_t t_first, int64_t nout) {
   if (!ctx || !x_ext || !y || !aligned8(x_ext) || !aligned8(y)) return LS_EINVAL;
-  const int64_t nt = ctx->nt, p = ctx->p;
+  const int64_t nt = ctx->nt, p = ctx->pt;  // the time band
   if (nout < 0 || t_first < 0 || t_first + nout > nt || s_rows < 0) return LS_EINVAL;
   if (nout > ctx->ntl) return LS_EINVAL;  // workspaces hold ntl (+ halo) slices
   // the stored rows must cover the time band of every output row (clipped to [0, n_t))
@@ -1177,7 +1193,7 @@ extern "C" int ls_rhs(ls_ctx* ctx, int kind, double* b) {
     std::copy(i2.begin(), i2.end(), stack.begin() + (3 + k) * NMAX_STACK);
   }
   const double pi = 3.14159265358979323846;
-  load_integrals(int(ctx->n_el[d]), ctx->p, false, kind == 0 ? 1 : 2, d * pi * pi, i0, i1, i2);
+  load_integrals(int(ctx->n_el[d]), ctx->pt, false, kind == 0 ? 1 : 2, d * pi * pi, i0, i1, i2);
   std::vector<double> G(2 * NMAX_STACK, 0.0);
   std::copy(i0.begin(), i0.end(), G.begin());
   std::copy(i1.begin(), i1.end(), G.begin() + NMAX_STACK);

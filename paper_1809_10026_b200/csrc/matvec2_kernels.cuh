@@ -333,6 +333,7 @@ struct MV2Plan {
   int num_sms;
 };
 // returns the CUDA error of the launches; *launches += number of kernels launched
-cudaError_t mv2_run(int p, const MV2Plan& plan, int64_t* launches);
+// p: space degree (direction passes), pt: time degree (time pass)
+cudaError_t mv2_run(int p, int pt, const MV2Plan& plan, int64_t* launches);
 
 }  // namespace ls

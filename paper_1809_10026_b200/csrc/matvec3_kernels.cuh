@@ -307,9 +307,10 @@ struct MV3Pass {
   MV3Args args;
   int kind;
   bool mode1;
+  int p;  // degree of this pass' direction (time pass: p_t)
 };
 // p: spline degree; returns the CUDA error; *launches += kernels launched
-cudaError_t mv3_run(int p, const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
+cudaError_t mv3_run(const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
 // dst[c'] = src[(c'/n1p)*n1 + c'%n1p] (0 in the padding) for one slice of Nsp padded columns
 cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, int n1p, cudaStream_t s,
                           int64_t* launches);

@@ -4,14 +4,20 @@
 namespace ls {
 
 template <int P>
-static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
+static cudaError_t run_time(const MV2Plan& pl, int64_t* launches) {
   constexpr int R = 8;
-  cudaError_t e;
   if (pl.grid_time) {
     mv_time_kernel<P, R><<<dim3(pl.grid_time, (pl.time.nout + R * MV_CY - 1) / (R * MV_CY)), dim3(32, MV_CY), 0, pl.stream>>>(pl.time);
     ++*launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaGetLastError();
   }
+  return cudaSuccess;
+}
+
+template <int P>
+static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
+  constexpr int R = 8;
+  cudaError_t e;
   if (pl.grid_dir) {
     const dim3 g(pl.grid_dir, (pl.dir.n + R * MV_CY - 1) / (R * MV_CY));
     if (pl.d == 1) mv_dir_kernel<P, R, true><<<g, dim3(32, MV_CY), 0, pl.stream>>>(pl.dir);
@@ -36,8 +42,20 @@ static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
   return cudaSuccess;
 }
 
-cudaError_t mv2_run(int p, const MV2Plan& plan, int64_t* launches) {
-  switch (p) {
+cudaError_t mv2_run(int p, int pt, const MV2Plan& plan, int64_t* launches) {
+  cudaError_t e;
+  switch (pt) {  // time pass: the time degree
+    case 2: e = run_time<2>(plan, launches); break;
+    case 3: e = run_time<3>(plan, launches); break;
+    case 4: e = run_time<4>(plan, launches); break;
+    case 5: e = run_time<5>(plan, launches); break;
+    case 6: e = run_time<6>(plan, launches); break;
+    case 7: e = run_time<7>(plan, launches); break;
+    case 8: e = run_time<8>(plan, launches); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  switch (p) {  // spatial passes: the space degree
     case 2: return run_p<2>(plan, launches);
     case 3: return run_p<3>(plan, launches);
     case 4: return run_p<4>(plan, launches);

@@ -64,10 +64,10 @@ cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, i
   return cudaGetLastError();
 }
 
-cudaError_t mv3_run(int p, const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches) {
+cudaError_t mv3_run(const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches) {
   for (int i = 0; i < npass; ++i) {
     cudaError_t e;
-    switch (p) {
+    switch (passes[i].p) {
       case 2: e = run_pass<2>(passes[i], num_sms, s); break;
       case 3: e = run_pass<3>(passes[i], num_sms, s); break;
       case 4: e = run_pass<4>(passes[i], num_sms, s); break;

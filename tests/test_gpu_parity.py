@@ -464,3 +464,80 @@ def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
         ctx.matvec(xin, yout)
         assert _rel(yout.cpu().numpy(), y_ref) <= 1e-12, mv
         assert bool((obig[:pad] == canary).all()) and bool((obig[pad + yout.numel():] == canary).all()), mv
+
+
+# separate degrees in space and time, p = (p_s, p_t) (PAPER.md 179-180;
+# p_s = p_t + 1 as in Fig. 2b, PAPER.md 1132)
+DEG_CASES = [(2, (3, 2), [8, 7, 9]), (3, (2, 1), [5, 6, 4, 7]), (3, (4, 3), [6, 5, 7, 8]),
+             (1, (5, 4), [20, 17]), (2, (8, 6), [20, 5, 30]), (3, (6, 5), [10, 9, 8, 12]),
+             (2, (2, 5), [9, 8, 11])]
+
+
+def _oracle_deg(d, ps, pt, n_elems):
+    space = [uv.space_factors(n, ps) for n in n_elems[:d]]
+    tf = uv.time_factors(n_elems[d], pt)
+    return space, tf, fd.setup(space, tf)
+
+
+@pytest.mark.parametrize("d,pp,n_elems", DEG_CASES)
+def test_degrees_fd_matvec_rhs_pcg(torch_cuda, d, pp, n_elems):
+    """p_s != p_t: setup sizes, fd_apply, every ls_matvec implementation that supports the
+    pair, ls_rhs and a PCG solve against the oracle."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    ps, pt = pp
+    ctx = ls.Context(d, pp, n_elems)
+    assert ctx.n_t == n_elems[d] + pt - 1 and ctx.n_s == [n + ps - 2 for n in n_elems[:d]]
+    space, tf, fdd = _oracle_deg(d, ps, pt, n_elems)
+    r = synth.residual(ctx.shape, 29)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert _rel(z, fd.fd_apply(r, fdd)) <= TOL
+    y_ref = op.apply_A(r, space, tf)
+    for mv in (1, 2, 3):
+        if mv > 1 and pt < 2:
+            continue
+        ctx.tune(2, mv)
+        y = ctx.matvec(torch.from_numpy(r).cuda()).cpu().numpy()
+        assert _rel(y, y_ref) <= 1e-12, mv
+    ctx.tune(2, 0)
+    b_ref = orhs.rhs(1, [bs.open_uniform_knots(n, ps) for n in n_elems[:d]], ps,
+                     bs.open_uniform_knots(n_elems[d], pt), pt)
+    b = ctx.rhs(1)
+    assert _rel(b.cpu().numpy(), b_ref) <= 1e-12
+    x, st = ctx.pcg(b, tol=1e-8)
+    xo, it, conv, _ = opcg.pcg(lambda v: op.apply_A(v, space, tf), lambda v: fd.fd_apply(v, fdd), b_ref)
+    assert st["status"] == 0 and st["iters"] == it
+    assert _rel(x.cpu().numpy(), xo) <= TOL
+
+
+def test_degrees_matvec_original_form_tiny(torch_cuda):
+    """p_s = 3, p_t = 2 against the dense ORIGINAL least-squares form (PAPER.md 406)."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    d, ps, pt, ne = 2, 3, 2, [3, 2, 3]
+    ctx = ls.Context(d, (ps, pt), ne)
+    A = op.dense_A_original_form([bs.open_uniform_knots(n, ps) for n in ne[:d]], ps,
+                                 bs.open_uniform_knots(ne[d], pt), pt)
+    x = synth.residual(ctx.shape, 31)
+    for mv in (1, 2, 3):
+        ctx.tune(2, mv)
+        y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy().ravel()
+        assert _rel(y, A @ x.ravel()) <= 1e-12, mv
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_degrees_matvec_slab(torch_cuda, variant):
+    """The halo of the distributed matvec is p_t slices wide."""
+    import paper_1809_10026_b200 as ls
+    torch = torch_cuda
+    d, ps, pt, ne, world = 2, 3, 6, [6, 5, 40], 4
+    ctx = ls.Context(d, (ps, pt), ne)
+    ctx.tune(2, variant)
+    space, tf, _ = _oracle_deg(d, ps, pt, ne)
+    x = synth.residual(ctx.shape, 37)
+    y_ref = op.apply_A(x, space, tf)
+    xg = torch.from_numpy(x).cuda()
+    for r in range(world):
+        t0, ntl, lo, hi = ls.halo_plan(ctx.shape[0], world, r, pt)
+        y = ctx.matvec_slab(xg[t0 - lo:t0 + ntl + hi].contiguous(), t0 - lo, t0, ntl).cpu().numpy()
+        assert _rel(y, y_ref[t0:t0 + ntl]) <= 1e-12, r
