@@ -191,6 +191,17 @@ int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
               ls_pcg_stats* st);
 
 /*
+ * ls_energy_error -- the least-squares functional at u_h = sum_i x_i B_i (PAPER.md
+ * 392-410): out4[0] = J = ||f - (d_t - Lap) u_h||^2_{L2(Q)} = ||f||^2 - 2 F(u_h) + A(u_h, u_h),
+ * out4[1] = ||f||^2 (closed form), out4[2] = F(u_h) = b.x, out4[3] = A(u_h, u_h) = x.A x,
+ * for the built-in forcing `kind` (ls_rhs).  With f = (d_t - Lap) u (kind 1, the cube's
+ * manufactured u), sqrt(J) is the error ||(d_t - Lap)(u - u_h)||, equivalent to the V_0 norm
+ * of Thm teo:a-priori (PAPER.md 600-610).  J is a difference of O(||f||^2) terms: it is
+ * resolved down to ~1e-13 ||f||^2.  x: device vector (this rank's slab).  Synchronous.
+ */
+int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4);
+
+/*
  * fd_apply_host -- fd_apply with HOST vectors: copies r host->device, runs
  * fd_apply, copies z device->host, synchronises.  The end-to-end entry point
  * of the public API (bench.py "e2e").  Single-GPU contexts pipeline the copies

@@ -32,7 +32,7 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
-            "ls_setup_dist_deg"]
+            "ls_setup_dist_deg", "ls_energy_error"]
 
 
 class PCGStats(ctypes.Structure):
@@ -84,6 +84,7 @@ def load_library(path=LIB_PATH):
                                            ctypes.POINTER(ctypes.c_double), i64p]),
         "ls_destroy": (None, [vp]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
+        "ls_energy_error": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.POINTER(ctypes.c_double)]),
         "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
         "fd_apply_scatter": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
@@ -274,6 +275,12 @@ class Context:
                                    int(max_iter), ctypes.byref(st))
         _check(code, "pcg_solve", ok=(LS_OK,) if raise_on_noconv else (LS_OK, LS_ENOCONV, LS_ENUMERIC))
         return x, st.as_dict()
+
+    def energy_error(self, kind, x):
+        """ls_energy_error: dict(J, f2, bx, xAx) of the least-squares functional at x."""
+        out = (ctypes.c_double * 4)()
+        _check(self._lib.ls_energy_error(self._h, int(kind), self._dev(x, "x"), out), "ls_energy_error")
+        return {"J": out[0], "f2": out[1], "bx": out[2], "xAx": out[3]}
 
     def fd_apply_host(self, r_host, z_host):
         """fd_apply on host tensors/arrays (pinned recommended); synchronous."""

@@ -1303,6 +1303,38 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
 }
 
 // ------------------------------------------------------------------------------------------
+// least-squares functional / energy error (PAPER.md 392-410)
+// ------------------------------------------------------------------------------------------
+extern "C" int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4) {
+  if (!ctx || !x || !out4 || !aligned8(x) || (kind != 0 && kind != 1)) return LS_EINVAL;
+  if (x == ctx->pz || x == ctx->pq) return LS_EINVAL;  // the library's scratch vectors
+  const double pi = 3.14159265358979323846;
+  const int d = ctx->d;
+  // ||f||^2 in closed form (T = 1, unit cube, reading c11): int sin^2(pi x) = 1/2 per direction
+  double f2 = std::ldexp(1.0, -d);
+  if (kind == 0) {
+    f2 *= (std::exp(2.0) - 1.0) / 2.0;
+  } else {
+    const double c = d * pi * pi;
+    f2 *= (0.5 + std::sin(2.0) / 4.0) + c * std::sin(1.0) * std::sin(1.0) + c * c * (0.5 - std::sin(2.0) / 4.0);
+  }
+  LS_CHECK(ls_rhs(ctx, kind, ctx->pz));         // b_i = F(B_i)
+  LS_CHECK(dot(ctx, ctx->pz, x, S_AUX));         // b . x = F(u_h)
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  LS_CHECK(read_scal(ctx));
+  const double bx = ctx->h_scal[S_AUX];
+  LS_CHECK(ls_matvec(ctx, x, ctx->pq));          // A x
+  LS_CHECK(dot(ctx, x, ctx->pq, S_AUX));         // x . A x = A(u_h, u_h)
+  LS_CHECK(read_scal(ctx));
+  const double xax = ctx->h_scal[S_AUX];
+  out4[0] = f2 - 2.0 * bx + xax;
+  out4[1] = f2;
+  out4[2] = bx;
+  out4[3] = xax;
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
 // host-buffer entry point, introspection, teardown
 // ------------------------------------------------------------------------------------------
 extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) {

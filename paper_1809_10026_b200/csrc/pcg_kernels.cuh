@@ -13,7 +13,7 @@ constexpr int RED_THREADS = 256;
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs; fixed for determinism
 
 // scalar slots
-enum { S_RHO0 = 0, S_RHO1 = 1, S_PQ = 2, S_RR = 3, S_BB = 4, S_ALPHA = 5, S_BETA = 6, S_NSLOT = 8 };
+enum { S_RHO0 = 0, S_RHO1 = 1, S_PQ = 2, S_RR = 3, S_BB = 4, S_ALPHA = 5, S_BETA = 6, S_AUX = 7, S_NSLOT = 8 };
 
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double sh[RED_THREADS / 32];

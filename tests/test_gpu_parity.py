@@ -541,3 +541,35 @@ def test_degrees_matvec_slab(torch_cuda, variant):
         t0, ntl, lo, hi = ls.halo_plan(ctx.shape[0], world, r, pt)
         y = ctx.matvec_slab(xg[t0 - lo:t0 + ntl + hi].contiguous(), t0 - lo, t0, ntl).cpu().numpy()
         assert _rel(y, y_ref[t0:t0 + ntl]) <= 1e-12, r
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("d,pp,n_elems", [(1, (2, 2), [4, 5]), (2, (3, 2), [3, 2, 4]), (2, (2, 2), [3, 3, 3])])
+def test_energy_error_matches_quadrature(torch_cuda, kind, d, pp, n_elems):
+    """ls_energy_error at the PCG solution against the oracle's direct space-time
+    quadrature of ||f - (d_t - Lap) u_h||^2 (PAPER.md 392-410)."""
+    import paper_1809_10026_b200 as ls
+    from oracle import error as oerr
+    ps, pt = pp
+    ctx = ls.Context(d, pp, n_elems)
+    x, st = ctx.pcg(ctx.rhs(kind), tol=1e-12)
+    e = ctx.energy_error(kind, x)
+    J = oerr.ls_functional_quadrature(x.cpu().numpy(), kind, [bs.open_uniform_knots(n, ps) for n in n_elems[:d]],
+                                      ps, bs.open_uniform_knots(n_elems[d], pt), pt)
+    assert abs(e["J"] - J) <= 1e-10 * e["f2"]
+    assert abs(e["f2"] - oerr.f_norm2(kind, d)) <= 1e-14 * e["f2"]
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_energy_error_convergence_rate(torch_cuda, p):
+    """The solve against the PDE: on the cube with u = prod sin(pi x_k) sin t (PAPER.md 1166),
+    the least-squares energy error ||(d_t - Lap)(u - u_h)|| of the PCG solution decays as
+    h^(p-1) for p_s = p_t = p (Thm teo:a-priori, PAPER.md 600-610; observed at PAPER.md 1131)."""
+    import paper_1809_10026_b200 as ls
+    errs = []
+    for n_el in (4, 8, 16):
+        ctx = ls.Context(2, p, [n_el] * 3)
+        x, st = ctx.pcg(ctx.rhs(1), tol=1e-12)
+        errs.append(np.sqrt(max(ctx.energy_error(1, x)["J"], 0.0)))
+    rates = [np.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert all(abs(r - (p - 1)) <= 0.3 for r in rates), (errs, rates)
