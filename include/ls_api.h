@@ -183,7 +183,8 @@ int ls_rhs(ls_ctx* ctx, int kind, double* b);
 /*
  * pcg_solve -- preconditioned CG for A x = b with P (PAPER.md 710-712, 1109):
  * x0 = 0, stop when ||r_k||_2 <= tol ||b||_2 (recurrence residual, reading c7)
- * or after max_iter A-products.  x is overwritten.  b == 0 returns x = 0 with
+ * or after max_iter A-products.  x is overwritten (x must not alias b: LS_EINVAL).
+ * b == 0 returns x = 0 with
  * 0 iterations.  Synchronous.  Returns LS_OK, LS_ENOCONV or LS_ENUMERIC (st
  * filled in all three cases; st may be NULL).
  */

@@ -1236,8 +1236,8 @@ static int read_scal(ls_ctx* ctx) {
 
 extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
                          ls_pcg_stats* st) {
-  if (!ctx || !b || !x || !aligned8(b) || !aligned8(x) || !(tol >= 0) || max_iter < 0)
-    return LS_EINVAL;
+  if (!ctx || !b || !x || b == x || !aligned8(b) || !aligned8(x) || !(tol >= 0) || max_iter < 0)
+    return LS_EINVAL;  // b == x: x is zeroed before b is read
   ls_pcg_stats s{0, 0.0, 0.0, LS_OK};
   const size_t bytes = size_t(ctx->Nl) * sizeof(double);
   LS_CUDA(cudaMemsetAsync(x, 0, bytes, ctx->stream));

@@ -573,3 +573,11 @@ def test_energy_error_convergence_rate(torch_cuda, p):
         errs.append(np.sqrt(max(ctx.energy_error(1, x)["J"], 0.0)))
     rates = [np.log2(errs[i] / errs[i + 1]) for i in range(2)]
     assert all(abs(r - (p - 1)) <= 0.3 for r in rates), (errs, rates)
+
+
+def test_pcg_rejects_aliasing(torch_cuda):
+    import paper_1809_10026_b200 as ls
+    ctx = _ctx(2, 2, [4, 4, 4])
+    b = ctx.rhs(1)
+    with pytest.raises(ls.LSError):
+        ctx.pcg(b, x=b)
