@@ -100,7 +100,13 @@ struct MV3Occ {
 #ifndef MV3_DIR_CTAS
 #define MV3_DIR_CTAS 2
 #endif
-  static constexpr int CTAS = (KIND == MV3_TIME) ? 2 : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? MV3_DIR_CTAS : 1;
+#ifndef MV3_TIME_CTAS
+#define MV3_TIME_CTAS 2
+#endif
+#ifndef MV3_MID_CTAS
+#define MV3_MID_CTAS 1
+#endif
+  static constexpr int CTAS = (KIND == MV3_TIME) ? MV3_TIME_CTAS : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? MV3_DIR_CTAS : MV3_MID_CTAS;
 };
 
 template <int P, int NT, int KIND, bool MODE1, bool FAST>
@@ -167,12 +173,16 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
         const size_t off = (m == 2 && (KIND == MV3_DIR || KIND == MV3_DIR_A))
                                ? size_t(boff[0] % Q)  // xT is one slice: (row, q)
                                : size_t(boff[0]);
+        if (NT == 1) {
+          v[0] = ok ? mv3_ld(src + off + size_t(sr) * rstride) : 0.0;
+        } else {
 #pragma unroll
-        for (int j = 0; j < NT; j += 2) {
-          double2 t = make_double2(0.0, 0.0);
-          if (ok) t = mv3_ld2(src + off + size_t(sr) * rstride + j);
-          v[j] = t.x;
-          v[j + 1] = t.y;
+          for (int j = 0; j + 1 < NT; j += 2) {
+            double2 t = make_double2(0.0, 0.0);
+            if (ok) t = mv3_ld2(src + off + size_t(sr) * rstride + j);
+            v[j] = t.x;
+            v[j + 1] = t.y;
+          }
         }
       } else {
 #pragma unroll
@@ -270,11 +280,15 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
                   const uint32_t pt = cs / Qo, q = cs - pt * Qo;
                   double* dst = Y + (size_t(pt) * nout + lrow) * Qo + q;
                   // accumulator column 2kq + h of n-tile j = physical column cs + NT*h + j
+                  if (NT == 1) {  // physical columns cs, cs + 1 = accumulator columns 2kq, 2kq + 1
+                    *reinterpret_cast<double2*>(dst) = make_double2(acc[o][0][0], acc[o][0][1]);
+                  } else {
 #pragma unroll
-                  for (int h = 0; h < 2; ++h)
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int j = 0; j < NT; j += 2)
-                      *reinterpret_cast<double2*>(dst + NT * h + j) = make_double2(acc[o][j][h], acc[o][j + 1][h]);
+                      for (int j = 0; j + 1 < NT; j += 2)
+                        *reinterpret_cast<double2*>(dst + NT * h + j) = make_double2(acc[o][j][h], acc[o][j + 1][h]);
+                  }
                 }
               } else {
 #pragma unroll
