@@ -22,10 +22,16 @@ PAPER.md by eye:
 * ``rhs``        -- b_i = F(B_i) = int int f (d_t B_i - Lap B_i) (PAPER.md 409).
 * ``pcg``        -- textbook preconditioned CG, x0 = 0, tol on the recurrence
                     residual (PAPER.md 710-712, 1109).
+* ``geometry``   -- mapped domains Omega = F([0,1]^d) (NURBS map, chain rule of
+                    PAPER.md 986-990): physical spatial factors M_s, L_s, J_s of
+                    eq:A_kron and the dense original-form A on tiny grids.
+* ``geo_precond``-- the geometry-aware preconditioner P^G (Sec. 4.4, PAPER.md
+                    969-1045): midpoint coefficients, separable fit, weighted
+                    univariate factors, diagonal scaling.
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py``; see DESIGN.md "Oracle pins".  No function is
 "parity unpinned".
 """
 
-from . import bspline, univariate, fd, operator, rhs, pcg  # noqa: F401
+from . import bspline, univariate, fd, operator, rhs, pcg, geometry, geo_precond  # noqa: F401
