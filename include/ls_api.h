@@ -203,6 +203,59 @@ int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
 int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4);
 
 /*
+ * ls_geometry -- a mapped spatial domain Omega = F([0,1]^d) (PAPER.md 226-250,
+ * Assumption 1; reading c19: a tensor-product NURBS map, rational when `weights`
+ * is given, e.g. the exact quarter annulus / revolved quarter annulus of Sec. 5,
+ * PAPER.md 1219).  Per direction k = 1..d (index k-1): degree[k-1] >= 1 and an
+ * open knot vector knots[k-1] on [0,1] of n_knots[k-1] entries, so
+ * m_k = n_knots - degree - 1 functions.  ctrl: host [m_1 m_2 .. m_d][d] control
+ * points in colex order (direction 1 fastest); weights: host [m_1 .. m_d], all
+ * > 0, or NULL for a polynomial spline map.  Copied by ls_setup_geo (caller keeps
+ * ownership).  The discrete space is the push-forward of the constrained B-spline
+ * basis (eq:disc_space, PAPER.md 291-300) on the uniform meshes of n_elems.
+ */
+typedef struct {
+  int degree[3];
+  int64_t n_knots[3];
+  const double* knots[3];
+  const double* ctrl;
+  const double* weights;
+} ls_geometry;
+
+#define LS_PRECOND_P 0  /* P of eq:preconditioner (parametric, PAPER.md 733) */
+#define LS_PRECOND_PG 1 /* P^G = D^{1/2} Pbar^G D^{1/2} of Sec. 4.4 (PAPER.md 969-1045) */
+
+/*
+ * ls_setup_geo -- single-GPU context on a mapped domain, T = 1.
+ *   ls_matvec: y = A x with A = K_t (x) M_s + M_t (x) J_s + W_t (x) L_s (eq:A_kron,
+ *     PAPER.md 686-703) and the PHYSICAL spatial factors [M_s]_ij = int_Omega B_i B_j,
+ *     [L_s]_ij = int grad B_i . grad B_j, [J_s]_ij = int Lap B_i Lap B_j, assembled on the
+ *     device at setup (chain rule of PAPER.md 986-990; p_s + 1 Gauss points per element
+ *     and direction, reading c6) and stored per row in a (2 p_s + 1)^d stencil layout
+ *     (3 (2 p_s + 1)^d N_s doubles).
+ *   fd_apply: z = P^{-1} r with precond = LS_PRECOND_P (the parametric P of the cube),
+ *     or z = (P^G)^{-1} r = D^{-1/2} Pbar^{-1} D^{-1/2} r with precond = LS_PRECOND_PG:
+ *     c_tau, c_k at the element midpoints, separable least-squares fit of their
+ *     logarithms (reading c21), factors interpolated piecewise linearly (reading c22),
+ *     weighted univariate matrices, Algorithm 1 for Pbar^G, D_ii = A_ii / Pbar^G_ii.
+ *   pcg_solve works unchanged; ls_rhs, ls_energy_error and the distributed / per-rank
+ *     entry points return LS_ENOTSUP (the caller supplies b).
+ * Limits: (p_s + 1)^d <= 343 local functions per element (d = 3: p_s <= 6).
+ * Errors: as ls_setup; LS_EINVAL also for an invalid map or a singular Jacobian at an
+ * element midpoint.
+ */
+int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
+                 ls_ctx** out);
+
+/*
+ * ls_geo_info -- out2[0] = max relative residual of the separable fit of c_tau, c_k at
+ * the element midpoints (0 for LS_PRECOND_P or an exactly separable map), out2[1] =
+ * number of stencil entries per spatial row ((2 p_s + 1)^d).  Errors: LS_EINVAL,
+ * LS_ENOTSUP (not a mapped-domain context).
+ */
+int ls_geo_info(const ls_ctx* ctx, double* out2);
+
+/*
  * fd_apply_host -- fd_apply with HOST vectors: copies r host->device, runs
  * fd_apply, copies z device->host, synchronises.  The end-to-end entry point
  * of the public API (bench.py "e2e").  Single-GPU contexts pipeline the copies

@@ -32,7 +32,15 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
-            "ls_setup_dist_deg", "ls_energy_error"]
+            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info"]
+
+LS_PRECOND_P, LS_PRECOND_PG = 0, 1
+
+
+class Geometry(ctypes.Structure):
+    """ls_geometry (include/ls_api.h): a tensor-product (NURBS) map F: [0,1]^d -> Omega."""
+    _fields_ = [("degree", ctypes.c_int * 3), ("n_knots", ctypes.c_int64 * 3),
+                ("knots", ctypes.c_void_p * 3), ("ctrl", ctypes.c_void_p), ("weights", ctypes.c_void_p)]
 
 
 class PCGStats(ctypes.Structure):
@@ -83,6 +91,9 @@ def load_library(path=LIB_PATH):
         "ls_profile_read": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double),
                                            ctypes.POINTER(ctypes.c_double), i64p]),
         "ls_destroy": (None, [vp]),
+        "ls_setup_geo": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(Geometry),
+                                        ctypes.c_int, ctypes.POINTER(vp)]),
+        "ls_geo_info": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "ls_energy_error": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.POINTER(ctypes.c_double)]),
         "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
@@ -172,9 +183,11 @@ def sizes(n_el, p):
 
 class Context:
     """One ls_ctx (one GPU).  ``p``: the degree, or (p_s, p_t) (ls_setup_deg); ``n_elems``:
-    d+1 element counts, directions 1..d then time."""
+    d+1 element counts, directions 1..d then time.  ``geometry``: a mapped spatial domain
+    (dict with ``degrees``, ``knots``, ``ctrl`` [prod m][d] colex, ``weights`` or None;
+    ls_setup_geo) with ``precond`` LS_PRECOND_P or LS_PRECOND_PG."""
 
-    def __init__(self, d, p, n_elems, rank=0, world=1, uid=None):
+    def __init__(self, d, p, n_elems, rank=0, world=1, uid=None, geometry=None, precond=LS_PRECOND_P):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1809_10026_b200 needs a CUDA device (no CPU fallback)")
@@ -184,7 +197,27 @@ class Context:
         h = ctypes.c_void_p()
         torch.cuda.init()
         ps, pt = (p, p) if isinstance(p, int) else (int(p[0]), int(p[1]))
-        if world == 1:
+        if geometry is not None:
+            if world != 1:
+                raise ValueError("mapped-domain contexts are single-GPU")
+            g = Geometry()
+            keep = []
+            for k in range(d):
+                kn = np.ascontiguousarray(geometry["knots"][k], dtype=np.float64)
+                keep.append(kn)
+                g.degree[k] = int(geometry["degrees"][k])
+                g.n_knots[k] = kn.size
+                g.knots[k] = kn.ctypes.data
+            ctrl = np.ascontiguousarray(geometry["ctrl"], dtype=np.float64)
+            keep.append(ctrl)
+            g.ctrl = ctrl.ctypes.data
+            if geometry.get("weights") is not None:
+                w = np.ascontiguousarray(geometry["weights"], dtype=np.float64)
+                keep.append(w)
+                g.weights = w.ctypes.data
+            _check(lib.ls_setup_geo(d, ps, pt, ne, ctypes.byref(g), int(precond), ctypes.byref(h)),
+                   "ls_setup_geo")
+        elif world == 1:
             _check(lib.ls_setup_deg(d, ps, pt, ne, ctypes.byref(h)), "ls_setup_deg")
         else:
             _check(lib.ls_setup_dist_deg(d, ps, pt, ne, rank, world, uid, ctypes.byref(h)), "ls_setup_dist_deg")
@@ -313,6 +346,12 @@ class Context:
         _check(self._lib.ls_get_factor(self._h, int(which), int(direction),
                                        ctypes.c_void_p(out.ctypes.data)), "ls_get_factor")
         return out
+
+    def geo_info(self):
+        """ls_geo_info: (separable-fit residual, stencil entries per row)."""
+        out = (ctypes.c_double * 2)()
+        _check(self._lib.ls_geo_info(self._h, out), "ls_geo_info")
+        return out[0], int(out[1])
 
     def tune(self, knob, value):
         """ls_tune: select an equivalent implementation (knob 1 = FD mode kernel:

@@ -20,6 +20,7 @@
 #include "matvec3_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
+#include "geo.hpp"
 
 using namespace ls;
 
@@ -101,6 +102,12 @@ struct ls_ctx {
   double* scal = nullptr;
   double* h_scal = nullptr;  // pinned
   double* rhs_buf = nullptr; // stacked univariate load vectors (device)
+  // mapped domain (ls_setup_geo): physical stencil factors, P^G scaling
+  std::unique_ptr<GeoMap> gmap;
+  std::unique_ptr<GeoDev> geo;
+  int precond = LS_PRECOND_P;
+  double* dm12 = nullptr;    // D^{-1/2} (N) for P^G
+  double fit_res = 0.0;
   std::vector<void*> allocs;
   // profiling of the mode kernel
   bool prof = false;
@@ -424,12 +431,21 @@ static int setup_common(ls_ctx* ctx) {
 
   // host assembly (PAPER.md 686-703, 738-757)
   int rc = LS_OK;
+  // P^G (PAPER.md 969-1045): weighted univariate pencils (M^G_k, J^G_k) for the eigen step
+  const bool pg = ctx->gmap && ctx->precond == LS_PRECOND_PG;
+  std::vector<double> mu[3], om[3], wM[3], wJ[3];
+  if (pg) LS_CHECK(pg_weights(*ctx->gmap, ctx->n_el, mu, om, &ctx->fit_res));
   for (int k = 0; k < d && rc == LS_OK; ++k) {
     Factors f = space_factors(int(ctx->n_el[k]), p);
     ctx->hM[k] = f.M;
     ctx->hK[k] = f.K;
     ctx->hJ[k] = f.J;
-    rc = gen_eig(f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
+    if (pg) {
+      weighted_space_factors(int(ctx->n_el[k]), p, mu[k], om[k], wM[k], wJ[k]);
+      rc = gen_eig(wJ[k], wM[k], f.n, ctx->hlam[k], ctx->hU[k]);
+    } else {
+      rc = gen_eig(f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
+    }
   }
   Factors ft = time_factors(int(ctx->n_el[d]), pt);
   ctx->hMt = ft.M;
@@ -500,6 +516,45 @@ static int setup_common(ls_ctx* ctx) {
   LS_CHECK(ctx->alloc(&ctx->scal, S_NSLOT));
   LS_CHECK(ctx->alloc(&ctx->rhs_buf, 6 * NMAX_STACK));
   LS_CUDA(cudaMallocHost(&ctx->h_scal, S_NSLOT * sizeof(double)));
+  if (ctx->gmap) {
+    // physical spatial factors on the device (eq:A_kron on Omega, PAPER.md 697-703)
+    ctx->geo.reset(new GeoDev());
+    ctx->geo->pt = pt;
+    LS_CHECK(geo_assemble(*ctx->geo, *ctx->gmap, d, p, ctx->n_el, ctx->stream, &ctx->launches));
+    if (pg) {
+      // diag(Pbar^G) = diag(K_t) (x) prod_k diag(M^G_k) + diag(M_t) (x) sum_k diag(J^G_k) prod_{j!=k} diag(M^G_j)
+      const int nt = ctx->nt;
+      std::vector<double> pdt(2 * size_t(nt)), pds(2 * size_t(ctx->Ns));
+      for (int t = 0; t < nt; ++t) {
+        pdt[t] = ctx->hKt[size_t(t) * nt + t];
+        pdt[nt + t] = ctx->hMt[size_t(t) * nt + t];
+      }
+      for (int64_t i = 0; i < ctx->Ns; ++i) {
+        int ik[3] = {0, 0, 0};
+        int64_t r = i;
+        for (int k = 0; k < d; ++k) {
+          ik[k] = int(r % ctx->n[k]);
+          r /= ctx->n[k];
+        }
+        double m = 1, j = 0;
+        for (int k = 0; k < d; ++k) {
+          const int n = ctx->n[k];
+          double jk = wJ[k][size_t(ik[k]) * n + ik[k]];
+          for (int l = 0; l < d; ++l)
+            if (l != k) jk *= wM[l][size_t(ik[l]) * ctx->n[l] + ik[l]];
+          j += jk;
+          m *= wM[k][size_t(ik[k]) * n + ik[k]];
+        }
+        pds[i] = m;
+        pds[ctx->Ns + i] = j;
+      }
+      double *dpdt, *dpds;
+      LS_CHECK(upload(ctx, pdt, &dpdt));
+      LS_CHECK(upload(ctx, pds, &dpds));
+      LS_CHECK(ctx->alloc(&ctx->dm12, ctx->Nl));
+      LS_CHECK(pg_scaling(*ctx->geo, ctx->bKt, ctx->bMt, nt, dpdt, dpds, ctx->dm12, ctx->stream, &ctx->launches));
+    }
+  }
   LS_CUDA(cudaDeviceSynchronize());
   return LS_OK;
 }
@@ -532,6 +587,51 @@ extern "C" int ls_setup_deg(int d, int p_s, int p_t, const int64_t* n_elems, ls_
 
 extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
   return ls_setup_deg(d, p, p, n_elems, out);
+}
+
+extern "C" int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
+                            ls_ctx** out) {
+  if (!out) return LS_EINVAL;
+  *out = nullptr;
+  LS_CHECK(validate(d, p_s, p_t, n_elems));
+  if (!geo || (precond != LS_PRECOND_P && precond != LS_PRECOND_PG)) return LS_EINVAL;
+  int nloc = 1;
+  for (int k = 0; k < d; ++k) nloc *= p_s + 1;
+  if (nloc > 343) return LS_EINVAL;
+  auto* ctx = new ls_ctx();
+  ctx->d = d;
+  ctx->p = p_s;
+  ctx->pt = p_t;
+  ctx->precond = precond;
+  for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
+  ctx->gmap.reset(new GeoMap());
+  int rc = geo_copy(geo, d, *ctx->gmap);
+  if (rc == LS_OK) {
+    // stencil storage 3 (2p+1)^d N_s on top of the usual estimate
+    int64_t Ns = 1, S = 1;
+    for (int k = 0; k < d; ++k) {
+      Ns *= n_elems[k] + p_s - 2;
+      S *= 2 * p_s + 1;
+    }
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) rc = LS_ECUDA;
+    else if (double(3 * S) * double(Ns) * 8.0 > 0.5 * double(fr)) rc = LS_ENOMEM;
+  }
+  if (rc == LS_OK) rc = setup_common(ctx);
+  if (rc != LS_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return LS_OK;
+}
+
+extern "C" int ls_geo_info(const ls_ctx* ctx, double* out2) {
+  if (!ctx || !out2) return LS_EINVAL;
+  if (!ctx->geo) return LS_ENOTSUP;
+  out2[0] = ctx->fit_res;
+  out2[1] = ctx->geo->S;
+  return LS_OK;
 }
 
 extern "C" int ls_get_unique_id(void* out128) {
@@ -617,8 +717,21 @@ static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0
   return LS_OK;
 }
 
+static int fd_core(ls_ctx* ctx, const double* r, double* z);
+
 extern "C" int fd_apply(ls_ctx* ctx, const double* r, double* z) {
   if (!ctx || !r || !z || !aligned8(r) || !aligned8(z)) return LS_EINVAL;
+  if (ctx->dm12) {
+    // P^G = D^{1/2} Pbar^G D^{1/2}: z = D^{-1/2} Pbar^{-1} D^{-1/2} r (PAPER.md 1040-1045)
+    double* rs = ctx->tmp[5];
+    LS_CHECK(scale_vec(ctx->dm12, r, rs, ctx->Nl, ctx->stream, &ctx->launches));
+    LS_CHECK(fd_core(ctx, rs, z));
+    return scale_vec(ctx->dm12, z, z, ctx->Nl, ctx->stream, &ctx->launches);
+  }
+  return fd_core(ctx, r, z);
+}
+
+static int fd_core(ls_ctx* ctx, const double* r, double* z) {
   double* A = ctx->tmp[0];
   double* B = ctx->tmp[1];
   double* C = ctx->tmp[2];
@@ -638,6 +751,7 @@ extern "C" int fd_apply(ls_ctx* ctx, const double* r, double* z) {
 // path runs between its all-to-alls; exposed for custom decompositions and for testing)
 extern "C" int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* out, int64_t a, int64_t b) {
   if (!ctx || !in || !out || in == out || !aligned8(in) || !aligned8(out)) return LS_EINVAL;
+  if (ctx->geo) return LS_ENOTSUP;
   switch (stage) {
     case 0:
     case 2: {  // spatial modes (forward / backward) on `a` time slices [a][N_s]
@@ -729,6 +843,7 @@ static int time_chunk_scatter(ls_ctx* ctx, const double* chunk, int64_t c0, int6
 extern "C" int fd_apply_scatter(ls_ctx* ctx, int stage, const double* in, int64_t a, int64_t b, int world, int me,
                                 double* const* dst_host) {
   if (!ctx || !in || !dst_host || world < 1 || world > 64 || me < 0 || me >= world || !aligned8(in)) return LS_EINVAL;
+  if (ctx->geo) return LS_ENOTSUP;
   if (ctx->d < 2) return LS_ENOTSUP;
   if (!ctx->scatter_tab) {
     LS_CHECK(ctx->alloc(reinterpret_cast<double**>(&ctx->scatter_tab), 64));
@@ -1154,6 +1269,9 @@ static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
 
 extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y || !aligned8(x) || !aligned8(y)) return LS_EINVAL;
+  if (ctx->geo)
+    return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, ctx->nt, x, y, ctx->tmp[3], ctx->tmp[4], ctx->stream,
+                      &ctx->launches);
   if (ctx->world == 1) return matvec_any(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
   int64_t lo, hi;
   ext_geom(ctx, &lo, &hi);
@@ -1167,6 +1285,7 @@ extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
 extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows,
                               double* y, int64_t t_first, int64_t nout) {
   if (!ctx || !x_ext || !y || !aligned8(x_ext) || !aligned8(y)) return LS_EINVAL;
+  if (ctx->geo) return LS_ENOTSUP;
   const int64_t nt = ctx->nt, p = ctx->pt;  // the time band
   if (nout < 0 || t_first < 0 || t_first + nout > nt || s_rows < 0) return LS_EINVAL;
   if (nout > ctx->ntl) return LS_EINVAL;  // workspaces hold ntl (+ halo) slices
@@ -1183,6 +1302,7 @@ extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first,
 // ------------------------------------------------------------------------------------------
 extern "C" int ls_rhs(ls_ctx* ctx, int kind, double* b) {
   if (!ctx || !b || !aligned8(b)) return LS_EINVAL;
+  if (ctx->geo) return LS_ENOTSUP;  // mapped domain: the caller supplies b
   if (kind != 0 && kind != 1) return LS_EINVAL;
   const int d = ctx->d;
   std::vector<double> stack(6 * NMAX_STACK, 0.0);  // S0[3], S2[3] ... G0, G1 stacked
@@ -1307,6 +1427,7 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
 // ------------------------------------------------------------------------------------------
 extern "C" int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4) {
   if (!ctx || !x || !out4 || !aligned8(x) || (kind != 0 && kind != 1)) return LS_EINVAL;
+  if (ctx->geo) return LS_ENOTSUP;  // mapped domain: the caller supplies b
   if (x == ctx->pz || x == ctx->pq) return LS_EINVAL;  // the library's scratch vectors
   const double pi = 3.14159265358979323846;
   const int d = ctx->d;
@@ -1341,7 +1462,7 @@ extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) 
   if (!ctx || !r_host || !z_host) return LS_EINVAL;
   const size_t bytes = size_t(ctx->Nl) * sizeof(double);
   constexpr int NCH = 8;
-  if (ctx->world == 1 && ctx->ntl >= NCH) {
+  if (ctx->world == 1 && ctx->ntl >= NCH && !ctx->dm12) {
     // pipelined over NCH time-slice chunks (the spatial modes act slice by slice): the
     // H2D copy of chunk k+1 overlaps the forward spatial modes of chunk k, the D2H copy of
     // chunk k overlaps the backward spatial modes of chunk k+1; the time mode needs all.

@@ -1,0 +1,606 @@
+// Device side of the mapped-domain path (geo.hpp).
+//
+// Layout of the physical spatial factors (PAPER.md 697-703) on the device: for each of
+// M_s, J_s, L_s a stencil array st[mat][o][i], i = the constrained spatial row (colex),
+// o = (o_1 + (2p+1)(o_2 + (2p+1) o_3)) with o_k = j_k - i_k + p the offset of the column
+// in direction k (tensor B-splines of degree p couple |j_k - i_k| <= p).  Entries whose
+// column falls outside the constrained grid stay 0.  Row-contiguous in i for every
+// offset, so consecutive threads (consecutive rows) read coalesced coefficients.
+//
+// Kernels:
+//   geo_qpoint_kernel   map derivatives at every tensor Gauss point -> |det J| w_q, J^{-1},
+//                       the first-order Laplacian coefficients b (chain rule, PAPER.md 986-990)
+//   geo_assemble_kernel one CTA per element: physical values / gradients / Laplacians of the
+//                       (p+1)^d local functions at a chunk of points in shared memory, pair
+//                       sums in registers, fp64 atomics into the stencil rows
+//   geo_time_kernel     t1 = K_t x, t2 = M_t x (banded, half-bandwidth p_t)
+//   geo_stencil_kernel  y = M_s t1 + J_s t2 (+ L_s x on the last slice: W_t = e e^T)
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "geo.hpp"
+#include "setup_host.hpp"
+
+namespace ls {
+
+#define GEO_CUDA(x)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      std::fprintf(stderr, "[libls] CUDA error %s at %s:%d\n", cudaGetErrorString(e_), \
+                   __FILE__, __LINE__);                                              \
+      return LS_ECUDA;                                                               \
+    }                                                                                \
+  } while (0)
+
+GeoDev::~GeoDev() {
+  for (void* a : allocs) cudaFree(a);
+}
+
+static int dalloc(std::vector<void*>& allocs, double** p, size_t n) {
+  void* v = nullptr;
+  if (cudaMalloc(&v, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) return LS_ENOMEM;
+  allocs.push_back(v);
+  *p = static_cast<double*>(v);
+  return LS_OK;
+}
+
+static int dupload(std::vector<void*>& allocs, const std::vector<double>& h, double** p) {
+  int rc = dalloc(allocs, p, h.size());
+  if (rc != LS_OK) return rc;
+  GEO_CUDA(cudaMemcpy(*p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// geometry at the quadrature points
+// ------------------------------------------------------------------------------------------
+struct GeoQArgs {
+  int d;
+  int nq[3];                 // Gauss points per direction (n_el (p+1))
+  int q[3];                  // geometry degrees
+  int m[3];                  // geometry functions per direction
+  const int* span[3];        // first non-zero geometry function at each point
+  const double* gt[3];       // [nq_k][q_k+1][3] values, 1st, 2nd derivatives
+  const double* wq[3];       // [nq_k] Gauss weights (element length included)
+  const double* ctrl;        // [prod m][d]
+  const double* w;           // [prod m]
+  double* out;               // [13][NQ]: wdet, Jinv[3][3] (row j = grad eta_j), b[3]
+  int64_t NQ;
+};
+
+__global__ void geo_qpoint_kernel(GeoQArgs a) {
+  for (int64_t qi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; qi < a.NQ;
+       qi += int64_t(gridDim.x) * blockDim.x) {
+    const int d = a.d;
+    int iq[3] = {0, 0, 0};
+    int64_t r = qi;
+    for (int k = 0; k < d; ++k) {
+      iq[k] = int(r % a.nq[k]);
+      r /= a.nq[k];
+    }
+    double N[3] = {0, 0, 0}, W = 0, dN[3][3] = {}, dW[3] = {}, hN[3][3][3] = {}, hW[3][3] = {};
+    const int c1n = a.q[0] + 1, c2n = d >= 2 ? a.q[1] + 1 : 1, c3n = d >= 3 ? a.q[2] + 1 : 1;
+    for (int c3 = 0; c3 < c3n; ++c3)
+      for (int c2 = 0; c2 < c2n; ++c2)
+        for (int c1 = 0; c1 < c1n; ++c1) {
+          const int cl[3] = {c1, c2, c3};
+          double v[3][3];  // [dir][deriv]
+          int64_t idx = 0, stride = 1;
+          for (int k = 0; k < 3; ++k) {
+            if (k < d) {
+              const double* t = a.gt[k] + (size_t(iq[k]) * (a.q[k] + 1) + cl[k]) * 3;
+              v[k][0] = t[0];
+              v[k][1] = t[1];
+              v[k][2] = t[2];
+              idx += stride * (a.span[k][iq[k]] + cl[k]);
+              stride *= a.m[k];
+            } else {
+              v[k][0] = 1;
+              v[k][1] = 0;
+              v[k][2] = 0;
+            }
+          }
+          const double wc = a.w[idx];
+          double val = v[0][0] * v[1][0] * v[2][0];
+          double der[3], hes[3][3];
+          for (int j = 0; j < 3; ++j) {
+            der[j] = 1;
+            for (int k = 0; k < 3; ++k) der[j] *= v[k][k == j ? 1 : 0];
+          }
+          for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) {
+              double h = 1;
+              for (int k = 0; k < 3; ++k) h *= v[k][(k == j) + (k == l)];
+              hes[j][l] = h;
+            }
+          W += wc * val;
+          for (int j = 0; j < d; ++j) {
+            dW[j] += wc * der[j];
+            for (int l = 0; l < d; ++l) hW[j][l] += wc * hes[j][l];
+          }
+          for (int i = 0; i < d; ++i) {
+            const double cw = wc * a.ctrl[idx * d + i];
+            N[i] += cw * val;
+            for (int j = 0; j < d; ++j) {
+              dN[i][j] += cw * der[j];
+              for (int l = 0; l < d; ++l) hN[i][j][l] += cw * hes[j][l];
+            }
+          }
+        }
+    // quotient rule: F = N / W
+    double F[3], J[3][3] = {}, H[3][3][3] = {};
+    for (int i = 0; i < d; ++i) F[i] = N[i] / W;
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) J[i][j] = (dN[i][j] - F[i] * dW[j]) / W;
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j)
+        for (int l = 0; l < d; ++l)
+          H[i][j][l] = (hN[i][j][l] - J[i][j] * dW[l] - J[i][l] * dW[j] - F[i] * hW[j][l]) / W;
+    // inverse (Jinv[j][i] = d eta_j / d x_i) and determinant
+    double inv[3][3] = {}, det;
+    if (d == 1) {
+      det = J[0][0];
+      inv[0][0] = 1.0 / det;
+    } else if (d == 2) {
+      det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      inv[0][0] = J[1][1] / det;
+      inv[0][1] = -J[0][1] / det;
+      inv[1][0] = -J[1][0] / det;
+      inv[1][1] = J[0][0] / det;
+    } else {
+      const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      inv[0][0] = c00 / det;
+      inv[1][0] = c01 / det;
+      inv[2][0] = c02 / det;
+      inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+      inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+      inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+      inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+      inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+      inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    }
+    // A = Jinv Jinv^T; c_m = sum_jl A_jl H[m][j][l]; b_j = -sum_m Jinv[j][m] c_m
+    double A[3][3] = {}, c[3] = {}, b[3] = {};
+    for (int j = 0; j < d; ++j)
+      for (int l = 0; l < d; ++l)
+        for (int i = 0; i < d; ++i) A[j][l] += inv[j][i] * inv[l][i];
+    for (int m_ = 0; m_ < d; ++m_)
+      for (int j = 0; j < d; ++j)
+        for (int l = 0; l < d; ++l) c[m_] += A[j][l] * H[m_][j][l];
+    for (int j = 0; j < d; ++j)
+      for (int m_ = 0; m_ < d; ++m_) b[j] -= inv[j][m_] * c[m_];
+    double wq = 1;
+    for (int k = 0; k < d; ++k) wq *= a.wq[k][iq[k]];
+    a.out[qi] = wq * fabs(det);
+    for (int j = 0; j < 3; ++j)
+      for (int i = 0; i < 3; ++i) a.out[(1 + j * 3 + i) * a.NQ + qi] = inv[j][i];
+    for (int j = 0; j < 3; ++j) a.out[(10 + j) * a.NQ + qi] = b[j];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// element assembly
+// ------------------------------------------------------------------------------------------
+struct GeoAsmArgs {
+  int d, p, nloc;
+  int nel[3], m[3], n[3];     // elements, full functions (n_el + p), constrained sizes
+  int nq[3];
+  const double* bt[3];        // [n_el][p+1 points][p+1 functions][3]
+  const double* qd;           // [13][NQ]
+  int64_t NQ, Ns;
+  int qc;                     // points per shared-memory chunk
+  double* st;                 // [3][S][Ns]
+  int S;
+};
+
+constexpr int ASM_THREADS = 256;
+constexpr int ASM_PP = 4;     // pairs per thread per round
+
+__global__ void __launch_bounds__(ASM_THREADS) geo_assemble_kernel(GeoAsmArgs a) {
+  extern __shared__ double sm[];
+  const int d = a.d, p = a.p, P1 = p + 1, nloc = a.nloc;
+  double* tab = sm;                               // [qc][nloc][5]: phi, grad_x (3), Lap
+  double* wts = sm + size_t(a.qc) * nloc * 5;     // [qc]
+  int e[3] = {0, 0, 0};
+  {
+    int64_t r = blockIdx.x;
+    for (int k = 0; k < d; ++k) {
+      e[k] = int(r % a.nel[k]);
+      r /= a.nel[k];
+    }
+  }
+  const int Q = nloc;  // (p+1)^d points per element
+  const int npairs = nloc * nloc;
+  for (int base = 0; base < npairs; base += ASM_THREADS * ASM_PP) {
+    double acc[ASM_PP][3];
+#pragma unroll
+    for (int j = 0; j < ASM_PP; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0;
+    for (int q0 = 0; q0 < Q; q0 += a.qc) {
+      const int qn = min(a.qc, Q - q0);
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < qn * nloc; idx += ASM_THREADS) {
+        const int ql = q0 + idx / nloc, f = idx % nloc;
+        int g[3] = {0, 0, 0}, fa[3] = {0, 0, 0};
+        int64_t qi = 0, stride = 1;
+        {
+          int rq = ql, rf = f;
+          for (int k = 0; k < d; ++k) {
+            g[k] = rq % P1;
+            rq /= P1;
+            fa[k] = rf % P1;
+            rf /= P1;
+            qi += stride * (int64_t(e[k]) * P1 + g[k]);
+            stride *= a.nq[k];
+          }
+        }
+        double v[3][3];
+        for (int k = 0; k < 3; ++k) {
+          if (k < d) {
+            const double* t = a.bt[k] + ((size_t(e[k]) * P1 + g[k]) * P1 + fa[k]) * 3;
+            v[k][0] = t[0];
+            v[k][1] = t[1];
+            v[k][2] = t[2];
+          } else {
+            v[k][0] = 1;
+            v[k][1] = 0;
+            v[k][2] = 0;
+          }
+        }
+        const double phi = v[0][0] * v[1][0] * v[2][0];
+        double gr[3], hs[3][3];
+        for (int j = 0; j < 3; ++j) {
+          gr[j] = 1;
+          for (int k = 0; k < 3; ++k) gr[j] *= v[k][k == j ? 1 : 0];
+        }
+        for (int j = 0; j < 3; ++j)
+          for (int l = 0; l < 3; ++l) {
+            double h = 1;
+            for (int k = 0; k < 3; ++k) h *= v[k][(k == j) + (k == l)];
+            hs[j][l] = h;
+          }
+        double inv[3][3], b[3];
+        for (int j = 0; j < 3; ++j)
+          for (int i = 0; i < 3; ++i) inv[j][i] = a.qd[(1 + j * 3 + i) * a.NQ + qi];
+        for (int j = 0; j < 3; ++j) b[j] = a.qd[(10 + j) * a.NQ + qi];
+        // grad_x = Jinv^T grad_eta ; Lap = sum_jl (Jinv Jinv^T)_jl d_jl + b . grad_eta
+        double gx[3];
+        for (int i = 0; i < 3; ++i) gx[i] = inv[0][i] * gr[0] + inv[1][i] * gr[1] + inv[2][i] * gr[2];
+        double lap = b[0] * gr[0] + b[1] * gr[1] + b[2] * gr[2];
+        for (int j = 0; j < d; ++j)
+          for (int l = 0; l < d; ++l) {
+            const double Ajl = inv[j][0] * inv[l][0] + inv[j][1] * inv[l][1] + inv[j][2] * inv[l][2];
+            lap += Ajl * hs[j][l];
+          }
+        double* o = tab + (size_t(idx / nloc) * nloc + f) * 5;
+        o[0] = phi;
+        o[1] = gx[0];
+        o[2] = gx[1];
+        o[3] = gx[2];
+        o[4] = lap;
+        if (f == 0) wts[idx / nloc] = a.qd[qi];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < ASM_PP; ++j) {
+        const int pid = base + j * ASM_THREADS + threadIdx.x;
+        if (pid >= npairs) continue;
+        const int fa = pid / nloc, fb = pid % nloc;
+        double s0 = 0, s1 = 0, s2 = 0;
+        for (int q = 0; q < qn; ++q) {
+          const double* ta = tab + (size_t(q) * nloc + fa) * 5;
+          const double* tb = tab + (size_t(q) * nloc + fb) * 5;
+          const double w = wts[q];
+          s0 += w * ta[0] * tb[0];
+          s1 += w * ta[4] * tb[4];
+          s2 += w * (ta[1] * tb[1] + ta[2] * tb[2] + ta[3] * tb[3]);
+        }
+        acc[j][0] += s0;
+        acc[j][1] += s1;
+        acc[j][2] += s2;
+      }
+    }
+    // scatter into the stencil rows of the constrained functions
+#pragma unroll
+    for (int j = 0; j < ASM_PP; ++j) {
+      const int pid = base + j * ASM_THREADS + threadIdx.x;
+      if (pid >= npairs) continue;
+      int fa = pid / nloc, fb = pid % nloc;
+      int64_t row = 0, rs = 1;
+      int o = 0, os = 1;
+      bool ok = true;
+      for (int k = 0; k < d; ++k) {
+        const int ga = e[k] + fa % P1, gb = e[k] + fb % P1;  // full indices
+        fa /= P1;
+        fb /= P1;
+        ok = ok && ga >= 1 && ga <= a.m[k] - 2 && gb >= 1 && gb <= a.m[k] - 2;
+        row += rs * (ga - 1);
+        rs *= a.n[k];
+        o += os * (gb - ga + p);
+        os *= 2 * p + 1;
+      }
+      if (!ok) continue;
+      atomicAdd(a.st + (size_t(0) * a.S + o) * a.Ns + row, acc[j][0]);
+      atomicAdd(a.st + (size_t(1) * a.S + o) * a.Ns + row, acc[j][1]);
+      atomicAdd(a.st + (size_t(2) * a.S + o) * a.Ns + row, acc[j][2]);
+    }
+  }
+}
+
+// host tables of one direction: Gauss points / weights, discretisation basis per element
+static void dir_tables(int n_el, int p, std::vector<double>& xq, std::vector<double>& wq, std::vector<double>& bt) {
+  auto kn = open_uniform_knots(n_el, p);
+  const int m = n_el + p, P1 = p + 1;
+  std::vector<long double> gx, gw;
+  gauss_legendre(P1, gx, gw);
+  std::vector<long double> v0(m), v1(m), v2(m);
+  xq.assign(size_t(n_el) * P1, 0);
+  wq.assign(size_t(n_el) * P1, 0);
+  bt.assign(size_t(n_el) * P1 * P1 * 3, 0);
+  for (int e = 0; e < n_el; ++e) {
+    const long double a = kn[p + e], b = kn[p + e + 1];
+    for (int g = 0; g < P1; ++g) {
+      const long double x = 0.5L * (a + b) + 0.5L * (b - a) * gx[g];
+      xq[size_t(e) * P1 + g] = double(x);
+      wq[size_t(e) * P1 + g] = double(0.5L * (b - a) * gw[g]);
+      bspline_eval(kn, p, x, v0.data(), v1.data(), v2.data());
+      for (int f = 0; f < P1; ++f) {
+        double* t = &bt[((size_t(e) * P1 + g) * P1 + f) * 3];
+        t[0] = double(v0[e + f]);
+        t[1] = double(v1[e + f]);
+        t[2] = double(v2[e + f]);
+      }
+    }
+  }
+}
+
+int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el, cudaStream_t s,
+                 int64_t* launches) {
+  gd.d = d;
+  gd.p = p;
+  gd.Ns = 1;
+  gd.S = 1;
+  int nq[3] = {1, 1, 1}, m[3] = {1, 1, 1};
+  for (int k = 0; k < d; ++k) {
+    gd.nel[k] = int(n_el[k]);
+    gd.n[k] = int(n_el[k]) + p - 2;
+    m[k] = int(n_el[k]) + p;
+    nq[k] = int(n_el[k]) * (p + 1);
+    gd.Ns *= gd.n[k];
+    gd.S *= 2 * p + 1;
+  }
+  int64_t NQ = 1, NE = 1;
+  for (int k = 0; k < d; ++k) {
+    NQ *= nq[k];
+    NE *= n_el[k];
+  }
+  // host tables
+  GeoQArgs qa{};
+  GeoAsmArgs aa{};
+  qa.d = d;
+  qa.NQ = NQ;
+  std::vector<int*> ispans;
+  for (int k = 0; k < d; ++k) {
+    std::vector<double> xq, wq, bt;
+    dir_tables(int(n_el[k]), p, xq, wq, bt);
+    // geometry basis at the points: span (first non-zero function) and q+1 values
+    const int q = g.q[k], mg = g.m[k];
+    std::vector<double> gt(xq.size() * (q + 1) * 3);
+    std::vector<int> span(xq.size());
+    std::vector<long double> v0(mg), v1(mg), v2(mg);
+    const auto& kn = g.knots[k];
+    for (size_t i = 0; i < xq.size(); ++i) {
+      const double x = xq[i];
+      int sp = q;  // knot span: kn[sp] <= x < kn[sp+1], sp in [q, mg-1]
+      while (sp < mg - 1 && kn[sp + 1] <= x) ++sp;
+      span[i] = sp - q;
+      bspline_eval(kn, q, x, v0.data(), v1.data(), v2.data());
+      for (int c = 0; c <= q; ++c) {
+        gt[(i * (q + 1) + c) * 3 + 0] = double(v0[sp - q + c]);
+        gt[(i * (q + 1) + c) * 3 + 1] = double(v1[sp - q + c]);
+        gt[(i * (q + 1) + c) * 3 + 2] = double(v2[sp - q + c]);
+      }
+    }
+    double *dgt, *dwq, *dbt;
+    int rc = dupload(gd.allocs, gt, &dgt);
+    if (rc == LS_OK) rc = dupload(gd.allocs, wq, &dwq);
+    if (rc == LS_OK) rc = dupload(gd.allocs, bt, &dbt);
+    if (rc != LS_OK) return rc;
+    int* dspan = nullptr;
+    GEO_CUDA(cudaMalloc(&dspan, span.size() * sizeof(int)));
+    gd.allocs.push_back(dspan);
+    GEO_CUDA(cudaMemcpy(dspan, span.data(), span.size() * sizeof(int), cudaMemcpyHostToDevice));
+    qa.nq[k] = nq[k];
+    qa.q[k] = q;
+    qa.m[k] = mg;
+    qa.span[k] = dspan;
+    qa.gt[k] = dgt;
+    qa.wq[k] = dwq;
+    aa.bt[k] = dbt;
+  }
+  double *dctrl, *dw, *qd;
+  int rc = dupload(gd.allocs, g.ctrl, &dctrl);
+  if (rc == LS_OK) rc = dupload(gd.allocs, g.w, &dw);
+  if (rc == LS_OK) rc = dalloc(gd.allocs, &qd, size_t(13) * NQ);
+  if (rc == LS_OK) rc = dalloc(gd.allocs, &gd.st, size_t(3) * gd.S * gd.Ns);
+  if (rc != LS_OK) return rc;
+  qa.ctrl = dctrl;
+  qa.w = dw;
+  qa.out = qd;
+  GEO_CUDA(cudaMemsetAsync(qd, 0, size_t(13) * NQ * sizeof(double), s));
+  GEO_CUDA(cudaMemsetAsync(gd.st, 0, size_t(3) * gd.S * gd.Ns * sizeof(double), s));
+  geo_qpoint_kernel<<<unsigned(std::min<int64_t>((NQ + 255) / 256, 148 * 16)), 256, 0, s>>>(qa);
+  GEO_CUDA(cudaGetLastError());
+  // assembly
+  aa.d = d;
+  aa.p = p;
+  aa.nloc = 1;
+  for (int k = 0; k < d; ++k) aa.nloc *= p + 1;
+  for (int k = 0; k < 3; ++k) {
+    aa.nel[k] = k < d ? int(n_el[k]) : 1;
+    aa.m[k] = m[k];
+    aa.n[k] = gd.n[k];
+    aa.nq[k] = nq[k];
+  }
+  aa.qd = qd;
+  aa.NQ = NQ;
+  aa.Ns = gd.Ns;
+  aa.st = gd.st;
+  aa.S = gd.S;
+  const size_t smem_budget = 96 * 1024;
+  aa.qc = int(std::max<size_t>(1, smem_budget / (size_t(aa.nloc) * 5 * 8 + 8)));
+  aa.qc = std::min(aa.qc, aa.nloc);
+  const size_t smem = (size_t(aa.qc) * aa.nloc * 5 + aa.qc) * sizeof(double);
+  GEO_CUDA(cudaFuncSetAttribute(geo_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  geo_assemble_kernel<<<unsigned(NE), ASM_THREADS, smem, s>>>(aa);
+  GEO_CUDA(cudaGetLastError());
+  GEO_CUDA(cudaStreamSynchronize(s));
+  if (launches) *launches += 2;
+  int centre = 0, cs = 1;
+  for (int k = 0; k < d; ++k) {
+    centre += cs * p;
+    cs *= 2 * p + 1;
+  }
+  for (int mat = 0; mat < 3; ++mat) gd.diag[mat] = gd.st + (size_t(mat) * gd.S + centre) * gd.Ns;
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// matvec
+// ------------------------------------------------------------------------------------------
+__global__ void geo_time_kernel(const double* __restrict__ x, double* __restrict__ t1, double* __restrict__ t2,
+                                const double* __restrict__ bK, const double* __restrict__ bM, int nt, int pt,
+                                int64_t Ns) {
+  const int W = 2 * pt + 1;
+  const int64_t total = int64_t(nt) * Ns;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int t = int(idx / Ns);
+    const int64_t i = idx - int64_t(t) * Ns;
+    double a = 0, b = 0;
+    const int lo = max(0, t - pt), hi = min(nt - 1, t + pt);
+    for (int s = lo; s <= hi; ++s) {
+      const double v = __ldg(x + int64_t(s) * Ns + i);
+      a += __ldg(bK + t * W + (s - t + pt)) * v;
+      b += __ldg(bM + t * W + (s - t + pt)) * v;
+    }
+    t1[idx] = a;
+    t2[idx] = b;
+  }
+}
+
+constexpr int ST_TC = 8;      // time slices per thread
+constexpr int ST_THREADS = 128;
+
+__global__ void __launch_bounds__(ST_THREADS) geo_stencil_kernel(
+    const double* __restrict__ st, const double* __restrict__ t1, const double* __restrict__ t2,
+    const double* __restrict__ x, double* __restrict__ y, int d, int p, int n1, int n2, int n3, int64_t Ns,
+    int S, int nt) {
+  const int64_t i = blockIdx.x * int64_t(ST_THREADS) + threadIdx.x;
+  if (i >= Ns) return;
+  const int t0 = blockIdx.y * ST_TC;
+  const int tn = min(ST_TC, nt - t0);
+  const bool last = (t0 + tn == nt);
+  const int i1 = int(i % n1), i2 = int((i / n1) % n2), i3 = int(i / (int64_t(n1) * n2));
+  const int W = 2 * p + 1;
+  const int r2 = d >= 2 ? p : 0, r3 = d >= 3 ? p : 0;
+  double acc[ST_TC];
+#pragma unroll
+  for (int k = 0; k < ST_TC; ++k) acc[k] = 0;
+  double accL = 0;
+  const double* Ms = st;
+  const double* Js = st + size_t(S) * Ns;
+  const double* Ls = st + size_t(2) * S * Ns;
+  for (int o3 = -r3; o3 <= r3; ++o3) {
+    const int j3 = i3 + o3;
+    if (j3 < 0 || j3 >= n3) continue;
+    for (int o2 = -r2; o2 <= r2; ++o2) {
+      const int j2 = i2 + o2;
+      if (j2 < 0 || j2 >= n2) continue;
+      const int ob = ((o3 + r3) * (d >= 2 ? W : 1) + (o2 + r2)) * W;
+      const int64_t jb = (int64_t(j3) * n2 + j2) * n1;
+      for (int o1 = -p; o1 <= p; ++o1) {
+        const int j1 = i1 + o1;
+        if (j1 < 0 || j1 >= n1) continue;
+        const int o = ob + o1 + p;
+        const int64_t j = jb + j1;
+        const double cm = __ldg(Ms + size_t(o) * Ns + i);
+        const double cj = __ldg(Js + size_t(o) * Ns + i);
+#pragma unroll
+        for (int k = 0; k < ST_TC; ++k)
+          if (k < tn) {
+            const int64_t off = int64_t(t0 + k) * Ns + j;
+            acc[k] += cm * __ldg(t1 + off) + cj * __ldg(t2 + off);
+          }
+        if (last) accL += __ldg(Ls + size_t(o) * Ns + i) * __ldg(x + int64_t(nt - 1) * Ns + j);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < ST_TC; ++k)
+    if (k < tn) y[int64_t(t0 + k) * Ns + i] = acc[k] + ((last && k == tn - 1) ? accL : 0.0);
+}
+
+int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* x, double* y,
+               double* t1, double* t2, cudaStream_t s, int64_t* launches) {
+  const int64_t total = int64_t(nt) * gd.Ns;
+  geo_time_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+      x, t1, t2, bKt, bMt, nt, gd.pt, gd.Ns);
+  GEO_CUDA(cudaGetLastError());
+  dim3 grid(unsigned((gd.Ns + ST_THREADS - 1) / ST_THREADS), unsigned((nt + ST_TC - 1) / ST_TC));
+  geo_stencil_kernel<<<grid, ST_THREADS, 0, s>>>(gd.st, t1, t2, x, y, gd.d, gd.p, gd.n[0], gd.n[1], gd.n[2],
+                                                 gd.Ns, gd.S, nt);
+  GEO_CUDA(cudaGetLastError());
+  if (launches) *launches += 2;
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// P^G diagonal scaling
+// ------------------------------------------------------------------------------------------
+__global__ void pg_scaling_kernel(const double* __restrict__ Md, const double* __restrict__ Jd,
+                                  const double* __restrict__ Ld, const double* __restrict__ bK,
+                                  const double* __restrict__ bM, int pt, const double* __restrict__ pdt,
+                                  const double* __restrict__ pds, double* __restrict__ out, int nt, int64_t Ns) {
+  const int W = 2 * pt + 1;
+  const int64_t total = int64_t(nt) * Ns;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int t = int(idx / Ns);
+    const int64_t i = idx - int64_t(t) * Ns;
+    double a = bK[t * W + pt] * Md[i] + bM[t * W + pt] * Jd[i];
+    if (t == nt - 1) a += Ld[i];  // W_t = e_{n_t} e_{n_t}^T
+    const double pb = pdt[t] * pds[i] + pdt[nt + t] * pds[Ns + i];
+    out[idx] = sqrt(pb / a);
+  }
+}
+
+int pg_scaling(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* pdiag_t,
+               const double* pdiag_s, double* dm12, cudaStream_t s, int64_t* launches) {
+  const int64_t total = int64_t(nt) * gd.Ns;
+  pg_scaling_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
+      gd.diag[0], gd.diag[1], gd.diag[2], bKt, bMt, gd.pt, pdiag_t, pdiag_s, dm12, nt, gd.Ns);
+  GEO_CUDA(cudaGetLastError());
+  if (launches) *launches += 1;
+  return LS_OK;
+}
+
+__global__ void scale_vec_kernel(const double* __restrict__ sc, const double* __restrict__ x,
+                                 double* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = sc[i] * x[i];
+}
+
+int scale_vec(const double* sc, const double* x, double* y, int64_t n, cudaStream_t s, int64_t* launches) {
+  scale_vec_kernel<<<unsigned(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, s>>>(sc, x, y, n);
+  GEO_CUDA(cudaGetLastError());
+  if (launches) *launches += 1;
+  return LS_OK;
+}
+
+}  // namespace ls

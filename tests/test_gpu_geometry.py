@@ -1,0 +1,175 @@
+"""GPU parity of the mapped-domain path (ls_setup_geo):
+the device-assembled physical factors (ls_matvec), P and P^G (fd_apply) and PCG
+against oracle/geometry.py and oracle/geo_precond.py on the same seeded inputs and
+the same maps (synth.GEOMETRIES).  Bars: matvec 1e-12, fd_apply / PCG 1e-9 (relative
+2-norm), PCG iteration counts equal."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import geometry as G, geo_precond as GP, univariate as uv, fd, pcg as opcg
+
+pytestmark = pytest.mark.gpu
+warnings.filterwarnings("ignore", category=DeprecationWarning)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def _setup(name, p, n_elems, precond, pt=None):
+    import paper_1809_10026_b200 as ls
+    geo = synth.GEOMETRIES[name]() if name != "affine" else synth.affine_box([2.0, 0.5, 1.5][:len(n_elems) - 1])
+    d = geo["d"]
+    pt = p if pt is None else pt
+    ctx = ls.Context(d, (p, pt), n_elems, geometry=geo, precond=precond)
+    sf = G.space_factors_physical(geo, list(n_elems[:d]), p)
+    tf = uv.time_factors(n_elems[d], pt)
+    return ctx, geo, sf, tf
+
+
+# (map, p_s, p_t, n_elems): ragged extents (N_s not a multiple of the 128-row CTA,
+# n_t not a multiple of the 8-slice thread tile), several elements per direction
+MV_CASES = [
+    ("affine", 2, 2, [3, 4, 5]),
+    ("annulus2d", 3, 3, [5, 7, 6]),
+    ("annulus2d", 2, 3, [24, 20, 13]),
+    ("annulus2d", 4, 2, [6, 5, 9]),
+    ("annulus3d", 2, 2, [4, 5, 3, 6]),
+    ("annulus3d", 3, 3, [5, 4, 6, 4]),
+    ("affine", 3, 2, [3, 4, 2, 5]),
+]
+
+
+@pytest.mark.parametrize("name,p,pt,n_elems", MV_CASES)
+def test_geo_matvec_matches_oracle(torch_cuda, name, p, pt, n_elems):
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    ctx, geo, sf, tf = _setup(name, p, n_elems, ls.LS_PRECOND_P, pt)
+    for seed in (1, 2):
+        x = synth.residual(ctx.shape, seed)
+        y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+        y_ref = G.apply_A_geo(x, sf, tf)
+        assert _rel(y, y_ref) <= 1e-12, (seed, _rel(y, y_ref))
+
+
+@pytest.mark.parametrize("name,p,n_elems", [("annulus2d", 3, [6, 5, 7]), ("annulus3d", 2, [4, 3, 5, 4])])
+def test_geo_plain_P_is_parametric(torch_cuda, name, p, n_elems):
+    """precond = LS_PRECOND_P: fd_apply is Algorithm 1 for the parametric P (eq:preconditioner)."""
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    ctx, geo, sf, tf = _setup(name, p, n_elems, ls.LS_PRECOND_P)
+    d = geo["d"]
+    plain = fd.setup([uv.space_factors(n, p) for n in n_elems[:d]], tf)
+    r = synth.residual(ctx.shape, 3)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert _rel(z, fd.fd_apply(r, plain)) <= 1e-9
+    assert ctx.geo_info()[0] == 0.0
+
+
+PG_CASES = [
+    ("affine", 2, [3, 4, 5]),
+    ("annulus2d", 3, [6, 5, 7]),
+    ("annulus2d", 2, [16, 12, 9]),
+    ("annulus3d", 2, [4, 3, 5, 4]),
+    ("annulus3d", 3, [5, 5, 5, 5]),
+]
+
+
+@pytest.mark.parametrize("name,p,n_elems", PG_CASES)
+def test_geo_PG_fd_apply_matches_oracle(torch_cuda, name, p, n_elems):
+    """(P^G)^{-1} r = D^{-1/2} Pbar^{-1} D^{-1/2} r (PAPER.md 969-1045, readings c20-c22)."""
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    ctx, geo, sf, tf = _setup(name, p, n_elems, ls.LS_PRECOND_PG)
+    d = geo["d"]
+    data = GP.setup(geo, list(n_elems[:d]), p, tf, GP.A_diagonal(sf, tf))
+    for seed in (4, 5):
+        r = synth.residual(ctx.shape, seed)
+        rt = torch.from_numpy(r).cuda()
+        z = ctx.fd_apply(rt).cpu().numpy()
+        err = _rel(z, GP.apply(r, data))
+        assert err <= 1e-9, (seed, err)
+    # in place (z == r)
+    ctx.fd_apply(rt, rt)
+    assert _rel(rt.cpu().numpy(), GP.apply(r, data)) <= 1e-9
+    res, S = ctx.geo_info()
+    assert S == (2 * p + 1) ** d
+    if name == "affine":
+        assert res < 1e-13          # constant coefficients: exactly separable
+    else:
+        assert 0 < res < 1e2   # shared mu_k: c_tau, c_k are not jointly separable on the annulus
+
+
+@pytest.mark.parametrize("name,p,n_elems,precond", [("annulus2d", 3, [8, 8, 8], 0), ("annulus2d", 3, [8, 8, 8], 1),
+                                                    ("annulus3d", 2, [4, 4, 4, 4], 0),
+                                                    ("annulus3d", 2, [4, 4, 4, 4], 1)])
+def test_geo_pcg_matches_oracle(torch_cuda, name, p, n_elems, precond):
+    """PCG with P or P^G on the mapped domain: same iteration count and iterate as the
+    oracle's PCG (x0 = 0, tol 1e-8 on the recurrence residual, PAPER.md 1109)."""
+    torch = torch_cuda
+    ctx, geo, sf, tf = _setup(name, p, n_elems, precond)
+    d = geo["d"]
+    b = synth.residual(ctx.shape, 7)
+    x, st = ctx.pcg(torch.from_numpy(b).cuda(), tol=1e-8)
+    A = lambda v: G.apply_A_geo(v, sf, tf)
+    if precond == 1:
+        data = GP.setup(geo, list(n_elems[:d]), p, tf, GP.A_diagonal(sf, tf))
+        Pinv = lambda r: GP.apply(r, data)
+    else:
+        plain = fd.setup([uv.space_factors(n, p) for n in n_elems[:d]], tf)
+        Pinv = lambda r: fd.fd_apply(r, plain)
+    x_ref, it, ok, _ = opcg.pcg(A, Pinv, b)
+    assert ok and st["status"] == 0
+    assert st["iters"] == it
+    assert _rel(x.cpu().numpy(), x_ref) <= 1e-9
+
+
+def test_geo_pg_fewer_iterations(torch_cuda):
+    """Table 2's claim (PAPER.md 1226-1228): P^G cuts the CG iterations on the rotated
+    quarter annulus several times against P."""
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    its = []
+    for pc in (ls.LS_PRECOND_P, ls.LS_PRECOND_PG):
+        ctx, geo, sf, tf = _setup("annulus3d", 3, [8, 8, 8, 8], pc)
+        b = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
+        _, st = ctx.pcg(b, tol=1e-8)
+        assert st["status"] == 0
+        its.append(st["iters"])
+    assert its[1] * 3 <= its[0], its
+
+
+def test_geo_errors(torch_cuda):
+    import paper_1809_10026_b200 as ls
+    geo = synth.quarter_annulus()
+    ctx = ls.Context(2, 2, [4, 4, 4], geometry=geo, precond=ls.LS_PRECOND_PG)
+    import torch
+    b = torch.zeros(ctx.shape, dtype=torch.float64, device="cuda")
+    with pytest.raises(ls.LSError) as e:
+        ctx.rhs(0, b)
+    assert e.value.code == ls.LS_ENOTSUP
+    bad = dict(geo)
+    bad["knots"] = [np.array([0.0, 0.0, 1.0]), geo["knots"][1]]       # too short for degree 1
+    with pytest.raises(ls.LSError) as e:
+        ls.Context(2, 2, [4, 4, 4], geometry=bad)
+    assert e.value.code == ls.LS_EINVAL
+    neg = dict(geo)
+    neg["weights"] = -geo["weights"]
+    with pytest.raises(ls.LSError):
+        ls.Context(2, 2, [4, 4, 4], geometry=neg)
+    with pytest.raises(ls.LSError):
+        ls.Context(3, 7, [2, 2, 2, 2], geometry=synth.revolved_quarter_annulus())   # (p+1)^3 > 343
+    # b = 0 -> x = 0, 0 iterations
+    x, st = ctx.pcg(b)
+    assert st["iters"] == 0 and float(x.abs().max()) == 0.0
