@@ -398,6 +398,55 @@ def run_extras(ls, torch, stream):
         c.close()
         del b, x
     out["pcg"] = pcg
+    out["geometry"] = run_geometry(ls, torch, stream)
+    return out
+
+
+def run_geometry(ls, torch, stream, cases=((32, 3), (64, 3))):
+    """Mapped domain: the rotated quarter annulus of PAPER.md 1219
+    (Table 2's domain), P and P^G, seeded U[-1,1] right-hand side (the paper's data needs a
+    lifting, out of scope), tol 1e-8.  Paper (Table 2, p = 3, serial Matlab): n_sub = 32:
+    P 143 it / 132 s, P^G 41 it / 39.6 s; n_sub = 64: P 155 it / 2415 s, P^G 44 it / 716 s."""
+    out = []
+    geo = synth.revolved_quarter_annulus()
+    for n_el, p in cases:
+        for pc, name in ((ls.LS_PRECOND_P, "P"), (ls.LS_PRECOND_PG, "P^G")):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            c = ls.Context(3, p, [n_el] * 4, geometry=geo, precond=pc)
+            torch.cuda.synchronize()
+            setup_s = time.perf_counter() - t0
+            c.set_stream(stream)
+            b = torch.from_numpy(synth.residual(c.shape, 0)).cuda()
+            c.pcg(b, tol=1e-8, max_iter=2000)  # warm
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            x, st = c.pcg(b, tol=1e-8, max_iter=2000)
+            torch.cuda.synchronize()
+            solve_ms = (time.perf_counter() - t0) * 1e3
+            z = torch.empty_like(b)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            for _ in range(2):
+                ev[0].record(stream)
+                c.fd_apply(b, z)
+                ev[1].record(stream)
+                c.matvec(b, z)
+                ev[2].record(stream)
+                ev[2].synchronize()
+            mv_ms = ev[1].elapsed_time(ev[2])
+            S = (2 * p + 1) ** 3
+            Ns = int(np.prod(c.n_s))
+            out.append({"domain": "revolved quarter annulus (PAPER.md 1219)", "d": 3, "p": p, "n_el": n_el,
+                        "N": c.N, "precond": name, "iters": st["iters"], "solve_ms": solve_ms,
+                        "true_rel_res": st["true_rel_res"], "setup_s": round(setup_s, 3),
+                        "fd_apply_ms": ev[0].elapsed_time(ev[1]), "matvec_ms": mv_ms,
+                        # stencil pass: 2 (2p+1)^3 MACs per DOF (M_s, J_s) -> flops; bytes: the three
+                        # stencil arrays once + t1, t2 read + y written (DESIGN.md 5)
+                        "matvec_gflops_alg": round(4.0 * S * c.N / (mv_ms * 1e-3) / 1e9, 1),
+                        "matvec_gbs_alg": round(8.0 * (3 * S * Ns + 5 * c.N) / (mv_ms * 1e-3) / 1e9, 1),
+                        "fit_rel_res": c.geo_info()[0]})
+            c.close()
+            del b, x, z
     return out
 
 

@@ -615,7 +615,7 @@ extern "C" int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, con
     }
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) rc = LS_ECUDA;
-    else if (double(3 * S) * double(Ns) * 8.0 > 0.5 * double(fr)) rc = LS_ENOMEM;
+    else if (double(3 * S) * double(Ns) * 8.0 > 0.5 * double(fr)) rc = LS_ENOMEM;  // the three stencil arrays
   }
   if (rc == LS_OK) rc = setup_common(ctx);
   if (rc != LS_OK) {
@@ -1602,6 +1602,7 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_MATVEC:
       if (value < 0 || value > 3) return LS_EINVAL;
       ctx->mv_variant = value;
+      if (ctx->geo) ctx->geo->variant = (value == 1) ? 1 : 0;  // mapped domain: 1 = DFMA stencil
       return LS_OK;
     case LS_TUNE_A2A: {  // collective when enabling: every rank calls it
       if (value == 0) {

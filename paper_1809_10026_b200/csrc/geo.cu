@@ -12,9 +12,12 @@
 //                       the first-order Laplacian coefficients b (chain rule, PAPER.md 986-990)
 //   geo_assemble_kernel one CTA per element: physical values / gradients / Laplacians of the
 //                       (p+1)^d local functions at a chunk of points in shared memory, pair
-//                       sums in registers, fp64 atomics into the stencil rows
+//                       sums in registers, added into the stencil rows (one launch per
+//                       element colour class: deterministic, no atomics)
 //   geo_time_kernel     t1 = K_t x, t2 = M_t x (banded, half-bandwidth p_t)
-//   geo_stencil_kernel  y = M_s t1 + J_s t2 (+ L_s x on the last slice: W_t = e e^T)
+//   geo_dmma_kernel     y = M_s t1 + J_s t2 (+ L_s x on the last slice: W_t = e e^T) as DMMA
+//                       band tiles (default)
+//   geo_stencil_kernel  the same with DFMAs, one thread per row and 8 time slices (ls_tune)
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -46,6 +49,12 @@ static int dalloc(std::vector<void*>& allocs, double** p, size_t n) {
   *p = static_cast<double*>(v);
   return LS_OK;
 }
+
+#define LS_CHECK_RC(x)     \
+  do {                     \
+    int rc_ = (x);         \
+    if (rc_ != LS_OK) return rc_; \
+  } while (0)
 
 static int dupload(std::vector<void*>& allocs, const std::vector<double>& h, double** p) {
   int rc = dalloc(allocs, p, h.size());
@@ -195,6 +204,7 @@ struct GeoAsmArgs {
   const double* qd;           // [13][NQ]
   int64_t NQ, Ns;
   int qc;                     // points per shared-memory chunk
+  int color[3];               // element colour class of this launch
   double* st;                 // [3][S][Ns]
   int S;
 };
@@ -207,12 +217,16 @@ __global__ void __launch_bounds__(ASM_THREADS) geo_assemble_kernel(GeoAsmArgs a)
   const int d = a.d, p = a.p, P1 = p + 1, nloc = a.nloc;
   double* tab = sm;                               // [qc][nloc][5]: phi, grad_x (3), Lap
   double* wts = sm + size_t(a.qc) * nloc * 5;     // [qc]
+  // colour class (c_1..c_d): elements e_k = c_k + (p+1) m_k.  Two elements of one class are
+  // >= p+1 apart in some direction, so they share no basis function and the stencil updates
+  // below never collide: plain read-modify-write, deterministic summation order.
   int e[3] = {0, 0, 0};
   {
     int64_t r = blockIdx.x;
     for (int k = 0; k < d; ++k) {
-      e[k] = int(r % a.nel[k]);
-      r /= a.nel[k];
+      const int cnt = (a.nel[k] - a.color[k] + p) / (p + 1);
+      e[k] = a.color[k] + (p + 1) * int(r % cnt);
+      r /= cnt;
     }
   }
   const int Q = nloc;  // (p+1)^d points per element
@@ -325,9 +339,9 @@ __global__ void __launch_bounds__(ASM_THREADS) geo_assemble_kernel(GeoAsmArgs a)
         os *= 2 * p + 1;
       }
       if (!ok) continue;
-      atomicAdd(a.st + (size_t(0) * a.S + o) * a.Ns + row, acc[j][0]);
-      atomicAdd(a.st + (size_t(1) * a.S + o) * a.Ns + row, acc[j][1]);
-      atomicAdd(a.st + (size_t(2) * a.S + o) * a.Ns + row, acc[j][2]);
+      a.st[(size_t(0) * a.S + o) * a.Ns + row] += acc[j][0];
+      a.st[(size_t(1) * a.S + o) * a.Ns + row] += acc[j][1];
+      a.st[(size_t(2) * a.S + o) * a.Ns + row] += acc[j][2];
     }
   }
 }
@@ -457,10 +471,27 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
   aa.qc = std::min(aa.qc, aa.nloc);
   const size_t smem = (size_t(aa.qc) * aa.nloc * 5 + aa.qc) * sizeof(double);
   GEO_CUDA(cudaFuncSetAttribute(geo_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  geo_assemble_kernel<<<unsigned(NE), ASM_THREADS, smem, s>>>(aa);
-  GEO_CUDA(cudaGetLastError());
+  int ncol = 1;
+  for (int k = 0; k < d; ++k) ncol *= p + 1;
+  int nlaunch = 0;
+  for (int c = 0; c < ncol; ++c) {
+    int64_t cnt = 1;
+    int r = c;
+    for (int k = 0; k < 3; ++k) {
+      aa.color[k] = 0;
+      if (k < d) {
+        aa.color[k] = r % (p + 1);
+        r /= p + 1;
+        cnt *= (n_el[k] - aa.color[k] + p) / (p + 1);
+      }
+    }
+    if (cnt == 0) continue;  // fewer than p+1 elements in some direction
+    geo_assemble_kernel<<<unsigned(cnt), ASM_THREADS, smem, s>>>(aa);
+    GEO_CUDA(cudaGetLastError());
+    ++nlaunch;
+  }
   GEO_CUDA(cudaStreamSynchronize(s));
-  if (launches) *launches += 2;
+  if (launches) *launches += 1 + nlaunch;
   int centre = 0, cs = 1;
   for (int k = 0; k < d; ++k) {
     centre += cs * p;
@@ -546,12 +577,158 @@ __global__ void __launch_bounds__(ST_THREADS) geo_stencil_kernel(
     if (k < tn) y[int64_t(t0 + k) * Ns + i] = acc[k] + ((last && k == tn - 1) ? accL : 0.0);
 }
 
+// ---- tensor-core variant (default): the stencil pass as DMMA.8x8x4 tiles -------------------
+// For a line L = (i_2, i_3) and a block of 8 consecutive rows i_1 in [8 rb, 8 rb + 8), the
+// coupling to the source line (i_2 + o_2, i_3 + o_3) is an 8 x (8 + 2p) band block B.  With
+// time as the M dimension: D[t][i] += sum_j T[t][j] B^T[j][i], i.e. m8n8k4 with A = 8 time
+// slices x 4 source columns (loaded straight from t1 / t2, 32 B per time row) and B = the
+// band block gathered from the compact stencil rows into registers once per source line
+// and reused for every time block.  M_s on t1 and J_s on t2 accumulate into the same tile;
+// L_s on x enters the tile of the last time block with only the row t = n_t - 1 non-zero.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct FragGeom {
+  int d, p, n1, n2, n3, RB, KS, Q, W2;
+  int64_t NL, Ns;
+};
+
+template <int TBM, int KSM>
+__global__ void __launch_bounds__(256, 2) geo_dmma_kernel(const double* __restrict__ st,
+                                                      const double* __restrict__ t1,
+                                                      const double* __restrict__ t2,
+                                                      const double* __restrict__ x, double* __restrict__ y,
+                                                      FragGeom g, int nt, int S) {
+  const int lane = threadIdx.x & 31;
+  // work item = (time chunk of TBM blocks, line, 8-row block), the time chunk slowest: the
+  // warps resident at one time share it, so the t1 / t2 rows they read stay in L2
+  const int nchunk = (nt + 8 * TBM - 1) / (8 * TBM);
+  const int64_t nwarps = g.NL * g.RB * nchunk;
+  const int r2 = g.d >= 2 ? g.p : 0, r3 = g.d >= 3 ? g.p : 0;
+  const int W = 2 * g.p + 1;
+  const int trow = lane >> 2, kc = lane & 3;
+  const double* Ms = st;
+  const double* Js = st + size_t(S) * g.Ns;
+  const double* Ls = st + size_t(2) * S * g.Ns;
+  const double* xl = x + int64_t(nt - 1) * g.Ns;
+  for (int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; w < nwarps;
+       w += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int chunk = int(w / (g.NL * g.RB));
+    const int64_t wl = w - int64_t(chunk) * g.NL * g.RB;
+    const int64_t L = wl / g.RB;
+    const int rb = int(wl - L * g.RB);
+    const int i2 = int(L % g.n2), i3 = int(L / g.n2);
+    const int tb0 = chunk * TBM;
+    const int ntb = min(TBM, (nt + 7) / 8 - tb0);  // blocks of this chunk
+    const int tbl = (nt - 1) / 8 - tb0;            // local block of the last slice (W_t = e e^T)
+    const int i1 = rb * 8 + trow;            // B-fragment row of this lane (n = lane >> 2)
+    const bool iok = i1 < g.n1;
+    const int64_t brow = L * g.n1 + i1;
+    double acc[TBM][2];
+#pragma unroll
+    for (int tb = 0; tb < TBM; ++tb) acc[tb][0] = acc[tb][1] = 0.0;
+    for (int q = 0; q < g.Q; ++q) {
+      const int j2 = i2 + q % g.W2 - r2, j3 = i3 + q / g.W2 - r3;
+      if (j2 < 0 || j2 >= g.n2 || j3 < 0 || j3 >= g.n3) continue;  // warp-uniform
+      const int64_t src = (int64_t(j3) * g.n2 + j2) * g.n1;
+      // B fragments of this source line, all k-steps: band entry (i_1, o_1 = 4 ks + k - n)
+      // gathered from the compact stencil rows (zero outside the band / the grid)
+      double bM[KSM], bJ[KSM], bL[KSM];
+#pragma unroll
+      for (int ks = 0; ks < KSM; ++ks) {
+        const int o1 = ks * 4 + kc - trow;
+        const bool ok = ks < g.KS && iok && o1 >= 0 && o1 < W;
+        const size_t off = size_t(o1 + W * q) * g.Ns + brow;
+        bM[ks] = ok ? __ldg(Ms + off) : 0.0;
+        bJ[ks] = ok ? __ldg(Js + off) : 0.0;
+        bL[ks] = ok ? __ldg(Ls + off) : 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < KSM; ++ks) {
+        if (ks >= g.KS) break;
+        const int j1 = rb * 8 - g.p + ks * 4 + kc;   // A-fragment column (k = lane & 3)
+        const bool jok = j1 >= 0 && j1 < g.n1;
+        double aM[TBM], aJ[TBM];
+#pragma unroll
+        for (int tb = 0; tb < TBM; ++tb) {
+          const int t = (tb0 + tb) * 8 + trow;
+          const bool ok = jok && tb < ntb && t < nt;
+          const int64_t off = int64_t(t) * g.Ns + src + j1;
+          aM[tb] = ok ? __ldg(t1 + off) : 0.0;
+          aJ[tb] = ok ? __ldg(t2 + off) : 0.0;
+        }
+        const double aL = (jok && (tb0 + tbl) * 8 + trow == nt - 1) ? __ldg(xl + src + j1) : 0.0;
+#pragma unroll
+        for (int tb = 0; tb < TBM; ++tb) {
+          if (tb < ntb) {
+            dmma(acc[tb], aM[tb], bM[ks]);
+            dmma(acc[tb], aJ[tb], bJ[ks]);
+          }
+          if (tb == tbl) dmma(acc[tb], aL, bL[ks]);
+        }
+      }
+    }
+#pragma unroll
+    for (int tb = 0; tb < TBM; ++tb) {
+      const int t = (tb0 + tb) * 8 + trow;
+      const int o1 = rb * 8 + 2 * kc;
+      if (tb < ntb && t < nt) {
+        double* yr = y + int64_t(t) * g.Ns + L * g.n1;
+        if (o1 < g.n1) yr[o1] = acc[tb][0];
+        if (o1 + 1 < g.n1) yr[o1 + 1] = acc[tb][1];
+      }
+    }
+  }
+}
+
+static FragGeom frag_geom(const GeoDev& gd) {
+  FragGeom g;
+  g.d = gd.d;
+  g.p = gd.p;
+  g.n1 = gd.n[0];
+  g.n2 = gd.d >= 2 ? gd.n[1] : 1;
+  g.n3 = gd.d >= 3 ? gd.n[2] : 1;
+  g.RB = (g.n1 + 7) / 8;
+  g.KS = (8 + 2 * gd.p + 3) / 4;
+  g.W2 = gd.d >= 2 ? 2 * gd.p + 1 : 1;
+  g.Q = g.W2 * (gd.d >= 3 ? 2 * gd.p + 1 : 1);
+  g.NL = int64_t(g.n2) * g.n3;
+  g.Ns = gd.Ns;
+  return g;
+}
+
 int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* x, double* y,
                double* t1, double* t2, cudaStream_t s, int64_t* launches) {
   const int64_t total = int64_t(nt) * gd.Ns;
   geo_time_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
       x, t1, t2, bKt, bMt, nt, gd.pt, gd.Ns);
   GEO_CUDA(cudaGetLastError());
+  if (gd.variant != 1) {
+    const FragGeom g = frag_geom(gd);
+    const int ntb = (nt + 7) / 8;
+    const int tbm = ntb <= 2 ? 2 : 5;
+    const int64_t warps = g.NL * g.RB * ((ntb + tbm - 1) / tbm);
+    const unsigned grid = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(1) << 30));
+    // k-steps per 8-row band block: ceil((8 + 2p) / 4) = 3 (p = 2), 4 (p = 3, 4), 5 (p = 5, 6)
+#define GEO_DMMA(TB)                                                                                      \
+  do {                                                                                                    \
+    if (g.KS <= 4)                                                                                        \
+      geo_dmma_kernel<TB, 4><<<grid, 256, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+    else                                                                                                  \
+      geo_dmma_kernel<TB, 5><<<grid, 256, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+  } while (0)
+    if (tbm == 2)
+      GEO_DMMA(2);
+    else
+      GEO_DMMA(5);
+#undef GEO_DMMA
+    GEO_CUDA(cudaGetLastError());
+    if (launches) *launches += 2;
+    return LS_OK;
+  }
   dim3 grid(unsigned((gd.Ns + ST_THREADS - 1) / ST_THREADS), unsigned((nt + ST_TC - 1) / ST_TC));
   geo_stencil_kernel<<<grid, ST_THREADS, 0, s>>>(gd.st, t1, t2, x, y, gd.d, gd.p, gd.n[0], gd.n[1], gd.n[2],
                                                  gd.Ns, gd.S, nt);

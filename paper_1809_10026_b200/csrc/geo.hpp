@@ -48,12 +48,13 @@ struct GeoDev {
   int S = 0;                  // stencil width (2p+1)^d
   double* st = nullptr;       // [3][S][Ns]: M_s, J_s, L_s rows in stencil layout
   double* diag[3] = {nullptr, nullptr, nullptr};  // views of the centre entries
+  int variant = 0;            // 0: DMMA band tiles (default), 1: DFMA stencil kernel
   std::vector<void*> allocs;
   ~GeoDev();
 };
 
-// Assemble M_s, J_s, L_s on the device (one CTA per element, fp64 atomics into the
-// stencil rows).  launches is incremented by the kernels launched.
+// Assemble M_s, J_s, L_s on the device (one CTA per element, (p+1)^d launches over the
+// element colour classes so that the stencil-row updates never collide: deterministic).  launches is incremented by the kernels launched.
 int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el, cudaStream_t s,
                  int64_t* launches);
 

@@ -48,14 +48,20 @@ MV_CASES = [
     ("annulus3d", 2, 2, [4, 5, 3, 6]),
     ("annulus3d", 3, 3, [5, 4, 6, 4]),
     ("affine", 3, 2, [3, 4, 2, 5]),
+    ("annulus2d", 3, 2, [5, 6, 130]),      # n_t = 131: 17 time blocks of the DMMA tile
+    ("annulus3d", 2, 4, [9, 3, 4, 60]),    # n_1 = 9: ragged 8-row block, n_t = 63
 ]
 
 
+@pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("name,p,pt,n_elems", MV_CASES)
-def test_geo_matvec_matches_oracle(torch_cuda, name, p, pt, n_elems):
+def test_geo_matvec_matches_oracle(torch_cuda, name, p, pt, n_elems, variant):
+    """variant 0: DMMA band tiles (default); 1: DFMA stencil kernel (ls_tune LS_TUNE_MATVEC = 1)."""
     torch = torch_cuda
     import paper_1809_10026_b200 as ls
     ctx, geo, sf, tf = _setup(name, p, n_elems, ls.LS_PRECOND_P, pt)
+    if variant:
+        ctx.tune(2, 1)
     for seed in (1, 2):
         x = synth.residual(ctx.shape, seed)
         y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
@@ -132,7 +138,15 @@ def test_geo_pcg_matches_oracle(torch_cuda, name, p, n_elems, precond):
     x_ref, it, ok, _ = opcg.pcg(A, Pinv, b)
     assert ok and st["status"] == 0
     assert st["iters"] == it
-    assert _rel(x.cpu().numpy(), x_ref) <= 1e-9
+    # the iterate at equal k: rounding-order differences grow with the iteration count on
+    # these worse-conditioned systems (P: ~65 iterations), so the unique solution is
+    # compared on a converged pair (tol 1e-12 on both sides)
+    if it <= 30:
+        assert _rel(x.cpu().numpy(), x_ref) <= 1e-9
+    x2, st2 = ctx.pcg(torch.from_numpy(b).cuda(), tol=1e-12)
+    x2_ref, _, ok2, _ = opcg.pcg(A, Pinv, b, tol=1e-12)
+    assert ok2 and st2["status"] == 0
+    assert _rel(x2.cpu().numpy(), x2_ref) <= 1e-9
 
 
 def test_geo_pg_fewer_iterations(torch_cuda):
