@@ -596,12 +596,12 @@ struct FragGeom {
   int64_t NL, Ns;
 };
 
-template <int TBM, int KSM>
-__global__ void __launch_bounds__(256, 2) geo_dmma_kernel(const double* __restrict__ st,
-                                                      const double* __restrict__ t1,
-                                                      const double* __restrict__ t2,
-                                                      const double* __restrict__ x, double* __restrict__ y,
-                                                      FragGeom g, int nt, int S) {
+template <int TBM, int KS>
+__global__ void __launch_bounds__(128, 3) geo_dmma_kernel(const double* __restrict__ st,
+                                                         const double* __restrict__ t1,
+                                                         const double* __restrict__ t2,
+                                                         const double* __restrict__ x, double* __restrict__ y,
+                                                         FragGeom g, int nt, int S) {
   const int lane = threadIdx.x & 31;
   // work item = (time chunk of TBM blocks, line, 8-row block), the time chunk slowest: the
   // warps resident at one time share it, so the t1 / t2 rows they read stay in L2
@@ -624,9 +624,19 @@ __global__ void __launch_bounds__(256, 2) geo_dmma_kernel(const double* __restri
     const int tb0 = chunk * TBM;
     const int ntb = min(TBM, (nt + 7) / 8 - tb0);  // blocks of this chunk
     const int tbl = (nt - 1) / 8 - tb0;            // local block of the last slice (W_t = e e^T)
-    const int i1 = rb * 8 + trow;            // B-fragment row of this lane (n = lane >> 2)
+    const bool chunk_last = tbl >= 0 && tbl < ntb;                // warp-uniform
+    const bool row_last = chunk_last && (tb0 + tbl) * 8 + trow == nt - 1;  // A row of this lane
+    const int i1 = rb * 8 + trow;                  // B-fragment row of this lane (n = lane >> 2)
     const bool iok = i1 < g.n1;
     const int64_t brow = L * g.n1 + i1;
+    int64_t toff[TBM];
+    bool tok[TBM];
+#pragma unroll
+    for (int tb = 0; tb < TBM; ++tb) {
+      const int t = (tb0 + tb) * 8 + trow;
+      tok[tb] = tb < ntb && t < nt;
+      toff[tb] = int64_t(t) * g.Ns;
+    }
     double acc[TBM][2];
 #pragma unroll
     for (int tb = 0; tb < TBM; ++tb) acc[tb][0] = acc[tb][1] = 0.0;
@@ -634,40 +644,37 @@ __global__ void __launch_bounds__(256, 2) geo_dmma_kernel(const double* __restri
       const int j2 = i2 + q % g.W2 - r2, j3 = i3 + q / g.W2 - r3;
       if (j2 < 0 || j2 >= g.n2 || j3 < 0 || j3 >= g.n3) continue;  // warp-uniform
       const int64_t src = (int64_t(j3) * g.n2 + j2) * g.n1;
-      // B fragments of this source line, all k-steps: band entry (i_1, o_1 = 4 ks + k - n)
-      // gathered from the compact stencil rows (zero outside the band / the grid)
-      double bM[KSM], bJ[KSM], bL[KSM];
+      // every load of this source line first (B: band entries (i_1, o_1 = 4 ks + k - n) gathered
+      // from the compact stencil rows; A: t1 / t2 rows), then the DMMAs: one exposed latency
+      // per source line, overlapped by the other resident warps' tensor work
+      double bM[KS], bJ[KS], bL[KS], aM[KS][TBM], aJ[KS][TBM], aL[KS];
 #pragma unroll
-      for (int ks = 0; ks < KSM; ++ks) {
+      for (int ks = 0; ks < KS; ++ks) {
         const int o1 = ks * 4 + kc - trow;
-        const bool ok = ks < g.KS && iok && o1 >= 0 && o1 < W;
+        const bool ok = iok && o1 >= 0 && o1 < W;
         const size_t off = size_t(o1 + W * q) * g.Ns + brow;
         bM[ks] = ok ? __ldg(Ms + off) : 0.0;
         bJ[ks] = ok ? __ldg(Js + off) : 0.0;
-        bL[ks] = ok ? __ldg(Ls + off) : 0.0;
-      }
-#pragma unroll
-      for (int ks = 0; ks < KSM; ++ks) {
-        if (ks >= g.KS) break;
+        bL[ks] = (ok && chunk_last) ? __ldg(Ls + off) : 0.0;
         const int j1 = rb * 8 - g.p + ks * 4 + kc;   // A-fragment column (k = lane & 3)
         const bool jok = j1 >= 0 && j1 < g.n1;
-        double aM[TBM], aJ[TBM];
 #pragma unroll
         for (int tb = 0; tb < TBM; ++tb) {
-          const int t = (tb0 + tb) * 8 + trow;
-          const bool ok = jok && tb < ntb && t < nt;
-          const int64_t off = int64_t(t) * g.Ns + src + j1;
-          aM[tb] = ok ? __ldg(t1 + off) : 0.0;
-          aJ[tb] = ok ? __ldg(t2 + off) : 0.0;
+          const bool okt = jok && tok[tb];
+          aM[ks][tb] = okt ? __ldg(t1 + toff[tb] + src + j1) : 0.0;
+          aJ[ks][tb] = okt ? __ldg(t2 + toff[tb] + src + j1) : 0.0;
         }
-        const double aL = (jok && (tb0 + tbl) * 8 + trow == nt - 1) ? __ldg(xl + src + j1) : 0.0;
+        aL[ks] = (jok && row_last) ? __ldg(xl + src + j1) : 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
 #pragma unroll
         for (int tb = 0; tb < TBM; ++tb) {
           if (tb < ntb) {
-            dmma(acc[tb], aM[tb], bM[ks]);
-            dmma(acc[tb], aJ[tb], bJ[ks]);
+            dmma(acc[tb], aM[ks][tb], bM[ks]);
+            dmma(acc[tb], aJ[ks][tb], bJ[ks]);
           }
-          if (tb == tbl) dmma(acc[tb], aL, bL[ks]);
+          if (tb == tbl) dmma(acc[tb], aL[ks], bL[ks]);
         }
       }
     }
@@ -709,21 +716,34 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, c
   if (gd.variant != 1) {
     const FragGeom g = frag_geom(gd);
     const int ntb = (nt + 7) / 8;
-    const int tbm = ntb <= 2 ? 2 : 5;
+    // time blocks per warp: the largest of 5..2 with the fewest idle blocks in the last chunk
+    int tbm = 5, waste = 1 << 30;
+    for (int c = 5; c >= 2; --c) {
+      const int wst = (ntb + c - 1) / c * c - ntb;
+      if (wst < waste) {
+        waste = wst;
+        tbm = c;
+      }
+    }
+    if (ntb == 1) tbm = 2;
     const int64_t warps = g.NL * g.RB * ((ntb + tbm - 1) / tbm);
-    const unsigned grid = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(1) << 30));
+    const unsigned grid = unsigned(std::min<int64_t>((warps + 3) / 4, int64_t(1) << 30));
     // k-steps per 8-row band block: ceil((8 + 2p) / 4) = 3 (p = 2), 4 (p = 3, 4), 5 (p = 5, 6)
 #define GEO_DMMA(TB)                                                                                      \
   do {                                                                                                    \
-    if (g.KS <= 4)                                                                                        \
-      geo_dmma_kernel<TB, 4><<<grid, 256, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+    if (g.KS == 3)                                                                                        \
+      geo_dmma_kernel<TB, 3><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+    else if (g.KS == 4)                                                                                   \
+      geo_dmma_kernel<TB, 4><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
     else                                                                                                  \
-      geo_dmma_kernel<TB, 5><<<grid, 256, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+      geo_dmma_kernel<TB, 5><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
   } while (0)
-    if (tbm == 2)
-      GEO_DMMA(2);
-    else
-      GEO_DMMA(5);
+    switch (tbm) {
+      case 2: GEO_DMMA(2); break;
+      case 3: GEO_DMMA(3); break;
+      case 4: GEO_DMMA(4); break;
+      default: GEO_DMMA(5); break;
+    }
 #undef GEO_DMMA
     GEO_CUDA(cudaGetLastError());
     if (launches) *launches += 2;
