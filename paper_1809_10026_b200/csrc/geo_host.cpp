@@ -199,7 +199,7 @@ int pg_weights(const GeoMap& g, const int64_t* n_el, std::vector<double> mu[3], 
         o[k][v] = nv;
       }
     }
-    if (change < 1e-17L) break;
+    if (change < 1e-16L) break;
   }
   // relative residual of the fit (max over equations of |c - approx| / c), reported
   R res = 0;
