@@ -241,8 +241,9 @@ typedef struct {
  *   pcg_solve works unchanged; ls_rhs, ls_energy_error and the distributed / per-rank
  *     entry points return LS_ENOTSUP (the caller supplies b).
  * Limits: (p_s + 1)^d <= 343 local functions per element (d = 3: p_s <= 6).
- * Errors: as ls_setup; LS_EINVAL also for an invalid map or a singular Jacobian at an
- * element midpoint.
+ * Errors: as ls_setup; LS_EINVAL also for an invalid map description, or a Jacobian
+ * determinant that vanishes, is not finite or changes sign at a quadrature point
+ * (Assumption 4, PAPER.md 238-240: F^{-1} with bounded derivatives).
  */
 int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
                  ls_ctx** out);

@@ -78,6 +78,7 @@ struct GeoQArgs {
   const double* w;           // [prod m]
   double* out;               // [13][NQ]: wdet, Jinv[3][3] (row j = grad eta_j), b[3]
   int64_t NQ;
+  int* flags;                // bit 0: det J <= 0 seen, bit 1: det J >= 0 seen, bit 2: det J = 0 / non-finite
 };
 
 __global__ void geo_qpoint_kernel(GeoQArgs a) {
@@ -184,6 +185,9 @@ __global__ void geo_qpoint_kernel(GeoQArgs a) {
         for (int l = 0; l < d; ++l) c[m_] += A[j][l] * H[m_][j][l];
     for (int j = 0; j < d; ++j)
       for (int m_ = 0; m_ < d; ++m_) b[j] -= inv[j][m_] * c[m_];
+    // Ass. 4: F^{-1} with bounded derivatives -> det J of one sign, bounded away from 0
+    if (!(fabs(det) > 1e-300) || !isfinite(det) || !isfinite(b[0] + b[1] + b[2])) atomicOr(a.flags, 4);
+    else atomicOr(a.flags, det < 0 ? 1 : 2);
     double wq = 1;
     for (int k = 0; k < d; ++k) wq *= a.wq[k][iq[k]];
     a.out[qi] = wq * fabs(det);
@@ -448,8 +452,17 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
   qa.out = qd;
   GEO_CUDA(cudaMemsetAsync(qd, 0, size_t(13) * NQ * sizeof(double), s));
   GEO_CUDA(cudaMemsetAsync(gd.st, 0, size_t(3) * gd.S * gd.Ns * sizeof(double), s));
+  int* dflags = nullptr;
+  GEO_CUDA(cudaMalloc(&dflags, sizeof(int)));
+  gd.allocs.push_back(dflags);
+  GEO_CUDA(cudaMemsetAsync(dflags, 0, sizeof(int), s));
+  qa.flags = dflags;
   geo_qpoint_kernel<<<unsigned(std::min<int64_t>((NQ + 255) / 256, 148 * 16)), 256, 0, s>>>(qa);
   GEO_CUDA(cudaGetLastError());
+  int hflags = 0;
+  GEO_CUDA(cudaMemcpyAsync(&hflags, dflags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GEO_CUDA(cudaStreamSynchronize(s));
+  if ((hflags & 4) || (hflags & 3) == 3) return LS_EINVAL;  // singular or folded map
   // assembly
   aa.d = d;
   aa.p = p;

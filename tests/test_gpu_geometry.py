@@ -184,6 +184,14 @@ def test_geo_errors(torch_cuda):
         ls.Context(2, 2, [4, 4, 4], geometry=neg)
     with pytest.raises(ls.LSError):
         ls.Context(3, 7, [2, 2, 2, 2], geometry=synth.revolved_quarter_annulus())   # (p+1)^3 > 343
+    # a folded map (one control point dragged across the domain: det J changes sign)
+    fold = dict(geo)
+    c = geo["ctrl"].copy()
+    c[0] = [3.0, 3.0]
+    fold["ctrl"] = c
+    with pytest.raises(ls.LSError) as e:
+        ls.Context(2, 2, [4, 4, 4], geometry=fold)
+    assert e.value.code == ls.LS_EINVAL
     # b = 0 -> x = 0, 0 iterations
     x, st = ctx.pcg(b)
     assert st["iters"] == 0 and float(x.abs().max()) == 0.0
