@@ -34,7 +34,7 @@ def timed(fn, stream, reps):
     return float(np.median(ts))
 
 
-def run(n_el, p, precond, reps, pcg, geo_name="annulus3d"):
+def run(n_el, p, precond, reps, pcg, geo_name="annulus3d", variant=0):
     geo = synth.GEOMETRIES[geo_name]()
     d = geo["d"]
     stream = torch.cuda.Stream()
@@ -44,6 +44,8 @@ def run(n_el, p, precond, reps, pcg, geo_name="annulus3d"):
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     ctx.set_stream(stream)
+    if variant:
+        ctx.tune(2, variant)
     with torch.cuda.stream(stream):
         x = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
         y = torch.empty_like(x)
@@ -56,7 +58,7 @@ def run(n_el, p, precond, reps, pcg, geo_name="annulus3d"):
     S = (2 * p + 1) ** d
     Ns = int(np.prod(ctx.n_s))
     N = ctx.N
-    out = {"geometry": geo_name, "d": d, "p": p, "n_el": n_el, "N": N, "precond": ["P", "P^G"][precond],
+    out = {"variant": variant, "geometry": geo_name, "d": d, "p": p, "n_el": n_el, "N": N, "precond": ["P", "P^G"][precond],
            "setup_s": round(setup_s, 3), "matvec_ms": mv, "fd_apply_ms": fdm,
            "stencil_bytes_alg": 8.0 * (3 * S * Ns + 3 * N), "stencil_flops_alg": 4.0 * S * N,
            "fit_rel_res": ctx.geo_info()[0]}
@@ -81,11 +83,13 @@ def main():
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--precond", type=int, nargs="+", default=[0, 1])
     ap.add_argument("--geometry", default="annulus3d")
+    ap.add_argument("--variant", type=int, nargs="+", default=[0])
     a = ap.parse_args()
     for n in a.n_el:
         for p in a.p:
             for pc in a.precond:
-                print(json.dumps(run(n, p, pc, a.reps, not a.no_pcg, a.geometry)), flush=True)
+                for v in a.variant:
+                    print(json.dumps(run(n, p, pc, a.reps, not a.no_pcg, a.geometry, v)), flush=True)
 
 
 if __name__ == "__main__":
