@@ -341,6 +341,10 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * over NVLink), each followed by a cross-GPU flag barrier.  Enabling is collective (every
  * rank calls it).  Not yet validated on a multi-GPU box. */
 #define LS_TUNE_A2A 4
+/* LS_TUNE_PCG_GRAPH: 1 = pcg_solve runs iterations 2.. as one CUDA-graph launch (a WHILE
+ * conditional node around the captured iteration; no per-iteration host round trip;
+ * default on one GPU), 0 = host-driven loop.  Same kernels in the same order either way. */
+#define LS_TUNE_PCG_GRAPH 5
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

@@ -108,6 +108,14 @@ struct ls_ctx {
   int precond = LS_PRECOND_P;
   double* dm12 = nullptr;    // D^{-1/2} (N) for P^G
   double fit_res = 0.0;
+  // graph-resident PCG loop (one GPU): the iteration body captured once under a WHILE node
+  int pcg_graph = 1;                 // ls_tune LS_TUNE_PCG_GRAPH
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t pcg_exec = nullptr;
+  const double* pcg_key_x = nullptr;
+  double pcg_key_tol = -1.0;
+  int pcg_key_iter = -1;
+  int64_t pcg_body_launches = 0;
   std::vector<void*> allocs;
   // profiling of the mode kernel
   bool prof = false;
@@ -128,6 +136,8 @@ struct ls_ctx {
     for (auto e : hev)
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
   }
   int alloc(double** ptr, size_t count) {
     void* v = nullptr;
@@ -1354,6 +1364,73 @@ static int read_scal(ls_ctx* ctx) {
   return LS_OK;
 }
 
+// One PCG iteration after the first, in the order of the host loop below (reading c7):
+// z = P r; rho1 = r.z; p = z + (rho1/rho0) p; rho0 = rho1; q = A p; pq; x += a p, r -= a q; rr;
+// k += 1 and the stopping test.  Captured into the body of a WHILE conditional node so the
+// whole solve after the first iteration is ONE graph launch: no per-iteration host
+// round trip (config 2 is launch / latency bound).
+static int pcg_build_graph(ls_ctx* ctx, double* x, double tol, int max_iter) {
+  if (ctx->pcg_exec) {
+    cudaGraphExecDestroy(ctx->pcg_exec);
+    ctx->pcg_exec = nullptr;
+  }
+  if (!ctx->cap_stream) LS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  LS_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  LS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wn;
+  LS_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t user = ctx->stream;
+  ctx->stream = ctx->cap_stream;
+  const int64_t l0 = ctx->launches;
+  int rc = LS_OK;
+  if (cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
+      cudaSuccess)
+    rc = LS_ECUDA;
+  double *r = ctx->pr, *z = ctx->pz, *p = ctx->pp, *q = ctx->pq;
+  const unsigned gb = RED_BLOCKS;
+  if (rc == LS_OK) rc = fd_apply(ctx, r, z);
+  if (rc == LS_OK) rc = dot(ctx, r, z, S_RHO1);
+  if (rc == LS_OK) {
+    update_p_kernel<<<gb, RED_THREADS, 0, ctx->stream>>>(p, z, uint64_t(ctx->Nl), ctx->scal, S_RHO1, S_RHO0);
+    copy_slot_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scal, S_RHO0, S_RHO1);
+    ctx->launches += 2;
+    rc = ls_matvec(ctx, p, q);
+  }
+  if (rc == LS_OK) rc = dot(ctx, p, q, S_PQ);
+  if (rc == LS_OK) {
+    update_xr_kernel<<<gb, RED_THREADS, 0, ctx->stream>>>(x, r, p, q, uint64_t(ctx->Nl), ctx->scal, S_RHO0,
+                                                         ctx->partials);
+    reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, S_RR);
+    pcg_check_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scal, tol, max_iter, h);
+    ctx->launches += 3;
+  }
+  cudaGraph_t out = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &out);
+  ctx->stream = user;
+  ctx->pcg_body_launches = ctx->launches - l0;
+  ctx->launches = l0;
+  if (rc == LS_OK && ec != cudaSuccess) rc = LS_ECUDA;
+  if (rc == LS_OK && cudaGraphInstantiate(&ctx->pcg_exec, g, 0) != cudaSuccess) {
+    ctx->pcg_exec = nullptr;
+    rc = LS_ECUDA;
+  }
+  cudaGraphDestroy(g);
+  cudaGetLastError();  // a failed capture leaves a sticky-free error: the host loop takes over
+  if (rc != LS_OK) return rc;
+  ctx->pcg_key_x = x;
+  ctx->pcg_key_tol = tol;
+  ctx->pcg_key_iter = max_iter;
+  return LS_OK;
+}
+
 extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
                          ls_pcg_stats* st) {
   if (!ctx || !b || !x || b == x || !aligned8(b) || !aligned8(x) || !(tol >= 0) || max_iter < 0)
@@ -1401,6 +1478,23 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
     if (rel <= tol) {
       s.status = LS_OK;
       break;
+    }
+    if (k == 1 && k < max_iter && ctx->world == 1 && ctx->pcg_graph && !ctx->prof) {
+      // iterations 2.. as one graph launch (cur == S_RHO0 here)
+      bool ok = ctx->pcg_exec && ctx->pcg_key_x == x && ctx->pcg_key_tol == tol && ctx->pcg_key_iter == max_iter;
+      if (!ok) ok = pcg_build_graph(ctx, x, tol, max_iter) == LS_OK;
+      if (ok) {
+        ctx->h_scal[S_K] = 1.0;
+        LS_CUDA(cudaMemcpyAsync(ctx->scal + S_K, ctx->h_scal + S_K, sizeof(double), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        LS_CUDA(cudaGraphLaunch(ctx->pcg_exec, ctx->stream));
+        LS_CHECK(read_scal(ctx));
+        k = int(ctx->h_scal[S_K]);
+        ctx->launches += ctx->pcg_body_launches * (k - 1);
+        rel = std::sqrt(ctx->h_scal[S_RR]) / bnorm;
+        s.status = int(ctx->h_scal[S_STAT]);
+        break;
+      }
     }
     LS_CHECK(fd_apply(ctx, r, z));
     LS_CHECK(dot(ctx, r, z, nxt));
@@ -1615,6 +1709,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       if (Q % 4 != 0) return LS_ENOTSUP;  // the scattering epilogue is a FAST-path variant
       return ctx->comm->setup_fused(ctx->tmp[1], ctx->tmp[0]);
     }
+    case LS_TUNE_PCG_GRAPH:  // 1 = graph-resident PCG loop (default on one GPU), 0 = host loop
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->pcg_graph = value;
+      return LS_OK;
     case LS_TUNE_MV3_PAD:  // row granularity of the v3 intermediates along direction 1
       if (value != 1 && value != 8 && value != 16) return LS_EINVAL;
       if (ctx->d < 2) return LS_OK;

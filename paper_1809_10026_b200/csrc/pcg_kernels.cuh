@@ -13,7 +13,8 @@ constexpr int RED_THREADS = 256;
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs; fixed for determinism
 
 // scalar slots
-enum { S_RHO0 = 0, S_RHO1 = 1, S_PQ = 2, S_RR = 3, S_BB = 4, S_ALPHA = 5, S_BETA = 6, S_AUX = 7, S_NSLOT = 8 };
+enum { S_RHO0 = 0, S_RHO1 = 1, S_PQ = 2, S_RR = 3, S_BB = 4, S_ALPHA = 5, S_BETA = 6, S_AUX = 7, S_K = 8, S_STAT = 9,
+       S_NSLOT = 10 };
 
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double sh[RED_THREADS / 32];
@@ -80,6 +81,33 @@ __global__ void __launch_bounds__(RED_THREADS) update_p_kernel(double* __restric
   for (uint64_t i = blockIdx.x * uint64_t(RED_THREADS) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * RED_THREADS)
     p[i] = fma(beta, p[i], z[i]);
+}
+
+// graph-resident PCG (pcg_solve, one GPU): scal[S_RHO0] = scal[S_RHO1] after update_p, so
+// the captured loop body uses fixed slots
+__global__ void copy_slot_kernel(double* scal, int dst, int src) { scal[dst] = scal[src]; }
+
+// end of a graph-resident iteration: k += 1 and the stopping test of the host loop
+// (reading c7: ||r_k|| / ||b|| <= tol; NaN/Inf -> LS_ENUMERIC; k = max_iter -> LS_ENOCONV),
+// written to scal[S_K], scal[S_STAT]; the WHILE node continues while the test fails
+__global__ void pcg_check_kernel(double* scal, double tol, int max_iter, cudaGraphConditionalHandle h) {
+  const double k = scal[S_K] + 1.0;
+  scal[S_K] = k;
+  const double rr = scal[S_RR], alpha = scal[S_ALPHA];
+  unsigned cont = 0;
+  double stat;
+  if (!isfinite(rr) || !isfinite(alpha)) {
+    stat = 4.0;  // LS_ENUMERIC
+  } else if (sqrt(rr) / sqrt(scal[S_BB]) <= tol) {
+    stat = 0.0;  // LS_OK
+  } else if (k >= double(max_iter)) {
+    stat = 3.0;  // LS_ENOCONV
+  } else {
+    stat = 3.0;
+    cont = 1;
+  }
+  scal[S_STAT] = stat;
+  cudaGraphSetConditional(h, cont);
 }
 
 // y = a - b
