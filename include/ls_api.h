@@ -4,8 +4,9 @@
  * (Montardini, Negri, Sangalli, Tani, arXiv 1809.10026; PAPER.md = the paper).
  *
  * Problem (PAPER.md 343-353, eq:heat_eq): d_t u - Lap u = f on the
- * identity-mapped unit hypercube [0,1]^d x [0,T], T = 1 (reading c9),
- * homogeneous Dirichlet and initial data.  Discretisation: tensor B-splines of
+ * identity-mapped unit hypercube [0,1]^d x [0,T], T = 1 (reading c9), or on a
+ * mapped domain Omega = F([0,1]^d) (ls_setup_geo), homogeneous Dirichlet and
+ * initial data.  Discretisation: tensor B-splines of
  * degree p, C^{p-1}, n_el uniform elements per direction (PAPER.md 144-213,
  * 1111-1112); space basis i_k = 2..m_k-1, time basis i_t = 2..m_t
  * (eq:basis_par, PAPER.md 266-267), so n_k = n_el,k + p - 2 and
@@ -186,7 +187,8 @@ int ls_rhs(ls_ctx* ctx, int kind, double* b);
  * or after max_iter A-products.  x is overwritten (x must not alias b: LS_EINVAL).
  * b == 0 returns x = 0 with
  * 0 iterations.  Synchronous.  Returns LS_OK, LS_ENOCONV or LS_ENUMERIC (st
- * filled in all three cases; st may be NULL).
+ * filled in all three cases; st may be NULL).  On one GPU, iterations 2.. run as one
+ * CUDA-graph launch (LS_TUNE_PCG_GRAPH; the graph is cached per (x, tol, max_iter)).
  */
 int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
               ls_pcg_stats* st);
