@@ -240,8 +240,9 @@ typedef struct {
  *     c_tau, c_k at the element midpoints, separable least-squares fit of their
  *     logarithms (reading c21), factors interpolated piecewise linearly (reading c22),
  *     weighted univariate matrices, Algorithm 1 for Pbar^G, D_ii = A_ii / Pbar^G_ii.
- *   pcg_solve works unchanged; ls_rhs, ls_energy_error and the distributed / per-rank
- *     entry points return LS_ENOTSUP (the caller supplies b).
+ *   pcg_solve works unchanged; ls_matvec_slab applies slab rows (as for the cube);
+ *     ls_rhs, ls_energy_error, fd_apply_stage and fd_apply_scatter return LS_ENOTSUP
+ *     (the caller supplies b).
  * Limits: (p_s + 1)^d <= 343 local functions per element (d = 3: p_s <= 6).
  * Errors: as ls_setup; LS_EINVAL also for an invalid map description, or a Jacobian
  * determinant that vanishes, is not finite or changes sign at a quadrature point
@@ -249,6 +250,17 @@ typedef struct {
  */
 int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
                  ls_ctx** out);
+
+/*
+ * ls_setup_geo_dist -- ls_setup_geo for rank `rank` of `world` processes (one GPU each), with
+ * the time-slab layout of ls_setup_dist: every rank assembles the (spatial)
+ * physical factors, ls_matvec exchanges p_t halo slices and applies the slab rows
+ * (ls_matvec_slab likewise), fd_apply = D^{-1/2} (slab-local) around the distributed
+ * Algorithm 1, pcg_solve all-reduces its scalars.  ls_setup_geo(...) is ls_setup_geo_dist
+ * with rank 0 of 1.  Errors: as ls_setup_geo plus LS_ENCCL.
+ */
+int ls_setup_geo_dist(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
+                      int rank, int world, const void* nccl_unique_id, ls_ctx** out);
 
 /*
  * ls_geo_info -- out2[0] = max relative residual of the separable fit of c_tau, c_k at

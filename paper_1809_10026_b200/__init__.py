@@ -32,7 +32,7 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
-            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info"]
+            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist"]
 
 LS_PRECOND_P, LS_PRECOND_PG = 0, 1
 
@@ -94,6 +94,9 @@ def load_library(path=LIB_PATH):
         "ls_setup_geo": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(Geometry),
                                         ctypes.c_int, ctypes.POINTER(vp)]),
         "ls_geo_info": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
+        "ls_setup_geo_dist": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p,
+                                             ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_char_p, ctypes.POINTER(vp)]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "ls_energy_error": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.POINTER(ctypes.c_double)]),
         "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
@@ -198,8 +201,6 @@ class Context:
         torch.cuda.init()
         ps, pt = (p, p) if isinstance(p, int) else (int(p[0]), int(p[1]))
         if geometry is not None:
-            if world != 1:
-                raise ValueError("mapped-domain contexts are single-GPU")
             g = Geometry()
             keep = []
             for k in range(d):
@@ -215,8 +216,8 @@ class Context:
                 w = np.ascontiguousarray(geometry["weights"], dtype=np.float64)
                 keep.append(w)
                 g.weights = w.ctypes.data
-            _check(lib.ls_setup_geo(d, ps, pt, ne, ctypes.byref(g), int(precond), ctypes.byref(h)),
-                   "ls_setup_geo")
+            _check(lib.ls_setup_geo_dist(d, ps, pt, ne, ctypes.byref(g), int(precond), int(rank), int(world),
+                                         uid, ctypes.byref(h)), "ls_setup_geo_dist")
         elif world == 1:
             _check(lib.ls_setup_deg(d, ps, pt, ne, ctypes.byref(h)), "ls_setup_deg")
         else:

@@ -562,7 +562,8 @@ static int setup_common(ls_ctx* ctx) {
       LS_CHECK(upload(ctx, pdt, &dpdt));
       LS_CHECK(upload(ctx, pds, &dpds));
       LS_CHECK(ctx->alloc(&ctx->dm12, ctx->Nl));
-      LS_CHECK(pg_scaling(*ctx->geo, ctx->bKt, ctx->bMt, nt, dpdt, dpds, ctx->dm12, ctx->stream, &ctx->launches));
+      LS_CHECK(pg_scaling(*ctx->geo, ctx->bKt, ctx->bMt, nt, dpdt, dpds, ctx->dm12, int(ctx->t0), int(ctx->ntl),
+                          ctx->stream, &ctx->launches));
     }
   }
   LS_CUDA(cudaDeviceSynchronize());
@@ -601,10 +602,17 @@ extern "C" int ls_setup(int d, int p, const int64_t* n_elems, ls_ctx** out) {
 
 extern "C" int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo, int precond,
                             ls_ctx** out) {
+  return ls_setup_geo_dist(d, p_s, p_t, n_elems, geo, precond, 0, 1, nullptr, out);
+}
+
+extern "C" int ls_setup_geo_dist(int d, int p_s, int p_t, const int64_t* n_elems, const ls_geometry* geo,
+                                 int precond, int rank, int world, const void* nccl_unique_id, ls_ctx** out) {
   if (!out) return LS_EINVAL;
   *out = nullptr;
   LS_CHECK(validate(d, p_s, p_t, n_elems));
   if (!geo || (precond != LS_PRECOND_P && precond != LS_PRECOND_PG)) return LS_EINVAL;
+  if (world < 1 || rank < 0 || rank >= world || (world > 1 && !nccl_unique_id)) return LS_EINVAL;
+  if (world > 1 && (n_elems[d] + p_t - 1) / world < p_t) return LS_EINVAL;  // slab thinner than the halo
   int nloc = 1;
   for (int k = 0; k < d; ++k) nloc *= p_s + 1;
   if (nloc > 343) return LS_EINVAL;
@@ -613,6 +621,8 @@ extern "C" int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, con
   ctx->p = p_s;
   ctx->pt = p_t;
   ctx->precond = precond;
+  ctx->rank = rank;
+  ctx->world = world;
   for (int k = 0; k <= d; ++k) ctx->n_el[k] = n_elems[k];
   ctx->gmap.reset(new GeoMap());
   int rc = geo_copy(geo, d, *ctx->gmap);
@@ -628,6 +638,10 @@ extern "C" int ls_setup_geo(int d, int p_s, int p_t, const int64_t* n_elems, con
     else if (double(3 * S) * double(Ns) * 8.0 > 0.5 * double(fr)) rc = LS_ENOMEM;  // the three stencil arrays
   }
   if (rc == LS_OK) rc = setup_common(ctx);
+  if (rc == LS_OK && world > 1) {
+    ctx->comm.reset(new Comm());
+    rc = ctx->comm->init(nccl_unique_id, rank, world, ctx->nt, ctx->Ns);
+  }
   if (rc != LS_OK) {
     delete ctx;
     return rc;
@@ -1279,9 +1293,9 @@ static void ext_geom(const ls_ctx* ctx, int64_t* lo, int64_t* hi) {
 
 extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   if (!ctx || !x || !y || x == y || !aligned8(x) || !aligned8(y)) return LS_EINVAL;
-  if (ctx->geo)
-    return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, ctx->nt, x, y, ctx->tmp[3], ctx->tmp[4], ctx->stream,
-                      &ctx->launches);
+  if (ctx->geo && ctx->world == 1)
+    return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, ctx->nt, x, 0, 0, ctx->nt, y, ctx->tmp[3], ctx->tmp[4],
+                      ctx->stream, &ctx->launches);
   if (ctx->world == 1) return matvec_any(ctx, x, y, ctx->nt, 0, 0, ctx->nt);
   int64_t lo, hi;
   ext_geom(ctx, &lo, &hi);
@@ -1289,13 +1303,15 @@ extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   if (x != own)
     LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->pt));
+  if (ctx->geo)  // mapped domain: slab-local time band + stencil pass (the spatial factors are replicated)
+    return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, ctx->nt, ctx->pp, int(ctx->t0 - lo), int(ctx->t0),
+                      int(ctx->ntl), y, ctx->tmp[3], ctx->tmp[4], ctx->stream, &ctx->launches);
   return matvec_any(ctx, ctx->pp, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl);
 }
 
 extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows,
                               double* y, int64_t t_first, int64_t nout) {
   if (!ctx || !x_ext || !y || !aligned8(x_ext) || !aligned8(y)) return LS_EINVAL;
-  if (ctx->geo) return LS_ENOTSUP;
   const int64_t nt = ctx->nt, p = ctx->pt;  // the time band
   if (nout < 0 || t_first < 0 || t_first + nout > nt || s_rows < 0) return LS_EINVAL;
   if (nout > ctx->ntl) return LS_EINVAL;  // workspaces hold ntl (+ halo) slices
@@ -1304,6 +1320,9 @@ extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first,
   if (nout > 0 && (s_first > need_lo || s_first + s_rows < need_hi)) return LS_EINVAL;
   if (s_rows > ctx->ntl + 2 * p) return LS_EINVAL;
   if (nout == 0) return LS_OK;
+  if (ctx->geo)
+    return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, int(nt), x_ext, int(s_first), int(t_first), int(nout), y,
+                      ctx->tmp[3], ctx->tmp[4], ctx->stream, &ctx->launches);
   return matvec_any(ctx, x_ext, y, s_rows, s_first, t_first, nout);
 }
 

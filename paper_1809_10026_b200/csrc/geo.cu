@@ -517,19 +517,23 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
 // ------------------------------------------------------------------------------------------
 // matvec
 // ------------------------------------------------------------------------------------------
+// rows [t_first, t_first + nout) of t1 = K_t x, t2 = M_t x (global time indices; the band is
+// clipped to [0, n_t)); x_ext holds the global rows [s_first, s_first + ...) that the band of
+// every output row needs (the time halo of a slab)
 __global__ void geo_time_kernel(const double* __restrict__ x, double* __restrict__ t1, double* __restrict__ t2,
                                 const double* __restrict__ bK, const double* __restrict__ bM, int nt, int pt,
-                                int64_t Ns) {
+                                int64_t Ns, int s_first, int t_first, int nout) {
   const int W = 2 * pt + 1;
-  const int64_t total = int64_t(nt) * Ns;
+  const int64_t total = int64_t(nout) * Ns;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    const int t = int(idx / Ns);
-    const int64_t i = idx - int64_t(t) * Ns;
+    const int tl = int(idx / Ns);
+    const int64_t i = idx - int64_t(tl) * Ns;
+    const int t = t_first + tl;
     double a = 0, b = 0;
     const int lo = max(0, t - pt), hi = min(nt - 1, t + pt);
     for (int s = lo; s <= hi; ++s) {
-      const double v = __ldg(x + int64_t(s) * Ns + i);
+      const double v = __ldg(x + int64_t(s - s_first) * Ns + i);
       a += __ldg(bK + t * W + (s - t + pt)) * v;
       b += __ldg(bM + t * W + (s - t + pt)) * v;
     }
@@ -543,13 +547,15 @@ constexpr int ST_THREADS = 128;
 
 __global__ void __launch_bounds__(ST_THREADS) geo_stencil_kernel(
     const double* __restrict__ st, const double* __restrict__ t1, const double* __restrict__ t2,
-    const double* __restrict__ x, double* __restrict__ y, int d, int p, int n1, int n2, int n3, int64_t Ns,
-    int S, int nt) {
+    const double* __restrict__ xl, double* __restrict__ y, int d, int p, int n1, int n2, int n3, int64_t Ns,
+    int S, int nt, int lastl) {
+  // nt: output rows (local); lastl: local row of the global last slice, -1 if not here;
+  // xl: that slice of x (W_t (x) L_s, W_t = e_{n_t} e_{n_t}^T)
   const int64_t i = blockIdx.x * int64_t(ST_THREADS) + threadIdx.x;
   if (i >= Ns) return;
   const int t0 = blockIdx.y * ST_TC;
   const int tn = min(ST_TC, nt - t0);
-  const bool last = (t0 + tn == nt);
+  const bool last = lastl >= t0 && lastl < t0 + tn;
   const int i1 = int(i % n1), i2 = int((i / n1) % n2), i3 = int(i / (int64_t(n1) * n2));
   const int W = 2 * p + 1;
   const int r2 = d >= 2 ? p : 0, r3 = d >= 3 ? p : 0;
@@ -581,13 +587,13 @@ __global__ void __launch_bounds__(ST_THREADS) geo_stencil_kernel(
             const int64_t off = int64_t(t0 + k) * Ns + j;
             acc[k] += cm * __ldg(t1 + off) + cj * __ldg(t2 + off);
           }
-        if (last) accL += __ldg(Ls + size_t(o) * Ns + i) * __ldg(x + int64_t(nt - 1) * Ns + j);
+        if (last) accL += __ldg(Ls + size_t(o) * Ns + i) * __ldg(xl + j);
       }
     }
   }
 #pragma unroll
   for (int k = 0; k < ST_TC; ++k)
-    if (k < tn) y[int64_t(t0 + k) * Ns + i] = acc[k] + ((last && k == tn - 1) ? accL : 0.0);
+    if (k < tn) y[int64_t(t0 + k) * Ns + i] = acc[k] + ((last && t0 + k == lastl) ? accL : 0.0);
 }
 
 // ---- tensor-core variant (default): the stencil pass as DMMA.8x8x4 tiles -------------------
@@ -613,8 +619,8 @@ template <int TBM, int KS>
 __global__ void __launch_bounds__(128, 3) geo_dmma_kernel(const double* __restrict__ st,
                                                          const double* __restrict__ t1,
                                                          const double* __restrict__ t2,
-                                                         const double* __restrict__ x, double* __restrict__ y,
-                                                         FragGeom g, int nt, int S) {
+                                                         const double* __restrict__ xl, double* __restrict__ y,
+                                                         FragGeom g, int nt, int S, int lastl) {
   const int lane = threadIdx.x & 31;
   // work item = (time chunk of TBM blocks, line, 8-row block), the time chunk slowest: the
   // warps resident at one time share it, so the t1 / t2 rows they read stay in L2
@@ -626,7 +632,6 @@ __global__ void __launch_bounds__(128, 3) geo_dmma_kernel(const double* __restri
   const double* Ms = st;
   const double* Js = st + size_t(S) * g.Ns;
   const double* Ls = st + size_t(2) * S * g.Ns;
-  const double* xl = x + int64_t(nt - 1) * g.Ns;
   for (int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; w < nwarps;
        w += (int64_t(gridDim.x) * blockDim.x) >> 5) {
     const int chunk = int(w / (g.NL * g.RB));
@@ -636,9 +641,10 @@ __global__ void __launch_bounds__(128, 3) geo_dmma_kernel(const double* __restri
     const int i2 = int(L % g.n2), i3 = int(L / g.n2);
     const int tb0 = chunk * TBM;
     const int ntb = min(TBM, (nt + 7) / 8 - tb0);  // blocks of this chunk
-    const int tbl = (nt - 1) / 8 - tb0;            // local block of the last slice (W_t = e e^T)
+    // local block of the global last slice (W_t = e e^T), -1 / out of range if not in this chunk
+    const int tbl = lastl >= 0 ? lastl / 8 - tb0 : -1;
     const bool chunk_last = tbl >= 0 && tbl < ntb;                // warp-uniform
-    const bool row_last = chunk_last && (tb0 + tbl) * 8 + trow == nt - 1;  // A row of this lane
+    const bool row_last = chunk_last && (tb0 + tbl) * 8 + trow == lastl;  // A row of this lane
     const int i1 = rb * 8 + trow;                  // B-fragment row of this lane (n = lane >> 2)
     const bool iok = i1 < g.n1;
     const int64_t brow = L * g.n1 + i1;
@@ -720,12 +726,17 @@ static FragGeom frag_geom(const GeoDev& gd) {
   return g;
 }
 
-int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* x, double* y,
-               double* t1, double* t2, cudaStream_t s, int64_t* launches) {
-  const int64_t total = int64_t(nt) * gd.Ns;
+int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt_global, const double* x,
+               int s_first, int t_first, int nout, double* y, double* t1, double* t2, cudaStream_t s,
+               int64_t* launches) {
+  if (nout <= 0) return LS_OK;
+  const int64_t total = int64_t(nout) * gd.Ns;
   geo_time_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
-      x, t1, t2, bKt, bMt, nt, gd.pt, gd.Ns);
+      x, t1, t2, bKt, bMt, nt_global, gd.pt, gd.Ns, s_first, t_first, nout);
   GEO_CUDA(cudaGetLastError());
+  const int nt = nout;  // rows of t1, t2, y below
+  const int lastl = (nt_global - 1 >= t_first && nt_global - 1 < t_first + nout) ? nt_global - 1 - t_first : -1;
+  const double* xl = x + int64_t(nt_global - 1 - s_first) * gd.Ns;  // dereferenced only if lastl >= 0
   if (gd.variant != 1) {
     const FragGeom g = frag_geom(gd);
     const int ntb = (nt + 7) / 8;
@@ -745,11 +756,11 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, c
 #define GEO_DMMA(TB)                                                                                      \
   do {                                                                                                    \
     if (g.KS == 3)                                                                                        \
-      geo_dmma_kernel<TB, 3><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+      geo_dmma_kernel<TB, 3><<<grid, 128, 0, s>>>(gd.st, t1, t2, xl, y, g, nt, gd.S, lastl);              \
     else if (g.KS == 4)                                                                                   \
-      geo_dmma_kernel<TB, 4><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+      geo_dmma_kernel<TB, 4><<<grid, 128, 0, s>>>(gd.st, t1, t2, xl, y, g, nt, gd.S, lastl);              \
     else                                                                                                  \
-      geo_dmma_kernel<TB, 5><<<grid, 128, 0, s>>>(gd.st, t1, t2, x, y, g, nt, gd.S);                      \
+      geo_dmma_kernel<TB, 5><<<grid, 128, 0, s>>>(gd.st, t1, t2, xl, y, g, nt, gd.S, lastl);              \
   } while (0)
     switch (tbm) {
       case 2: GEO_DMMA(2); break;
@@ -763,8 +774,8 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, c
     return LS_OK;
   }
   dim3 grid(unsigned((gd.Ns + ST_THREADS - 1) / ST_THREADS), unsigned((nt + ST_TC - 1) / ST_TC));
-  geo_stencil_kernel<<<grid, ST_THREADS, 0, s>>>(gd.st, t1, t2, x, y, gd.d, gd.p, gd.n[0], gd.n[1], gd.n[2],
-                                                 gd.Ns, gd.S, nt);
+  geo_stencil_kernel<<<grid, ST_THREADS, 0, s>>>(gd.st, t1, t2, xl, y, gd.d, gd.p, gd.n[0], gd.n[1], gd.n[2],
+                                                 gd.Ns, gd.S, nt, lastl);
   GEO_CUDA(cudaGetLastError());
   if (launches) *launches += 2;
   return LS_OK;
@@ -776,13 +787,14 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, c
 __global__ void pg_scaling_kernel(const double* __restrict__ Md, const double* __restrict__ Jd,
                                   const double* __restrict__ Ld, const double* __restrict__ bK,
                                   const double* __restrict__ bM, int pt, const double* __restrict__ pdt,
-                                  const double* __restrict__ pds, double* __restrict__ out, int nt, int64_t Ns) {
+                                  const double* __restrict__ pds, double* __restrict__ out, int nt, int64_t Ns,
+                                  int t0, int nrows) {
   const int W = 2 * pt + 1;
-  const int64_t total = int64_t(nt) * Ns;
+  const int64_t total = int64_t(nrows) * Ns;
   for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    const int t = int(idx / Ns);
-    const int64_t i = idx - int64_t(t) * Ns;
+    const int t = t0 + int(idx / Ns);  // global time index of this slab row
+    const int64_t i = idx % Ns;
     double a = bK[t * W + pt] * Md[i] + bM[t * W + pt] * Jd[i];
     if (t == nt - 1) a += Ld[i];  // W_t = e_{n_t} e_{n_t}^T
     const double pb = pdt[t] * pds[i] + pdt[nt + t] * pds[Ns + i];
@@ -791,10 +803,10 @@ __global__ void pg_scaling_kernel(const double* __restrict__ Md, const double* _
 }
 
 int pg_scaling(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* pdiag_t,
-               const double* pdiag_s, double* dm12, cudaStream_t s, int64_t* launches) {
-  const int64_t total = int64_t(nt) * gd.Ns;
+               const double* pdiag_s, double* dm12, int t0, int nrows, cudaStream_t s, int64_t* launches) {
+  const int64_t total = int64_t(nrows) * gd.Ns;
   pg_scaling_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(
-      gd.diag[0], gd.diag[1], gd.diag[2], bKt, bMt, gd.pt, pdiag_t, pdiag_s, dm12, nt, gd.Ns);
+      gd.diag[0], gd.diag[1], gd.diag[2], bKt, bMt, gd.pt, pdiag_t, pdiag_s, dm12, nt, gd.Ns, t0, nrows);
   GEO_CUDA(cudaGetLastError());
   if (launches) *launches += 1;
   return LS_OK;

@@ -58,15 +58,19 @@ struct GeoDev {
 int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el, cudaStream_t s,
                  int64_t* launches);
 
-// y = (K_t (x) M_s + M_t (x) J_s + W_t (x) L_s) x, W_t = e_{n_t} e_{n_t}^T (T = 1):
-// banded time products into t1, t2 (each n_t * N_s), then the stencil pass.
-int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* x, double* y,
-               double* t1, double* t2, cudaStream_t s, int64_t* launches);
+// Rows [t_first, t_first + nout) of y = (K_t (x) M_s + M_t (x) J_s + W_t (x) L_s) x,
+// W_t = e_{n_t} e_{n_t}^T (T = 1), from the global rows [s_first, ...) of x held in x (a time
+// slab with its halo; the whole vector with s_first = t_first = 0, nout = n_t on one GPU):
+// banded time products into t1, t2 (nout * N_s each), then the stencil pass.
+int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt_global, const double* x,
+               int s_first, int t_first, int nout, double* y, double* t1, double* t2, cudaStream_t s,
+               int64_t* launches);
 
 // D^{-1/2} of P^G = D^{1/2} Pbar^G D^{1/2}, D_ii = A_ii / Pbar_ii, as an N-vector
 // (diag(A) from the stencil centres and the banded time diagonals).
+// for the slab rows [t0, t0 + nrows) of the global time axis
 int pg_scaling(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* pdiag_t,
-               const double* pdiag_s, double* dm12, cudaStream_t s, int64_t* launches);
+               const double* pdiag_s, double* dm12, int t0, int nrows, cudaStream_t s, int64_t* launches);
 
 // y = s * x elementwise (the D^{-1/2} pre / post scaling of the P^G application)
 int scale_vec(const double* s_, const double* x, double* y, int64_t n, cudaStream_t s, int64_t* launches);

@@ -125,6 +125,54 @@ def _matvec_rank(rank, world, d, p, ne):
     return float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
 
 
+def _geo_matvec_rank(rank, world, name, p, ne):
+    """The mapped-domain ls_matvec of ls_setup_geo_dist: p_t halo slices exchanged with the
+    neighbours (ls_halo_plan), then the slab rows of K_t(x)M_s + M_t(x)J_s + W_t(x)L_s from
+    the extended slab (spatial factors replicated on every rank)."""
+    import warnings
+    warnings.filterwarnings("ignore")
+    import paper_1809_10026_b200 as ls
+    from oracle import geometry as og
+    geo = synth.GEOMETRIES[name]()
+    d = geo["d"]
+    sf = og.space_factors_physical(geo, ne[:d], p)
+    tf = uv.time_factors(ne[d], p)
+    nt = tf["Mt"].shape[0]
+    gshape = (nt,) + tuple(reversed(sf["n_s"]))
+    x = synth.residual(gshape, 2)
+    t0, ntl, lo, hi = ls.halo_plan(nt, world, rank, p)
+    own = x[t0:t0 + ntl].copy()
+    ext = np.zeros((lo + ntl + hi,) + gshape[1:])
+    ext[lo:lo + ntl] = own
+    reqs = []
+    if lo > 0:
+        lo_buf = torch.empty(ext[:lo].shape, dtype=torch.float64)
+        reqs.append(dist.irecv(lo_buf, src=rank - 1))
+        reqs.append(dist.isend(torch.from_numpy(own[:lo].copy()), dst=rank - 1))
+    if hi > 0:
+        hi_buf = torch.empty(ext[lo + ntl:].shape, dtype=torch.float64)
+        reqs.append(dist.irecv(hi_buf, src=rank + 1))
+        reqs.append(dist.isend(torch.from_numpy(own[ntl - hi:].copy()), dst=rank + 1))
+    for q in reqs:
+        q.wait()
+    if lo > 0:
+        ext[:lo] = lo_buf.numpy()
+    if hi > 0:
+        ext[lo + ntl:] = hi_buf.numpy()
+    s_first = t0 - lo
+    E = ext.reshape(ext.shape[0], -1)
+    SM, SJ, SL = (sf["M"] @ E.T).T, (sf["J"] @ E.T).T, (sf["L"] @ E.T).T
+    y = np.zeros((ntl, E.shape[1]))
+    for tl in range(ntl):
+        t = t0 + tl
+        for i in range(max(0, t - p), min(nt - 1, t + p) + 1):
+            y[tl] += tf["Kt"][t, i] * SM[i - s_first] + tf["Mt"][t, i] * SJ[i - s_first]
+        if t == nt - 1:
+            y[tl] += tf["Wt"][t, t] * SL[t - s_first]
+    ref = og.apply_A_geo(x, sf, tf)[t0:t0 + ntl].reshape(ntl, -1)
+    return float(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+
+
 def _dist_fd(r_slab, rank, world, fdd, d, gshape):
     """One rank's share of the distributed fd_apply (comm_fd_apply's NCCL schedule, over gloo)."""
     import paper_1809_10026_b200 as ls
@@ -264,6 +312,13 @@ def test_distributed_fd_schedule(world, d, p, ne):
 @pytest.mark.parametrize("d,p,ne", [(1, 2, [6, 9]), (2, 3, [3, 4, 12])])
 def test_distributed_matvec_halo(world, d, p, ne):
     errs = _run(world, "_matvec_rank", (d, p, ne))
+    assert max(errs) <= 1e-12, errs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name,p,ne", [("annulus2d", 3, [4, 5, 12]), ("annulus3d", 2, [2, 3, 2, 9])])
+def test_distributed_geo_matvec_halo(world, name, p, ne):
+    errs = _run(world, "_geo_matvec_rank", (name, p, ne))
     assert max(errs) <= 1e-12, errs
 
 

@@ -69,6 +69,33 @@ def test_geo_matvec_matches_oracle(torch_cuda, name, p, pt, n_elems, variant):
         assert _rel(y, y_ref) <= 1e-12, (seed, _rel(y, y_ref))
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("name,p,n_elems,world", [("annulus2d", 3, [6, 5, 30], 3),
+                                                  ("annulus3d", 2, [4, 3, 5, 25], 4),
+                                                  ("annulus2d", 2, [5, 4, 9], 2)])
+def test_geo_matvec_slab_decomposition(torch_cuda, variant, name, p, n_elems, world):
+    """The per-rank kernel of the distributed mapped-domain ls_matvec (ls_setup_geo_dist):
+    a time slab plus p_t halo slices each side (ls_matvec_slab, what ls_matvec runs after
+    its halo exchange), for every rank of a `world`-way split, against the oracle's A x;
+    the last slice's W_t (x) L_s term lands on the last rank only."""
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    ctx, geo, sf, tf = _setup(name, p, n_elems, ls.LS_PRECOND_P)
+    if variant:
+        ctx.tune(2, variant)
+    x = synth.residual(ctx.shape, 6)
+    y_ref = G.apply_A_geo(x, sf, tf)
+    xg = torch.from_numpy(x).cuda()
+    nt = ctx.shape[0]
+    y_full = ctx.matvec(xg).cpu().numpy()
+    for r in range(world):
+        t0, ntl, lo, hi = ls.halo_plan(nt, world, r, p)
+        x_ext = xg[t0 - lo:t0 + ntl + hi].contiguous()
+        y = ctx.matvec_slab(x_ext, t0 - lo, t0, ntl).cpu().numpy()
+        assert _rel(y, y_ref[t0:t0 + ntl]) <= 1e-12, (r, t0, ntl)
+        assert np.array_equal(y, y_full[t0:t0 + ntl])   # same kernels, same summation order
+
+
 @pytest.mark.parametrize("name,p,n_elems", [("annulus2d", 3, [6, 5, 7]), ("annulus3d", 2, [4, 3, 5, 4])])
 def test_geo_plain_P_is_parametric(torch_cuda, name, p, n_elems):
     """precond = LS_PRECOND_P: fd_apply is Algorithm 1 for the parametric P (eq:preconditioner)."""
