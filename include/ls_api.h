@@ -359,6 +359,10 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * conditional node around the captured iteration; no per-iteration host round trip;
  * default on one GPU), 0 = host-driven loop.  Same kernels in the same order either way. */
 #define LS_TUNE_PCG_GRAPH 5
+/* LS_TUNE_PDL (process-wide): 1 = the FD mode kernels use programmatic dependent launch
+ * (their shared-memory staging of U / lambda overlaps the previous kernel's tail; default),
+ * 0 = plain stream order. */
+#define LS_TUNE_PDL 6
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

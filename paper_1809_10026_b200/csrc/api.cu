@@ -24,6 +24,8 @@
 
 using namespace ls;
 
+int ls::g_ls_pdl = 1;  // programmatic dependent launch of the FD mode kernels (LS_TUNE_PDL)
+
 #define LS_CUDA(x)                                                                        \
   do {                                                                                    \
     cudaError_t err_ = (x);                                                               \
@@ -173,7 +175,7 @@ static int launch_mode_cfg(ls_ctx* ctx, const ModeArgs& a0) {
     rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
     cudaEventRecord(rec.a, ctx->stream);
   }
-  fd_mode_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  LS_CUDA(launch_pdl(fd_mode_kernel<C>, grid, C::THREADS, C::SMEM, ctx->stream, a));
   ctx->launches++;
   if (ctx->prof) {
     cudaEventRecord(rec.b, ctx->stream);
@@ -202,7 +204,7 @@ static int launch_mode_pp(ls_ctx* ctx, const ModeArgs& a0) {
     rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
     cudaEventRecord(rec.a, ctx->stream);
   }
-  fd_mode_pp_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  LS_CUDA(launch_pdl(fd_mode_pp_kernel<C>, grid, C::THREADS, C::SMEM, ctx->stream, a));
   ctx->launches++;
   if (ctx->prof) {
     cudaEventRecord(rec.b, ctx->stream);
@@ -951,7 +953,7 @@ static int launch_tile(ls_ctx* ctx, BandArgs a) {
   a.ntiles = (a.ncols + C::BN - 1) / C::BN;
   if (a.ntiles == 0) return LS_OK;
   const unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms * occ));
-  band_tile_kernel<P, RB, KIND, 3, NWARPS><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  LS_CUDA(launch_pdl(band_tile_kernel<P, RB, KIND, 3, NWARPS>, grid, C::THREADS, C::SMEM, ctx->stream, a));
   ctx->launches++;
   LS_CUDA(cudaGetLastError());
   return LS_OK;
@@ -965,7 +967,7 @@ static int launch_first(ls_ctx* ctx, BandArgs a) {
   a.ntiles = (a.ncols + C::BN - 1) / C::BN;
   if (a.ntiles == 0) return LS_OK;
   const unsigned grid = std::min<unsigned>(a.ntiles, unsigned(ctx->num_sms * occ));
-  band_first_kernel<P, NMAX, 2><<<grid, 256, C::SMEM, ctx->stream>>>(a);
+  LS_CUDA(launch_pdl(band_first_kernel<P, NMAX, 2>, grid, 256, C::SMEM, ctx->stream, a));
   ctx->launches++;
   LS_CUDA(cudaGetLastError());
   return LS_OK;
@@ -1368,8 +1370,10 @@ extern "C" int ls_rhs(ls_ctx* ctx, int kind, double* b) {
 // PCG
 // ------------------------------------------------------------------------------------------
 static int dot(ls_ctx* ctx, const double* a, const double* b, int slot) {
-  dot_partial_kernel<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(a, b, uint64_t(ctx->Nl), ctx->partials);
-  reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, slot);
+  LS_CUDA(launch_pdl(dot_partial_kernel, RED_BLOCKS, RED_THREADS, 0, ctx->stream, a, b, uint64_t(ctx->Nl),
+                     ctx->partials));
+  LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS), ctx->scal,
+                     slot));
   ctx->launches += 2;
   LS_CUDA(cudaGetLastError());
   if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + slot));
@@ -1418,17 +1422,19 @@ static int pcg_build_graph(ls_ctx* ctx, double* x, double tol, int max_iter) {
   if (rc == LS_OK) rc = fd_apply(ctx, r, z);
   if (rc == LS_OK) rc = dot(ctx, r, z, S_RHO1);
   if (rc == LS_OK) {
-    update_p_kernel<<<gb, RED_THREADS, 0, ctx->stream>>>(p, z, uint64_t(ctx->Nl), ctx->scal, S_RHO1, S_RHO0);
-    copy_slot_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scal, S_RHO0, S_RHO1);
+    LS_CUDA(launch_pdl(update_p_kernel, gb, RED_THREADS, 0, ctx->stream, p, z, uint64_t(ctx->Nl), ctx->scal,
+                       int(S_RHO1), int(S_RHO0)));
+    LS_CUDA(launch_pdl(copy_slot_kernel, 1, 1, 0, ctx->stream, ctx->scal, int(S_RHO0), int(S_RHO1)));
     ctx->launches += 2;
     rc = ls_matvec(ctx, p, q);
   }
   if (rc == LS_OK) rc = dot(ctx, p, q, S_PQ);
   if (rc == LS_OK) {
-    update_xr_kernel<<<gb, RED_THREADS, 0, ctx->stream>>>(x, r, p, q, uint64_t(ctx->Nl), ctx->scal, S_RHO0,
-                                                         ctx->partials);
-    reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, S_RR);
-    pcg_check_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scal, tol, max_iter, h);
+    LS_CUDA(launch_pdl(update_xr_kernel, gb, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
+                       int(S_RHO0), ctx->partials));
+    LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS),
+                       ctx->scal, int(S_RR)));
+    LS_CUDA(launch_pdl(pcg_check_kernel, 1, 1, 0, ctx->stream, ctx->scal, tol, max_iter, h));
     ctx->launches += 3;
   }
   cudaGraph_t out = nullptr;
@@ -1480,9 +1486,10 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
   while (k < max_iter) {
     LS_CHECK(ls_matvec(ctx, p, q));
     LS_CHECK(dot(ctx, p, q, S_PQ));
-    update_xr_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(x, r, p, q, uint64_t(ctx->Nl), ctx->scal, cur,
-                                                         ctx->partials);
-    reduce_final_kernel<<<1, RED_THREADS, 0, ctx->stream>>>(ctx->partials, RED_BLOCKS, ctx->scal, S_RR);
+    LS_CUDA(launch_pdl(update_xr_kernel, g, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
+                       cur, ctx->partials));
+    LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS),
+                       ctx->scal, int(S_RR)));
     ctx->launches += 2;
     LS_CUDA(cudaGetLastError());
     if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + S_RR));
@@ -1517,7 +1524,8 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
     }
     LS_CHECK(fd_apply(ctx, r, z));
     LS_CHECK(dot(ctx, r, z, nxt));
-    update_p_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(p, z, uint64_t(ctx->Nl), ctx->scal, nxt, cur);
+    LS_CUDA(launch_pdl(update_p_kernel, g, RED_THREADS, 0, ctx->stream, p, z, uint64_t(ctx->Nl), ctx->scal, nxt,
+                       cur));
     ctx->launches++;
     LS_CUDA(cudaGetLastError());
     std::swap(cur, nxt);
@@ -1526,7 +1534,7 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
   s.rel_res = rel;
   // true residual ||b - A x|| / ||b||
   LS_CHECK(ls_matvec(ctx, x, q));
-  sub_kernel<<<g, RED_THREADS, 0, ctx->stream>>>(z, b, q, uint64_t(ctx->Nl));
+  LS_CUDA(launch_pdl(sub_kernel, g, RED_THREADS, 0, ctx->stream, z, b, q, uint64_t(ctx->Nl)));
   ctx->launches++;
   LS_CHECK(dot(ctx, z, z, S_RR));
   LS_CHECK(read_scal(ctx));
@@ -1728,6 +1736,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       if (Q % 4 != 0) return LS_ENOTSUP;  // the scattering epilogue is a FAST-path variant
       return ctx->comm->setup_fused(ctx->tmp[1], ctx->tmp[0]);
     }
+    case LS_TUNE_PDL:  // process-wide: programmatic dependent launch of the FD mode kernels
+      if (value != 0 && value != 1) return LS_EINVAL;
+      g_ls_pdl = value;
+      return LS_OK;
     case LS_TUNE_PCG_GRAPH:  // 1 = graph-resident PCG loop (default on one GPU), 0 = host loop
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->pcg_graph = value;

@@ -38,6 +38,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pdl.cuh"
+
 #include "plan.hpp"
 
 namespace ls {
@@ -57,6 +59,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
@@ -264,6 +267,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
 
   const uint32_t stride = gridDim.x;
   uint32_t tile = blockIdx.x;
+  pdl_wait();  // X is the previous kernel's output
 #pragma unroll 1
   for (int s = 0; s < C::NSTAGE - 1; ++s) {
     uint32_t tt = tile + s * stride;
@@ -482,6 +486,7 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
     lam_row[mt] = (C::SCALE && a < n) ? __ldg(args.lam_a + a) : 0.0;
   }
   __syncthreads();
+  pdl_wait();  // X is the previous kernel's output
 
   // CTA tile sequence: local k -> blockIdx.x + k*gridDim.x; set s takes k = s, s+2, ...
   const uint32_t stride = gridDim.x;

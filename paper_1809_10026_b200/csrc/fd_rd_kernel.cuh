@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
   auto row_ok = [&](int kk) { return 4 * kk + kq < n; };
   const double* wl = wsm + lane * 2;
 
+  pdl_wait();  // X is the previous kernel's output (fd_kernels.cuh)
   RDIn<C::NT> cur = rd_make_in<C>(args, tile, lane);
   double bw[C::D][C::NT];
 #pragma unroll

@@ -29,7 +29,8 @@ static cudaError_t rd_launch_cfg(const ModeArgs& a, cudaStream_t s, int num_sms)
   const uint32_t ntw = (a.ncols + C::TW - 1) / C::TW;
   if (ntw == 0) return cudaSuccess;
   const unsigned grid = std::min<unsigned>((ntw + C::WARPS - 1) / C::WARPS, unsigned(num_sms));
-  fd_mode_rd_kernel<C><<<grid, C::THREADS, C::SMEM, s>>>(a);
+  const cudaError_t e = launch_pdl(fd_mode_rd_kernel<C>, grid, C::THREADS, C::SMEM, s, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -35,6 +35,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pdl.cuh"
+
 namespace ls {
 
 constexpr int MV_MAXW = 17;  // 2P + 1 for P <= 8
@@ -95,6 +97,7 @@ constexpr int MV_CY = 8;
 
 template <int P, int R>
 __global__ void __launch_bounds__(32 * MV_CY) mv_time_kernel(const __grid_constant__ MVArgs a) {
+  pdl_wait();
   const uint32_t c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = (blockIdx.y * MV_CY + threadIdx.y) * R;  // local output row of acc[0]
   if (c >= a.ncols || r0 >= a.nout) return;
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(32 * MV_CY) mv_time_kernel(const __grid_consta
 // --------------------------------------------------------------------------------------
 template <int P, int R, bool AONLY>
 __global__ void __launch_bounds__(32 * MV_CY) mv_dir_kernel(const __grid_constant__ MVArgs a) {
+  pdl_wait();
   const uint32_t c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = (blockIdx.y * MV_CY + threadIdx.y) * R;
   const int n = a.n;
@@ -206,6 +210,7 @@ __host__ __device__ inline int mv_plane_pitch(int n1, int P) {
 
 template <int P, int R, bool PHASE1>
 __global__ void __launch_bounds__(MV_PLANE_THREADS, 2) mv_plane_kernel(const __grid_constant__ MVArgs a) {
+  pdl_wait();
   extern __shared__ __align__(16) double sm[];
   const int n1 = a.n1, n2 = a.n;
   const int pitch = mv_plane_pitch(n1, P);

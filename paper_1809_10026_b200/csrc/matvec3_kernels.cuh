@@ -111,6 +111,7 @@ struct MV3Occ {
 
 template <int P, int NT, int KIND, bool MODE1, bool FAST>
 __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const __grid_constant__ MV3Args a) {
+  pdl_wait();
   using Gm = MV3Geom<P, KIND>;
   using IO = MV3IO<KIND>;
   constexpr int NKB = Gm::NKB, OFF = Gm::OFF, RING = Gm::RING, G = Gm::G;

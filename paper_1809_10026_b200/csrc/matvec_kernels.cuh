@@ -64,6 +64,7 @@ struct BandCfg {
 // KIND 1 (directions >= 2) and KIND 2 (time).
 template <int P, int RB, int KIND, int NSTAGE, int NWARPS>
 __global__ void __launch_bounds__(32 * NWARPS, 1) band_tile_kernel(BandArgs a) {
+  pdl_wait();
   using C = BandCfg<P, RB, KIND, NSTAGE, NWARPS>;
   constexpr int W = C::W;
   constexpr int NIN = C::NIN;
@@ -243,6 +244,7 @@ struct FirstCfg {
 // Direction 1 (contiguous axis): x viewed as [ncols][n].
 template <int P, int NMAX, int NSTAGE>
 __global__ void __launch_bounds__(256, 2) band_first_kernel(BandArgs a) {
+  pdl_wait();
   using C = FirstCfg<P, NMAX, NSTAGE>;
   constexpr int W = 2 * P + 1;
   constexpr int BN = C::BN, LD = C::LD, TILE = C::TILE;

@@ -7,7 +7,9 @@ template <int P>
 static cudaError_t run_time(const MV2Plan& pl, int64_t* launches) {
   constexpr int R = 8;
   if (pl.grid_time) {
-    mv_time_kernel<P, R><<<dim3(pl.grid_time, (pl.time.nout + R * MV_CY - 1) / (R * MV_CY)), dim3(32, MV_CY), 0, pl.stream>>>(pl.time);
+    const cudaError_t e0 = launch_pdl(mv_time_kernel<P, R>, dim3(pl.grid_time, (pl.time.nout + R * MV_CY - 1) / (R * MV_CY)),
+                                      dim3(32, MV_CY), 0, pl.stream, pl.time);
+    if (e0 != cudaSuccess) return e0;
     ++*launches;
     return cudaGetLastError();
   }
@@ -20,8 +22,9 @@ static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
   cudaError_t e;
   if (pl.grid_dir) {
     const dim3 g(pl.grid_dir, (pl.dir.n + R * MV_CY - 1) / (R * MV_CY));
-    if (pl.d == 1) mv_dir_kernel<P, R, true><<<g, dim3(32, MV_CY), 0, pl.stream>>>(pl.dir);
-    else mv_dir_kernel<P, R, false><<<g, dim3(32, MV_CY), 0, pl.stream>>>(pl.dir);
+    e = (pl.d == 1) ? launch_pdl(mv_dir_kernel<P, R, true>, g, dim3(32, MV_CY), 0, pl.stream, pl.dir)
+                    : launch_pdl(mv_dir_kernel<P, R, false>, g, dim3(32, MV_CY), 0, pl.stream, pl.dir);
+    if (e != cudaSuccess) return e;
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -34,8 +37,9 @@ static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
       if (e != cudaSuccess) return e;
       attr[ph] = true;
     }
-    if (ph) mv_plane_kernel<P, R, true><<<pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream>>>(pl.plane);
-    else mv_plane_kernel<P, R, false><<<pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream>>>(pl.plane);
+    e = ph ? launch_pdl(mv_plane_kernel<P, R, true>, pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream, pl.plane)
+           : launch_pdl(mv_plane_kernel<P, R, false>, pl.grid_plane, MV_PLANE_THREADS, pl.smem_plane, pl.stream, pl.plane);
+    if (e != cudaSuccess) return e;
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }

@@ -28,7 +28,10 @@ static cudaError_t launch(const MV3Args& a, int num_sms, cudaStream_t s) {
   const uint32_t nstrips = (a.ncols + 8 * NT - 1) / (8 * NT);
   const unsigned grid = std::min<unsigned>((nstrips + 7) / 8, unsigned(num_sms * MV3Occ<KIND>::CTAS));
   if (grid == 0 || a.mt1 <= a.mt0) return cudaSuccess;
-  mv3_band_kernel<P, NT, KIND, MODE1, FAST><<<grid, 256, smem, s>>>(a);
+  {
+    const cudaError_t e = launch_pdl(mv3_band_kernel<P, NT, KIND, MODE1, FAST>, grid, 256, smem, s, a);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pdl.cuh"
+
 namespace ls {
 
 constexpr int RED_THREADS = 256;
@@ -35,6 +37,7 @@ __device__ __forceinline__ double block_sum(double v) {
 __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* __restrict__ a,
                                                                   const double* __restrict__ b,
                                                                   uint64_t n, double* partials) {
+  pdl_wait();
   double s = 0;
   for (uint64_t i = blockIdx.x * uint64_t(RED_THREADS) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * RED_THREADS)
@@ -46,6 +49,7 @@ __global__ void __launch_bounds__(RED_THREADS) dot_partial_kernel(const double* 
 // scal[slot] = sum partials (single block, fixed order)
 __global__ void __launch_bounds__(RED_THREADS) reduce_final_kernel(const double* partials, int np,
                                                                    double* scal, int slot) {
+  pdl_wait();
   double s = 0;
   for (int i = threadIdx.x; i < np; i += RED_THREADS) s += partials[i];
   s = block_sum(s);
@@ -58,6 +62,7 @@ __global__ void __launch_bounds__(RED_THREADS) update_xr_kernel(double* __restri
                                                                 const double* __restrict__ q, uint64_t n,
                                                                 double* scal, int rho_slot,
                                                                 double* partials) {
+  pdl_wait();
   const double alpha = scal[rho_slot] / scal[S_PQ];
   if (blockIdx.x == 0 && threadIdx.x == 0) scal[S_ALPHA] = alpha;
   double s = 0;
@@ -76,6 +81,7 @@ __global__ void __launch_bounds__(RED_THREADS) update_xr_kernel(double* __restri
 __global__ void __launch_bounds__(RED_THREADS) update_p_kernel(double* __restrict__ p, const double* __restrict__ z,
                                                                uint64_t n, double* scal, int new_slot,
                                                                int old_slot) {
+  pdl_wait();
   const double beta = scal[new_slot] / scal[old_slot];
   if (blockIdx.x == 0 && threadIdx.x == 0) scal[S_BETA] = beta;
   for (uint64_t i = blockIdx.x * uint64_t(RED_THREADS) + threadIdx.x; i < n;
@@ -85,12 +91,14 @@ __global__ void __launch_bounds__(RED_THREADS) update_p_kernel(double* __restric
 
 // graph-resident PCG (pcg_solve, one GPU): scal[S_RHO0] = scal[S_RHO1] after update_p, so
 // the captured loop body uses fixed slots
-__global__ void copy_slot_kernel(double* scal, int dst, int src) { scal[dst] = scal[src]; }
+__global__ void copy_slot_kernel(double* scal, int dst, int src) {
+  pdl_wait(); scal[dst] = scal[src]; }
 
 // end of a graph-resident iteration: k += 1 and the stopping test of the host loop
 // (reading c7: ||r_k|| / ||b|| <= tol; NaN/Inf -> LS_ENUMERIC; k = max_iter -> LS_ENOCONV),
 // written to scal[S_K], scal[S_STAT]; the WHILE node continues while the test fails
 __global__ void pcg_check_kernel(double* scal, double tol, int max_iter, cudaGraphConditionalHandle h) {
+  pdl_wait();
   const double k = scal[S_K] + 1.0;
   scal[S_K] = k;
   const double rr = scal[S_RR], alpha = scal[S_ALPHA];
@@ -113,6 +121,7 @@ __global__ void pcg_check_kernel(double* scal, double tol, int max_iter, cudaGra
 // y = a - b
 __global__ void __launch_bounds__(RED_THREADS) sub_kernel(double* __restrict__ y, const double* __restrict__ a,
                                                           const double* __restrict__ b, uint64_t n) {
+  pdl_wait();
   for (uint64_t i = blockIdx.x * uint64_t(RED_THREADS) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * RED_THREADS)
     y[i] = a[i] - b[i];
