@@ -187,8 +187,9 @@ int ls_rhs(ls_ctx* ctx, int kind, double* b);
  * or after max_iter A-products.  x is overwritten (x must not alias b: LS_EINVAL).
  * b == 0 returns x = 0 with
  * 0 iterations.  Synchronous.  Returns LS_OK, LS_ENOCONV or LS_ENUMERIC (st
- * filled in all three cases; st may be NULL).  On one GPU, iterations 2.. run as one
- * CUDA-graph launch (LS_TUNE_PCG_GRAPH; the graph is cached per (x, tol, max_iter)).
+ * filled in all three cases; st may be NULL).  On one GPU the solve after the b.b test is
+ * one CUDA-graph launch (LS_TUNE_PCG_GRAPH; cached per (b, x, tol, max_iter), dropped by
+ * ls_tune).
  */
 int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
               ls_pcg_stats* st);
@@ -355,9 +356,9 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * over NVLink), each followed by a cross-GPU flag barrier.  Enabling is collective (every
  * rank calls it).  Not yet validated on a multi-GPU box. */
 #define LS_TUNE_A2A 4
-/* LS_TUNE_PCG_GRAPH: 1 = pcg_solve runs iterations 2.. as one CUDA-graph launch (a WHILE
- * conditional node around the captured iteration; no per-iteration host round trip;
- * default on one GPU), 0 = host-driven loop.  Same kernels in the same order either way. */
+/* LS_TUNE_PCG_GRAPH: 1 = pcg_solve runs as one CUDA-graph launch (first iteration, a WHILE
+ * conditional node around the captured iteration, true residual; no per-iteration host
+ * round trip; default on one GPU), 0 = host-driven loop.  Same kernels in the same order. */
 #define LS_TUNE_PCG_GRAPH 5
 /* LS_TUNE_PDL (process-wide): 1 = the FD mode kernels use programmatic dependent launch
  * (their shared-memory staging of U / lambda overlaps the previous kernel's tail; default),

@@ -113,8 +113,11 @@ struct ls_ctx {
   // graph-resident PCG loop (one GPU): the iteration body captured once under a WHILE node
   int pcg_graph = 1;                 // ls_tune LS_TUNE_PCG_GRAPH
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cap_stream2 = nullptr;
   cudaGraphExec_t pcg_exec = nullptr;
+  const double* pcg_key_b = nullptr;
   const double* pcg_key_x = nullptr;
+  int64_t pcg_fixed_launches = 0;
   double pcg_key_tol = -1.0;
   int pcg_key_iter = -1;
   int64_t pcg_body_launches = 0;
@@ -140,6 +143,7 @@ struct ls_ctx {
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (cap_stream2) cudaStreamDestroy(cap_stream2);
   }
   int alloc(double** ptr, size_t count) {
     void* v = nullptr;
@@ -1387,69 +1391,114 @@ static int read_scal(ls_ctx* ctx) {
   return LS_OK;
 }
 
-// One PCG iteration after the first, in the order of the host loop below (reading c7):
-// z = P r; rho1 = r.z; p = z + (rho1/rho0) p; rho0 = rho1; q = A p; pq; x += a p, r -= a q; rr;
-// k += 1 and the stopping test.  Captured into the body of a WHILE conditional node so the
-// whole solve after the first iteration is ONE graph launch: no per-iteration host
-// round trip (config 2 is launch / latency bound).
-static int pcg_build_graph(ls_ctx* ctx, double* x, double tol, int max_iter) {
+// The whole single-GPU solve after the b.b test as ONE graph launch (reading c7 order):
+//   r = b; z = P r; rho0 = r.z; p = z; q = A p; pq; x += a p, r -= a q; rr; k = 1, test
+//   WHILE (test fails): z = P r; rho1 = r.z; p = z + (rho1/rho0) p; rho0 = rho1; q = A p; pq;
+//                       x += a p, r -= a q; rr; k += 1, test
+//   true residual: z = b - A x; z.z
+// The stopping test runs on the device (pcg_check_kernel sets the WHILE condition), so no
+// per-iteration host round trip (config 2 is launch / latency bound).  The
+// captured kernels and their order are those of the host loop: iterates are bit-identical.
+static int pcg_build_graph(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter) {
   if (ctx->pcg_exec) {
     cudaGraphExecDestroy(ctx->pcg_exec);
     ctx->pcg_exec = nullptr;
   }
   if (!ctx->cap_stream) LS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+  if (!ctx->cap_stream2) LS_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream2, cudaStreamNonBlocking));
   cudaGraph_t g = nullptr;
   LS_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle h;
-  LS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t wn;
-  LS_CUDA(cudaGraphAddNode(&wn, g, nullptr, 0, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  LS_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault));
   cudaStream_t user = ctx->stream;
-  ctx->stream = ctx->cap_stream;
   const int64_t l0 = ctx->launches;
-  int rc = LS_OK;
-  if (cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) !=
-      cudaSuccess)
-    rc = LS_ECUDA;
+  const size_t bytes = size_t(ctx->Nl) * sizeof(double);
   double *r = ctx->pr, *z = ctx->pz, *p = ctx->pp, *q = ctx->pq;
   const unsigned gb = RED_BLOCKS;
-  if (rc == LS_OK) rc = fd_apply(ctx, r, z);
-  if (rc == LS_OK) rc = dot(ctx, r, z, S_RHO1);
-  if (rc == LS_OK) {
-    LS_CUDA(launch_pdl(update_p_kernel, gb, RED_THREADS, 0, ctx->stream, p, z, uint64_t(ctx->Nl), ctx->scal,
-                       int(S_RHO1), int(S_RHO0)));
-    LS_CUDA(launch_pdl(copy_slot_kernel, 1, 1, 0, ctx->stream, ctx->scal, int(S_RHO0), int(S_RHO1)));
-    ctx->launches += 2;
-    rc = ls_matvec(ctx, p, q);
-  }
-  if (rc == LS_OK) rc = dot(ctx, p, q, S_PQ);
-  if (rc == LS_OK) {
-    LS_CUDA(launch_pdl(update_xr_kernel, gb, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
-                       int(S_RHO0), ctx->partials));
-    LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS),
-                       ctx->scal, int(S_RR)));
-    LS_CUDA(launch_pdl(pcg_check_kernel, 1, 1, 0, ctx->stream, ctx->scal, tol, max_iter, h));
+  int rc = LS_OK;
+  auto ck = [&](cudaError_t e) {
+    if (rc == LS_OK && e != cudaSuccess) rc = LS_ECUDA;
+  };
+  // the iteration tail shared by the first iteration and the loop body
+  auto tail = [&]() {
+    if (rc == LS_OK) rc = ls_matvec(ctx, p, q);
+    if (rc == LS_OK) rc = dot(ctx, p, q, S_PQ);
+    if (rc != LS_OK) return;
+    ck(launch_pdl(update_xr_kernel, gb, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
+                  int(S_RHO0), ctx->partials));
+    ck(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS), ctx->scal,
+                  int(S_RR)));
+    ck(launch_pdl(pcg_check_kernel, 1, 1, 0, ctx->stream, ctx->scal, tol, max_iter, h));
     ctx->launches += 3;
+  };
+  ctx->stream = ctx->cap_stream;
+  ck(cudaStreamBeginCaptureToGraph(ctx->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  const bool capturing = rc == LS_OK;
+  // first iteration
+  ck(cudaMemcpyAsync(r, b, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (rc == LS_OK) rc = fd_apply(ctx, r, z);
+  if (rc == LS_OK) rc = dot(ctx, r, z, S_RHO0);
+  ck(cudaMemcpyAsync(p, z, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  ck(cudaMemsetAsync(ctx->scal + S_K, 0, sizeof(double), ctx->stream));  // k = 0 (all-zero bits)
+  tail();
+  // WHILE node after the first test, its body captured on the second stream
+  cudaGraphNode_t wn = nullptr;
+  if (rc == LS_OK) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    ck(cudaStreamGetCaptureInfo(ctx->stream, &cs, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (rc == LS_OK) ck(cudaGraphAddNode(&wn, cg, deps, nd, &cp));
+    if (rc == LS_OK) ck(cudaStreamUpdateCaptureDependencies(ctx->stream, &wn, 1, cudaStreamSetCaptureDependencies));
+    if (rc == LS_OK) {
+      const int64_t lb = ctx->launches;
+      cudaStream_t outer = ctx->stream;
+      ctx->stream = ctx->cap_stream2;
+      ck(cudaStreamBeginCaptureToGraph(ctx->stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeRelaxed));
+      if (rc == LS_OK) rc = fd_apply(ctx, r, z);
+      if (rc == LS_OK) rc = dot(ctx, r, z, S_RHO1);
+      if (rc == LS_OK) {
+        ck(launch_pdl(update_p_kernel, gb, RED_THREADS, 0, ctx->stream, p, z, uint64_t(ctx->Nl), ctx->scal,
+                      int(S_RHO1), int(S_RHO0)));
+        ck(launch_pdl(copy_slot_kernel, 1, 1, 0, ctx->stream, ctx->scal, int(S_RHO0), int(S_RHO1)));
+        ctx->launches += 2;
+      }
+      tail();
+      cudaGraph_t bo = nullptr;
+      ck(cudaStreamEndCapture(ctx->stream, &bo));
+      ctx->stream = outer;
+      ctx->pcg_body_launches = ctx->launches - lb;
+    }
   }
-  cudaGraph_t out = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &out);
+  // true residual ||b - A x|| -> scal[S_AUX]
+  if (rc == LS_OK) rc = ls_matvec(ctx, x, q);
+  if (rc == LS_OK) {
+    ck(launch_pdl(sub_kernel, gb, RED_THREADS, 0, ctx->stream, z, b, q, uint64_t(ctx->Nl)));
+    ctx->launches++;
+  }
+  if (rc == LS_OK) rc = dot(ctx, z, z, S_AUX);
+  if (capturing) {
+    cudaGraph_t out = nullptr;
+    ck(cudaStreamEndCapture(ctx->cap_stream, &out));
+  }
   ctx->stream = user;
-  ctx->pcg_body_launches = ctx->launches - l0;
+  ctx->pcg_fixed_launches = ctx->launches - l0 - ctx->pcg_body_launches;
   ctx->launches = l0;
-  if (rc == LS_OK && ec != cudaSuccess) rc = LS_ECUDA;
   if (rc == LS_OK && cudaGraphInstantiate(&ctx->pcg_exec, g, 0) != cudaSuccess) {
     ctx->pcg_exec = nullptr;
     rc = LS_ECUDA;
   }
   cudaGraphDestroy(g);
-  cudaGetLastError();  // a failed capture leaves a sticky-free error: the host loop takes over
+  cudaGetLastError();  // a failed capture is not sticky: the host loop takes over
   if (rc != LS_OK) return rc;
+  ctx->pcg_key_b = b;
   ctx->pcg_key_x = x;
   ctx->pcg_key_tol = tol;
   ctx->pcg_key_iter = max_iter;
@@ -1469,6 +1518,22 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
   if (bnorm == 0.0) {
     if (st) *st = s;
     return LS_OK;
+  }
+  if (max_iter >= 1 && ctx->world == 1 && ctx->pcg_graph && !ctx->prof) {
+    bool ok = ctx->pcg_exec && ctx->pcg_key_b == b && ctx->pcg_key_x == x && ctx->pcg_key_tol == tol &&
+              ctx->pcg_key_iter == max_iter;
+    if (!ok) ok = pcg_build_graph(ctx, b, x, tol, max_iter) == LS_OK;
+    if (ok) {
+      LS_CUDA(cudaGraphLaunch(ctx->pcg_exec, ctx->stream));
+      LS_CHECK(read_scal(ctx));
+      s.iters = int(ctx->h_scal[S_K]);
+      ctx->launches += ctx->pcg_fixed_launches + ctx->pcg_body_launches * (s.iters - 1);
+      s.rel_res = std::sqrt(ctx->h_scal[S_RR]) / bnorm;
+      s.true_rel_res = std::sqrt(ctx->h_scal[S_AUX]) / bnorm;
+      s.status = int(ctx->h_scal[S_STAT]);
+      if (st) *st = s;
+      return s.status;
+    }
   }
   int64_t lo = 0, hi = 0;
   if (ctx->world > 1) ext_geom(ctx, &lo, &hi);
@@ -1504,23 +1569,6 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
     if (rel <= tol) {
       s.status = LS_OK;
       break;
-    }
-    if (k == 1 && k < max_iter && ctx->world == 1 && ctx->pcg_graph && !ctx->prof) {
-      // iterations 2.. as one graph launch (cur == S_RHO0 here)
-      bool ok = ctx->pcg_exec && ctx->pcg_key_x == x && ctx->pcg_key_tol == tol && ctx->pcg_key_iter == max_iter;
-      if (!ok) ok = pcg_build_graph(ctx, x, tol, max_iter) == LS_OK;
-      if (ok) {
-        ctx->h_scal[S_K] = 1.0;
-        LS_CUDA(cudaMemcpyAsync(ctx->scal + S_K, ctx->h_scal + S_K, sizeof(double), cudaMemcpyHostToDevice,
-                                ctx->stream));
-        LS_CUDA(cudaGraphLaunch(ctx->pcg_exec, ctx->stream));
-        LS_CHECK(read_scal(ctx));
-        k = int(ctx->h_scal[S_K]);
-        ctx->launches += ctx->pcg_body_launches * (k - 1);
-        rel = std::sqrt(ctx->h_scal[S_RR]) / bnorm;
-        s.status = int(ctx->h_scal[S_STAT]);
-        break;
-      }
     }
     LS_CHECK(fd_apply(ctx, r, z));
     LS_CHECK(dot(ctx, r, z, nxt));
@@ -1715,6 +1763,10 @@ extern "C" int64_t ls_kernel_launches(const ls_ctx* ctx) { return ctx ? ctx->lau
 
 extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
   if (!ctx) return LS_EINVAL;
+  if (ctx->pcg_exec) {  // the cached PCG graph holds the kernels chosen so far
+    cudaGraphExecDestroy(ctx->pcg_exec);
+    ctx->pcg_exec = nullptr;
+  }
   switch (knob) {
     case LS_TUNE_FD_KERNEL:
       if (value < 0 || value > 2) return LS_EINVAL;
