@@ -177,7 +177,10 @@ int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_
  * built-in separable forcing (reading c11):
  *   kind 0: f = e^t prod_k sin(pi x_k)                        (BASELINE config 2)
  *   kind 1: f = prod_k sin(pi x_k) (cos t + d pi^2 sin t)     (cube, PAPER.md 1166)
- * b: device vector (this rank's slab).  Errors: LS_EINVAL for an unknown kind.
+ *   kind 2: mapped 2D domains only (ls_setup_geo, d = 2): f = (d_t - Lap) u for
+ *           u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t) (quarter annulus, PAPER.md 1129)
+ * b: device vector (this rank's slab).  Errors: LS_EINVAL for an unknown kind,
+ * LS_ENOTSUP for a kind the context does not support.
  */
 int ls_rhs(ls_ctx* ctx, int kind, double* b);
 
@@ -242,8 +245,10 @@ typedef struct {
  *     logarithms (reading c21), factors interpolated piecewise linearly (reading c22),
  *     weighted univariate matrices, Algorithm 1 for Pbar^G, D_ii = A_ii / Pbar^G_ii.
  *   pcg_solve works unchanged; ls_matvec_slab applies slab rows (as for the cube);
- *     ls_rhs, ls_energy_error, fd_apply_stage and fd_apply_scatter return LS_ENOTSUP
- *     (the caller supplies b).
+ *     ls_rhs / ls_energy_error support kind 2 only: the 2D quarter-annulus benchmark
+ *     u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t) of PAPER.md 1128-1129 (d = 2; f = d_t u - Lap u,
+ *     spatial integrals with p_s + 5 Gauss points per element on Omega, reading c16), other
+ *     kinds LS_ENOTSUP (the caller supplies b); fd_apply_stage / fd_apply_scatter LS_ENOTSUP.
  * Limits: (p_s + 1)^d <= 343 local functions per element (d = 3: p_s <= 6).
  * Errors: as ls_setup; LS_EINVAL also for an invalid map description, or a Jacobian
  * determinant that vanishes, is not finite or changes sign at a quadrature point

@@ -123,8 +123,9 @@ def physical_laplacian(v_grad, v_hess, Jac, Hes):
     return np.einsum("qjk,qjk->q", A, v_hess) + np.einsum("qj,qj->q", b, v_grad)
 
 
-def space_tables(geo, n_el, p, drop_boundary=True):
-    """Physical evaluation matrices of the spatial basis at the tensor Gauss points.
+def space_tables(geo, n_el, p, drop_boundary=True, q=None):
+    """Physical evaluation matrices of the spatial basis at the tensor Gauss points
+    (q per element and direction, default p + 1).
 
     ``n_el``: elements per direction (list of d).  Returns dict with W (quadrature
     weight x |det Jac|, [nq]), Phi (nq x N_s), Grad (list of d: d/dx_i, nq x N_s),
@@ -132,7 +133,7 @@ def space_tables(geo, n_el, p, drop_boundary=True):
     (eq:basis_par: i_k = 2..m_k-1) unless drop_boundary is False (all m_k functions)."""
     d = geo["d"]
     knots = [open_uniform_knots(n_el[k], p) for k in range(d)]
-    rules = [gauss_legendre_rule(kn, p + 1) for kn in knots]
+    rules = [gauss_legendre_rule(kn, p + 1 if q is None else q) for kn in knots]
     sl = slice(1, -1) if drop_boundary else slice(None)
     tabs = [[_ders(knots[k], p, r, rules[k][0])[:, sl] for r in range(3)] for k in range(d)]
     g = eval_map(geo, [r[0] for r in rules])

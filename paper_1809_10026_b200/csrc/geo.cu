@@ -76,7 +76,7 @@ struct GeoQArgs {
   const double* wq[3];       // [nq_k] Gauss weights (element length included)
   const double* ctrl;        // [prod m][d]
   const double* w;           // [prod m]
-  double* out;               // [13][NQ]: wdet, Jinv[3][3] (row j = grad eta_j), b[3]
+  double* out;               // [16][NQ]: wdet, Jinv[3][3] (row j = grad eta_j), b[3], x[3]
   int64_t NQ;
   int* flags;                // bit 0: det J <= 0 seen, bit 1: det J >= 0 seen, bit 2: det J = 0 / non-finite
 };
@@ -194,6 +194,7 @@ __global__ void geo_qpoint_kernel(GeoQArgs a) {
     for (int j = 0; j < 3; ++j)
       for (int i = 0; i < 3; ++i) a.out[(1 + j * 3 + i) * a.NQ + qi] = inv[j][i];
     for (int j = 0; j < 3; ++j) a.out[(10 + j) * a.NQ + qi] = b[j];
+    for (int j = 0; j < 3; ++j) a.out[(13 + j) * a.NQ + qi] = j < d ? F[j] : 0.0;
   }
 }
 
@@ -351,30 +352,117 @@ __global__ void __launch_bounds__(ASM_THREADS) geo_assemble_kernel(GeoAsmArgs a)
 }
 
 // host tables of one direction: Gauss points / weights, discretisation basis per element
-static void dir_tables(int n_el, int p, std::vector<double>& xq, std::vector<double>& wq, std::vector<double>& bt) {
+// host tables of one direction for qpe Gauss points per element: points / weights and the
+// p+1 local basis functions' values, 1st and 2nd derivatives [n_el][qpe][p+1][3]
+static void dir_tables(int n_el, int p, int qpe, std::vector<double>& xq, std::vector<double>& wq,
+                       std::vector<double>& bt) {
   auto kn = open_uniform_knots(n_el, p);
-  const int m = n_el + p, P1 = p + 1;
+  const int m = n_el + p, P1 = p + 1, QP = qpe;
   std::vector<long double> gx, gw;
-  gauss_legendre(P1, gx, gw);
+  gauss_legendre(QP, gx, gw);
   std::vector<long double> v0(m), v1(m), v2(m);
-  xq.assign(size_t(n_el) * P1, 0);
-  wq.assign(size_t(n_el) * P1, 0);
-  bt.assign(size_t(n_el) * P1 * P1 * 3, 0);
+  xq.assign(size_t(n_el) * QP, 0);
+  wq.assign(size_t(n_el) * QP, 0);
+  bt.assign(size_t(n_el) * QP * P1 * 3, 0);
   for (int e = 0; e < n_el; ++e) {
     const long double a = kn[p + e], b = kn[p + e + 1];
-    for (int g = 0; g < P1; ++g) {
+    for (int g = 0; g < QP; ++g) {
       const long double x = 0.5L * (a + b) + 0.5L * (b - a) * gx[g];
-      xq[size_t(e) * P1 + g] = double(x);
-      wq[size_t(e) * P1 + g] = double(0.5L * (b - a) * gw[g]);
+      xq[size_t(e) * QP + g] = double(x);
+      wq[size_t(e) * QP + g] = double(0.5L * (b - a) * gw[g]);
       bspline_eval(kn, p, x, v0.data(), v1.data(), v2.data());
       for (int f = 0; f < P1; ++f) {
-        double* t = &bt[((size_t(e) * P1 + g) * P1 + f) * 3];
+        double* t = &bt[((size_t(e) * QP + g) * P1 + f) * 3];
         t[0] = double(v0[e + f]);
         t[1] = double(v1[e + f]);
         t[2] = double(v2[e + f]);
       }
     }
   }
+}
+
+// Point data of the mapped domain at qpe Gauss points per element and direction: the
+// discretisation tables (bt) and, from geo_qpoint_kernel, |det J| w, J^{-1}, the Laplacian's
+// first-order coefficients and x (qd, [16][NQ]).  LS_EINVAL for a singular / folded map.
+struct GeoPts {
+  double* qd = nullptr;
+  const double* bt[3] = {nullptr, nullptr, nullptr};
+  int nq[3] = {1, 1, 1};
+  int64_t NQ = 1;
+  int qpe = 0;
+};
+
+static int geo_points(const GeoMap& g, int d, int p, const int64_t* n_el, int qpe, std::vector<void*>& allocs,
+                      cudaStream_t s, GeoPts& out, int64_t* launches) {
+  GeoQArgs qa{};
+  qa.d = d;
+  out.qpe = qpe;
+  out.NQ = 1;
+  for (int k = 0; k < d; ++k) {
+    out.nq[k] = int(n_el[k]) * qpe;
+    out.NQ *= out.nq[k];
+  }
+  qa.NQ = out.NQ;
+  for (int k = 0; k < d; ++k) {
+    std::vector<double> xq, wq, bt;
+    dir_tables(int(n_el[k]), p, qpe, xq, wq, bt);
+    // geometry basis at the points: span (first non-zero function) and q+1 values
+    const int q = g.q[k], mg = g.m[k];
+    std::vector<double> gt(xq.size() * (q + 1) * 3);
+    std::vector<int> span(xq.size());
+    std::vector<long double> v0(mg), v1(mg), v2(mg);
+    const auto& kn = g.knots[k];
+    for (size_t i = 0; i < xq.size(); ++i) {
+      const double x = xq[i];
+      int sp = q;  // knot span: kn[sp] <= x < kn[sp+1], sp in [q, mg-1]
+      while (sp < mg - 1 && kn[sp + 1] <= x) ++sp;
+      span[i] = sp - q;
+      bspline_eval(kn, q, x, v0.data(), v1.data(), v2.data());
+      for (int c = 0; c <= q; ++c) {
+        gt[(i * (q + 1) + c) * 3 + 0] = double(v0[sp - q + c]);
+        gt[(i * (q + 1) + c) * 3 + 1] = double(v1[sp - q + c]);
+        gt[(i * (q + 1) + c) * 3 + 2] = double(v2[sp - q + c]);
+      }
+    }
+    double *dgt, *dwq, *dbt;
+    int rc = dupload(allocs, gt, &dgt);
+    if (rc == LS_OK) rc = dupload(allocs, wq, &dwq);
+    if (rc == LS_OK) rc = dupload(allocs, bt, &dbt);
+    if (rc != LS_OK) return rc;
+    int* dspan = nullptr;
+    GEO_CUDA(cudaMalloc(&dspan, span.size() * sizeof(int)));
+    allocs.push_back(dspan);
+    GEO_CUDA(cudaMemcpy(dspan, span.data(), span.size() * sizeof(int), cudaMemcpyHostToDevice));
+    qa.nq[k] = out.nq[k];
+    qa.q[k] = q;
+    qa.m[k] = mg;
+    qa.span[k] = dspan;
+    qa.gt[k] = dgt;
+    qa.wq[k] = dwq;
+    out.bt[k] = dbt;
+  }
+  double *dctrl, *dw;
+  int rc = dupload(allocs, g.ctrl, &dctrl);
+  if (rc == LS_OK) rc = dupload(allocs, g.w, &dw);
+  if (rc == LS_OK) rc = dalloc(allocs, &out.qd, size_t(16) * out.NQ);
+  if (rc != LS_OK) return rc;
+  qa.ctrl = dctrl;
+  qa.w = dw;
+  qa.out = out.qd;
+  GEO_CUDA(cudaMemsetAsync(out.qd, 0, size_t(16) * out.NQ * sizeof(double), s));
+  int* dflags = nullptr;
+  GEO_CUDA(cudaMalloc(&dflags, sizeof(int)));
+  allocs.push_back(dflags);
+  GEO_CUDA(cudaMemsetAsync(dflags, 0, sizeof(int), s));
+  qa.flags = dflags;
+  geo_qpoint_kernel<<<unsigned(std::min<int64_t>((out.NQ + 255) / 256, 148 * 16)), 256, 0, s>>>(qa);
+  GEO_CUDA(cudaGetLastError());
+  if (launches) *launches += 1;
+  int hflags = 0;
+  GEO_CUDA(cudaMemcpyAsync(&hflags, dflags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GEO_CUDA(cudaStreamSynchronize(s));
+  if ((hflags & 4) || (hflags & 3) == 3) return LS_EINVAL;  // singular or folded map
+  return LS_OK;
 }
 
 int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el, cudaStream_t s,
@@ -397,72 +485,13 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
     NQ *= nq[k];
     NE *= n_el[k];
   }
-  // host tables
-  GeoQArgs qa{};
   GeoAsmArgs aa{};
-  qa.d = d;
-  qa.NQ = NQ;
-  std::vector<int*> ispans;
-  for (int k = 0; k < d; ++k) {
-    std::vector<double> xq, wq, bt;
-    dir_tables(int(n_el[k]), p, xq, wq, bt);
-    // geometry basis at the points: span (first non-zero function) and q+1 values
-    const int q = g.q[k], mg = g.m[k];
-    std::vector<double> gt(xq.size() * (q + 1) * 3);
-    std::vector<int> span(xq.size());
-    std::vector<long double> v0(mg), v1(mg), v2(mg);
-    const auto& kn = g.knots[k];
-    for (size_t i = 0; i < xq.size(); ++i) {
-      const double x = xq[i];
-      int sp = q;  // knot span: kn[sp] <= x < kn[sp+1], sp in [q, mg-1]
-      while (sp < mg - 1 && kn[sp + 1] <= x) ++sp;
-      span[i] = sp - q;
-      bspline_eval(kn, q, x, v0.data(), v1.data(), v2.data());
-      for (int c = 0; c <= q; ++c) {
-        gt[(i * (q + 1) + c) * 3 + 0] = double(v0[sp - q + c]);
-        gt[(i * (q + 1) + c) * 3 + 1] = double(v1[sp - q + c]);
-        gt[(i * (q + 1) + c) * 3 + 2] = double(v2[sp - q + c]);
-      }
-    }
-    double *dgt, *dwq, *dbt;
-    int rc = dupload(gd.allocs, gt, &dgt);
-    if (rc == LS_OK) rc = dupload(gd.allocs, wq, &dwq);
-    if (rc == LS_OK) rc = dupload(gd.allocs, bt, &dbt);
-    if (rc != LS_OK) return rc;
-    int* dspan = nullptr;
-    GEO_CUDA(cudaMalloc(&dspan, span.size() * sizeof(int)));
-    gd.allocs.push_back(dspan);
-    GEO_CUDA(cudaMemcpy(dspan, span.data(), span.size() * sizeof(int), cudaMemcpyHostToDevice));
-    qa.nq[k] = nq[k];
-    qa.q[k] = q;
-    qa.m[k] = mg;
-    qa.span[k] = dspan;
-    qa.gt[k] = dgt;
-    qa.wq[k] = dwq;
-    aa.bt[k] = dbt;
-  }
-  double *dctrl, *dw, *qd;
-  int rc = dupload(gd.allocs, g.ctrl, &dctrl);
-  if (rc == LS_OK) rc = dupload(gd.allocs, g.w, &dw);
-  if (rc == LS_OK) rc = dalloc(gd.allocs, &qd, size_t(13) * NQ);
-  if (rc == LS_OK) rc = dalloc(gd.allocs, &gd.st, size_t(3) * gd.S * gd.Ns);
-  if (rc != LS_OK) return rc;
-  qa.ctrl = dctrl;
-  qa.w = dw;
-  qa.out = qd;
-  GEO_CUDA(cudaMemsetAsync(qd, 0, size_t(13) * NQ * sizeof(double), s));
+  GeoPts pts;
+  LS_CHECK_RC(geo_points(g, d, p, n_el, p + 1, gd.allocs, s, pts, launches));
+  for (int k = 0; k < d; ++k) aa.bt[k] = pts.bt[k];
+  double* qd = pts.qd;
+  LS_CHECK_RC(dalloc(gd.allocs, &gd.st, size_t(3) * gd.S * gd.Ns));
   GEO_CUDA(cudaMemsetAsync(gd.st, 0, size_t(3) * gd.S * gd.Ns * sizeof(double), s));
-  int* dflags = nullptr;
-  GEO_CUDA(cudaMalloc(&dflags, sizeof(int)));
-  gd.allocs.push_back(dflags);
-  GEO_CUDA(cudaMemsetAsync(dflags, 0, sizeof(int), s));
-  qa.flags = dflags;
-  geo_qpoint_kernel<<<unsigned(std::min<int64_t>((NQ + 255) / 256, 148 * 16)), 256, 0, s>>>(qa);
-  GEO_CUDA(cudaGetLastError());
-  int hflags = 0;
-  GEO_CUDA(cudaMemcpyAsync(&hflags, dflags, sizeof(int), cudaMemcpyDeviceToHost, s));
-  GEO_CUDA(cudaStreamSynchronize(s));
-  if ((hflags & 4) || (hflags & 3) == 3) return LS_EINVAL;  // singular or folded map
   // assembly
   aa.d = d;
   aa.p = p;
@@ -504,13 +533,170 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
     ++nlaunch;
   }
   GEO_CUDA(cudaStreamSynchronize(s));
-  if (launches) *launches += 1 + nlaunch;
+  if (launches) *launches += nlaunch;
   int centre = 0, cs = 1;
   for (int k = 0; k < d; ++k) {
     centre += cs * p;
     cs *= 2 * p + 1;
   }
   for (int mat = 0; mat < 3; ++mat) gd.diag[mat] = gd.st + (size_t(mat) * gd.S + centre) * gd.Ns;
+  return LS_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// load vector of the 2D quarter-annulus benchmark (PAPER.md 1128-1129; ls_rhs kind 2)
+// ------------------------------------------------------------------------------------------
+// u = P(x, y) sin(pi t), P = -(x^2 + y^2 - 1)(x^2 + y^2 - 4) x y^2, so
+// f = d_t u - Lap u = pi cos(pi t) P - sin(pi t) Lap P,
+// Lap P = -2x (x^4 + 22 x^2 y^2 - 5 x^2 + 21 y^4 - 45 y^2 + 4).
+__device__ __forceinline__ double annulus_P(double x, double y) {
+  const double r2 = x * x + y * y;
+  return -(r2 - 1.0) * (r2 - 4.0) * x * y * y;
+}
+__device__ __forceinline__ double annulus_lapP(double x, double y) {
+  const double x2 = x * x, y2 = y * y;
+  return -2.0 * x * (x2 * x2 + 22.0 * x2 * y2 - 5.0 * x2 + 21.0 * y2 * y2 - 45.0 * y2 + 4.0);
+}
+
+struct GeoLoadArgs {
+  int p, qpe;
+  int nel[2], m[2], n[2], nq[2];
+  int color[2];
+  const double* bt[2];   // [n_el][qpe][p+1][3]
+  const double* qd;      // [16][NQ]
+  int64_t NQ, Ns;
+  double* lv;            // [4][Ns]: int P phi, int (-Lap P) phi, int P Lap phi, int (-Lap P) Lap phi
+};
+
+// one CTA per element of a colour class (e_k mod (p+1) fixed: no two CTAs share a row),
+// one thread per local function
+__global__ void geo_load_kernel(GeoLoadArgs a) {
+  const int P1 = a.p + 1, nloc = P1 * P1, QP = a.qpe;
+  const int c1 = (a.nel[0] - a.color[0] + a.p) / P1;
+  const int e1 = a.color[0] + P1 * int(blockIdx.x % c1), e2 = a.color[1] + P1 * int(blockIdx.x / c1);
+  for (int f = threadIdx.x; f < nloc; f += blockDim.x) {
+    const int f1 = f % P1, f2 = f / P1;
+    const int g1 = e1 + f1, g2 = e2 + f2;  // full indices
+    if (g1 < 1 || g1 > a.m[0] - 2 || g2 < 1 || g2 > a.m[1] - 2) continue;  // Dirichlet
+    double s0p = 0, s0l = 0, s2p = 0, s2l = 0;
+    for (int q2 = 0; q2 < QP; ++q2)
+      for (int q1 = 0; q1 < QP; ++q1) {
+        const double* t1 = a.bt[0] + ((size_t(e1) * QP + q1) * P1 + f1) * 3;
+        const double* t2 = a.bt[1] + ((size_t(e2) * QP + q2) * P1 + f2) * 3;
+        const int64_t qi = (int64_t(e2) * QP + q2) * a.nq[0] + int64_t(e1) * QP + q1;
+        const double phi = t1[0] * t2[0];
+        const double gr[2] = {t1[1] * t2[0], t1[0] * t2[1]};
+        const double hs[2][2] = {{t1[2] * t2[0], t1[1] * t2[1]}, {t1[1] * t2[1], t1[0] * t2[2]}};
+        double inv[2][2], b[2];
+        for (int j = 0; j < 2; ++j)
+          for (int i = 0; i < 2; ++i) inv[j][i] = a.qd[(1 + j * 3 + i) * a.NQ + qi];
+        for (int j = 0; j < 2; ++j) b[j] = a.qd[(10 + j) * a.NQ + qi];
+        double lap = b[0] * gr[0] + b[1] * gr[1];
+        for (int j = 0; j < 2; ++j)
+          for (int l = 0; l < 2; ++l) lap += (inv[j][0] * inv[l][0] + inv[j][1] * inv[l][1]) * hs[j][l];
+        const double w = a.qd[qi];
+        const double x = a.qd[13 * a.NQ + qi], y = a.qd[14 * a.NQ + qi];
+        const double sp = annulus_P(x, y), sl = -annulus_lapP(x, y);
+        s0p += w * sp * phi;
+        s0l += w * sl * phi;
+        s2p += w * sp * lap;
+        s2l += w * sl * lap;
+      }
+    const int64_t row = int64_t(g2 - 1) * a.n[0] + (g1 - 1);
+    a.lv[row] += s0p;
+    a.lv[a.Ns + row] += s0l;
+    a.lv[2 * a.Ns + row] += s2p;
+    a.lv[3 * a.Ns + row] += s2l;
+  }
+}
+
+// int_Omega P^2 and int_Omega (Lap P)^2 (||f||^2 of ls_energy_error kind 2)
+__global__ void geo_fnorm_kernel(const double* __restrict__ qd, int64_t NQ, double* out2) {
+  double a0 = 0, a1 = 0;
+  for (int64_t qi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; qi < NQ; qi += int64_t(gridDim.x) * blockDim.x) {
+    const double w = qd[qi], x = qd[13 * NQ + qi], y = qd[14 * NQ + qi];
+    const double sp = annulus_P(x, y), sl = annulus_lapP(x, y);
+    a0 += w * sp * sp;
+    a1 += w * sl * sl;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a0 += __shfl_down_sync(0xffffffffu, a0, o);
+    a1 += __shfl_down_sync(0xffffffffu, a1, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out2, a0);
+    atomicAdd(out2 + 1, a1);
+  }
+}
+
+int geo_load_annulus(GeoDev& gd, const GeoMap& g, const int64_t* n_el, cudaStream_t s, int64_t* launches) {
+  if (gd.d != 2) return LS_ENOTSUP;
+  if (gd.lv) return LS_OK;  // cached
+  const int p = gd.p, qpe = p + 5;  // reading c16 on Omega
+  std::vector<void*> tmp;  // point data of this computation only
+  GeoPts pts;
+  int rc = geo_points(g, 2, p, n_el, qpe, tmp, s, pts, launches);
+  if (rc == LS_OK) rc = dalloc(gd.allocs, &gd.lv, size_t(4) * gd.Ns);
+  double* dn = nullptr;
+  if (rc == LS_OK) rc = dalloc(tmp, &dn, 2);
+  if (rc == LS_OK) {
+    GEO_CUDA(cudaMemsetAsync(gd.lv, 0, size_t(4) * gd.Ns * sizeof(double), s));
+    GEO_CUDA(cudaMemsetAsync(dn, 0, 2 * sizeof(double), s));
+    GeoLoadArgs la{};
+    la.p = p;
+    la.qpe = qpe;
+    for (int k = 0; k < 2; ++k) {
+      la.nel[k] = int(n_el[k]);
+      la.m[k] = int(n_el[k]) + p;
+      la.n[k] = gd.n[k];
+      la.nq[k] = pts.nq[k];
+      la.bt[k] = pts.bt[k];
+    }
+    la.qd = pts.qd;
+    la.NQ = pts.NQ;
+    la.Ns = gd.Ns;
+    la.lv = gd.lv;
+    const int P1 = p + 1;
+    for (int c = 0; c < P1 * P1; ++c) {
+      la.color[0] = c % P1;
+      la.color[1] = c / P1;
+      const int64_t cnt = int64_t((n_el[0] - la.color[0] + p) / P1) * ((n_el[1] - la.color[1] + p) / P1);
+      if (cnt == 0) continue;
+      geo_load_kernel<<<unsigned(cnt), 64, 0, s>>>(la);
+      GEO_CUDA(cudaGetLastError());
+      if (launches) *launches += 1;
+    }
+    geo_fnorm_kernel<<<unsigned(std::min<int64_t>((pts.NQ + 255) / 256, 148 * 8)), 256, 0, s>>>(pts.qd, pts.NQ, dn);
+    GEO_CUDA(cudaGetLastError());
+    if (launches) *launches += 1;
+    GEO_CUDA(cudaMemcpyAsync(gd.fint, dn, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GEO_CUDA(cudaStreamSynchronize(s));
+  }
+  for (void* v : tmp) cudaFree(v);
+  return rc;
+}
+
+// b[t][i] = sum_m ( G1_m[t] S0_m[i] - G0_m[t] S2_m[i] ), m = 1 (g = pi cos(pi t), s = P),
+// m = 2 (g = sin(pi t), s = -Lap P); G0_m = int g_m b_t, G1_m = int g_m b_t' (host, 80-bit)
+__global__ void geo_rhs_kernel(const double* __restrict__ lv, const double* __restrict__ G, double* __restrict__ b,
+                               int t0, int nrows, int nt, int64_t Ns) {
+  const int64_t total = int64_t(nrows) * Ns;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int t = t0 + int(idx / Ns);
+    const int64_t i = idx % Ns;
+    // G: [G0_1 | G1_1 | G0_2 | G1_2], each of length nt
+    b[idx] = G[nt + t] * lv[i] - G[t] * lv[2 * Ns + i] + G[3 * nt + t] * lv[Ns + i] - G[2 * nt + t] * lv[3 * Ns + i];
+  }
+}
+
+int geo_rhs(const GeoDev& gd, const double* G, double* b, int t0, int nrows, int nt, cudaStream_t s,
+            int64_t* launches) {
+  const int64_t total = int64_t(nrows) * gd.Ns;
+  geo_rhs_kernel<<<unsigned(std::min<int64_t>((total + 255) / 256, 148 * 16)), 256, 0, s>>>(gd.lv, G, b, t0, nrows,
+                                                                                           nt, gd.Ns);
+  GEO_CUDA(cudaGetLastError());
+  if (launches) *launches += 1;
   return LS_OK;
 }
 

@@ -49,6 +49,8 @@ struct GeoDev {
   double* st = nullptr;       // [3][S][Ns]: M_s, J_s, L_s rows in stencil layout
   double* diag[3] = {nullptr, nullptr, nullptr};  // views of the centre entries
   int variant = 0;            // 0: DMMA band tiles (default), 1: DFMA stencil kernel
+  double* lv = nullptr;        // ls_rhs kind 2: [4][N_s] spatial load integrals (geo_load_annulus)
+  double fint[2] = {0.0, 0.0};  // int_Omega P^2, int_Omega (Lap P)^2
   std::vector<void*> allocs;
   ~GeoDev();
 };
@@ -65,6 +67,17 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
 int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt_global, const double* x,
                int s_first, int t_first, int nout, double* y, double* t1, double* t2, cudaStream_t s,
                int64_t* launches);
+
+// Spatial load integrals of the 2D quarter-annulus benchmark u = P(x, y) sin(pi t)
+// (PAPER.md 1128-1129): int P phi_i, int (-Lap P) phi_i, int P Lap phi_i, int (-Lap P) Lap phi_i
+// on Omega with p+5 Gauss points per element (reading c16), and int P^2, int (Lap P)^2.
+// d = 2 only (LS_ENOTSUP otherwise); computed once and cached in gd.
+int geo_load_annulus(GeoDev& gd, const GeoMap& g, const int64_t* n_el, cudaStream_t s, int64_t* launches);
+
+// b on the slab rows [t0, t0 + nrows) from gd.lv and the time integrals G (device,
+// [G0_1 | G1_1 | G0_2 | G1_2] x n_t): the load vector F(B_i) of PAPER.md 409.
+int geo_rhs(const GeoDev& gd, const double* G, double* b, int t0, int nrows, int nt, cudaStream_t s,
+            int64_t* launches);
 
 // D^{-1/2} of P^G = D^{1/2} Pbar^G D^{1/2}, D_ii = A_ii / Pbar_ii, as an N-vector
 // (diag(A) from the stencil centres and the banded time diagonals).

@@ -222,3 +222,55 @@ def test_geo_errors(torch_cuda):
     # b = 0 -> x = 0, 0 iterations
     x, st = ctx.pcg(b)
     assert st["iters"] == 0 and float(x.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("p,pt,n_elems", [(2, 2, [5, 6, 7]), (3, 3, [8, 8, 8]), (3, 2, [6, 9, 5])])
+def test_geo_rhs_kind2_matches_oracle(torch_cuda, p, pt, n_elems):
+    """ls_rhs kind 2 on the quarter annulus (PAPER.md 1128-1129): the separable device
+    evaluation against the oracle's direct space-time quadrature of f (d_t B_i - Lap B_i)."""
+    import paper_1809_10026_b200 as ls
+    from oracle import geo_rhs as R
+    geo = synth.quarter_annulus()
+    ctx = ls.Context(2, (p, pt), n_elems, geometry=geo, precond=ls.LS_PRECOND_PG)
+    b = ctx.rhs(2).cpu().numpy()
+    b_ref = R.load_vector(geo, n_elems[:2], p, n_elems[2], pt)
+    assert _rel(b, b_ref) <= 1e-12
+
+
+def test_geo_energy_error_and_convergence(torch_cuda):
+    """ls_energy_error kind 2 equals the oracle's ||f||^2 - 2 b.x + x.A x, and the GPU
+    solutions converge at O(h^{p-1}) in the least-squares energy norm (Fig. 2 setting)."""
+    import paper_1809_10026_b200 as ls
+    from oracle import geo_rhs as R
+    geo = synth.quarter_annulus()
+    for p, want in ((2, 1.0), (3, 2.0)):
+        errs = []
+        for ne in (8, 16, 32):
+            ctx = ls.Context(2, p, [ne] * 3, geometry=geo, precond=ls.LS_PRECOND_PG)
+            b = ctx.rhs(2)
+            x, st = ctx.pcg(b, tol=1e-12)
+            assert st["status"] == 0
+            e = ctx.energy_error(2, x)
+            if ne == 8:
+                f2 = R.f_norm2(geo, [ne, ne], p, ne, p)
+                assert abs(e["f2"] - f2) <= 1e-12 * f2
+                sf = G.space_factors_physical(geo, [ne, ne], p)
+                tf = uv.time_factors(ne, p)
+                xh = x.cpu().numpy()
+                J = f2 - 2 * np.sum(R.load_vector(geo, [ne, ne], p, ne, p) * xh) + np.sum(xh * G.apply_A_geo(xh, sf, tf))
+                assert abs(e["J"] - J) <= 1e-9 * f2
+            errs.append(np.sqrt(e["J"] / e["f2"]))
+        rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+        assert abs(rates[-1] - want) < 0.15, (p, errs, rates)
+
+
+def test_geo_rhs_kind_errors(torch_cuda):
+    import paper_1809_10026_b200 as ls
+    c3 = ls.Context(3, 2, [2, 2, 2, 3], geometry=synth.revolved_quarter_annulus())
+    with pytest.raises(ls.LSError) as e:
+        c3.rhs(2)
+    assert e.value.code == ls.LS_ENOTSUP
+    cube = ls.Context(2, 2, [4, 4, 4])
+    with pytest.raises(ls.LSError) as e:
+        cube.rhs(2)
+    assert e.value.code == ls.LS_EINVAL

@@ -216,3 +216,46 @@ def test_PG_reduces_iterations_on_revolved_annulus():
     _, it_g, ok2, _ = pcg.pcg(A, lambda r: GP.apply(r, pg), b)
     assert ok1 and ok2
     assert it_g * 3 <= it_p, (it_p, it_g)
+
+
+def test_annulus_benchmark_solution_has_homogeneous_data():
+    """u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t) (PAPER.md 1129) vanishes on the whole
+    boundary of the quarter annulus and at t = 0, so no lifting is needed; the sympy f
+    equals d_t u - Lap u by central differences."""
+    from oracle import geo_rhs as R
+    u, f = R.annulus_solution()
+    geo = synth.quarter_annulus()
+    e = np.linspace(0.0, 1.0, 9)
+    for side in ([np.array([0.0]), e], [np.array([1.0]), e], [e, np.array([0.0])], [e, np.array([1.0])]):
+        X = G.eval_map(geo, side)["X"]
+        assert np.max(np.abs(u(X[:, 0], X[:, 1], 0.7))) < 1e-13
+    X = G.eval_map(geo, [np.linspace(0.1, 0.9, 5)] * 2)["X"]
+    assert np.max(np.abs(u(X[:, 0], X[:, 1], 0.0))) == 0.0
+    h = 1e-4
+    x, y, t = X[:, 0], X[:, 1], 0.37
+    dt = (u(x, y, t + h) - u(x, y, t - h)) / (2 * h)
+    lap = (u(x + h, y, t) + u(x - h, y, t) + u(x, y + h, t) + u(x, y - h, t) - 4 * u(x, y, t)) / h ** 2
+    assert np.max(np.abs(f(x, y, t) - (dt - lap))) < 1e-5 * np.max(np.abs(f(x, y, t)))
+
+
+def test_annulus_energy_error_converges_at_rate_p_minus_1():
+    """Least-squares energy error ||(d_t - Lap)(u - u_h)|| on the quarter annulus (the
+    setting of Fig. 2, PAPER.md 1128-1139) decreases as O(h^{p-1}) (Thm teo:a-priori)."""
+    from oracle import geo_rhs as R
+    geo = synth.quarter_annulus()
+    for p, want in ((2, 1.0), (3, 2.0)):
+        errs = []
+        for ne in (4, 8, 16):
+            sf = G.space_factors_physical(geo, [ne, ne], p)
+            tf = uv.time_factors(ne, p)
+            b = R.load_vector(geo, [ne, ne], p, ne, p)
+            f2 = R.f_norm2(geo, [ne, ne], p, ne, p)
+            A = lambda v: G.apply_A_geo(v, sf, tf)
+            data = GP.setup(geo, [ne, ne], p, tf, GP.A_diagonal(sf, tf))
+            x, _, ok, _ = pcg.pcg(A, lambda r: GP.apply(r, data), b, tol=1e-12)
+            assert ok
+            J = f2 - 2 * np.sum(b * x) + np.sum(x * A(x))
+            assert J > 0 and np.sum(x * A(x)) <= f2     # J(c) >= 0, J(0) = ||f||^2
+            errs.append(np.sqrt(J / f2))
+        rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+        assert abs(rates[-1] - want) < 0.15, (p, errs, rates)
