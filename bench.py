@@ -447,6 +447,25 @@ def run_geometry(ls, torch, stream, cases=((32, 3), (64, 3))):
                         "fit_rel_res": c.geo_info()[0]})
             c.close()
             del b, x, z
+    # the Fig. 2 setting (PAPER.md 1128-1139): 2D quarter annulus, u = -(r^2-1)(r^2-4) x y^2 sin(pi t)
+    for n_el, p in ((64, 3), (128, 3)):
+        for pc, name in ((ls.LS_PRECOND_P, "P"), (ls.LS_PRECOND_PG, "P^G")):
+            c = ls.Context(2, p, [n_el] * 3, geometry=synth.quarter_annulus(), precond=pc)
+            c.set_stream(stream)
+            b = c.rhs(2)
+            c.pcg(b, tol=1e-8, max_iter=2000)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            x, st = c.pcg(b, tol=1e-8, max_iter=2000)
+            torch.cuda.synchronize()
+            solve_ms = (time.perf_counter() - t0) * 1e3
+            e = c.energy_error(2, x)
+            out.append({"domain": "quarter annulus, u of PAPER.md 1129 (ls_rhs kind 2)", "d": 2, "p": p,
+                        "n_el": n_el, "N": c.N, "precond": name, "iters": st["iters"], "solve_ms": solve_ms,
+                        "true_rel_res": st["true_rel_res"],
+                        "ls_energy_rel": float(np.sqrt(max(e["J"], 0.0) / e["f2"]))})
+            c.close()
+            del b, x
     return out
 
 
