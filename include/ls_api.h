@@ -179,6 +179,9 @@ int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_
  *   kind 1: f = prod_k sin(pi x_k) (cos t + d pi^2 sin t)     (cube, PAPER.md 1166)
  *   kind 2: mapped 2D domains only (ls_setup_geo, d = 2): f = (d_t - Lap) u for
  *           u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t) (quarter annulus, PAPER.md 1129)
+ *   kind 3: mapped 3D domains only (d = 3): f = -Lap u for the time-independent
+ *           u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(z) of the rotated quarter annulus
+ *           (PAPER.md 1221), with homogeneous boundary / initial data (DESIGN.md c23)
  * b: device vector (this rank's slab).  Errors: LS_EINVAL for an unknown kind,
  * LS_ENOTSUP for a kind the context does not support.
  */
@@ -245,8 +248,8 @@ typedef struct {
  *     logarithms (reading c21), factors interpolated piecewise linearly (reading c22),
  *     weighted univariate matrices, Algorithm 1 for Pbar^G, D_ii = A_ii / Pbar^G_ii.
  *   pcg_solve works unchanged; ls_matvec_slab applies slab rows (as for the cube);
- *     ls_rhs / ls_energy_error support kind 2 only: the 2D quarter-annulus benchmark
- *     u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t) of PAPER.md 1128-1129 (d = 2; f = d_t u - Lap u,
+ *     ls_rhs / ls_energy_error support kinds 2 (d = 2) and 3 (d = 3) only: the forcings of
+ *     the paper's quarter-annulus benchmarks (PAPER.md 1128-1129, 1219-1221; see ls_rhs;
  *     spatial integrals with p_s + 5 Gauss points per element on Omega, reading c16), other
  *     kinds LS_ENOTSUP (the caller supplies b); fd_apply_stage / fd_apply_scatter LS_ENOTSUP.
  * Limits: (p_s + 1)^d <= 343 local functions per element (d = 3: p_s <= 6).

@@ -1338,23 +1338,32 @@ extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first,
 extern "C" int ls_rhs(ls_ctx* ctx, int kind, double* b) {
   if (!ctx || !b || !aligned8(b)) return LS_EINVAL;
   if (ctx->geo) {
-    // mapped domain: kind 2 = the 2D quarter-annulus benchmark u = P(x, y) sin(pi t) of
-    // PAPER.md 1128-1129 (d = 2); b = G1_1 (x) S0_P + G1_2 (x) S0_{-Lap P} - G0_1 (x) S2_P - G0_2 (x) S2_{-Lap P}
-    if (kind != 2) return LS_ENOTSUP;
-    if (ctx->d != 2) return LS_ENOTSUP;
-    LS_CHECK(geo_load_annulus(*ctx->geo, *ctx->gmap, ctx->n_el, ctx->stream, &ctx->launches));
-    const int nt = ctx->nt;
-    std::vector<double> G(4 * size_t(nt)), i0, i1, i2;
+    // mapped domains: kind 2 = the 2D quarter-annulus benchmark u = P(x, y) sin(pi t) of
+    // PAPER.md 1128-1129 (d = 2); kind 3 = the rotated quarter annulus' f = (P - Lap P) sin z of
+    // PAPER.md 1219-1221 with homogeneous data (d = 3, reading c23);
+    // b = sum_m G1_m (x) S0_m - G0_m (x) S2_m (geo_rhs_kernel)
+    if (kind != 2 && kind != 3) return LS_ENOTSUP;
+    LS_CHECK(geo_load(*ctx->geo, *ctx->gmap, ctx->n_el, kind, ctx->stream, &ctx->launches));
+    const int nt = ctx->nt, d = ctx->d;
+    std::vector<double> G(4 * size_t(nt), 0.0), i0, i1, i2;
     const double pi = 3.14159265358979323846;
-    load_integrals(int(ctx->n_el[2]), ctx->pt, false, 3, 0.0, i0, i1, i2);  // cos(pi t)
-    for (int t = 0; t < nt; ++t) {
-      G[t] = pi * i0[t];       // G0_1 = int pi cos(pi t) b_t
-      G[nt + t] = pi * i1[t];  // G1_1 = int pi cos(pi t) b_t'
-    }
-    load_integrals(int(ctx->n_el[2]), ctx->pt, false, 0, 0.0, i0, i1, i2);  // sin(pi t)
-    for (int t = 0; t < nt; ++t) {
-      G[2 * nt + t] = i0[t];
-      G[3 * nt + t] = i1[t];
+    if (kind == 2) {
+      load_integrals(int(ctx->n_el[d]), ctx->pt, false, 3, 0.0, i0, i1, i2);  // cos(pi t)
+      for (int t = 0; t < nt; ++t) {
+        G[t] = pi * i0[t];       // G0_1 = int pi cos(pi t) b_t
+        G[nt + t] = pi * i1[t];  // G1_1 = int pi cos(pi t) b_t'
+      }
+      load_integrals(int(ctx->n_el[d]), ctx->pt, false, 0, 0.0, i0, i1, i2);  // sin(pi t)
+      for (int t = 0; t < nt; ++t) {
+        G[2 * nt + t] = i0[t];
+        G[3 * nt + t] = i1[t];
+      }
+    } else {
+      load_integrals(int(ctx->n_el[d]), ctx->pt, false, 4, 0.0, i0, i1, i2);  // g = 1
+      for (int t = 0; t < nt; ++t) {
+        G[t] = i0[t];
+        G[nt + t] = i1[t];
+      }
     }
     LS_CUDA(cudaMemcpyAsync(ctx->rhs_buf, G.data(), G.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     LS_CHECK(geo_rhs(*ctx->geo, ctx->rhs_buf, b, int(ctx->t0), int(ctx->ntl), nt, ctx->stream, &ctx->launches));
@@ -1618,17 +1627,18 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
 // least-squares functional / energy error (PAPER.md 392-410)
 // ------------------------------------------------------------------------------------------
 extern "C" int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4) {
-  if (!ctx || !x || !out4 || !aligned8(x) || kind < 0 || kind > 2) return LS_EINVAL;
-  if (ctx->geo ? kind != 2 : kind == 2) return ctx->geo ? LS_ENOTSUP : LS_EINVAL;
+  if (!ctx || !x || !out4 || !aligned8(x) || kind < 0 || kind > 3) return LS_EINVAL;
+  if (ctx->geo ? kind < 2 : kind >= 2) return ctx->geo ? LS_ENOTSUP : LS_EINVAL;
   if (x == ctx->pz || x == ctx->pq) return LS_EINVAL;  // the library's scratch vectors
   const double pi = 3.14159265358979323846;
   const int d = ctx->d;
   // ||f||^2 in closed form (T = 1, unit cube, reading c11): int sin^2(pi x) = 1/2 per direction
   double f2 = std::ldexp(1.0, -d);
-  if (kind == 2) {
-    // mapped domain, u = P sin(pi t): int_0^1 (pi cos)^2 = pi^2 / 2, int sin^2 = 1/2, cross term 0
-    LS_CHECK(geo_load_annulus(*ctx->geo, *ctx->gmap, ctx->n_el, ctx->stream, &ctx->launches));
-    f2 = 0.5 * pi * pi * ctx->geo->fint[0] + 0.5 * ctx->geo->fint[1];
+  if (kind >= 2) {
+    // mapped domains. kind 2, u = P sin(pi t): int_0^1 (pi cos)^2 = pi^2 / 2, int sin^2 = 1/2,
+    // cross term 0.  kind 3: f time independent, T = 1.
+    LS_CHECK(geo_load(*ctx->geo, *ctx->gmap, ctx->n_el, kind, ctx->stream, &ctx->launches));
+    f2 = kind == 2 ? 0.5 * pi * pi * ctx->geo->fint[0] + 0.5 * ctx->geo->fint[1] : ctx->geo->fint[0];
   } else if (kind == 0) {
     f2 *= (std::exp(2.0) - 1.0) / 2.0;
   } else {

@@ -544,11 +544,16 @@ int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el,
 }
 
 // ------------------------------------------------------------------------------------------
-// load vector of the 2D quarter-annulus benchmark (PAPER.md 1128-1129; ls_rhs kind 2)
+// load vectors of the mapped-domain benchmarks (ls_rhs kinds 2, 3)
 // ------------------------------------------------------------------------------------------
-// u = P(x, y) sin(pi t), P = -(x^2 + y^2 - 1)(x^2 + y^2 - 4) x y^2, so
-// f = d_t u - Lap u = pi cos(pi t) P - sin(pi t) Lap P,
-// Lap P = -2x (x^4 + 22 x^2 y^2 - 5 x^2 + 21 y^4 - 45 y^2 + 4).
+// P(x, y) = -(x^2 + y^2 - 1)(x^2 + y^2 - 4) x y^2,
+// Lap P   = -2x (x^4 + 22 x^2 y^2 - 5 x^2 + 21 y^4 - 45 y^2 + 4)   (2D Laplacian).
+// kind 2 (2D quarter annulus, PAPER.md 1128-1129): u = P sin(pi t),
+//   f = pi cos(pi t) P - sin(pi t) Lap P: two terms (s_1 = P, g_1 = pi cos(pi t)),
+//   (s_2 = -Lap P, g_2 = sin(pi t)).
+// kind 3 (rotated quarter annulus, PAPER.md 1219-1221): u = P sin(z) (time independent),
+//   f = -Lap_3D u = (P - Lap P) sin(z): one term (s_1 = f, g_1 = 1) -- the paper's forcing
+//   for homogeneous data (reading c23: Table 2's lifting is out of scope).
 __device__ __forceinline__ double annulus_P(double x, double y) {
   const double r2 = x * x + y * y;
   return -(r2 - 1.0) * (r2 - 4.0) * x * y * y;
@@ -557,67 +562,126 @@ __device__ __forceinline__ double annulus_lapP(double x, double y) {
   const double x2 = x * x, y2 = y * y;
   return -2.0 * x * (x2 * x2 + 22.0 * x2 * y2 - 5.0 * x2 + 21.0 * y2 * y2 - 45.0 * y2 + 4.0);
 }
-
-struct GeoLoadArgs {
-  int p, qpe;
-  int nel[2], m[2], n[2], nq[2];
-  int color[2];
-  const double* bt[2];   // [n_el][qpe][p+1][3]
-  const double* qd;      // [16][NQ]
-  int64_t NQ, Ns;
-  double* lv;            // [4][Ns]: int P phi, int (-Lap P) phi, int P Lap phi, int (-Lap P) Lap phi
-};
-
-// one CTA per element of a colour class (e_k mod (p+1) fixed: no two CTAs share a row),
-// one thread per local function
-__global__ void geo_load_kernel(GeoLoadArgs a) {
-  const int P1 = a.p + 1, nloc = P1 * P1, QP = a.qpe;
-  const int c1 = (a.nel[0] - a.color[0] + a.p) / P1;
-  const int e1 = a.color[0] + P1 * int(blockIdx.x % c1), e2 = a.color[1] + P1 * int(blockIdx.x / c1);
-  for (int f = threadIdx.x; f < nloc; f += blockDim.x) {
-    const int f1 = f % P1, f2 = f / P1;
-    const int g1 = e1 + f1, g2 = e2 + f2;  // full indices
-    if (g1 < 1 || g1 > a.m[0] - 2 || g2 < 1 || g2 > a.m[1] - 2) continue;  // Dirichlet
-    double s0p = 0, s0l = 0, s2p = 0, s2l = 0;
-    for (int q2 = 0; q2 < QP; ++q2)
-      for (int q1 = 0; q1 < QP; ++q1) {
-        const double* t1 = a.bt[0] + ((size_t(e1) * QP + q1) * P1 + f1) * 3;
-        const double* t2 = a.bt[1] + ((size_t(e2) * QP + q2) * P1 + f2) * 3;
-        const int64_t qi = (int64_t(e2) * QP + q2) * a.nq[0] + int64_t(e1) * QP + q1;
-        const double phi = t1[0] * t2[0];
-        const double gr[2] = {t1[1] * t2[0], t1[0] * t2[1]};
-        const double hs[2][2] = {{t1[2] * t2[0], t1[1] * t2[1]}, {t1[1] * t2[1], t1[0] * t2[2]}};
-        double inv[2][2], b[2];
-        for (int j = 0; j < 2; ++j)
-          for (int i = 0; i < 2; ++i) inv[j][i] = a.qd[(1 + j * 3 + i) * a.NQ + qi];
-        for (int j = 0; j < 2; ++j) b[j] = a.qd[(10 + j) * a.NQ + qi];
-        double lap = b[0] * gr[0] + b[1] * gr[1];
-        for (int j = 0; j < 2; ++j)
-          for (int l = 0; l < 2; ++l) lap += (inv[j][0] * inv[l][0] + inv[j][1] * inv[l][1]) * hs[j][l];
-        const double w = a.qd[qi];
-        const double x = a.qd[13 * a.NQ + qi], y = a.qd[14 * a.NQ + qi];
-        const double sp = annulus_P(x, y), sl = -annulus_lapP(x, y);
-        s0p += w * sp * phi;
-        s0l += w * sl * phi;
-        s2p += w * sp * lap;
-        s2l += w * sl * lap;
-      }
-    const int64_t row = int64_t(g2 - 1) * a.n[0] + (g1 - 1);
-    a.lv[row] += s0p;
-    a.lv[a.Ns + row] += s0l;
-    a.lv[2 * a.Ns + row] += s2p;
-    a.lv[3 * a.Ns + row] += s2l;
+// the spatial factors s_1, s_2 of the kind at a physical point
+__device__ __forceinline__ void load_terms(int kind, double x, double y, double z, double& s1, double& s2) {
+  if (kind == 2) {
+    s1 = annulus_P(x, y);
+    s2 = -annulus_lapP(x, y);
+  } else {
+    s1 = (annulus_P(x, y) - annulus_lapP(x, y)) * sin(z);
+    s2 = 0.0;
   }
 }
 
-// int_Omega P^2 and int_Omega (Lap P)^2 (||f||^2 of ls_energy_error kind 2)
-__global__ void geo_fnorm_kernel(const double* __restrict__ qd, int64_t NQ, double* out2) {
+struct GeoLoadArgs {
+  int d, p, qpe, kind;
+  int nel[3], m[3], n[3], nq[3];
+  int color[3];
+  const double* bt[3];   // [n_el][qpe][p+1][3]
+  const double* qd;      // [16][NQ]
+  int64_t NQ, Ns;
+  double* lv;            // [4][Ns]: int s_1 phi, int s_2 phi, int s_1 Lap phi, int s_2 Lap phi
+};
+
+// one CTA per element of a colour class (e_k mod (p+1) fixed: no two CTAs share a row),
+// threads over the local functions
+__global__ void geo_load_kernel(GeoLoadArgs a) {
+  const int d = a.d, P1 = a.p + 1, QP = a.qpe;
+  int nloc = 1, nqe = 1;
+  for (int k = 0; k < d; ++k) {
+    nloc *= P1;
+    nqe *= QP;
+  }
+  int e[3] = {0, 0, 0};
+  {
+    int64_t r = blockIdx.x;
+    for (int k = 0; k < d; ++k) {
+      const int cnt = (a.nel[k] - a.color[k] + a.p) / P1;
+      e[k] = a.color[k] + P1 * int(r % cnt);
+      r /= cnt;
+    }
+  }
+  for (int f = threadIdx.x; f < nloc; f += blockDim.x) {
+    int fl[3] = {0, 0, 0};
+    int64_t row = 0, rs = 1;
+    bool ok = true;
+    {
+      int r = f;
+      for (int k = 0; k < d; ++k) {
+        fl[k] = r % P1;
+        r /= P1;
+        const int gk = e[k] + fl[k];  // full index
+        ok = ok && gk >= 1 && gk <= a.m[k] - 2;
+        row += rs * (gk - 1);
+        rs *= a.n[k];
+      }
+    }
+    if (!ok) continue;  // Dirichlet
+    double s0a = 0, s0b = 0, s2a = 0, s2b = 0;
+    for (int ql = 0; ql < nqe; ++ql) {
+      double v[3][3];
+      int64_t qi = 0, qs = 1;
+      int r = ql;
+      for (int k = 0; k < 3; ++k) {
+        if (k < d) {
+          const int g = r % QP;
+          r /= QP;
+          const double* t = a.bt[k] + ((size_t(e[k]) * QP + g) * P1 + fl[k]) * 3;
+          v[k][0] = t[0];
+          v[k][1] = t[1];
+          v[k][2] = t[2];
+          qi += qs * (int64_t(e[k]) * QP + g);
+          qs *= a.nq[k];
+        } else {
+          v[k][0] = 1;
+          v[k][1] = 0;
+          v[k][2] = 0;
+        }
+      }
+      const double phi = v[0][0] * v[1][0] * v[2][0];
+      double gr[3], hs[3][3];
+      for (int j = 0; j < 3; ++j) {
+        gr[j] = 1;
+        for (int k = 0; k < 3; ++k) gr[j] *= v[k][k == j ? 1 : 0];
+      }
+      for (int j = 0; j < 3; ++j)
+        for (int l = 0; l < 3; ++l) {
+          double h = 1;
+          for (int k = 0; k < 3; ++k) h *= v[k][(k == j) + (k == l)];
+          hs[j][l] = h;
+        }
+      double inv[3][3], b[3];
+      for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) inv[j][i] = a.qd[(1 + j * 3 + i) * a.NQ + qi];
+      for (int j = 0; j < 3; ++j) b[j] = a.qd[(10 + j) * a.NQ + qi];
+      double lap = b[0] * gr[0] + b[1] * gr[1] + b[2] * gr[2];
+      for (int j = 0; j < d; ++j)
+        for (int l = 0; l < d; ++l)
+          lap += (inv[j][0] * inv[l][0] + inv[j][1] * inv[l][1] + inv[j][2] * inv[l][2]) * hs[j][l];
+      const double w = a.qd[qi];
+      double s1, s2;
+      load_terms(a.kind, a.qd[13 * a.NQ + qi], a.qd[14 * a.NQ + qi], a.qd[15 * a.NQ + qi], s1, s2);
+      s0a += w * s1 * phi;
+      s0b += w * s2 * phi;
+      s2a += w * s1 * lap;
+      s2b += w * s2 * lap;
+    }
+    a.lv[row] += s0a;
+    a.lv[a.Ns + row] += s0b;
+    a.lv[2 * a.Ns + row] += s2a;
+    a.lv[3 * a.Ns + row] += s2b;
+  }
+}
+
+// int_Omega s_1^2 and int_Omega s_2^2 (||f||^2 of ls_energy_error)
+__global__ void geo_fnorm_kernel(const double* __restrict__ qd, int64_t NQ, int kind, double* out2) {
   double a0 = 0, a1 = 0;
   for (int64_t qi = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; qi < NQ; qi += int64_t(gridDim.x) * blockDim.x) {
-    const double w = qd[qi], x = qd[13 * NQ + qi], y = qd[14 * NQ + qi];
-    const double sp = annulus_P(x, y), sl = annulus_lapP(x, y);
-    a0 += w * sp * sp;
-    a1 += w * sl * sl;
+    double s1, s2;
+    load_terms(kind, qd[13 * NQ + qi], qd[14 * NQ + qi], qd[15 * NQ + qi], s1, s2);
+    const double w = qd[qi];
+    a0 += w * s1 * s1;
+    a1 += w * s2 * s2;
   }
   for (int o = 16; o > 0; o >>= 1) {
     a0 += __shfl_down_sync(0xffffffffu, a0, o);
@@ -629,25 +693,27 @@ __global__ void geo_fnorm_kernel(const double* __restrict__ qd, int64_t NQ, doub
   }
 }
 
-int geo_load_annulus(GeoDev& gd, const GeoMap& g, const int64_t* n_el, cudaStream_t s, int64_t* launches) {
-  if (gd.d != 2) return LS_ENOTSUP;
-  if (gd.lv) return LS_OK;  // cached
-  const int p = gd.p, qpe = p + 5;  // reading c16 on Omega
+int geo_load(GeoDev& gd, const GeoMap& g, const int64_t* n_el, int kind, cudaStream_t s, int64_t* launches) {
+  if (!((kind == 2 && gd.d == 2) || (kind == 3 && gd.d == 3))) return LS_ENOTSUP;
+  if (gd.lv && gd.lv_kind == kind) return LS_OK;  // cached
+  const int d = gd.d, p = gd.p, qpe = p + 5;  // reading c16 on Omega
   std::vector<void*> tmp;  // point data of this computation only
   GeoPts pts;
-  int rc = geo_points(g, 2, p, n_el, qpe, tmp, s, pts, launches);
-  if (rc == LS_OK) rc = dalloc(gd.allocs, &gd.lv, size_t(4) * gd.Ns);
+  int rc = geo_points(g, d, p, n_el, qpe, tmp, s, pts, launches);
+  if (rc == LS_OK && !gd.lv) rc = dalloc(gd.allocs, &gd.lv, size_t(4) * gd.Ns);
   double* dn = nullptr;
   if (rc == LS_OK) rc = dalloc(tmp, &dn, 2);
   if (rc == LS_OK) {
     GEO_CUDA(cudaMemsetAsync(gd.lv, 0, size_t(4) * gd.Ns * sizeof(double), s));
     GEO_CUDA(cudaMemsetAsync(dn, 0, 2 * sizeof(double), s));
     GeoLoadArgs la{};
+    la.d = d;
     la.p = p;
     la.qpe = qpe;
-    for (int k = 0; k < 2; ++k) {
-      la.nel[k] = int(n_el[k]);
-      la.m[k] = int(n_el[k]) + p;
+    la.kind = kind;
+    for (int k = 0; k < 3; ++k) {
+      la.nel[k] = k < d ? int(n_el[k]) : 1;
+      la.m[k] = k < d ? int(n_el[k]) + p : 1;
       la.n[k] = gd.n[k];
       la.nq[k] = pts.nq[k];
       la.bt[k] = pts.bt[k];
@@ -657,27 +723,38 @@ int geo_load_annulus(GeoDev& gd, const GeoMap& g, const int64_t* n_el, cudaStrea
     la.Ns = gd.Ns;
     la.lv = gd.lv;
     const int P1 = p + 1;
-    for (int c = 0; c < P1 * P1; ++c) {
-      la.color[0] = c % P1;
-      la.color[1] = c / P1;
-      const int64_t cnt = int64_t((n_el[0] - la.color[0] + p) / P1) * ((n_el[1] - la.color[1] + p) / P1);
+    int ncol = 1;
+    for (int k = 0; k < d; ++k) ncol *= P1;
+    for (int c = 0; c < ncol; ++c) {
+      int64_t cnt = 1;
+      int r = c;
+      for (int k = 0; k < 3; ++k) {
+        la.color[k] = 0;
+        if (k < d) {
+          la.color[k] = r % P1;
+          r /= P1;
+          cnt *= (n_el[k] - la.color[k] + p) / P1;
+        }
+      }
       if (cnt == 0) continue;
       geo_load_kernel<<<unsigned(cnt), 64, 0, s>>>(la);
       GEO_CUDA(cudaGetLastError());
       if (launches) *launches += 1;
     }
-    geo_fnorm_kernel<<<unsigned(std::min<int64_t>((pts.NQ + 255) / 256, 148 * 8)), 256, 0, s>>>(pts.qd, pts.NQ, dn);
+    geo_fnorm_kernel<<<unsigned(std::min<int64_t>((pts.NQ + 255) / 256, 148 * 8)), 256, 0, s>>>(pts.qd, pts.NQ, kind,
+                                                                                                dn);
     GEO_CUDA(cudaGetLastError());
     if (launches) *launches += 1;
     GEO_CUDA(cudaMemcpyAsync(gd.fint, dn, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     GEO_CUDA(cudaStreamSynchronize(s));
+    gd.lv_kind = kind;
   }
   for (void* v : tmp) cudaFree(v);
   return rc;
 }
 
-// b[t][i] = sum_m ( G1_m[t] S0_m[i] - G0_m[t] S2_m[i] ), m = 1 (g = pi cos(pi t), s = P),
-// m = 2 (g = sin(pi t), s = -Lap P); G0_m = int g_m b_t, G1_m = int g_m b_t' (host, 80-bit)
+// b[t][i] = G1_1[t] S0_1[i] - G0_1[t] S2_1[i] + G1_2[t] S0_2[i] - G0_2[t] S2_2[i] with
+// G0_m = int g_m b_t, G1_m = int g_m b_t' (host, 80-bit), G = [G0_1 | G1_1 | G0_2 | G1_2]
 __global__ void geo_rhs_kernel(const double* __restrict__ lv, const double* __restrict__ G, double* __restrict__ b,
                                int t0, int nrows, int nt, int64_t Ns) {
   const int64_t total = int64_t(nrows) * Ns;
@@ -685,7 +762,6 @@ __global__ void geo_rhs_kernel(const double* __restrict__ lv, const double* __re
        idx += int64_t(gridDim.x) * blockDim.x) {
     const int t = t0 + int(idx / Ns);
     const int64_t i = idx % Ns;
-    // G: [G0_1 | G1_1 | G0_2 | G1_2], each of length nt
     b[idx] = G[nt + t] * lv[i] - G[t] * lv[2 * Ns + i] + G[3 * nt + t] * lv[Ns + i] - G[2 * nt + t] * lv[3 * Ns + i];
   }
 }

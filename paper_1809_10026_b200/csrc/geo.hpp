@@ -49,8 +49,9 @@ struct GeoDev {
   double* st = nullptr;       // [3][S][Ns]: M_s, J_s, L_s rows in stencil layout
   double* diag[3] = {nullptr, nullptr, nullptr};  // views of the centre entries
   int variant = 0;            // 0: DMMA band tiles (default), 1: DFMA stencil kernel
-  double* lv = nullptr;        // ls_rhs kind 2: [4][N_s] spatial load integrals (geo_load_annulus)
-  double fint[2] = {0.0, 0.0};  // int_Omega P^2, int_Omega (Lap P)^2
+  double* lv = nullptr;        // ls_rhs kinds 2, 3: [4][N_s] spatial load integrals (geo_load)
+  int lv_kind = 0;
+  double fint[2] = {0.0, 0.0};  // int_Omega s_1^2, int_Omega s_2^2
   std::vector<void*> allocs;
   ~GeoDev();
 };
@@ -68,11 +69,11 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt_gl
                int s_first, int t_first, int nout, double* y, double* t1, double* t2, cudaStream_t s,
                int64_t* launches);
 
-// Spatial load integrals of the 2D quarter-annulus benchmark u = P(x, y) sin(pi t)
-// (PAPER.md 1128-1129): int P phi_i, int (-Lap P) phi_i, int P Lap phi_i, int (-Lap P) Lap phi_i
-// on Omega with p+5 Gauss points per element (reading c16), and int P^2, int (Lap P)^2.
-// d = 2 only (LS_ENOTSUP otherwise); computed once and cached in gd.
-int geo_load_annulus(GeoDev& gd, const GeoMap& g, const int64_t* n_el, cudaStream_t s, int64_t* launches);
+// Spatial load integrals of the mapped-domain benchmarks (PAPER.md 1128-1129, 1219-1221):
+// kind 2 (d = 2): u = P sin(pi t), s_1 = P, s_2 = -Lap P; kind 3 (d = 3): f = (P - Lap P) sin z.
+// int s_m phi_i, int s_m Lap phi_i on Omega with p+5 Gauss points per element (reading c16)
+// and int s_m^2; computed once per kind and cached in gd.  LS_ENOTSUP for another d.
+int geo_load(GeoDev& gd, const GeoMap& g, const int64_t* n_el, int kind, cudaStream_t s, int64_t* launches);
 
 // b on the slab rows [t0, t0 + nrows) from gd.lv and the time integrals G (device,
 // [G0_1 | G1_1 | G0_2 | G1_2] x n_t): the load vector F(B_i) of PAPER.md 409.

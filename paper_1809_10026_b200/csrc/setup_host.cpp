@@ -171,7 +171,8 @@ void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<d
     for (size_t g = 0; g < gx.size(); ++g) {
       const R x = 0.5L * (a + b) + 0.5L * (b - a) * gx[g];
       const R w = 0.5L * (b - a) * gw[g];
-      const R f = fn == 0 ? sinl(pi * x) : fn == 1 ? expl(x) : fn == 3 ? cosl(pi * x) : cosl(x) + R(c) * sinl(x);
+      const R f = fn == 0 ? sinl(pi * x) : fn == 1 ? expl(x) : fn == 3 ? cosl(pi * x) : fn == 4 ? 1.0L
+                                                                                  : cosl(x) + R(c) * sinl(x);
       bspline_eval(kn, p, x, v0.data(), v1.data(), v2.data());
       for (int i = 0; i < n; ++i) {
         a0[i] += w * f * v0[i + lo];

@@ -30,7 +30,7 @@ Factors space_factors(int n_el, int p);
 Factors time_factors(int n_el, int p);
 
 // Univariate load integrals for a separable forcing with q = p + 5 Gauss points
-// per element (reading c16).  fn: 0 = sin(pi x), 1 = e^t, 2 = cos t + c sin t, 3 = cos(pi x).
+// per element (reading c16).  fn: 0 = sin(pi x), 1 = e^t, 2 = cos t + c sin t, 3 = cos(pi x), 4 = 1.
 // Returns int fn b_i, int fn b_i', int fn b_i'' over the constrained basis.
 void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<double>& i0,
                     std::vector<double>& i1, std::vector<double>& i2);

@@ -274,3 +274,33 @@ def test_geo_rhs_kind_errors(torch_cuda):
     with pytest.raises(ls.LSError) as e:
         cube.rhs(2)
     assert e.value.code == ls.LS_EINVAL
+
+
+@pytest.mark.parametrize("p,n_elems", [(2, [3, 4, 3, 5]), (3, [4, 3, 4, 4])])
+def test_geo_rhs_kind3_matches_oracle(torch_cuda, p, n_elems):
+    """ls_rhs kind 3 on the rotated quarter annulus (PAPER.md 1221, reading c23) against the
+    oracle's direct space-time quadrature."""
+    import paper_1809_10026_b200 as ls
+    from oracle import geo_rhs as R
+    geo = synth.revolved_quarter_annulus()
+    ctx = ls.Context(3, p, n_elems, geometry=geo)
+    b = ctx.rhs(3).cpu().numpy()
+    b_ref = R.load_vector(geo, n_elems[:3], p, n_elems[3], p, kind=3)
+    assert _rel(b, b_ref) <= 1e-12
+    x = torch_cuda.from_numpy(synth.residual(ctx.shape, 9)).cuda()
+    e = ctx.energy_error(3, x)
+    assert abs(e["f2"] - R.f_norm2(geo, n_elems[:3], p, n_elems[3], p, kind=3)) <= 1e-12 * e["f2"]
+
+
+@pytest.mark.parametrize("ne,p", [(8, 2), (8, 3), (16, 2), (16, 3)])
+def test_geo_table2_iterations(torch_cuda, golden_loader, ne, p):
+    """CG iterations with P and P^G on the rotated quarter annulus against Table 2
+    (PAPER.md 1244-1262), forcing of kind 3 (reading c23: homogeneous data, so within 20 %)."""
+    import paper_1809_10026_b200 as ls
+    tab = golden_loader("table2_iterations.json")
+    geo = synth.revolved_quarter_annulus()
+    for pc, key in ((ls.LS_PRECOND_P, "P"), (ls.LS_PRECOND_PG, "PG")):
+        ctx = ls.Context(3, p, [ne] * 4, geometry=geo, precond=pc)
+        _, st = ctx.pcg(ctx.rhs(3), tol=1e-8)
+        ref = tab[key][str(ne)][str(p)]
+        assert st["status"] == 0 and abs(st["iters"] - ref) <= 0.2 * ref, (key, st["iters"], ref)

@@ -259,3 +259,31 @@ def test_annulus_energy_error_converges_at_rate_p_minus_1():
             errs.append(np.sqrt(J / f2))
         rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
         assert abs(rates[-1] - want) < 0.15, (p, errs, rates)
+
+
+def test_revolved_forcing_and_table2_iterations(golden_loader):
+    """Kind 3 (PAPER.md 1219-1221): f = -Lap u for the time-independent u of the rotated
+    quarter annulus (central differences), and CG iteration counts with P and P^G on the
+    n_sub = 8, p = 2 mesh against Table 2 (PAPER.md 1244-1262).  Reading c23: homogeneous
+    data instead of the paper's lifting, so the counts agree within 20 %, not exactly."""
+    from oracle import geo_rhs as R
+    u, f = R.revolved_solution()
+    geo = synth.revolved_quarter_annulus()
+    X = G.eval_map(geo, [np.linspace(0.1, 0.9, 3)] * 3)["X"]
+    x, y, z = X.T
+    h = 1e-3
+    lap = sum((u(*(X + h * np.eye(3)[k]).T, 0.0) + u(*(X - h * np.eye(3)[k]).T, 0.0) - 2 * u(x, y, z, 0.0)) / h ** 2
+              for k in range(3))
+    assert np.max(np.abs(f(x, y, z, 0.3) + lap)) < 1e-5 * np.max(np.abs(lap))
+    tab = golden_loader("table2_iterations.json")
+    ne, p = 8, 2
+    sf = G.space_factors_physical(geo, [ne] * 3, p)
+    tf = uv.time_factors(ne, p)
+    b = R.load_vector(geo, [ne] * 3, p, ne, p, kind=3)
+    A = lambda v: G.apply_A_geo(v, sf, tf)
+    plain = fd.setup([uv.space_factors(ne, p)] * 3, tf)
+    pg = GP.setup(geo, [ne] * 3, p, tf, GP.A_diagonal(sf, tf))
+    _, it_p, _, _ = pcg.pcg(A, lambda r: fd.fd_apply(r, plain), b)
+    _, it_g, _, _ = pcg.pcg(A, lambda r: GP.apply(r, pg), b)
+    for it, ref in ((it_p, tab["P"]["8"]["2"]), (it_g, tab["PG"]["8"]["2"])):
+        assert abs(it - ref) <= 0.2 * ref, (it, ref)
