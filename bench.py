@@ -404,9 +404,10 @@ def run_extras(ls, torch, stream):
 
 def run_geometry(ls, torch, stream, cases=((32, 3), (64, 3))):
     """Mapped domain: the rotated quarter annulus of PAPER.md 1219
-    (Table 2's domain), P and P^G, seeded U[-1,1] right-hand side (the paper's data needs a
-    lifting, out of scope), tol 1e-8.  Paper (Table 2, p = 3, serial Matlab): n_sub = 32:
+    (Table 2's domain), P and P^G, the paper's forcing with homogeneous data (ls_rhs kind 3,
+    DESIGN.md c23), tol 1e-8.  Paper (Table 2, p = 3, serial Matlab, with lifting): n_sub = 32:
     P 143 it / 132 s, P^G 41 it / 39.6 s; n_sub = 64: P 155 it / 2415 s, P^G 44 it / 716 s."""
+    paper = {(32, "P"): (143, 132.24), (32, "P^G"): (41, 39.57), (64, "P"): (155, 2415.23), (64, "P^G"): (44, 716.03)}
     out = []
     geo = synth.revolved_quarter_annulus()
     for n_el, p in cases:
@@ -417,7 +418,7 @@ def run_geometry(ls, torch, stream, cases=((32, 3), (64, 3))):
             torch.cuda.synchronize()
             setup_s = time.perf_counter() - t0
             c.set_stream(stream)
-            b = torch.from_numpy(synth.residual(c.shape, 0)).cuda()
+            b = c.rhs(3)
             c.pcg(b, tol=1e-8, max_iter=2000)  # warm
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -444,7 +445,8 @@ def run_geometry(ls, torch, stream, cases=((32, 3), (64, 3))):
                         # stencil arrays once + t1, t2 read + y written
                         "matvec_gflops_alg": round(4.0 * S * c.N / (mv_ms * 1e-3) / 1e9, 1),
                         "matvec_gbs_alg": round(8.0 * (3 * S * Ns + 5 * c.N) / (mv_ms * 1e-3) / 1e9, 1),
-                        "fit_rel_res": c.geo_info()[0]})
+                        "fit_rel_res": c.geo_info()[0], "rhs": "kind 3 (DESIGN.md c23)",
+                        "paper_table2_iters_s": paper.get((n_el, name))})
             c.close()
             del b, x, z
     # the Fig. 2 setting (PAPER.md 1128-1139): 2D quarter annulus, u = -(r^2-1)(r^2-4) x y^2 sin(pi t)
