@@ -54,7 +54,7 @@ static void dir_eval(const GeoMap& g, int k, R eta, std::vector<R>& v0, std::vec
 }
 
 // F and Jac at one point from per-direction tables (quotient rule, PAPER.md 226-250)
-static void tensor_eval(const GeoMap& g, const std::vector<R>* v0, const std::vector<R>* v1, R* x, R* jac) {
+static void tensor_eval(const GeoMap& g, const R* const* v0, const R* const* v1, R* x, R* jac) {
   const int d = g.d;
   R N[3] = {0, 0, 0}, W = 0, dN[3][3] = {{0}}, dW[3] = {0, 0, 0};
   const int m1 = g.m[0], m2 = d >= 2 ? g.m[1] : 1, m3 = d >= 3 ? g.m[2] : 1;
@@ -85,8 +85,10 @@ static void tensor_eval(const GeoMap& g, const std::vector<R>* v0, const std::ve
 void geo_eval(const GeoMap& g, const double* eta, double* x, double* jac) {
   std::vector<R> v0[3], v1[3];
   for (int k = 0; k < g.d; ++k) dir_eval(g, k, eta[k], v0[k], v1[k]);
+  const R* p0[3] = {v0[0].data(), v0[1].data(), v0[2].data()};
+  const R* p1[3] = {v1[0].data(), v1[1].data(), v1[2].data()};
   R xr[3], jr[9];
-  tensor_eval(g, v0, v1, xr, jr);
+  tensor_eval(g, p0, p1, xr, jr);
   for (int i = 0; i < g.d; ++i) x[i] = double(xr[i]);
   for (int i = 0; i < g.d * g.d; ++i) jac[i] = double(jr[i]);
 }
@@ -136,10 +138,11 @@ int pg_weights(const GeoMap& g, const int64_t* n_el, std::vector<double> mu[3], 
   std::vector<R> L(size_t(NE) * (d + 1));
   for (int64_t e = 0; e < NE; ++e) {
     const int ei[3] = {int(e % ne[0]), int((e / ne[0]) % ne[1]), int(e / (int64_t(ne[0]) * ne[1]))};
-    std::vector<R> v0[3], v1[3];
+    const R* v0[3] = {nullptr, nullptr, nullptr};
+    const R* v1[3] = {nullptr, nullptr, nullptr};
     for (int k = 0; k < d; ++k) {
-      v0[k] = t0[k][ei[k]];
-      v1[k] = t1[k][ei[k]];
+      v0[k] = t0[k][ei[k]].data();
+      v1[k] = t1[k][ei[k]].data();
     }
     R x[3], jac[9], inv[9];
     tensor_eval(g, v0, v1, x, jac);
@@ -154,47 +157,52 @@ int pg_weights(const GeoMap& g, const int64_t* n_el, std::vector<double> mu[3], 
   }
   // alternating least-squares sweeps on the logarithms (reading c21):
   //   log c_tau(e) ~ sum_j m_j(e_j);  log c_k(e) ~ o_k(e_k) + sum_{j != k} m_j(e_j)
-  std::vector<R> m[3], o[3];
+  // Every update is an average over the elements with e_j = v of separable terms, so it
+  // needs only the marginals A_q[j][v] = sum_{e: e_j = v} L_q(e) (one pass over the
+  // elements) and the sums S(m_l), S(o_k): O(d^2 n_el) per sweep.
+  std::vector<R> m[3], o[3], Am[4][3];
   for (int k = 0; k < 3; ++k) {
     m[k].assign(ne[k], 0);
     o[k].assign(ne[k], 0);
   }
-  std::vector<R> acc[3];
+  for (int q = 0; q <= d; ++q)
+    for (int j = 0; j < d; ++j) Am[q][j].assign(ne[j], 0);
+  for (int64_t e = 0; e < NE; ++e) {
+    const int ei[3] = {int(e % ne[0]), int((e / ne[0]) % ne[1]), int(e / (int64_t(ne[0]) * ne[1]))};
+    for (int q = 0; q <= d; ++q)
+      for (int j = 0; j < d; ++j) Am[q][j][ei[j]] += L[size_t(e) * (d + 1) + q];
+  }
+  auto sum = [](const std::vector<R>& v) {
+    R s = 0;
+    for (R x : v) s += x;
+    return s;
+  };
   for (int sweep = 0; sweep < 5000; ++sweep) {
     R change = 0;
-    for (int j = 0; j < d; ++j) {  // m_j: every equation contains it with coefficient 1 (k != j)
-      acc[j].assign(ne[j], 0);
-      for (int64_t e = 0; e < NE; ++e) {
-        const int ei[3] = {int(e % ne[0]), int((e / ne[0]) % ne[1]), int(e / (int64_t(ne[0]) * ne[1]))};
-        R others = 0;
-        for (int l = 0; l < d; ++l)
-          if (l != j) others += m[l][ei[l]];
-        R t = L[size_t(e) * (d + 1) + d] - others;  // c_tau equation
-        for (int k = 0; k < d; ++k) {
-          if (k == j) continue;
-          t += L[size_t(e) * (d + 1) + k] - o[k][ei[k]] - (others - m[k][ei[k]]);
-        }
-        acc[j][ei[j]] += t;
-      }
-      const R cnt = R(NE / ne[j]) * R(d);  // equations per value: c_tau + (d - 1) c_k
+    for (int j = 0; j < d; ++j) {  // m_j: the c_tau equation and the c_k equations, k != j
+      const R cnt = R(NE / ne[j]);
       for (int v = 0; v < ne[j]; ++v) {
-        const R nv = acc[j][v] / cnt;
+        R t = Am[d][j][v];  // c_tau: L_tau - sum_{l != j} m_l
+        for (int l = 0; l < d; ++l)
+          if (l != j) t -= cnt / ne[l] * sum(m[l]);
+        for (int k = 0; k < d; ++k) {  // c_k: L_k - o_k - sum_{l != j, k} m_l
+          if (k == j) continue;
+          t += Am[k][j][v] - cnt / ne[k] * sum(o[k]);
+          for (int l = 0; l < d; ++l)
+            if (l != j && l != k) t -= cnt / ne[l] * sum(m[l]);
+        }
+        const R nv = t / (cnt * R(d));
         change = std::max(change, std::fabs(nv - m[j][v]));
         m[j][v] = nv;
       }
     }
     for (int k = 0; k < d; ++k) {  // o_k: only the c_k equation
-      acc[k].assign(ne[k], 0);
-      for (int64_t e = 0; e < NE; ++e) {
-        const int ei[3] = {int(e % ne[0]), int((e / ne[0]) % ne[1]), int(e / (int64_t(ne[0]) * ne[1]))};
-        R others = 0;
-        for (int l = 0; l < d; ++l)
-          if (l != k) others += m[l][ei[l]];
-        acc[k][ei[k]] += L[size_t(e) * (d + 1) + k] - others;
-      }
       const R cnt = R(NE / ne[k]);
       for (int v = 0; v < ne[k]; ++v) {
-        const R nv = acc[k][v] / cnt;
+        R t = Am[k][k][v];
+        for (int l = 0; l < d; ++l)
+          if (l != k) t -= cnt / ne[l] * sum(m[l]);
+        const R nv = t / cnt;
         change = std::max(change, std::fabs(nv - o[k][v]));
         o[k][v] = nv;
       }
