@@ -161,6 +161,36 @@ def oracle_sample(cfg_id, seconds_min=10.0, max_reps=8):
     return N / dt, sample, cores
 
 
+def oracle_extras():
+    """SURVEY 8(d) "Oracle timing": the oracle fd_apply on one thread (the paper's
+    single-thread discipline, PAPER.md 1106) on the same bounded sample as cpu_baseline, and
+    oracle PCG solves: config 2 in full (kind 0) and config 5 p = 2 on its spatial grid with
+    the time direction truncated to 8 elements (per-iteration time; the full solve would take
+    minutes on the host).  A reported baseline, not the target."""
+    from threadpoolctl import threadpool_limits
+    from oracle import univariate as uv, fd, operator as op, rhs as orhs, pcg as opcg
+    out = {}
+    with threadpool_limits(limits=1):
+        v, sample, _ = oracle_sample(4, seconds_min=5.0, max_reps=2)
+    out["oracle_fd_1thread"] = {"value": v, "unit": "DOF/s", "cores": 1, "sample": sample}
+    for cfg, p, n_el_t, kind in ((2, 3, 64, 0), (5, 2, 8, 1)):
+        d, n_el = synth.CONFIGS[cfg]["d"], synth.CONFIGS[cfg]["n_el"]
+        space = [uv.space_factors(n_el, p)] * d
+        tf = uv.time_factors(n_el_t, p)
+        fdd = fd.setup(space, tf)
+        b = orhs.rhs(kind, [space[0]["knots"]] * d, p, tf["knots"], p)
+        t0 = time.perf_counter()
+        _, it, ok, _ = opcg.pcg(lambda x: op.apply_A(x, space, tf), lambda r: fd.fd_apply(r, fdd), b,
+                                max_iter=1000 if cfg == 2 else 3)
+        dt = time.perf_counter() - t0
+        out[f"oracle_pcg_config{cfg}"] = {
+            "N": int(b.size), "iters": it, "solve_s": dt, "s_per_iter": dt / max(it, 1),
+            "cores": len(os.sched_getaffinity(0)),
+            "sample": ("full config 2, kind 0" if cfg == 2 else
+                       f"config 5 p = 2 spatial grid, time truncated to n_el_t = {n_el_t}, first 3 iterations")}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the oracle, as it stands, on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -307,6 +337,10 @@ def main():
         cpu_val, cpu_sample, cores = (None, "skipped", None)
         if world == 1 and not args.no_extras:
             cpu_val, cpu_sample, cores = oracle_sample(args.config)
+            try:
+                extras["oracle_timing"] = oracle_extras()
+            except Exception as exc:  # a baseline only: never fail the bench line on it
+                extras["oracle_timing"] = {"error": repr(exc)[:200]}
         line = {
             "metric": "fd_apply DOF/s (fp64)",
             "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
