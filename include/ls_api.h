@@ -372,6 +372,10 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * (their shared-memory staging of U / lambda overlaps the previous kernel's tail; default),
  * 0 = plain stream order. */
 #define LS_TUNE_PDL 6
+/* LS_TUNE_FD_TAIL: 1 = when n = 8 m + 1 or 8 m + 2 in an odd k-step bucket (e.g. n = 65, 66),
+ * the shared-memory FD kernel computes the last one or two output rows with DFMAs instead of
+ * a 7/8- or 3/4-padded DMMA m-tile (default), 0 = all rows on DMMAs. */
+#define LS_TUNE_FD_TAIL 7
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

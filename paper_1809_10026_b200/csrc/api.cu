@@ -60,6 +60,7 @@ struct ls_ctx {
   int num_sms = 148;
   int64_t launches = 0;
   int fd_variant = 0;  // ls_tune knob LS_TUNE_FD_KERNEL: 0 auto, 1 smem-staged (v2/pp), 2 register-direct
+  int fd_tail = 1;     // ls_tune knob LS_TUNE_FD_TAIL: DFMA tail rows in the ping-pong FD kernel
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
   // matvec v2: Toeplitz stencil + boundary corrections per band matrix (matvec2_kernels.cuh)
   struct Split {
@@ -219,11 +220,23 @@ static int launch_mode_pp(ls_ctx* ctx, const ModeArgs& a0) {
 }
 
 // ping-pong kernel: SPS stages per warp set (buckets A-C)
+template <int KS, int NT, int SPS, int TAIL>
+static int launch_mode_ks_t(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
+  if (mode1) return launch_mode_pp<PPCfg<KS, NT, true, false, SPS, TAIL>>(ctx, a);
+  if (scale) return launch_mode_pp<PPCfg<KS, NT, false, true, SPS, TAIL>>(ctx, a);
+  return launch_mode_pp<PPCfg<KS, NT, false, false, SPS, TAIL>>(ctx, a);
+}
+
 template <int KS, int NT, int SPS>
 static int launch_mode_ks(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
-  if (mode1) return launch_mode_pp<PPCfg<KS, NT, true, false, SPS>>(ctx, a);
-  if (scale) return launch_mode_pp<PPCfg<KS, NT, false, true, SPS>>(ctx, a);
-  return launch_mode_pp<PPCfg<KS, NT, false, false, SPS>>(ctx, a);
+  // odd k-step buckets: n = 8 (MTILES - 1) + 1 or + 2 (e.g. 65, 66 in bucket 17) leaves 1-2
+  // valid rows in the last m-tile; those rows go to DFMAs (compute_tile_tail)
+  if constexpr ((KS & 1) != 0) {
+    const int tail = a.n - 8 * ((KS + 1) / 2 - 1);
+    if (ctx->fd_tail && tail == 1) return launch_mode_ks_t<KS, NT, SPS, 1>(ctx, a, mode1, scale);
+    if (ctx->fd_tail && tail == 2) return launch_mode_ks_t<KS, NT, SPS, 2>(ctx, a, mode1, scale);
+  }
+  return launch_mode_ks_t<KS, NT, SPS, 0>(ctx, a, mode1, scale);
 }
 
 // balanced m-half kernel (bucket D, n <= 136: W fills 148 KB of shared memory, one tile
@@ -1825,6 +1838,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       if (Q % 4 != 0) return LS_ENOTSUP;  // the scattering epilogue is a FAST-path variant
       return ctx->comm->setup_fused(ctx->tmp[1], ctx->tmp[0]);
     }
+    case LS_TUNE_FD_TAIL:
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->fd_tail = value;
+      return LS_OK;
     case LS_TUNE_PDL:  // process-wide: programmatic dependent launch of the FD mode kernels
       if (value != 0 && value != 1) return LS_EINVAL;
       g_ls_pdl = value;

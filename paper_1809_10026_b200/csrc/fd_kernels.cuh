@@ -175,6 +175,88 @@ __device__ __forceinline__ void compute_tile(double (&acc)[MA][C::NT][2], const 
   }
 }
 
+// compute_tile with the last m-tile replaced by DFMAs for its TAIL (1 or 2) valid rows:
+// when n = 8 (MTILES - 1) + TAIL, that m-tile's DMMAs would be 7/8 or 3/4 padding.  Lane
+// (row r = lane/4, k = lane%4) holds B[4 ks + k][col r (+8 nt)]; it accumulates
+// sum_ks W[8 MC + t][4 ks + k] B[4 ks + k][col] for t < TAIL, and the four lanes of a quad
+// are summed by two shuffles: tacc[t][nt] = D[8 MC + t][col0 + 8 nt] in every lane of the quad.
+template <class C, int MC, int TAIL>
+__device__ __forceinline__ void compute_tile_tail(double (&acc)[C::MTILES][C::NT][2], double (&tacc)[2][C::NT],
+                                                  const double* wsm, const double* t, int grp, int lane) {
+#pragma unroll
+  for (int mt = 0; mt < C::MTILES; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) tacc[r][nt] = 0.0;
+  const double* wl = wsm + lane * 2;
+  const int col0 = grp * C::NT * 8 + (lane >> 2);
+  const double* tb = C::MODE1 ? (t + col0 * C::SK + (lane & 3)) : (t + (lane & 3) * C::SN + col0);
+  auto bfrag = [&](int ks, int nt) -> double {
+    return C::MODE1 ? tb[nt * 8 * C::SK + ks * 4] : tb[ks * 4 * C::SN + nt * 8];
+  };
+  auto apair = [&](int mt, int ksp) -> double2 {
+    return *reinterpret_cast<const double2*>(wl + (mt * C::KSP + ksp) * 64);
+  };
+  auto tpair = [&](int r, int ksp) -> double2 {  // W[8 MC + r][4 (2 ksp) + k], W[..][4 (2 ksp + 1) + k]
+    return *reinterpret_cast<const double2*>(wsm + ((MC * C::KSP + ksp) * 32 + r * 4 + (lane & 3)) * 2);
+  };
+  double2 af[2][MC];
+  double2 tw[2][TAIL];
+  double bf[2][2][C::NT];
+#pragma unroll
+  for (int mt = 0; mt < MC; ++mt) af[0][mt] = apair(mt, 0);
+#pragma unroll
+  for (int r = 0; r < TAIL; ++r) tw[0][r] = tpair(r, 0);
+#pragma unroll
+  for (int nt = 0; nt < C::NT; ++nt) {
+    bf[0][0][nt] = bfrag(0, nt);
+    bf[0][1][nt] = (1 < C::KS) ? bfrag(1, nt) : 0.0;
+  }
+#pragma unroll
+  for (int ksp = 0; ksp < C::KSP; ++ksp) {
+    const int cur = ksp & 1, nxt = cur ^ 1;
+    if (ksp + 1 < C::KSP) {
+#pragma unroll
+      for (int mt = 0; mt < MC; ++mt) af[nxt][mt] = apair(mt, ksp + 1);
+#pragma unroll
+      for (int r = 0; r < TAIL; ++r) tw[nxt][r] = tpair(r, ksp + 1);
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) {
+        bf[nxt][0][nt] = bfrag(2 * ksp + 2, nt);
+        bf[nxt][1][nt] = (2 * ksp + 3 < C::KS) ? bfrag(2 * ksp + 3, nt) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MC; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].x, bf[cur][0][nt]);
+#pragma unroll
+    for (int r = 0; r < TAIL; ++r)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt) tacc[r][nt] = fma(tw[cur][r].x, bf[cur][0][nt], tacc[r][nt]);
+    if (2 * ksp + 1 < C::KS) {
+#pragma unroll
+      for (int mt = 0; mt < MC; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].y, bf[cur][1][nt]);
+#pragma unroll
+      for (int r = 0; r < TAIL; ++r)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) tacc[r][nt] = fma(tw[cur][r].y, bf[cur][1][nt], tacc[r][nt]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < TAIL; ++r)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      tacc[r][nt] += __shfl_xor_sync(0xffffffffu, tacc[r][nt], 1);
+      tacc[r][nt] += __shfl_xor_sync(0xffffffffu, tacc[r][nt], 2);
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
   extern __shared__ __align__(16) double smem[];
@@ -362,9 +444,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) fd_mode_kernel(ModeArgs args) {
 // n-tiles (acc[MTILES][NT]); a set's 4 warps cover the tile's 4 n-tile groups.
 // Stage s of the ring belongs to set s % 2 (SPS stages per set).
 // =====================================================================================
-template <int KS_, int NT_, bool MODE1_, bool SCALE_, int SPS_>
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, int SPS_, int TAIL_ = 0>
 struct PPCfg {
   static constexpr int KS = KS_, NT = NT_, SPS = SPS_;
+  static constexpr int TAIL = TAIL_;  // 0, or the 1-2 rows of the last m-tile done by DFMAs
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_;
   static constexpr int THREADS = 256, SET_THREADS = 128;
   static constexpr int NSTAGE = 2 * SPS;
@@ -522,7 +605,12 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
       }
     }
     double acc[C::MTILES][C::NT][2];
-    compute_tile<C, C::MTILES, C::MTILES>(acc, wsm + lane * 2, t, grp, lane);
+    double tacc[2][C::NT];
+    constexpr int MCD = C::MTILES - (C::TAIL ? 1 : 0);  // m-tiles on the tensor pipe
+    if constexpr (C::TAIL > 0)
+      compute_tile_tail<C, MCD, C::TAIL>(acc, tacc, wsm, t, grp, lane);
+    else
+      compute_tile<C, C::MTILES, C::MTILES>(acc, wsm + lane * 2, t, grp, lane);
     // hand the tensor pipes to the other set if it has a tile for this turn
     if ((set == 0 && j < other) || (set == 1 && j + 1 < other)) named_arrive(BAR_OTHER_TURN, 256);
     named_sync(BAR_SET, 128);                        // all 4 warps done reading the stage
@@ -558,7 +646,7 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
         lc1 = lcp[C::SCALE ? nt : 0][1];
       }
 #pragma unroll
-      for (int mt = 0; mt < C::MTILES; ++mt) {
+      for (int mt = 0; mt < MCD; ++mt) {
         const int a = mt * 8 + (lane >> 2);
         if (a < n) {
           double v0 = acc[mt][nt][0], v1 = acc[mt][nt][1];
@@ -572,6 +660,25 @@ __global__ void __launch_bounds__(256, 1) fd_mode_pp_kernel(ModeArgs args) {
           } else {
             args.Y[base + off] = v0;
             if (two) args.Y[base2 + off] = v1;
+          }
+        }
+      }
+    }
+    if constexpr (C::TAIL > 0) {  // rows 8 MCD .. 8 MCD + TAIL - 1: lane k = lane % 4 < TAIL stores row 8 MCD + k
+      const int r = lane & 3;
+      if (r < C::TAIL) {
+        const int a = 8 * MCD + r;
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) {
+          const uint32_t c = c0 + grp * C::NT * 8 + nt * 8 + (lane >> 2);
+          if (c >= ncols || a >= n) continue;
+          double v = (r == 0) ? tacc[0][nt] : tacc[C::TAIL > 1 ? 1 : 0][nt];
+          if (C::SCALE) v *= fast_rcp(__ldg(args.lam_a + a) + __ldg(args.lam_c + c));
+          if (C::MODE1) {
+            args.Y[size_t(c) * n + a] = v;
+          } else {
+            const uint32_t p = c / Q, q = c - p * Q;
+            args.Y[size_t(p) * n * Q + size_t(a) * Q + q] = v;
           }
         }
       }

@@ -581,3 +581,23 @@ def test_pcg_rejects_aliasing(torch_cuda):
     b = ctx.rhs(1)
     with pytest.raises(ls.LSError):
         ctx.pcg(b, x=b)
+
+
+@pytest.mark.parametrize("d,p,n_elems", [(2, 3, [64, 63, 64]), (3, 2, [15, 16, 17, 17]), (1, 4, [95, 94]),
+                                         (3, 3, [64, 8, 9, 63])])
+def test_fd_tail_rows(torch_cuda, d, p, n_elems):
+    """n = 8 m + 1 or 8 m + 2 in an odd k-step bucket (65, 66 in bucket 17; 17, 18 in bucket
+    5; 97 in bucket 25): the last one or two output rows computed with DFMAs
+    (LS_TUNE_FD_TAIL = 1, default) against the oracle and against all-DMMA tiles."""
+    torch = torch_cuda
+    ctx = _ctx(d, p, n_elems)
+    space, tf, fdd = _oracle(d, p, n_elems)
+    r = synth.residual(ctx.shape, 11)
+    rg = torch.from_numpy(r).cuda()
+    z1 = ctx.fd_apply(rg).cpu().numpy()
+    ctx.tune(7, 0)
+    z0 = ctx.fd_apply(rg).cpu().numpy()
+    ctx.tune(7, 1)
+    z_ref = fd.fd_apply(r, fdd)
+    assert _rel(z1, z_ref) <= TOL
+    assert _rel(z1, z0) <= 1e-13
