@@ -33,7 +33,9 @@
  * ERRORS: every int-returning call returns LS_OK (0) or one of the codes
  * below; ls_strerror maps a code to a static string.  A failed call leaves
  * the output unspecified and the context usable unless LS_ECUDA is returned.
- * Not thread-safe per context; one context per device.
+ * Not thread-safe per context; one context per device, and one device per process (the
+ * kernels' shared-memory attributes are set once per process, on the first launch; the
+ * multi-GPU path runs one process per GPU).
  */
 #ifndef LS_API_H
 #define LS_API_H
