@@ -304,3 +304,25 @@ def test_geo_table2_iterations(torch_cuda, golden_loader, ne, p):
         _, st = ctx.pcg(ctx.rhs(3), tol=1e-8)
         ref = tab[key][str(ne)][str(p)]
         assert st["status"] == 0 and abs(st["iters"] - ref) <= 0.2 * ref, (key, st["iters"], ref)
+
+
+@pytest.mark.parametrize("n_el,p", [(32, 3), (64, 2)])
+def test_geo_fullsize_properties(torch_cuda, n_el, p):
+    """At the bench sizes (revolved quarter annulus, beyond the oracle's reach): A and
+    (P^G)^{-1} are symmetric (x.Ay = y.Ax) and positive, on seeded inputs, in the launch
+    configuration bench.py times; the PCG solve of the kind-3 forcing reaches its true
+    residual."""
+    torch = torch_cuda
+    import paper_1809_10026_b200 as ls
+    ctx = ls.Context(3, p, [n_el] * 4, geometry=synth.revolved_quarter_annulus(), precond=ls.LS_PRECOND_PG)
+    x = torch.from_numpy(synth.residual(ctx.shape, 1)).cuda()
+    y = torch.from_numpy(synth.residual(ctx.shape, 2)).cuda()
+    Ax, Ay = ctx.matvec(x), ctx.matvec(y)
+    xAy, yAx = float((x * Ay).sum()), float((y * Ax).sum())
+    assert abs(xAy - yAx) <= 1e-12 * float(x.norm() * Ay.norm())
+    assert float((x * Ax).sum()) > 0
+    Px, Py = ctx.fd_apply(x), ctx.fd_apply(y)
+    assert abs(float((x * Py).sum()) - float((y * Px).sum())) <= 1e-10 * float(x.norm() * Py.norm())
+    assert float((x * Px).sum()) > 0
+    _, st = ctx.pcg(ctx.rhs(3), tol=1e-8)
+    assert st["status"] == 0 and st["true_rel_res"] < 1e-7
