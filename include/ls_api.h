@@ -274,6 +274,18 @@ int ls_setup_geo_dist(int d, int p_s, int p_t, const int64_t* n_elems, const ls_
                       int rank, int world, const void* nccl_unique_id, ls_ctx** out);
 
 /*
+ * ls_pg_factors -- host only (no device work): the P^G setup of ls_setup_geo for a map and
+ * spatial mesh, for inspection and CPU tests.  mu, omega: per-element univariate factors,
+ * directions concatenated (sum_k n_elems[k] values each; defined up to the gauge
+ * mu_j -> a_j mu_j, omega_k -> omega_k a_k / prod_j a_j of reading c21, which leaves every
+ * product and Pbar^G unchanged); Mw, Jw: the weighted constrained factors M^G_k, J^G_k
+ * (row-major n_k x n_k, n_k = n_elems[k] + p_s - 2, concatenated); fit_rel_res as
+ * ls_geo_info.  Errors: LS_EINVAL (arguments, invalid or singular map).
+ */
+int ls_pg_factors(const ls_geometry* geo, int d, int p_s, const int64_t* n_elems, double* mu, double* omega,
+                  double* Mw, double* Jw, double* fit_rel_res);
+
+/*
  * ls_geo_info -- out2[0] = max relative residual of the separable fit of c_tau, c_k at
  * the element midpoints (0 for LS_PRECOND_P or an exactly separable map), out2[1] =
  * number of stencil entries per spatial row ((2 p_s + 1)^d).  Errors: LS_EINVAL,

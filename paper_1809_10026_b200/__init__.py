@@ -32,7 +32,7 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
-            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist"]
+            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist", "ls_pg_factors"]
 
 LS_PRECOND_P, LS_PRECOND_PG = 0, 1
 
@@ -94,6 +94,8 @@ def load_library(path=LIB_PATH):
         "ls_setup_geo": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p, ctypes.POINTER(Geometry),
                                         ctypes.c_int, ctypes.POINTER(vp)]),
         "ls_geo_info": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_double)]),
+        "ls_pg_factors": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, i64p, dp, dp, dp,
+                                         dp, ctypes.POINTER(ctypes.c_double)]),
         "ls_setup_geo_dist": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, i64p,
                                              ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_char_p, ctypes.POINTER(vp)]),
@@ -179,6 +181,47 @@ def halo_plan(n_t, world, rank, p):
     return tuple(x.value for x in v)
 
 
+def _geometry_struct(geometry, d):
+    """ls_geometry from the dict of synth.GEOMETRIES (the numpy arrays it points to are
+    returned too: keep them alive while the struct is used)."""
+    g = Geometry()
+    keep = []
+    for k in range(d):
+        kn = np.ascontiguousarray(geometry["knots"][k], dtype=np.float64)
+        keep.append(kn)
+        g.degree[k] = int(geometry["degrees"][k])
+        g.n_knots[k] = kn.size
+        g.knots[k] = kn.ctypes.data
+    ctrl = np.ascontiguousarray(geometry["ctrl"], dtype=np.float64)
+    keep.append(ctrl)
+    g.ctrl = ctrl.ctypes.data
+    if geometry.get("weights") is not None:
+        w = np.ascontiguousarray(geometry["weights"], dtype=np.float64)
+        keep.append(w)
+        g.weights = w.ctypes.data
+    return g, keep
+
+
+def pg_factors(geometry, p_s, n_elems):
+    """ls_pg_factors (host only): (mu, omega, Mw, Jw, fit_rel_res) per direction."""
+    d = geometry["d"]
+    g, keep = _geometry_struct(geometry, d)
+    ne = [int(v) for v in n_elems[:d]]
+    nn = [v + p_s - 2 for v in ne]
+    mu, om = np.zeros(sum(ne)), np.zeros(sum(ne))
+    Mw, Jw = np.zeros(sum(v * v for v in nn)), np.zeros(sum(v * v for v in nn))
+    res = ctypes.c_double()
+    vp = lambda a: ctypes.c_void_p(a.ctypes.data)
+    _check(load_library().ls_pg_factors(ctypes.byref(g), d, int(p_s), (ctypes.c_int64 * d)(*ne), vp(mu), vp(om),
+                                         vp(Mw), vp(Jw), ctypes.byref(res)), "ls_pg_factors")
+    del keep
+    splits = np.cumsum(ne)[:-1]
+    msplit = np.cumsum([v * v for v in nn])[:-1]
+    return (np.split(mu, splits), np.split(om, splits),
+            [m.reshape(n, n) for m, n in zip(np.split(Mw, msplit), nn)],
+            [j.reshape(n, n) for j, n in zip(np.split(Jw, msplit), nn)], res.value)
+
+
 def sizes(n_el, p):
     """(n_s, n_t) for n_el uniform elements (reading c1)."""
     return n_el + p - 2, n_el + p - 1
@@ -201,21 +244,7 @@ class Context:
         torch.cuda.init()
         ps, pt = (p, p) if isinstance(p, int) else (int(p[0]), int(p[1]))
         if geometry is not None:
-            g = Geometry()
-            keep = []
-            for k in range(d):
-                kn = np.ascontiguousarray(geometry["knots"][k], dtype=np.float64)
-                keep.append(kn)
-                g.degree[k] = int(geometry["degrees"][k])
-                g.n_knots[k] = kn.size
-                g.knots[k] = kn.ctypes.data
-            ctrl = np.ascontiguousarray(geometry["ctrl"], dtype=np.float64)
-            keep.append(ctrl)
-            g.ctrl = ctrl.ctypes.data
-            if geometry.get("weights") is not None:
-                w = np.ascontiguousarray(geometry["weights"], dtype=np.float64)
-                keep.append(w)
-                g.weights = w.ctypes.data
+            g, keep = _geometry_struct(geometry, d)
             _check(lib.ls_setup_geo_dist(d, ps, pt, ne, ctypes.byref(g), int(precond), int(rank), int(world),
                                          uid, ctypes.byref(h)), "ls_setup_geo_dist")
         elif world == 1:

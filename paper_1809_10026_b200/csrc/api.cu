@@ -669,6 +669,29 @@ extern "C" int ls_setup_geo_dist(int d, int p_s, int p_t, const int64_t* n_elems
   return LS_OK;
 }
 
+extern "C" int ls_pg_factors(const ls_geometry* geo, int d, int p_s, const int64_t* n_elems, double* mu,
+                             double* omega, double* Mw, double* Jw, double* fit_rel_res) {
+  if (!geo || d < 1 || d > 3 || p_s < 2 || !n_elems || !mu || !omega || !Mw || !Jw) return LS_EINVAL;
+  for (int k = 0; k < d; ++k)
+    if (n_elems[k] < 1 || n_elems[k] > 100000) return LS_EINVAL;
+  GeoMap g;
+  LS_CHECK(geo_copy(geo, d, g));
+  std::vector<double> m[3], o[3];
+  LS_CHECK(pg_weights(g, n_elems, m, o, fit_rel_res));
+  size_t off = 0, moff = 0;
+  for (int k = 0; k < d; ++k) {
+    std::copy(m[k].begin(), m[k].end(), mu + off);
+    std::copy(o[k].begin(), o[k].end(), omega + off);
+    off += m[k].size();
+    std::vector<double> M, J;
+    weighted_space_factors(int(n_elems[k]), p_s, m[k], o[k], M, J);
+    std::copy(M.begin(), M.end(), Mw + moff);
+    std::copy(J.begin(), J.end(), Jw + moff);
+    moff += M.size();
+  }
+  return LS_OK;
+}
+
 extern "C" int ls_geo_info(const ls_ctx* ctx, double* out2) {
   if (!ctx || !out2) return LS_EINVAL;
   if (!ctx->geo) return LS_ENOTSUP;

@@ -136,6 +136,7 @@ int pg_weights(const GeoMap& g, const int64_t* n_el, std::vector<double> mu[3], 
   const int64_t NE = int64_t(ne[0]) * ne[1] * ne[2];
   // logarithms of c_tau and c_k (T = 1; reading c20 for c_k)
   std::vector<R> L(size_t(NE) * (d + 1));
+  int signs = 0;
   for (int64_t e = 0; e < NE; ++e) {
     const int ei[3] = {int(e % ne[0]), int((e / ne[0]) % ne[1]), int(e / (int64_t(ne[0]) * ne[1]))};
     const R* v0[3] = {nullptr, nullptr, nullptr};
@@ -146,8 +147,11 @@ int pg_weights(const GeoMap& g, const int64_t* n_el, std::vector<double> mu[3], 
     }
     R x[3], jac[9], inv[9];
     tensor_eval(g, v0, v1, x, jac);
-    const R det = std::fabs(inv_det(d, jac, inv));
+    const R sdet = inv_det(d, jac, inv);
+    const R det = std::fabs(sdet);
     if (!(det > 0) || !std::isfinite(double(det))) return LS_EINVAL;  // singular map
+    signs |= sdet > 0 ? 1 : 2;
+    if (signs == 3) return LS_EINVAL;  // det J_F changes sign: a folded map (Assumption 4)
     L[size_t(e) * (d + 1) + d] = std::log(det);
     for (int k = 0; k < d; ++k) {
       R s = 0;
