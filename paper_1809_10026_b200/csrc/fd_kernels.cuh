@@ -229,10 +229,36 @@ __device__ __forceinline__ void compute_tile_tail(double (&acc)[C::MTILES][C::NT
         bf[nxt][1][nt] = (2 * ksp + 3 < C::KS) ? bfrag(2 * ksp + 3, nt) : 0.0;
       }
     }
+    if (ksp == C::KSP - 1 && (C::KS & 1)) {
+      // the last k-step holds TAIL (= n - 4 (KS - 1)) valid columns of W: a rank-1 / rank-2
+      // DFMA update of this lane's D entries instead of a 3/4- or 1/2-padded DMMA k-step
+      const int kb = 4 * (C::KS - 1);
 #pragma unroll
-    for (int mt = 0; mt < MC; ++mt)
+      for (int kv = 0; kv < TAIL; ++kv) {
+        double xv[C::NT][2];
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].x, bf[cur][0][nt]);
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = grp * C::NT * 8 + nt * 8 + 2 * (lane & 3) + h;
+            xv[nt][h] = C::MODE1 ? t[col * C::SK + kb + kv] : t[(kb + kv) * C::SN + col];
+          }
+#pragma unroll
+        for (int mt = 0; mt < MC; ++mt) {
+          const double w = wsm[((mt * C::KSP + ksp) * 32 + (lane >> 2) * 4 + kv) * 2];
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt) {
+            acc[mt][nt][0] = fma(w, xv[nt][0], acc[mt][nt][0]);
+            acc[mt][nt][1] = fma(w, xv[nt][1], acc[mt][nt][1]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MC; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) dmma_8x8x4(acc[mt][nt], af[cur][mt].x, bf[cur][0][nt]);
+    }
 #pragma unroll
     for (int r = 0; r < TAIL; ++r)
 #pragma unroll
