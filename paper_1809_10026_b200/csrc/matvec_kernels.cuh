@@ -63,7 +63,9 @@ struct BandCfg {
 
 // KIND 1 (directions >= 2) and KIND 2 (time).
 template <int P, int RB, int KIND, int NSTAGE, int NWARPS>
-__global__ void __launch_bounds__(32 * NWARPS, 1) band_tile_kernel(BandArgs a) {
+// two CTAs per SM for RB <= 9 (<= 128 registers: config 3 matvec 0.81 -> 0.75 ms, n_el = 48
+// 0.31 -> 0.28 ms); larger row blocks keep one (they would spill)
+__global__ void __launch_bounds__(32 * NWARPS, (RB <= 9 ? 2 : 1)) band_tile_kernel(BandArgs a) {
   pdl_wait();
   using C = BandCfg<P, RB, KIND, NSTAGE, NWARPS>;
   constexpr int W = C::W;
