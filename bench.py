@@ -315,7 +315,7 @@ def main():
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_bytes = int(pin_r.numel() * 8)
+    e2e_bytes = int(8 * w["N"])  # every rank copies its slab: the whole job moves N doubles each way
 
     # roofline of the dominant kernel (fd_mode_kernel): algorithmic flops / device time
     achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
