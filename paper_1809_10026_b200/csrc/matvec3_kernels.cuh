@@ -70,15 +70,25 @@ struct MV3Geom {
   static constexpr int S0 = (P % 4) ? (P % 4) - 8 : 0;
   static constexpr int OFF = (P - S0) / 4;  // first k-step of m-tile mt: 2mt - OFF
   static constexpr int NKB = 2 + (P + 1) / 2;
-  // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 2 for 2 or 3
-  // (the 2-input pass runs 2 CTAs per SM within 128 registers)
+  // prefetch depth (m-tiles ahead) by register budget: 4 for 1 ring input, 2 for 2 (the
+  // 2-input pass runs 2 CTAs per SM within 128 registers), 3 for 3 inputs up to p = 6 and
+  // 2 above (tools/mv3_ab.sh: config 4 11.96 -> 11.87 ms, config 5 p = 4 3.43 -> 3.34 ms;
+  // p = 8 is 0.8 % slower at depth 3)
+#ifndef MV3_AHEAD1
+#define MV3_AHEAD1 4
+#endif
 #ifndef MV3_AHEAD2
-#define MV3_AHEAD2 2
+#define MV3_AHEAD2 1
 #endif
 #ifndef MV3_AHEAD3
-#define MV3_AHEAD3 2
+#define MV3_AHEAD3 4
 #endif
-  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? 4 : MV3IO<KIND>::NIN == 2 ? MV3_AHEAD2 : MV3_AHEAD3;
+#ifndef MV3_AHEAD3_HI
+#define MV3_AHEAD3_HI 2
+#endif
+  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? MV3_AHEAD1
+                               : MV3IO<KIND>::NIN == 2 ? MV3_AHEAD2
+                               : (P <= 6 ? MV3_AHEAD3 : MV3_AHEAD3_HI);
   static constexpr int RING = NKB + 2 * AHEAD + (NKB & 1);  // even: static slots per RING/2 m-tiles
   static constexpr int G = RING / 2;  // m-tiles per unrolled group
 };
