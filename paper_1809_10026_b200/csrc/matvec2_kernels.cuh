@@ -200,8 +200,17 @@ __global__ void __launch_bounds__(32 * MV_CY) mv_dir_kernel(const __grid_constan
 // back through shared memory for coalesced stores.  !PHASE1 (d = 2): the work item
 // is 32 consecutive rows of [rows][n1], phase 1 only copies A, B, C into shared.
 // --------------------------------------------------------------------------------------
-constexpr int MV_PLANE_THREADS = 288;  // 9 warps
-constexpr int MV_PLANE_ROWS = 16;      // rows per work item
+#ifndef MV_PLANE_WARPS
+#define MV_PLANE_WARPS 6
+#endif
+#ifndef MV_PLANE_CTAS
+#define MV_PLANE_CTAS 4
+#endif
+#ifndef MV_PLANE_ROWS_
+#define MV_PLANE_ROWS_ 16
+#endif
+constexpr int MV_PLANE_THREADS = 32 * MV_PLANE_WARPS;
+constexpr int MV_PLANE_ROWS = MV_PLANE_ROWS_;  // rows per work item
 
 __host__ __device__ inline int mv_plane_pitch(int n1, int P) {
   const int w = n1 + 2 * P;
@@ -209,7 +218,7 @@ __host__ __device__ inline int mv_plane_pitch(int n1, int P) {
 }
 
 template <int P, int R, bool PHASE1>
-__global__ void __launch_bounds__(MV_PLANE_THREADS, 2) mv_plane_kernel(const __grid_constant__ MVArgs a) {
+__global__ void __launch_bounds__(MV_PLANE_THREADS, MV_PLANE_CTAS) mv_plane_kernel(const __grid_constant__ MVArgs a) {
   pdl_wait();
   extern __shared__ __align__(16) double sm[];
   const int n1 = a.n1, n2 = a.n;
