@@ -877,8 +877,19 @@ struct FragGeom {
   int64_t NL, Ns;
 };
 
+// CTAs per SM (register cap): 4 (128 registers) for up to 3 time blocks per warp, where
+// that fits without spills, else 3
+#ifndef GEO_DMMA_CTAS
+#define GEO_DMMA_CTAS 3
+#endif
+#ifndef GEO_DMMA_CTAS_SMALL
+#define GEO_DMMA_CTAS_SMALL 4
+#endif
+#ifndef GEO_TBM_MAX
+#define GEO_TBM_MAX 5
+#endif
 template <int TBM, int KS>
-__global__ void __launch_bounds__(128, 3) geo_dmma_kernel(const double* __restrict__ st,
+__global__ void __launch_bounds__(128, (TBM <= 3 ? GEO_DMMA_CTAS_SMALL : GEO_DMMA_CTAS)) geo_dmma_kernel(const double* __restrict__ st,
                                                          const double* __restrict__ t1,
                                                          const double* __restrict__ t2,
                                                          const double* __restrict__ xl, double* __restrict__ y,
@@ -1003,8 +1014,8 @@ int geo_matvec(const GeoDev& gd, const double* bKt, const double* bMt, int nt_gl
     const FragGeom g = frag_geom(gd);
     const int ntb = (nt + 7) / 8;
     // time blocks per warp: the largest of 5..2 with the fewest idle blocks in the last chunk
-    int tbm = 5, waste = 1 << 30;
-    for (int c = 5; c >= 2; --c) {
+    int tbm = GEO_TBM_MAX, waste = 1 << 30;
+    for (int c = GEO_TBM_MAX; c >= 2; --c) {
       const int wst = (ntb + c - 1) / c * c - ntb;
       if (wst < waste) {
         waste = wst;
