@@ -1186,7 +1186,7 @@ static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
       items = (uint64_t(a.ncols) + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS;
     }
     pl.smem_plane = size_t(3) * MV_PLANE_ROWS * mv_plane_pitch(ctx->n[0], P) * sizeof(double);
-    const int per_sm = int(std::max<size_t>(1, std::min<size_t>(MV_PLANE_CTAS, (227 * 1024) / pl.smem_plane)));
+    const int per_sm = int(std::max<size_t>(1, std::min<size_t>(mv_plane_ctas(P), (227 * 1024) / pl.smem_plane)));
     pl.grid_plane = unsigned(std::min<uint64_t>(items, uint64_t(ctx->num_sms) * per_sm));
   }
   LS_CUDA(mv2_run(P, ctx->pt, pl, &ctx->launches));

@@ -200,17 +200,23 @@ __global__ void __launch_bounds__(32 * MV_CY) mv_dir_kernel(const __grid_constan
 // back through shared memory for coalesced stores.  !PHASE1 (d = 2): the work item
 // is 32 consecutive rows of [rows][n1], phase 1 only copies A, B, C into shared.
 // --------------------------------------------------------------------------------------
+// geometry (tools/mv2_ab.sh, config 5 p = 2): 8-row work items, 3 warps, 8 CTAs per SM
+// (80 registers; spills grow with P, so P > 3 keeps 4 CTAs)
 #ifndef MV_PLANE_WARPS
-#define MV_PLANE_WARPS 6
+#define MV_PLANE_WARPS 3
 #endif
 #ifndef MV_PLANE_CTAS
-#define MV_PLANE_CTAS 4
+#define MV_PLANE_CTAS 8
+#endif
+#ifndef MV_PLANE_CTAS_HI
+#define MV_PLANE_CTAS_HI 4
 #endif
 #ifndef MV_PLANE_ROWS_
-#define MV_PLANE_ROWS_ 16
+#define MV_PLANE_ROWS_ 8
 #endif
 constexpr int MV_PLANE_THREADS = 32 * MV_PLANE_WARPS;
 constexpr int MV_PLANE_ROWS = MV_PLANE_ROWS_;  // rows per work item
+__host__ __device__ constexpr int mv_plane_ctas(int P) { return P <= 3 ? MV_PLANE_CTAS : MV_PLANE_CTAS_HI; }
 
 __host__ __device__ inline int mv_plane_pitch(int n1, int P) {
   const int w = n1 + 2 * P;
@@ -218,7 +224,7 @@ __host__ __device__ inline int mv_plane_pitch(int n1, int P) {
 }
 
 template <int P, int R, bool PHASE1>
-__global__ void __launch_bounds__(MV_PLANE_THREADS, MV_PLANE_CTAS) mv_plane_kernel(const __grid_constant__ MVArgs a) {
+__global__ void __launch_bounds__(MV_PLANE_THREADS, mv_plane_ctas(P)) mv_plane_kernel(const __grid_constant__ MVArgs a) {
   pdl_wait();
   extern __shared__ __align__(16) double sm[];
   const int n1 = a.n1, n2 = a.n;
@@ -235,7 +241,9 @@ __global__ void __launch_bounds__(MV_PLANE_THREADS, MV_PLANE_CTAS) mv_plane_kern
   const int bpp = PHASE1 ? (n2 + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS : 1;  // blocks per plane
   const uint32_t nitems = PHASE1 ? a.ncols * uint32_t(bpp) : (a.ncols + MV_PLANE_ROWS - 1) / MV_PLANE_ROWS;
   // phase 2: thread = (row, segment of R direction-1 outputs)
-  const int prow = lane & (MV_PLANE_ROWS - 1);
+  static_assert(32 % MV_PLANE_ROWS == 0, "a warp covers whole row groups");
+  constexpr int SEGW = 32 / MV_PLANE_ROWS;  // segments per warp and phase-2 step
+  const int prow = lane % MV_PLANE_ROWS;
   const int nseg = (n1 + R - 1) / R;
   for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
     size_t row0;  // global row (of the [rows][n1] view) of local row 0
@@ -314,7 +322,7 @@ __global__ void __launch_bounds__(MV_PLANE_THREADS, MV_PLANE_CTAS) mv_plane_kern
     __syncthreads();
     // ---- phase 2: direction 1 along the shared rows; thread = (row, segment); outputs go
     //      straight to global memory (a thread's R outputs are contiguous)
-    for (int seg = warp * 2 + (lane >> 4); seg < nseg; seg += 2 * (MV_PLANE_THREADS / 32)) {
+    for (int seg = warp * SEGW + lane / MV_PLANE_ROWS; seg < nseg; seg += SEGW * (MV_PLANE_THREADS / 32)) {
       if (prow >= nr) continue;
       const int c0 = seg * R;
       const bool corr = c0 < a.r_lo1 || c0 + R > a.r_hi1;
