@@ -304,7 +304,12 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   const bool mode1 = (Q == 1) && !scale;  // the scaled (time) mode always uses the strided variant
   // auto (measured, tools/fd_variants.py): register-direct for n > 116 (config 4: 75% -> 86% of
   // the FP64 peak), smem-staged ping-pong / m-half kernels below (config 3: 56% vs 37%)
-  if (ctx->fd_variant == 2 || (ctx->fd_variant == 0 && (n + 3) / 4 >= 30)) return launch_mode_rd(ctx, a, mode1, scale);
+  // it also wins from n = 96 when the last m-tile has at most one padding row, i.e. when
+  // n % 8 <= 1 (tools/fdk_sel.py, config 5 p = 2, n = 96 / 97: 4.67 -> 4.45 ms; rd for n = 96
+  // only: 4.51 ms; p = 4 / 8, n = 98 / 99, 102 / 103: the smem-staged kernels stay 13 / 9 %
+  // faster)
+  const bool rd_auto = (n + 3) / 4 >= 30 || (n >= 96 && n % 8 <= 1);
+  if (ctx->fd_variant == 2 || (ctx->fd_variant == 0 && rd_auto)) return launch_mode_rd(ctx, a, mode1, scale);
   switch (round_ks((n + 3) / 4)) {
     KS_A(2) KS_A(4) KS_A(5) KS_A(8)
     KS_B(12) KS_B(16) KS_B(17) KS_B(18)
