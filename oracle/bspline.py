@@ -20,12 +20,16 @@ i.e. values at eta = 1 are the left limits.
 import numpy as np
 
 
-def open_uniform_knots(n_el, p):
+def open_uniform_knots(n_el, p, dtype=np.float64):
     """Open knot vector with n_el uniform elements on [0,1] (PAPER.md 144-147,
     1111-1112: h_s = h_t = h, n_el elements per parametric direction).
-    No repeated interior knots, so the space is C^{p-1} (k-method, PAPER.md 60-61)."""
-    interior = [i / n_el for i in range(1, n_el)]
-    return np.array([0.0] * (p + 1) + interior + [1.0] * (p + 1), dtype=np.float64)
+    No repeated interior knots, so the space is C^{p-1} (k-method, PAPER.md 60-61).
+    The knots are i / n_el computed in ``dtype`` (np.longdouble for the
+    extended-precision assembly of reading c17: fp64 knots are inexact when
+    n_el is not a power of two and perturb the factor matrices by up to
+    ~2.5e-14 relative at n_el = 130)."""
+    interior = [dtype(i) / dtype(n_el) for i in range(1, n_el)]
+    return np.array([dtype(0)] * (p + 1) + interior + [dtype(1)] * (p + 1), dtype=dtype)
 
 
 def n_functions(knots, p):

@@ -49,8 +49,9 @@ def space_factors(n_el, p, knots=None):
     """Space pencil matrices on the Dirichlet-constrained basis i = 2..m-1.
     Returns dict with M, K, J, G, each (n_s x n_s), n_s = n_el + p - 2."""
     if knots is None:
-        knots = open_uniform_knots(n_el, p)
+        knots = open_uniform_knots(n_el, p, np.longdouble)
     M, K, J, G = full_matrices(knots, p)
+    knots = np.asarray(knots, dtype=np.float64)
     s = slice(1, -1)
     return {"M": M[s, s], "K": K[s, s], "J": J[s, s], "G": G[s, s], "knots": knots}
 
@@ -60,8 +61,9 @@ def time_factors(n_el, p, T=1.0, knots=None):
     Returns dict with the parametric Kt_hat, Mt_hat (used by P) and the physical
     Kt, Mt, Wt (used by A), each (n_t x n_t), n_t = n_el + p - 1."""
     if knots is None:
-        knots = open_uniform_knots(n_el, p)
+        knots = open_uniform_knots(n_el, p, np.longdouble)
     M, K, _, _ = full_matrices(knots, p)
+    knots = np.asarray(knots, dtype=np.float64)
     bT = basis_values(knots, p, [1.0])[0]
     s = slice(1, None)
     Mh, Kh = M[s, s], K[s, s]

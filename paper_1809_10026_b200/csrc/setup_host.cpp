@@ -17,6 +17,18 @@ std::vector<double> open_uniform_knots(int n_el, int p) {
   return kn;
 }
 
+// The same knots i / n_el in 80-bit (reading c17): fp64 knots are inexact unless n_el is a
+// power of two and would perturb the assembled matrices by up to ~2.5e-14 relative
+// (n_el = 130; tests/test_oracle_highprec.py pins the assembly to the exact rationals).
+std::vector<long double> open_uniform_knots_ld(int n_el, int p) {
+  std::vector<long double> kn;
+  kn.reserve(n_el + 2 * p + 1);
+  for (int i = 0; i <= p; ++i) kn.push_back(0.0L);
+  for (int i = 1; i < n_el; ++i) kn.push_back((long double)i / (long double)n_el);
+  for (int i = 0; i <= p; ++i) kn.push_back(1.0L);
+  return kn;
+}
+
 void gauss_legendre(int q, std::vector<long double>& x, std::vector<long double>& w) {
   typedef long double R;
   x.assign(q, 0.0L);
@@ -53,9 +65,13 @@ static inline long double ratio(long double num, long double den) { return den =
 
 void bspline_eval(const std::vector<double>& kd, int p, long double x, long double* v0,
                   long double* v1, long double* v2) {
+  bspline_eval(std::vector<long double>(kd.begin(), kd.end()), p, x, v0, v1, v2);
+}
+
+void bspline_eval(const std::vector<long double>& kn, int p, long double x, long double* v0,
+                  long double* v1, long double* v2) {
   typedef long double R;
-  const int n0 = int(kd.size()) - 1;
-  std::vector<R> kn(kd.begin(), kd.end());
+  const int n0 = int(kn.size()) - 1;
   // N[q][i] for degrees 0..p (Cox-de Boor, PAPER.md 148-166)
   std::vector<std::vector<R>> N(p + 1);
   N[0].assign(n0, 0.0L);
@@ -93,7 +109,7 @@ void bspline_eval(const std::vector<double>& kd, int p, long double x, long doub
 // Dense unconstrained m x m matrices M = int b b, K = int b' b', J = int b'' b''
 // with q = p + 1 Gauss points per element (exact, reading c6), evaluated and summed
 // in 80-bit extended precision and rounded once to fp64 (reading c17).
-static void assemble_full(const std::vector<double>& kn, int p, std::vector<double>& Mo,
+static void assemble_full(const std::vector<long double>& kn, int p, std::vector<double>& Mo,
                           std::vector<double>& Ko, std::vector<double>& Jo) {
   typedef long double R;
   const int m = int(kn.size()) - p - 1;
@@ -130,7 +146,7 @@ static std::vector<double> slice(const std::vector<double>& A, int m, int lo, in
 }
 
 Factors space_factors(int n_el, int p) {
-  auto kn = open_uniform_knots(n_el, p);
+  auto kn = open_uniform_knots_ld(n_el, p);
   const int m = n_el + p;
   std::vector<double> M, K, J;
   assemble_full(kn, p, M, K, J);
@@ -143,7 +159,7 @@ Factors space_factors(int n_el, int p) {
 }
 
 Factors time_factors(int n_el, int p) {
-  auto kn = open_uniform_knots(n_el, p);
+  auto kn = open_uniform_knots_ld(n_el, p);
   const int m = n_el + p;
   std::vector<double> M, K, J;
   assemble_full(kn, p, M, K, J);
@@ -157,7 +173,7 @@ Factors time_factors(int n_el, int p) {
 void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<double>& i0,
                     std::vector<double>& i1, std::vector<double>& i2) {
   typedef long double R;
-  auto kn = open_uniform_knots(n_el, p);
+  auto kn = open_uniform_knots_ld(n_el, p);
   const int m = n_el + p;
   const int lo = 1, n = space ? m - 2 : m - 1;
   std::vector<R> a0(n, 0.0L), a1(n, 0.0L), a2(n, 0.0L);

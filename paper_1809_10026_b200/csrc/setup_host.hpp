@@ -9,6 +9,7 @@ namespace ls {
 
 // Open uniform knot vector on [0,1] with n_el elements (PAPER.md 144-147, 1111-1112).
 std::vector<double> open_uniform_knots(int n_el, int p);
+std::vector<long double> open_uniform_knots_ld(int n_el, int p);
 
 // q-point Gauss-Legendre nodes/weights on [-1,1] (Newton on the Legendre recurrence),
 // in 80-bit extended precision.
@@ -16,6 +17,8 @@ void gauss_legendre(int q, std::vector<long double>& x, std::vector<long double>
 
 // Values and first/second derivatives of all m = len(knots)-p-1 B-splines at x
 // (Cox-de Boor, PAPER.md 148-166; derivative recursion of de Boor), extended precision.
+void bspline_eval(const std::vector<long double>& knots, int p, long double x, long double* v0,
+                  long double* v1, long double* v2);
 void bspline_eval(const std::vector<double>& knots, int p, long double x, long double* v0,
                   long double* v1, long double* v2);
 
