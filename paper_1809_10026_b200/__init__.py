@@ -273,6 +273,15 @@ class Context:
             raise ValueError(f"{name} has {t.numel()} elements, expected {self.N}")
         return ctypes.c_void_p(t.data_ptr())
 
+    def _chk(self, t, name, need):
+        """Contiguous float64 CUDA tensor with at least ``need`` elements (the raw-pointer
+        per-rank entry points cannot see buffer sizes)."""
+        torch = self._torch
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+        if t.numel() < need:
+            raise ValueError(f"{name} has {t.numel()} elements, needs {need}")
+
     def _new(self):
         return self._torch.empty(self.shape, dtype=self._torch.float64, device="cuda")
 
@@ -295,10 +304,10 @@ class Context:
     def fd_stage(self, stage, inp, out, a, b=0):
         """fd_apply_stage: 0/2 = forward/backward spatial modes on `a` time slices,
         1 = time mode of a spatial chunk [n_t][b] at spatial offset a."""
-        torch = self._torch
+        Ns = int(np.prod(self.n_s))
+        need = int(a) * Ns if stage in (0, 2) else self.n_t * int(b)
         for t, nm in ((inp, "in"), (out, "out")):
-            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-                raise TypeError(f"{nm} must be a contiguous float64 CUDA tensor")
+            self._chk(t, nm, need)
         _check(self._lib.fd_apply_stage(self._h, int(stage), ctypes.c_void_p(inp.data_ptr()),
                                         ctypes.c_void_p(out.data_ptr()), int(a), int(b)), "fd_apply_stage")
         return out
@@ -307,6 +316,14 @@ class Context:
         """fd_apply_scatter: stage 0 = forward spatial modes of rank `me`'s slab scattered into
         the chunk buffers `dsts`; stage 1 = time mode of its chunk scattered into the slab
         buffers `dsts` (lists of `world` CUDA tensors)."""
+        if len(dsts) != int(world):
+            raise ValueError(f"dsts has {len(dsts)} buffers, expected world = {world}")
+        Ns = int(np.prod(self.n_s))
+        self._chk(inp, "inp", int(a) * Ns if stage == 0 else self.n_t * int(b))
+        for t in dsts:
+            # receive buffers: a spatial chunk [n_t][chunk] (stage 0) or a time slab (stage 1);
+            # the library cannot see their sizes, so at least the smaller bound is enforced
+            self._chk(t, "dsts[i]", 1)
         arr = (ctypes.c_void_p * world)(*[t.data_ptr() for t in dsts])
         _check(self._lib.fd_apply_scatter(self._h, int(stage), ctypes.c_void_p(inp.data_ptr()), int(a), int(b),
                                           int(world), int(me), arr), "fd_apply_scatter")
@@ -315,11 +332,14 @@ class Context:
         """Rows [t_first, t_first + nout) of A x from the stored rows [s_first, s_first +
         x_ext.shape[0]) of x (ls_matvec_slab)."""
         torch = self._torch
-        if not (x_ext.is_cuda and x_ext.dtype == torch.float64 and x_ext.is_contiguous()):
-            raise TypeError("x_ext must be a contiguous float64 CUDA tensor")
-        s_rows = x_ext.shape[0]
+        Ns = int(np.prod(self.n_s))
+        self._chk(x_ext, "x_ext", 1)
+        if x_ext.numel() % Ns:
+            raise ValueError(f"x_ext has {x_ext.numel()} elements, not a whole number of time slices of {Ns}")
+        s_rows = x_ext.numel() // Ns
         if y is None:
             y = torch.empty((nout,) + tuple(self.shape[1:]), dtype=torch.float64, device="cuda")
+        self._chk(y, "y", int(nout) * Ns)
         _check(self._lib.ls_matvec_slab(self._h, ctypes.c_void_p(x_ext.data_ptr()), int(s_first), int(s_rows),
                                         ctypes.c_void_p(y.data_ptr()), int(t_first), int(nout)), "ls_matvec_slab")
         return y

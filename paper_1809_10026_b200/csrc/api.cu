@@ -304,11 +304,11 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   const bool mode1 = (Q == 1) && !scale;  // the scaled (time) mode always uses the strided variant
   // auto (measured, tools/fd_variants.py): register-direct for n > 116 (config 4: 75% -> 86% of
   // the FP64 peak), smem-staged ping-pong / m-half kernels below (config 3: 56% vs 37%)
-  // it also wins from n = 96 when the last m-tile has at most one padding row, i.e. when
-  // n % 8 <= 1 (tools/fdk_sel.py, config 5 p = 2, n = 96 / 97: 4.67 -> 4.45 ms; rd for n = 96
-  // only: 4.51 ms; p = 4 / 8, n = 98 / 99, 102 / 103: the smem-staged kernels stay 13 / 9 %
-  // faster)
-  const bool rd_auto = (n + 3) / 4 >= 30 || (n >= 96 && n % 8 <= 1);
+  // it also wins at n = 96 / 97 (bucket 24 / 25: the last m-tile of n = 96 is full, n = 97
+  // adds one 8-row tile with one valid row; tools/fdk_sel.py, config 5 p = 2: 4.67 -> 4.45 ms;
+  // rd for n = 96 only: 4.51 ms).  Only these measured extents: at n = 98 / 99 and 102 / 103
+  // (config 5 p = 4 / 8) the smem-staged kernels stay 13 / 9 % faster.
+  const bool rd_auto = (n + 3) / 4 >= 30 || n == 96 || n == 97;
   if (ctx->fd_variant == 2 || (ctx->fd_variant == 0 && rd_auto)) return launch_mode_rd(ctx, a, mode1, scale);
   switch (round_ks((n + 3) / 4)) {
     KS_A(2) KS_A(4) KS_A(5) KS_A(8)
@@ -953,6 +953,9 @@ int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
     // barrier.  Receive buffers: B = tmp[1] (chunk), A = tmp[0] (slab); every workspace
     // written locally after a barrier (tmp[2..4]) is never a peer's destination.
     const int64_t c0 = cm.chunk_off[ctx->rank], len = cm.chunk_len[ctx->rank];
+    // entry barrier: tmp[0] / tmp[1] are also ls_matvec workspaces, so no rank may scatter
+    // into a peer's receive buffers before that peer has finished its previous call
+    LS_CHECK(cm.barrier());
     LS_CHECK(spatial_fwd_scatter(ctx, r, uint64_t(ctx->ntl), cm.d_peer_chunk, ctx->world, ctx->rank));
     LS_CHECK(cm.barrier());
     if (len > 0) LS_CHECK(time_chunk_scatter(ctx, B, c0, len, C, cm.d_peer_slab, ctx->world, ctx->rank));

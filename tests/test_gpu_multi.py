@@ -41,5 +41,6 @@ def test_distributed_matches_single_gpu(world, extra):
     line = [l for l in out.stdout.splitlines() if l.startswith("{")][-1]
     res = json.loads(line)
     assert res["fd_rel"] <= 1e-12 and res["matvec_rel"] <= 1e-12, res
+    assert res["fd_after_matvec_rel"] <= 1e-12, res
     assert all(it == res["iters_1gpu"] for it in res["iters"]), res
     assert res["pcg_rel"] <= 1e-9, res

@@ -594,6 +594,8 @@ def test_fd_tail_rows(torch_cuda, d, p, n_elems):
     space, tf, fdd = _oracle(d, p, n_elems)
     r = synth.residual(ctx.shape, 11)
     rg = torch.from_numpy(r).cuda()
+    z_auto = ctx.fd_apply(rg).cpu().numpy()     # automatic dispatch (n = 97: register-direct)
+    ctx.tune(1, 1)                               # the smem-staged family, which has the tail path
     z1 = ctx.fd_apply(rg).cpu().numpy()
     ctx.tune(7, 0)
     z0 = ctx.fd_apply(rg).cpu().numpy()
@@ -601,3 +603,4 @@ def test_fd_tail_rows(torch_cuda, d, p, n_elems):
     z_ref = fd.fd_apply(r, fdd)
     assert _rel(z1, z_ref) <= TOL
     assert _rel(z1, z0) <= 1e-13
+    assert _rel(z_auto, z_ref) <= TOL

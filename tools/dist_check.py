@@ -49,24 +49,30 @@ def main():
     r = torch.from_numpy(r_glob[sl].copy()).cuda()
     z = ctx.fd_apply(r)
     y = ctx.matvec(r)
+    # back to back, no host sync: ls_matvec's workspaces are the fused all-to-all's receive
+    # buffers (the entry barrier of comm_fd_apply orders them)
+    w = ctx.fd_apply(ctx.matvec(z))
     b = ctx.rhs(3 if a.geometry else 1)
     x, st = ctx.pcg(b, tol=1e-8)
     torch.cuda.synchronize()
     parts = [None] * world
-    dist.all_gather_object(parts, (ctx.t0, z.cpu().numpy(), y.cpu().numpy(), x.cpu().numpy(), st))
+    dist.all_gather_object(parts, (ctx.t0, z.cpu().numpy(), y.cpu().numpy(), x.cpu().numpy(), st, w.cpu().numpy()))
     if rank == 0:
         one = ls.Context(a.d, a.p, ne, **kw)
         rg = torch.from_numpy(r_glob).cuda()
-        z1, y1 = one.fd_apply(rg).cpu().numpy(), one.matvec(rg).cpu().numpy()
+        z1t = one.fd_apply(rg)
+        z1, y1 = z1t.cpu().numpy(), one.matvec(rg).cpu().numpy()
+        w1 = one.fd_apply(one.matvec(z1t)).cpu().numpy()
         x1, st1 = one.pcg(one.rhs(3 if a.geometry else 1), tol=1e-8)
         x1 = x1.cpu().numpy()
         parts.sort(key=lambda t: t[0])
         Z = np.concatenate([t[1] for t in parts])
         Y = np.concatenate([t[2] for t in parts])
         X = np.concatenate([t[3] for t in parts])
+        Wv = np.concatenate([t[5] for t in parts])
         rel = lambda u, v: float(np.linalg.norm(u - v) / np.linalg.norm(v))
         print(json.dumps({"world": world, "a2a": a.a2a, "geometry": a.geometry, "fd_rel": rel(Z, z1),
-                          "matvec_rel": rel(Y, y1), "pcg_rel": rel(X, x1), "iters": [t[4]["iters"] for t in parts],
+                          "matvec_rel": rel(Y, y1), "fd_after_matvec_rel": rel(Wv, w1), "pcg_rel": rel(X, x1), "iters": [t[4]["iters"] for t in parts],
                           "iters_1gpu": st1["iters"]}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
