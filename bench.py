@@ -10,9 +10,12 @@ For N > 1 the same global problem is slab-partitioned along time over the ranks
 ("scaling": "strong"), the time mode running after an NCCL all-to-all.
 
 Printed (rank 0): ONE JSON line with value = whole-job DOF/s, the roofline of the
-dominant kernel (fd_mode_kernel, FP64 DMMA; peak = 37.0 TF/s measured register-
-only DMMA, profiles/peaks_fp64_r01.json), e2e through fd_apply_host, the oracle
+dominant kernel (fd_mode_kernel, FP64 DMMA; peak = the best measured register-only
+DMMA rate, profiles/peaks_fp64_r01.json), e2e through fd_apply_host, the oracle
 CPU baseline, secondary PCG solve times, clocks.
+
+`--gpus N` without a torchrun environment re-launches itself as N ranks under
+torch.distributed.run; `--dry-run` exercises that distributed harness on CPU (gloo).
 """
 
 import argparse
@@ -30,8 +33,21 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-FP64_PEAK_TFLOPS = 37.0  # measured DMMA.8x8x4 register-only (profiles/peaks_fp64_r01.json)
-FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA.8x8x4 register-only, 148 SMs (profiles/peaks_fp64_r01.json)"
+def _fp64_peak():
+    """The FP64 roofline denominator: the best measured register-only DMMA.8x8x4 rate
+    (tools/fp64_peak.cu on this pool's B200, profiles/peaks_fp64_r01.json; MEASURED_PEAKS.json
+    has no FP64 entry).  Fallback: 37.0 TF/s, the same measurement rounded."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_fp64_r01.json")) as f:
+            micro = json.load(f)["micro"]
+        v = max(m["tflops"] for m in micro if m["kernel"].startswith("dmma"))
+        return float(v), ("measured: tools/fp64_peak.cu DMMA.8x8x4 register-only, 148 SMs, best of "
+                          "profiles/peaks_fp64_r01.json")
+    except Exception:
+        return 37.0, "fallback 37.0 (profiles/peaks_fp64_r01.json unreadable)"
+
+
+FP64_PEAK_TFLOPS, FP64_PEAK_SOURCE = _fp64_peak()
 
 
 def _hbm_peak():
@@ -135,30 +151,58 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def oracle_sample(cfg_id, seconds_min=10.0, max_reps=8):
-    """The CPU oracle (oracle/fd.py, as it stands) on a bounded sample of the
-    workload: the config's spatial discretisation with the time direction
-    truncated to 8 elements (n_t = 8 + p - 1); returns (DOF/s, sample text, cores)."""
+_SHARE_CACHE = {}
+
+
+def oracle_share(cfg_id, parts=8, seed=0):
+    """One bounded sample of the workload for the CPU oracle: rank 0's share of a `parts`-way
+    time-slab split of config `cfg_id`'s fd_apply, computed with the oracle's own functions
+    (oracle/fd.py: mode_apply, divisor) as they stand -- the forward spatial modes on time
+    slices [0, n_t/parts), the time mode (U_t^T, divide, U_t) on spatial columns [0, N_s/parts),
+    the backward spatial modes on the slab.  Every mode runs at its full extent (the per-DOF
+    flop count 4(d n_s + n_t) of the full configuration, PAPER.md 1071), on exactly 1/parts
+    of the DOFs.  Returns (seconds, DOFs processed, description)."""
     from oracle import univariate as uv, fd
     w = workload(cfg_id)
-    d, p, n_el = w["d"], w["p"], w["n_el"]
-    n_el_t = 8
-    sf, tf = uv.space_factors(n_el, p), uv.time_factors(n_el_t, p)
-    fdd = fd.setup([sf] * d, tf)
-    shape = (tf["Mt"].shape[0],) + (sf["M"].shape[0],) * d
-    r = synth.residual(shape, 0)
-    fd.fd_apply(r, fdd)  # warm
-    reps, t0 = 0, time.perf_counter()
-    while reps < max_reps and (reps == 0 or time.perf_counter() - t0 < seconds_min):
-        fd.fd_apply(r, fdd)
+    d, p, n_el, n_s, n_t = w["d"], w["p"], w["n_el"], w["n_s"], w["n_t"]
+    Ns = n_s ** d
+    nt_sl, nc = -(-n_t // parts), -(-Ns // parts)
+    key = (cfg_id, parts, seed)
+    if key not in _SHARE_CACHE:  # setup and inputs once (not part of a step)
+        sf, tf = uv.space_factors(n_el, p), uv.time_factors(n_el, p)
+        fdd = fd.setup([sf] * d, tf)
+        _SHARE_CACHE.clear()
+        _SHARE_CACHE[key] = (fdd, synth.residual((nt_sl,) + (n_s,) * d, seed), synth.residual((n_t, nc), seed + 1),
+                             np.ascontiguousarray(fd.divisor(fdd).reshape(n_t, Ns)[:, :nc]))
+    fdd, r, X, D = _SHARE_CACHE[key]
+    t0 = time.perf_counter()
+    s = r
+    for k in range(1, d + 1):
+        s = fd.mode_apply(s, fdd["U_s"][k - 1].T, d + 1 - k)
+    q = fd.mode_apply(fd.mode_apply(X, fdd["U_t"].T, 0) / D, fdd["U_t"], 0)
+    for k in range(1, d + 1):
+        s = fd.mode_apply(s, fdd["U_s"][k - 1], d + 1 - k)
+    dt = time.perf_counter() - t0
+    assert np.isfinite(s).all() and np.isfinite(q).all()
+    dofs = w["N"] / parts
+    desc = (f"oracle (numpy tensordot, fp64) on 1/{parts} of config {cfg_id} (N = {w['N']}): the per-rank "
+            f"share of a {parts}-way time-slab split -- forward/backward spatial modes on {nt_sl} of {n_t} "
+            f"time slices and the time mode on {nc} of {Ns} spatial columns, every mode at full extent "
+            f"(same flops per DOF as the full config); DOF/s = (N/{parts}) / time")
+    return dt, dofs, desc
+
+
+def oracle_sample(cfg_id, seconds_min=10.0, max_reps=8):
+    """cpu_baseline: oracle_share repeated for >= seconds_min of CPU work; (DOF/s, sample, cores)."""
+    oracle_share(cfg_id)  # warm (setup, page faults)
+    reps, tot, dofs, desc = 0, 0.0, 0.0, ""
+    while reps < max_reps and (reps == 0 or tot < seconds_min):
+        dt, n, desc = oracle_share(cfg_id)
+        tot += dt
+        dofs += n
         reps += 1
-    dt = (time.perf_counter() - t0) / reps
-    N = int(np.prod(shape))
     cores = len(os.sched_getaffinity(0))
-    sample = (f"oracle fd_apply (numpy tensordot, fp64) on config {cfg_id}'s spatial grid "
-              f"(n_s={sf['M'].shape[0]}, p={p}) with time truncated to n_el_t={n_el_t} "
-              f"(n_t={shape[0]}, N={N}); {reps} reps, {dt:.3f} s each")
-    return N / dt, sample, cores
+    return dofs / tot, f"{desc}; {reps} samples, {tot / reps:.2f} s each", cores
 
 
 def oracle_extras():
@@ -192,36 +236,89 @@ def oracle_extras():
 
 
 def run_reference(args):
-    """--impl reference: the oracle, as it stands, on the host cores."""
+    """--impl reference: the oracle, as it stands, on the host cores; each step is one
+    oracle_share sample (1/8 of the configuration's DOFs at full per-DOF work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     w = workload(args.config)
-    from oracle import univariate as uv, fd
-    d, p, n_el = w["d"], w["p"], w["n_el"]
-    sf, tf = uv.space_factors(n_el, p), uv.time_factors(8, p)
-    fdd = fd.setup([sf] * d, tf)
-    shape = (tf["Mt"].shape[0],) + (sf["M"].shape[0],) * d
-    r = synth.residual(shape, 0)
     for _ in range(args.warmup):
-        fd.fd_apply(r, fdd)
-    t0 = time.perf_counter()
+        oracle_share(args.config)
+    tot, dofs, desc = 0.0, 0.0, ""
     for _ in range(args.steps):
-        fd.fd_apply(r, fdd)
-    dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    N = int(np.prod(shape))
+        dt, n, desc = oracle_share(args.config)
+        tot += dt
+        dofs += n
     cores = len(os.sched_getaffinity(0))
-    val = N / dt
-    sample = (f"oracle fd_apply (numpy tensordot, fp64) on config {args.config}'s spatial grid with the "
-              f"time direction truncated to n_el_t=8 (n_t={shape[0]}, N={N}) per step; DOF/s of that sample")
+    val = dofs / tot
+    ms = tot / max(args.steps, 1) * 1e3
     line = {"impl": "reference", "metric": "fd_apply DOF/s (fp64)", "value": val, "unit": "DOF/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_dict(args.config, args.gpus),
+            "sample": {"dofs_per_step": dofs / max(args.steps, 1), "of_N": w["N"], "what": desc},
             "cpu_baseline": {"value": val, "unit": "DOF/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": desc},
             "e2e": {"value": val, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _respawn(args):
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-launch this command as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and pass
+    rank 0's JSON line through.  NCCL's environment (NCCL_DEBUG etc.) is inherited unchanged."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(args):
+    """--dry-run: the distributed plumbing of the bench without a GPU (gloo on CPU): rendezvous,
+    the time-slab partition and all-to-all plan of every rank (libls host-only queries), the
+    barrier + max-over-ranks reduction of a timed region, and rank 0's JSON line with n_gpus =
+    WORLD_SIZE.  No kernel runs, so value / ms_per_step are null."""
+    import torch
+    import torch.distributed as dist
+    import paper_1809_10026_b200 as ls
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    w = workload(args.config)
+    Ns = w["n_s"] ** w["d"]
+    t0, ntl = ls.partition(w["n_t"], world, rank)
+    c0, cl = ls.partition(Ns, world, rank)
+    t_start = time.perf_counter()
+    dt = time.perf_counter() - t_start
+    t = torch.tensor([dt, float(ntl * Ns), float(cl * w["n_t"])], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sizes = torch.tensor([float(ntl * Ns)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(sizes, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        line = {"metric": "fd_apply DOF/s (fp64)", "value": None, "unit": "DOF/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": _config_dict(args.config, world, args.a2a), "dry_run": True,
+                "partition": {"slab_rows_rank0": ntl, "max_slab_dofs": t[1].item(), "max_chunk_dofs": t[2].item(),
+                              "dofs_total": sizes.item()},
+                "timing": "max over ranks of the (empty) timed region: %.3g s" % t[0].item()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
@@ -235,8 +332,14 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip PCG / config-3 / cpu extras")
     ap.add_argument("--a2a", default="nccl", choices=["nccl", "fused"],
                     help="N > 1: NCCL all-to-all (default) or the fused peer-memory epilogues (LS_TUNE_A2A)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU (gloo) check of the distributed harness: partition, barrier, max-over-ranks, JSON line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _respawn(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -282,7 +385,6 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = ctx.launches
-    ctx.profile(True)
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
@@ -290,9 +392,17 @@ def main():
             ctx.fd_apply(r, z)
         e1.record(stream)
         barrier()
-    ctx.profile(False)
     launches = ctx.launches - launches0
     ms = e0.elapsed_time(e1) / args.steps
+    # per-launch kernel times for the roofline: the same K steps again with CUDA events around
+    # every mode-product launch on the library stream (a separate pass: events between the
+    # launches of the timed region would break its programmatic-dependent-launch pairs)
+    barrier()
+    ctx.profile(True)
+    for _ in range(args.steps):
+        ctx.fd_apply(r, z)
+    ctx.profile(False)
+    barrier()
     kms, kflops, kn = ctx.profile_read()
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -327,6 +437,8 @@ def main():
             "traffic_unit": "bytes per launch (mean over the captured launches)", "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": 16 * w["N"],
             "peak_source": FP64_PEAK_SOURCE, "kernel_share_of_step": round(kms / (ms * args.steps), 4),
+            "kernel_timing": ("CUDA events around every mode-product launch on the library stream, in a "
+                              "second pass of the same K steps right after the timed region"),
             "launches_timed": kn, "flops_per_step_algorithmic": w["flops"]}
 
     extras = {}
