@@ -214,6 +214,25 @@ int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, int max_iter,
 int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* out4);
 
 /*
+ * ls_error_norms -- discretisation error of u_h = sum_i x_i B_i against the exact solution
+ * of a built-in benchmark, by direct space-time Gauss quadrature (p_s + 3 points per element
+ * and space direction, p_t + 3 in time; reading c24), T = 1:
+ *   kind 1: the cube, u = prod_k sin(pi x_k) sin t (PAPER.md 1166; ls_rhs kind 1), any d;
+ *   kind 2: the quarter annulus of ls_setup_geo (d = 2), u = -(x^2+y^2-1)(x^2+y^2-4) x y^2
+ *           sin(pi t) (PAPER.md 1128-1129; ls_rhs kind 2).
+ * out8 (host): [0] ||e||^2_L2(Q), [1] ||d_t e||^2, [2] ||grad_x e||^2, [3] ||Lap e||^2, and
+ * [4..7] the same four integrals of u (e = u - u_h, Q = Omega x (0, 1)).  Hence
+ * ||e||_V0^2 = [1] + [3] (the norm of PAPER.md 318-323, Thm teo:a-priori), ||e||_L2^2 = [0],
+ * and the space-time ||e||_H1^2 = [0] + [1] + [2] (Fig. 2, PAPER.md 1131-1139).  Every term
+ * is a sum of non-negative quadrature contributions (no cancellation).
+ * x: device vector (the whole [n_t][N_s] tensor; single-GPU contexts only).  Synchronous.
+ * Errors: LS_EINVAL (null / misaligned), LS_ENOTSUP (kind without an exact solution for this
+ * context: kind 1 on a mapped domain, kind 2 on the cube or d != 2, a distributed context,
+ * shared-memory footprint above 200 KB, e.g. d = 3 with p_s > 7), LS_ENOMEM, LS_ECUDA.
+ */
+int ls_error_norms(ls_ctx* ctx, int kind, const double* x, double* out8);
+
+/*
  * ls_geometry -- a mapped spatial domain Omega = F([0,1]^d) (PAPER.md 226-250,
  * Assumption 1; reading c19: a tensor-product NURBS map, rational when `weights`
  * is given, e.g. the exact quarter annulus / revolved quarter annulus of Sec. 5,

@@ -32,7 +32,7 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
-            "ls_setup_dist_deg", "ls_energy_error", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist", "ls_pg_factors"]
+            "ls_setup_dist_deg", "ls_energy_error", "ls_error_norms", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist", "ls_pg_factors"]
 
 LS_PRECOND_P, LS_PRECOND_PG = 0, 1
 
@@ -101,6 +101,7 @@ def load_library(path=LIB_PATH):
                                              ctypes.c_char_p, ctypes.POINTER(vp)]),
         "ls_tune": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "ls_energy_error": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.POINTER(ctypes.c_double)]),
+        "ls_error_norms": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.POINTER(ctypes.c_double)]),
         "fd_apply_stage": (ctypes.c_int, [vp, ctypes.c_int, dp, dp, ctypes.c_int64, ctypes.c_int64]),
         "fd_apply_scatter": (ctypes.c_int, [vp, ctypes.c_int, dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
@@ -364,6 +365,18 @@ class Context:
         out = (ctypes.c_double * 4)()
         _check(self._lib.ls_energy_error(self._h, int(kind), self._dev(x, "x"), out), "ls_energy_error")
         return {"J": out[0], "f2": out[1], "bx": out[2], "xAx": out[3]}
+
+    def error_norms(self, kind, x):
+        """ls_error_norms: the space-time integrals of e = u - u_h and of u (kind 1: cube,
+        kind 2: quarter annulus) and the relative V_0, L^2, H^1 errors derived from them."""
+        o = (ctypes.c_double * 8)()
+        _check(self._lib.ls_error_norms(self._h, int(kind), self._dev(x, "x"), o), "ls_error_norms")
+        v = list(o)
+        return {"e_L2": v[0], "e_dt": v[1], "e_grad": v[2], "e_lap": v[3],
+                "u_L2": v[4], "u_dt": v[5], "u_grad": v[6], "u_lap": v[7],
+                "rel_V0": float(np.sqrt((v[1] + v[3]) / (v[5] + v[7]))),
+                "rel_L2": float(np.sqrt(v[0] / v[4])),
+                "rel_H1": float(np.sqrt((v[0] + v[1] + v[2]) / (v[4] + v[5] + v[6])))}
 
     def fd_apply_host(self, r_host, z_host):
         """fd_apply on host tensors/arrays (pinned recommended); synchronous."""

@@ -21,6 +21,7 @@
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 #include "geo.hpp"
+#include "err.hpp"
 
 using namespace ls;
 
@@ -1703,6 +1704,21 @@ extern "C" int ls_energy_error(ls_ctx* ctx, int kind, const double* x, double* o
   out4[2] = bx;
   out4[3] = xax;
   return LS_OK;
+}
+
+// discretisation-error norms against the exact solution (err.cu)
+extern "C" int ls_error_norms(ls_ctx* ctx, int kind, const double* x, double* out8) {
+  if (!ctx || !x || !out8 || !aligned8(x)) return LS_EINVAL;
+  if (ctx->world != 1) return LS_ENOTSUP;
+  ErrSetup es;
+  es.d = ctx->d;
+  es.ps = ctx->p;
+  es.pt = ctx->pt;
+  es.kind = kind;
+  es.nt = ctx->nt;
+  for (int k = 0; k <= ctx->d; ++k) es.n_el[k] = ctx->n_el[k];
+  es.gmap = ctx->gmap.get();
+  return error_norms(es, x, ctx->stream, &ctx->launches, out8);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(ASM_THREADS) geo_assemble_kernel(GeoAsmArgs a)
 // host tables of one direction: Gauss points / weights, discretisation basis per element
 // host tables of one direction for qpe Gauss points per element: points / weights and the
 // p+1 local basis functions' values, 1st and 2nd derivatives [n_el][qpe][p+1][3]
-static void dir_tables(int n_el, int p, int qpe, std::vector<double>& xq, std::vector<double>& wq,
+void dir_tables(int n_el, int p, int qpe, std::vector<double>& xq, std::vector<double>& wq,
                        std::vector<double>& bt) {
   auto kn = open_uniform_knots(n_el, p);
   const int m = n_el + p, P1 = p + 1, QP = qpe;
@@ -463,6 +463,15 @@ static int geo_points(const GeoMap& g, int d, int p, const int64_t* n_el, int qp
   GEO_CUDA(cudaStreamSynchronize(s));
   if ((hflags & 4) || (hflags & 3) == 3) return LS_EINVAL;  // singular or folded map
   return LS_OK;
+}
+
+int geo_point_data(const GeoMap& g, int d, int p, const int64_t* n_el, int qpe, std::vector<void*>& allocs,
+                   cudaStream_t s, double** qd, int64_t* NQ, int64_t* launches) {
+  GeoPts pts;
+  const int rc = geo_points(g, d, p, n_el, qpe, allocs, s, pts, launches);
+  *qd = pts.qd;
+  *NQ = pts.NQ;
+  return rc;
 }
 
 int geo_assemble(GeoDev& gd, const GeoMap& g, int d, int p, const int64_t* n_el, cudaStream_t s,

@@ -86,6 +86,18 @@ int geo_rhs(const GeoDev& gd, const double* G, double* b, int t0, int nrows, int
 int pg_scaling(const GeoDev& gd, const double* bKt, const double* bMt, int nt, const double* pdiag_t,
                const double* pdiag_s, double* dm12, int t0, int nrows, cudaStream_t s, int64_t* launches);
 
+// Host tables of one direction for qpe Gauss points per element (uniform open knots, 80-bit,
+// rounded once): points xq and weights wq [n_el * qpe], and the p + 1 local B-splines' values,
+// 1st and 2nd derivatives bt [n_el][qpe][p + 1][3] (full, unconstrained local numbering).
+void dir_tables(int n_el, int p, int qpe, std::vector<double>& xq, std::vector<double>& wq,
+                std::vector<double>& bt);
+
+// Map data at the tensor Gauss points of the uniform meshes n_el (qpe per element and
+// direction; device, allocations appended to `allocs`): qd = [16][NQ] with |det J| w_q,
+// J^{-1}[3][3] (row j = grad eta_j), the Laplacian's first-order coefficients b[3], x[3].
+int geo_point_data(const GeoMap& g, int d, int p, const int64_t* n_el, int qpe, std::vector<void*>& allocs,
+                   cudaStream_t s, double** qd, int64_t* NQ, int64_t* launches);
+
 // y = s * x elementwise (the D^{-1/2} pre / post scaling of the P^G application)
 int scale_vec(const double* s_, const double* x, double* y, int64_t n, cudaStream_t s, int64_t* launches);
 

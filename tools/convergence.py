@@ -1,5 +1,6 @@
-"""Energy-norm convergence of the PCG solution: prints ||(d_t - Lap)(u - u_h)|| / ||f|| and
-observed rates, on the cube (u = prod sin(pi x_k) sin t, PAPER.md 1166) or, with
+"""Convergence of the PCG solution: prints the least-squares energy error
+||(d_t - Lap)(u - u_h)|| / ||f|| and the relative V_0, L^2 and H^1 errors (ls_error_norms) with
+their observed rates, on the cube (u = prod sin(pi x_k) sin t, PAPER.md 1166) or, with
 --annulus, on the 2D quarter annulus (u = -(x^2+y^2-1)(x^2+y^2-4) x y^2 sin(pi t),
 PAPER.md 1128-1129, the setting of Fig. 2; P^G preconditioner).
     python tools/convergence.py [--d 3] [--p 2 3 4] [--nel 4 8 16 32] [--annulus]"""
@@ -25,10 +26,16 @@ for p in a.p:
         else:
             ctx = ls.Context(a.d, p, [ne] * (a.d + 1))
             kind = 1
-        x, st = ctx.pcg(ctx.rhs(kind), tol=1e-12)
+        x, st = ctx.pcg(ctx.rhs(kind), tol=1e-12, max_iter=3000)
         e = ctx.energy_error(kind, x)
-        errs.append(float(np.sqrt(max(e["J"], 0.0) / e["f2"])))
+        n = ctx.error_norms(kind, x)
+        errs.append([float(np.sqrt(max(e["J"], 0.0) / e["f2"])), n["rel_V0"], n["rel_L2"], n["rel_H1"]])
         ctx.close()
-    rates = [float(np.log2(errs[i] / errs[i + 1])) for i in range(len(errs) - 1)]
+    E = np.array(errs)
+    rates = np.log2(E[:-1] / E[1:]).T.tolist()
     print(json.dumps({"domain": "quarter annulus" if a.annulus else "cube", "d": a.d, "p": p, "n_el": a.nel,
-                      "rel_energy_error": errs, "rates": rates, "expected_rate": p - 1}))
+                      "rel_energy_error": E[:, 0].tolist(), "rel_V0": E[:, 1].tolist(),
+                      "rel_L2": E[:, 2].tolist(), "rel_H1": E[:, 3].tolist(),
+                      "rates": {"energy": rates[0], "V0": rates[1], "L2": rates[2], "H1": rates[3]},
+                      "expected": {"energy": p - 1, "V0": p - 1, "H1": p, "L2": p + 1 if p >= 3 else "suboptimal"}}),
+          flush=True)
