@@ -385,7 +385,9 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  *   LS_TUNE_MATVEC:    0 = automatic per degree (default),
  *                      1 = four banded passes, 152 B/DOF,
  *                      2 = three fused banded passes (Toeplitz stencils), 96 B/DOF,
- *                      3 = four banded passes on the FP64 tensor pipe (DMMA).
+ *                      3 = four banded passes on the FP64 tensor pipe (DMMA),
+ *                      4 = plane pass (directions 1 + 2 fused, DMMA) + direction-3 and time
+ *                          DMMA passes, 96 B/DOF (d >= 2, 2 <= p_s, p_t <= 8; else LS_ENOTSUP).
  * Errors: LS_EINVAL for an unknown knob or value.
  */
 #define LS_TUNE_FD_KERNEL 1
@@ -409,6 +411,9 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * the shared-memory FD kernel computes the last one or two output rows with DFMAs instead of
  * a 7/8- or 3/4-padded DMMA m-tile (default), 0 = all rows on DMMAs. */
 #define LS_TUNE_FD_TAIL 7
+/* LS_TUNE_MV4_CTAS: process-wide; the v4 plane pass' register budget, 1 or 2 CTAs of 256
+ * threads per SM (<= 255 / <= 128 registers per thread); default 2. */
+#define LS_TUNE_MV4_CTAS 8
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

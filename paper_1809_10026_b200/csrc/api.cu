@@ -18,12 +18,16 @@
 #include "matvec_kernels.cuh"
 #include "matvec2_kernels.cuh"
 #include "matvec3_kernels.cuh"
+#include "mv4_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 #include "geo.hpp"
 #include "err.hpp"
 
 using namespace ls;
+namespace ls {
+extern int g_mv4_ctas;  // mv4.cu
+}
 
 int ls::g_ls_pdl = 1;  // programmatic dependent launch of the FD mode kernels (LS_TUNE_PDL)
 
@@ -63,6 +67,10 @@ struct ls_ctx {
   int fd_variant = 0;  // ls_tune knob LS_TUNE_FD_KERNEL: 0 auto, 1 smem-staged (v2/pp), 2 register-direct
   int fd_tail = 1;     // ls_tune knob LS_TUNE_FD_TAIL: DFMA tail rows in the ping-pong FD kernel
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
+  // PCG: the next ls_matvec also forms p.q (x.y) into scal[fuse_dot_slot] when its last pass can
+  // (v4 time-pass epilogue); fuse_dot_done reports whether it did
+  int fuse_dot_slot = -1;
+  bool fuse_dot_done = false;
   // matvec v2: Toeplitz stencil + boundary corrections per band matrix (matvec2_kernels.cuh)
   struct Split {
     std::vector<double> s;  // 2p+1
@@ -1321,6 +1329,100 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   return LS_OK;
 }
 
+// ---- matvec v4 (mv4_kernels.cuh): plane pass (directions 1 + 2) -> direction 3 -> time ------
+static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
+                      int64_t t_first, int64_t nout) {
+  const int d = ctx->d, P = ctx->p, PT = ctx->pt;
+  if (d < 2 || P < 2 || P > 8 || PT < 2 || PT > 8) return LS_ENOTSUP;
+  const int n1 = ctx->n[0], n2 = ctx->n[1];
+  double *PM = ctx->tmp[0], *PK = ctx->tmp[1], *PJ = ctx->tmp[2];
+  {
+    MV4PlaneArgs a{};
+    a.x = x;
+    a.out[0] = PM;
+    a.out[1] = PK;
+    a.out[2] = PJ;
+    a.frag1 = ctx->frag_dir[0];
+    a.frag2 = ctx->frag_dir[1];
+    a.n1 = n1;
+    a.n2 = n2;
+    a.mt1 = mv3_mt(P, n1);
+    a.mt2 = mv3_mt(P, n2);
+    a.nplanes = rows * (d == 3 ? ctx->n[2] : 1);
+    LS_CUDA(mv4_plane_run(a, P, ctx->num_sms, ctx->stream));
+    ctx->launches++;
+  }
+  const int64_t tT = (ctx->nt - 1) - s_first;  // the last time slice among the stored rows
+  const bool have_last = tT >= 0 && tT < rows;
+  const double *v1 = PM, *v2 = PJ, *v3 = have_last ? PK + tT * ctx->Ns : nullptr;
+  MV3Pass ps[2];
+  int np = 0;
+  if (d == 3) {  // direction 3: (P_M, P_K, P_J) -> v1, v2 (+ v3 on the last slice)
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = MV3_D3;
+    q.mode1 = false;
+    q.p = P;
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_dir[2];
+    a.in[0] = PM;
+    a.in[1] = PK;
+    a.in[2] = PJ;
+    a.out[0] = ctx->tmp[3];
+    a.out[1] = ctx->tmp[4];
+    a.v3 = ctx->xT_pad;
+    a.tT = have_last ? int(tT) : -1;
+    a.n = ctx->n[2];
+    a.mt = mv3_mt(P, a.n);
+    a.Q = uint32_t(int64_t(n1) * n2);
+    a.ncols = uint32_t(rows * a.Q);
+    a.mt0 = 0;
+    a.mt1 = a.mt;
+    v1 = ctx->tmp[3];
+    v2 = ctx->tmp[4];
+    v3 = have_last ? ctx->xT_pad : nullptr;
+  }
+  {  // time: y = K_t v1 + M_t v2 + W_t v3 on the output rows [t_first, t_first + nout)
+    MV3Pass& q = ps[np++];
+    q = MV3Pass{};
+    q.kind = MV3_T2;
+    q.mode1 = false;
+    q.p = PT;
+    MV3Args& a = q.args;
+    a.frag = ctx->frag_time;
+    a.in[0] = v1;
+    a.in[1] = v2;
+    a.v3 = const_cast<double*>(v3);
+    a.out[0] = y;
+    a.n = ctx->nt;
+    a.mt = mv3_mt(PT, ctx->nt);
+    a.Q = uint32_t(ctx->Ns);
+    a.ncols = uint32_t(ctx->Ns);
+    a.tT = -1;
+    a.s_first = int(s_first);
+    a.s_rows = int(rows);
+    a.t_first = int(t_first);
+    a.nout = int(nout);
+    const int S0 = mv3_s0(PT);
+    a.mt0 = int((t_first - S0) / 8);
+    a.mt1 = int((t_first + nout - S0 + 7) / 8);
+    if (ctx->fuse_dot_slot >= 0) {  // p.q in the epilogue: p = the own rows of x
+      a.dotp = x + (t_first - s_first) * ctx->Ns;
+      a.dot_part = ctx->partials;
+    }
+  }
+  LS_CUDA(mv3_run(ps, np, ctx->num_sms, ctx->stream, &ctx->launches));
+  if (ctx->fuse_dot_slot >= 0) {
+    LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(ps[np - 1].grid),
+                       ctx->scal, ctx->fuse_dot_slot));
+    ctx->launches++;
+    LS_CUDA(cudaGetLastError());
+    if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + ctx->fuse_dot_slot));
+    ctx->fuse_dot_done = true;
+  }
+  return LS_OK;
+}
+
 static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
                       int64_t t_first, int64_t nout) {
   // auto (measured, tools/mv_variants.py, r01):
@@ -1329,6 +1431,12 @@ static int matvec_any(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   //   p >= 4: v3, DMMA band passes (config 4: 12.0 ms vs v1 16.4; config 5 p=8: 5.04 vs 6.49,
   //           p=4: 3.96 vs 4.08)
   //   (v2 / v3 have time passes for p_t >= 2 only; p_t = 1 runs v1)
+  // r02 (tools/mv_variants.py, L2 flushed): v4 (plane pass first) for d >= 2, p >= 3: config 4
+  //   10.1 ms (v3 11.5), config 5 p = 8 / 4: 3.70 / 2.95 ms (v3 3.95 / 3.33), config 3: 0.73 ms
+  //   (v1 0.75); p = 2 stays on v2 (config 5 p = 2: 2.18 ms vs v4 2.55)
+  if (ctx->mv_variant == 4 ||
+      (ctx->mv_variant == 0 && ctx->d >= 2 && ctx->p >= 3 && ctx->pt >= 2 && ctx->p <= 8 && ctx->pt <= 8))
+    return mv4_launch(ctx, x, y, rows, s_first, t_first, nout);
   if (ctx->mv_variant == 3 || (ctx->mv_variant == 0 && ctx->p >= 4 && ctx->pt >= 2))
     return mv3_launch(ctx, x, y, rows, s_first, t_first, nout);
   const bool v2 = ctx->mv_variant == 2 || (ctx->mv_variant == 0 && ctx->p == 2 && ctx->pt >= 2);
@@ -1461,6 +1569,18 @@ static int dot(ls_ctx* ctx, const double* a, const double* b, int slot) {
   return LS_OK;
 }
 
+// q = A p and scal[slot] = p.q: fused into the matvec's last pass when the v4 path runs,
+// otherwise ls_matvec + dot
+static int matvec_dot(ls_ctx* ctx, const double* p, double* q, int slot) {
+  ctx->fuse_dot_slot = ctx->geo ? -1 : slot;
+  ctx->fuse_dot_done = false;
+  const int rc = ls_matvec(ctx, p, q);
+  ctx->fuse_dot_slot = -1;
+  if (rc != LS_OK) return rc;
+  if (ctx->fuse_dot_done) return LS_OK;
+  return dot(ctx, p, q, slot);
+}
+
 static int read_scal(ls_ctx* ctx) {
   LS_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal, S_NSLOT * sizeof(double), cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -1498,8 +1618,7 @@ static int pcg_build_graph(ls_ctx* ctx, const double* b, double* x, double tol, 
   };
   // the iteration tail shared by the first iteration and the loop body
   auto tail = [&]() {
-    if (rc == LS_OK) rc = ls_matvec(ctx, p, q);
-    if (rc == LS_OK) rc = dot(ctx, p, q, S_PQ);
+    if (rc == LS_OK) rc = matvec_dot(ctx, p, q, S_PQ);
     if (rc != LS_OK) return;
     ck(launch_pdl(update_xr_kernel, gb, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
                   int(S_RHO0), ctx->partials));
@@ -1626,8 +1745,7 @@ extern "C" int pcg_solve(ls_ctx* ctx, const double* b, double* x, double tol, in
   s.status = LS_ENOCONV;
   const unsigned g = RED_BLOCKS;
   while (k < max_iter) {
-    LS_CHECK(ls_matvec(ctx, p, q));
-    LS_CHECK(dot(ctx, p, q, S_PQ));
+    LS_CHECK(matvec_dot(ctx, p, q, S_PQ));
     LS_CUDA(launch_pdl(update_xr_kernel, g, RED_THREADS, 0, ctx->stream, x, r, p, q, uint64_t(ctx->Nl), ctx->scal,
                        cur, ctx->partials));
     LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(RED_BLOCKS),
@@ -1870,7 +1988,7 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       ctx->fd_variant = value;
       return LS_OK;
     case LS_TUNE_MATVEC:
-      if (value < 0 || value > 3) return LS_EINVAL;
+      if (value < 0 || value > 4) return LS_EINVAL;
       ctx->mv_variant = value;
       if (ctx->geo) ctx->geo->variant = (value == 1) ? 1 : 0;  // mapped domain: 1 = DFMA stencil
       return LS_OK;
@@ -1885,6 +2003,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       if (Q % 4 != 0) return LS_ENOTSUP;  // the scattering epilogue is a FAST-path variant
       return ctx->comm->setup_fused(ctx->tmp[1], ctx->tmp[0]);
     }
+    case LS_TUNE_MV4_CTAS:  // process-wide: plane-pass register budget (CTAs per SM)
+      if (value != 1 && value != 2) return LS_EINVAL;
+      g_mv4_ctas = value;
+      return LS_OK;
     case LS_TUNE_FD_TAIL:
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->fd_tail = value;

@@ -30,7 +30,15 @@
 
 namespace ls {
 
-enum MV3Kind { MV3_TIME = 0, MV3_DIR = 1, MV3_DIR_A = 2, MV3_MID = 3, MV3_LAST = 4 };
+enum MV3Kind { MV3_TIME = 0, MV3_DIR = 1, MV3_DIR_A = 2, MV3_MID = 3, MV3_LAST = 4, MV3_D3 = 5, MV3_T2 = 6 };
+// v4 order (mv4_kernels.cuh: the plane pass of directions 1 + 2 comes first):
+//   MV3_D3 (direction 3): in (P_M, P_K, P_J) -> v1 = M P_M, v2 = J P_M + M P_J + 2K P_K, and on
+//                         the last time slice v3 = K P_M + M P_K (one slice, into a.v3)
+//   MV3_T2 (time):        in (v1, v2) -> y = K_t v1 + M_t v2 (+ v3 on the last time row: W_t)
+template <int KIND>
+struct MV3IsTime {
+  static constexpr bool v = KIND == MV3_TIME || KIND == MV3_T2;
+};
 
 struct MV3Args {
   const double* frag;  // [nmat][MT][NKB][32] band A-fragments of this pass' direction
@@ -51,15 +59,21 @@ struct MV3Args {
   uint32_t Qout;       // output row stride of strided passes (0: = Q)
   int map_n1, map_n1p; // time pass: padded column c' -> input column (c'/n1p)*n1 + c'%n1p (0: identity)
   int in_fiber, out_fiber;  // contiguous (MODE1) passes: fibre strides of input / output
+  double* v3;          // MV3_D3: output slice of the last time slice's v3 ([n][Q]); MV3_T2: input v3 ([Q])
+  // MV3_T2 only: fused PCG scalar p.q (SURVEY 3 pcg_solve) -- when dotp != nullptr every stored
+  // y element is multiplied by dotp at the same offset and the CTA's sum is written to
+  // dot_part[blockIdx.x] (fixed grid: deterministic)
+  const double* dotp;
+  double* dot_part;
 };
 
 template <int KIND>
 struct MV3IO {
   // ring inputs (the xT input of the direction-d pass is loaded without the ring: only
   // the warps holding last-slice columns need it)
-  static constexpr int NIN = (KIND == MV3_TIME) ? 1 : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? 2 : 3;
-  static constexpr int NOUT = (KIND == MV3_TIME) ? 2 : (KIND == MV3_DIR || KIND == MV3_MID) ? 3 : 1;
-  static constexpr int NMAT = (KIND == MV3_TIME) ? 2 : (KIND == MV3_LAST) ? 3 : 4;
+  static constexpr int NIN = (KIND == MV3_TIME) ? 1 : (KIND == MV3_DIR || KIND == MV3_DIR_A || KIND == MV3_T2) ? 2 : 3;
+  static constexpr int NOUT = (KIND == MV3_TIME || KIND == MV3_D3) ? 2 : (KIND == MV3_DIR || KIND == MV3_MID) ? 3 : 1;
+  static constexpr int NMAT = (KIND == MV3_TIME || KIND == MV3_T2) ? 2 : (KIND == MV3_LAST) ? 3 : 4;
 };
 
 template <int P, int KIND>
@@ -86,7 +100,11 @@ struct MV3Geom {
 #ifndef MV3_AHEAD3_HI
 #define MV3_AHEAD3_HI 2
 #endif
-  static constexpr int AHEAD = MV3IO<KIND>::NIN == 1 ? MV3_AHEAD1
+#ifndef MV3_AHEAD_T2
+#define MV3_AHEAD_T2 3
+#endif
+  static constexpr int AHEAD = KIND == MV3_T2 ? MV3_AHEAD_T2
+                               : MV3IO<KIND>::NIN == 1 ? MV3_AHEAD1
                                : MV3IO<KIND>::NIN == 2 ? MV3_AHEAD2
                                : (P <= 6 ? MV3_AHEAD3 : MV3_AHEAD3_HI);
   static constexpr int RING = NKB + 2 * AHEAD + (NKB & 1);  // even: static slots per RING/2 m-tiles
@@ -116,7 +134,9 @@ struct MV3Occ {
 #ifndef MV3_MID_CTAS
 #define MV3_MID_CTAS 1
 #endif
-  static constexpr int CTAS = (KIND == MV3_TIME) ? MV3_TIME_CTAS : (KIND == MV3_DIR || KIND == MV3_DIR_A) ? MV3_DIR_CTAS : MV3_MID_CTAS;
+  static constexpr int CTAS = (KIND == MV3_TIME) ? MV3_TIME_CTAS
+                              : (KIND == MV3_DIR || KIND == MV3_DIR_A || KIND == MV3_T2) ? MV3_DIR_CTAS
+                                                                                         : MV3_MID_CTAS;
 };
 
 template <int P, int NT, int KIND, bool MODE1, bool FAST>
@@ -139,12 +159,14 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
   const uint32_t Qo = a.Qout ? a.Qout : a.Q;
   const uint32_t nstrips = (ncols + TW - 1) / TW;
   // time pass: band row of stored input row 0 / of output row 0
-  const int gin0 = (KIND == MV3_TIME) ? a.s_first : 0;
-  const int in_rows = (KIND == MV3_TIME) ? a.s_rows : n;
-  const int gout0 = (KIND == MV3_TIME) ? a.t_first : 0;
-  const int nout = (KIND == MV3_TIME) ? a.nout : n;
+  constexpr bool TPASS = MV3IsTime<KIND>::v;
+  const int gin0 = TPASS ? a.s_first : 0;
+  const int in_rows = TPASS ? a.s_rows : n;
+  const int gout0 = TPASS ? a.t_first : 0;
+  const int nout = TPASS ? a.nout : n;
   const size_t rstride = MODE1 ? 1 : size_t(Q);
 
+  double dacc = 0.0;  // MV3_T2: fused p.q of this thread
   for (uint32_t strip = blockIdx.x * 8 + warp; strip < nstrips; strip += gridDim.x * 8) {
     // ---- this lane's B columns (NT) and store columns (2NT)
     const uint32_t cb = strip * TW + NT * nq;  // first B column
@@ -158,7 +180,7 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
       if (c < ncols) {
         bmask |= 1u << j;
         // the time pass has one column per (padded) spatial index: no slow index
-        const uint32_t pt = (KIND == MV3_TIME) ? 0u : c / Q, q = c - pt * Q;
+        const uint32_t pt = TPASS ? 0u : c / Q, q = c - pt * Q;
         if (MODE1) {
           boff[j] = c * uint32_t(a.in_fiber);
         } else if (KIND == MV3_TIME && a.map_n1) {  // padded column -> unpadded input column
@@ -168,11 +190,11 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
         } else {
           boff[j] = pt * uint32_t(in_rows) * Q + q;
         }
-        if (KIND == MV3_DIR || KIND == MV3_DIR_A) is_last |= int(pt) == a.tT;
+        if (KIND == MV3_DIR || KIND == MV3_DIR_A || KIND == MV3_D3) is_last |= int(pt) == a.tT;
       }
     }
     // W_t term: only warps holding a column of the last time slice do the xT products
-    const bool warp_last = (KIND == MV3_DIR || KIND == MV3_DIR_A) && __any_sync(0xffffffffu, is_last);
+    const bool warp_last = (KIND == MV3_DIR || KIND == MV3_DIR_A || KIND == MV3_D3) && __any_sync(0xffffffffu, is_last);
     // B fragment of input m, k-step ks (rows 4ks + kq) -> v[NT]
     auto loadB = [&](double (&v)[NT], int m, int ks) {
       const int row = 4 * ks + kq;           // band row
@@ -229,6 +251,9 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
           for (int o = 0; o < NOUT; ++o)
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[o][j][0] = acc[o][j][1] = 0.0;
+          double acc3[KIND == MV3_D3 ? NT : 1][2];  // MV3_D3: v3 of the last time slice
+#pragma unroll
+          for (int j = 0; j < (KIND == MV3_D3 ? NT : 1); ++j) acc3[j][0] = acc3[j][1] = 0.0;
           // sum over the NKB band k-steps: acc[o] += W_mat * ring[in]
 #pragma unroll
           for (int jk = 0; jk < NKB; ++jk) {
@@ -258,6 +283,21 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
                   for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[2][j], fr(0), xv[j]);
                 }
               }
+            } else if (KIND == MV3_D3) {     // mats: 0 M, 1 J, 2 K, 3 2K; in: P_M, P_K, P_J
+              mma(0, 0, 0);
+              mma(1, 1, 0);
+              mma(1, 0, 2);
+              mma(1, 3, 1);
+              if (warp_last) {
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                  dmma_8x8x4(acc3[j], fr(2), ring[0][slot][j]);
+                  dmma_8x8x4(acc3[j], fr(0), ring[1][slot][j]);
+                }
+              }
+            } else if (KIND == MV3_T2) {     // mats: 0 K_t, 1 M_t; in: v1, v2
+              mma(0, 0, 0);
+              mma(0, 1, 1);
             } else if (KIND == MV3_MID) {    // mats: 0 M, 1 J, 2 K, 3 2K; in: A, B, C
               mma(0, 0, 0);
               mma(0, 1, 1);
@@ -283,6 +323,25 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
           const int brow = 8 * mt + Gm::S0 + nq;  // band row
           const int lrow = brow - gout0;          // local output row (time pass: slab rows)
           if (brow < n && lrow >= 0 && lrow < nout) {
+            if (KIND == MV3_T2 && brow == n - 1) {  // W_t = e e^T: y_T += v3 (one slice, [Q])
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                  const uint32_t c = cs + NT * h + j;
+                  if (c < ncols) acc[0][j][h] += a.v3[c];
+                }
+            }
+            if (KIND == MV3_D3 && warp_last) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                  const uint32_t c = cs + NT * h + j;
+                  const uint32_t pt = c / Q;
+                  if (c < ncols && int(pt) == a.tT) a.v3[size_t(lrow) * Q + (c - pt * Q)] = acc3[j][h];
+                }
+            }
 #pragma unroll
             for (int o = 0; o < NOUT; ++o) {
               double* Y = a.out[o];
@@ -293,12 +352,21 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
                   // accumulator column 2kq + h of n-tile j = physical column cs + NT*h + j
                   if (NT == 1) {  // physical columns cs, cs + 1 = accumulator columns 2kq, 2kq + 1
                     *reinterpret_cast<double2*>(dst) = make_double2(acc[o][0][0], acc[o][0][1]);
+                    if (KIND == MV3_T2 && a.dotp) {
+                      const double2 pv = *reinterpret_cast<const double2*>(a.dotp + (dst - Y));
+                      dacc = fma(acc[o][0][0], pv.x, fma(acc[o][0][1], pv.y, dacc));
+                    }
                   } else {
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
 #pragma unroll
-                      for (int j = 0; j + 1 < NT; j += 2)
+                      for (int j = 0; j + 1 < NT; j += 2) {
                         *reinterpret_cast<double2*>(dst + NT * h + j) = make_double2(acc[o][j][h], acc[o][j + 1][h]);
+                        if (KIND == MV3_T2 && a.dotp) {
+                          const double2 pv = *reinterpret_cast<const double2*>(a.dotp + (dst - Y) + NT * h + j);
+                          dacc = fma(acc[o][j][h], pv.x, fma(acc[o][j + 1][h], pv.y, dacc));
+                        }
+                      }
                   }
                 }
               } else {
@@ -316,6 +384,7 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
                         o_off = (size_t(pt) * nout + lrow) * Qo + q;
                       }
                       Y[o_off] = acc[o][j][h];
+                      if (KIND == MV3_T2 && a.dotp) dacc = fma(acc[o][j][h], a.dotp[o_off], dacc);
                     }
                   }
               }
@@ -323,6 +392,19 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
           }
         }
       }
+    }
+  }
+  if (KIND == MV3_T2 && a.dotp) {  // CTA sum of the fused p.q in a fixed order
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    if (lane == 0) red[warp] = dacc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w];
+      a.dot_part[blockIdx.x] = t;
     }
   }
 }
@@ -333,9 +415,10 @@ struct MV3Pass {
   int kind;
   bool mode1;
   int p;  // degree of this pass' direction (time pass: p_t)
+  unsigned grid = 0;  // set by mv3_run: the grid launched (number of dot_part entries)
 };
 // p: spline degree; returns the CUDA error; *launches += kernels launched
-cudaError_t mv3_run(const MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
+cudaError_t mv3_run(MV3Pass* passes, int npass, int num_sms, cudaStream_t s, int64_t* launches);
 // dst[c'] = src[(c'/n1p)*n1 + c'%n1p] (0 in the padding) for one slice of Nsp padded columns
 cudaError_t mv3_pad_slice(const double* src, double* dst, int64_t nsp, int n1, int n1p, cudaStream_t s,
                           int64_t* launches);
@@ -344,5 +427,10 @@ int mv3_nkb(int p);
 int mv3_off(int p);
 int mv3_s0(int p);          // band row of the first m-tile's row 0 (<= 0)
 int mv3_mt(int p, int n);   // m-tiles covering [0, n)
+
+// v4 plane pass (mv4_kernels.cuh / mv4.cu)
+struct MV4PlaneArgs;
+cudaError_t mv4_plane_run(const MV4PlaneArgs& a, int p, int num_sms, cudaStream_t s);
+size_t mv4_plane_smem(int p, int mt2);
 
 }  // namespace ls

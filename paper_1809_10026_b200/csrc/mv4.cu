@@ -1,0 +1,52 @@
+// ls_matvec v4 plane-pass launches (mv4_kernels.cuh), one translation unit of their own.
+#include "mv4_kernels.cuh"
+
+#include <algorithm>
+
+namespace ls {
+
+extern int g_mv4_ctas;
+
+template <int P, int CTAS>
+static cudaError_t plane_c(const MV4PlaneArgs& a, int num_sms, cudaStream_t s) {
+  const size_t smem = size_t(4) * a.mt2 * MV4Geom<P>::NKB * 32 * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(mv4_plane_kernel<P, CTAS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 / CTAS);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int ctas = CTAS;
+  if (CTAS > 1 && smem * CTAS > 220 * 1024) ctas = 1;  // shared memory bounds the residency
+  const int64_t warps = a.nplanes * a.mt1;
+  const unsigned grid = unsigned(std::min<int64_t>((warps + 7) / 8, int64_t(num_sms) * ctas));
+  if (grid == 0) return cudaSuccess;
+  const cudaError_t e = launch_pdl(mv4_plane_kernel<P, CTAS>, grid, 256, smem, s, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <int P>
+static cudaError_t plane(const MV4PlaneArgs& a, int num_sms, cudaStream_t s) {
+  return g_mv4_ctas == 2 ? plane_c<P, 2>(a, num_sms, s) : plane_c<P, 1>(a, num_sms, s);
+}
+
+int g_mv4_ctas = 2;
+
+size_t mv4_plane_smem(int p, int mt2) { return size_t(4) * mt2 * (2 + (p + 1) / 2) * 32 * sizeof(double); }
+
+cudaError_t mv4_plane_run(const MV4PlaneArgs& a, int p, int num_sms, cudaStream_t s) {
+  switch (p) {
+    case 2: return plane<2>(a, num_sms, s);
+    case 3: return plane<3>(a, num_sms, s);
+    case 4: return plane<4>(a, num_sms, s);
+    case 5: return plane<5>(a, num_sms, s);
+    case 6: return plane<6>(a, num_sms, s);
+    case 7: return plane<7>(a, num_sms, s);
+    case 8: return plane<8>(a, num_sms, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ls

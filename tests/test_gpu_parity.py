@@ -156,12 +156,15 @@ MV_VARIANT_CASES = MV_CASES + [
 ]
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 @pytest.mark.parametrize("d,p,n_elems", MV_VARIANT_CASES)
 def test_matvec_variants_match_oracle(torch_cuda, variant, d, p, n_elems):
-    """Both ls_matvec implementations (ls_tune knob 2: 1 = four banded passes,
-    2 = three fused passes with Toeplitz stencils + boundary corrections)."""
+    """Every ls_matvec implementation (ls_tune knob 2: 1 = four banded passes,
+    2 = three fused passes with Toeplitz stencils + boundary corrections, 3 = four DMMA band
+    passes, 4 = DMMA plane pass + direction-3 / time passes, d >= 2)."""
     torch = torch_cuda
+    if variant == 4 and d < 2:
+        pytest.skip("v4 needs d >= 2 (LS_ENOTSUP)")
     ctx = _ctx(d, p, n_elems)
     ctx.tune(2, variant)
     space, tf, _ = _oracle(d, p, n_elems)
@@ -321,7 +324,7 @@ def test_pcg_nonconvergence_status(torch_cuda):
     assert st["status"] == ls.LS_ENOCONV and st["iters"] == 3 and st["rel_res"] > 1e-12
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 @pytest.mark.parametrize("d,p,n_elems,world", [(3, 6, [9, 8, 7, 40], 4), (3, 2, [6, 5, 7, 29], 3),
                                                 (2, 8, [20, 12, 37], 2), (1, 3, [30, 50], 5),
                                                 (3, 3, [12, 10, 8, 61], 8)])
@@ -331,6 +334,8 @@ def test_matvec_slab_decomposition(torch_cuda, variant, d, p, n_elems, world):
     for every rank of a `world`-way split, against the oracle's full A x."""
     import paper_1809_10026_b200 as ls
     torch = torch_cuda
+    if variant == 4 and d < 2:
+        pytest.skip("v4 needs d >= 2 (LS_ENOTSUP)")
     ctx = _ctx(d, p, n_elems)
     ctx.tune(2, variant)
     space, tf, _ = _oracle(d, p, n_elems)
@@ -456,7 +461,7 @@ def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
         assert _rel(zout.cpu().numpy(), z_ref) <= TOL, fdk
         assert bool((obig[:pad] == canary).all()) and bool((obig[pad + zout.numel():] == canary).all()), fdk
     ctx.tune(1, 0)
-    for mv in (1, 2, 3):
+    for mv in ((1, 2, 3, 4) if d >= 2 else (1, 2, 3)):
         ctx.tune(2, mv)
         _, xin, _ = _guarded(torch, ctx.shape, float("nan"))
         xin.copy_(torch.from_numpy(r))
@@ -493,8 +498,8 @@ def test_degrees_fd_matvec_rhs_pcg(torch_cuda, d, pp, n_elems):
     z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
     assert _rel(z, fd.fd_apply(r, fdd)) <= TOL
     y_ref = op.apply_A(r, space, tf)
-    for mv in (1, 2, 3):
-        if mv > 1 and pt < 2:
+    for mv in (1, 2, 3, 4):
+        if (mv > 1 and pt < 2) or (mv == 4 and d < 2):
             continue
         ctx.tune(2, mv)
         y = ctx.matvec(torch.from_numpy(r).cuda()).cpu().numpy()
@@ -519,13 +524,13 @@ def test_degrees_matvec_original_form_tiny(torch_cuda):
     A = op.dense_A_original_form([bs.open_uniform_knots(n, ps) for n in ne[:d]], ps,
                                  bs.open_uniform_knots(ne[d], pt), pt)
     x = synth.residual(ctx.shape, 31)
-    for mv in (1, 2, 3):
+    for mv in (1, 2, 3, 4):
         ctx.tune(2, mv)
         y = ctx.matvec(torch.from_numpy(x).cuda()).cpu().numpy().ravel()
         assert _rel(y, A @ x.ravel()) <= 1e-12, mv
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 def test_degrees_matvec_slab(torch_cuda, variant):
     """The halo of the distributed matvec is p_t slices wide."""
     import paper_1809_10026_b200 as ls

@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--variants", nargs="+", type=int, default=[1, 2])
 ap.add_argument("--pcg", action="store_true")
 ap.add_argument("--pad", type=int, default=0, help="ls_tune knob 3 (v3 row padding), 0 = default")
+ap.add_argument("--tune", nargs="*", default=[], help="extra ls_tune knob=value pairs applied before timing")
 a = ap.parse_args()
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
 for cs in a.configs:
@@ -34,6 +35,9 @@ for cs in a.configs:
     outs = {}
     if a.pad:
         ctx.tune(3, a.pad)
+    for kv in a.tune:
+        k, v = kv.split("=")
+        ctx.tune(int(k), int(v))
     for v in a.variants:
         ctx.tune(2, v)
         y = torch.empty_like(x)
