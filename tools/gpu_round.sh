@@ -8,6 +8,7 @@
 tag=${1:-r01}
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvidia_smi_$tag.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo "smoke_rc=$?"; tail -2 gpurun_out/smoke_$tag.log
 if [ "$2" != "notests" ]; then
   timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu_$tag.log 2>&1
   echo "pytest_rc=$?"; tail -3 gpurun_out/pytest_gpu_$tag.log
@@ -31,7 +32,7 @@ timeout 300 $P > gpurun_out/plain_prof_$tag.log 2>&1 && \
 echo "ncu_full_rc=$?"
 M="python tools/profile_fd.py --config 4 --reps 1 --matvec"
 timeout 300 $M > gpurun_out/plain_mv_$tag.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:band -c 4 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k 'regex:band|mv4_plane' -c 4 \
     -o gpurun_out/prof_mv_$tag -f $M > gpurun_out/ncu_mv_$tag.log 2>&1
 echo "ncu_mv_rc=$?"
 for r in gpurun_out/prof_c4_$tag gpurun_out/prof_mv_$tag; do
