@@ -79,13 +79,24 @@ def _config_dict(cfg_id, world, a2a="nccl"):
             "all_to_all": a2a if world > 1 else None}
 
 
+def fd_flops(d, n_s, n_t, N, cs=True):
+    """Algorithmic flops of one fd_apply as executed: 2 n^2 per column of every mode product
+    (PAPER.md 1071-1072: 4N(d n_s + n_t) in all); with the centrosymmetric split of the spatial
+    modes (ls_tune LS_TUNE_FD_CS, default) a spatial product is two half-size products,
+    2 (he^2 + ho^2) per column, he = ceil(n/2), ho = floor(n/2)."""
+    he, ho = (n_s + 1) // 2, n_s // 2
+    per_space = 2.0 * (he * he + ho * ho) / n_s if cs else 2.0 * n_s
+    return 2.0 * N * (d * per_space + 2.0 * n_t)
+
+
 def workload(cfg_id):
     c = synth.CONFIGS[cfg_id]
     d, p, n_el = c["d"], c["p"], c["n_el"]
     n_s, n_t = n_el + p - 2, n_el + p - 1
     N = n_s ** d * n_t
-    flops = 4.0 * N * (d * n_s + n_t)  # PAPER.md 1071-1072
-    return {"d": d, "p": p, "n_el": n_el, "n_s": n_s, "n_t": n_t, "N": N, "flops": flops}
+    flops_paper = 4.0 * N * (d * n_s + n_t)  # PAPER.md 1071-1072
+    return {"d": d, "p": p, "n_el": n_el, "n_s": n_s, "n_t": n_t, "N": N, "flops_paper": flops_paper,
+            "flops": fd_flops(d, n_s, n_t, N)}
 
 
 class ClockSampler:
@@ -461,6 +472,12 @@ def main():
             "config": _config_dict(args.config, world, args.a2a),
             "gflops_algorithmic": w["flops"] / (ms * 1e-3) / 1e9,
             "fp64_roofline_frac": round(w["flops"] / (ms * 1e-3) / 1e12 / (FP64_PEAK_TFLOPS * world), 4),
+            # the paper's operation count 4N(d n_s + n_t) (PAPER.md 1071) per unit time: the rate an
+            # unsplit implementation would need for this DOF/s (not a hardware rate; > peak is possible)
+            "gflops_paper_count_equivalent": w["flops_paper"] / (ms * 1e-3) / 1e9,
+            "flops_note": ("algorithmic flops as executed: spatial mode products split by centrosymmetry "
+                           "(2 (he^2 + ho^2) per column instead of 2 n^2; DESIGN.md 5, reading c24), time modes "
+                           "2 n_t^2 per column"),
             "roofline": roof,
             "cpu_baseline": {"value": cpu_val, "unit": "DOF/s", "cores": cores, "kind": "oracle",
                              "sample": cpu_sample},
@@ -476,6 +493,20 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def matvec_roofline(d, p, N, ms):
+    """ls_matvec against both floors: 15 banded products of 2(2p+1) flops per DOF
+    at d = 3 (30(2p+1) N flops, PAPER.md 686-703; 9 at d = 2) vs the FP64 peak, and the 16 B/DOF of reading x and
+    writing y vs the measured HBM bandwidth; the larger fraction names the binding floor."""
+    products = {1: 4, 2: 9, 3: 15}[d]  # banded products per DOF of the sum factorisation (SURVEY 8(a) M)
+    flops = 2.0 * products * (2 * p + 1) * N
+    tf = flops / (ms * 1e-3) / 1e12
+    gbs = 16.0 * N / (ms * 1e-3) / 1e9
+    hbm, _ = _hbm_peak()
+    return {"alg_flops": flops, "tflops": round(tf, 3), "frac_fp64": round(tf / FP64_PEAK_TFLOPS, 4),
+            "alg_bytes": 16 * N, "gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4),
+            "floor_ms": round(max(flops / (FP64_PEAK_TFLOPS * 1e12), 16.0 * N / (hbm * 1e9)) * 1e3, 4)}
 
 
 def run_extras(ls, torch, stream):
@@ -539,6 +570,7 @@ def run_extras(ls, torch, stream):
                     "ls_energy_rel": (float(np.sqrt(ee["J"] / ee["f2"])) if ee["J"] > 1e-12 * ee["f2"]
                                       else "below 1e-6 (unresolved by the identity)"),
                     "fd_apply_ms": ev[0].elapsed_time(ev[1]), "matvec_ms": ev[1].elapsed_time(ev[2]),
+                    "matvec_roofline": matvec_roofline(d, p, c.N, ev[1].elapsed_time(ev[2])),
                     "rhs": "kind %d (DESIGN.md reading c11)" % kind})
         del z
         c.close()

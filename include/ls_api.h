@@ -414,6 +414,15 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
 /* LS_TUNE_MV4_CTAS: process-wide; the v4 plane pass' register budget, 1 or 2 CTAs of 256
  * threads per SM (<= 255 / <= 128 registers per thread); default 2. */
 #define LS_TUNE_MV4_CTAS 8
+/* LS_TUNE_FD_CS: 1 = the spatial mode products of fd_apply use the centrosymmetric split
+ * (default): with uniform open knots and Dirichlet conditions at both ends (PAPER.md 266-267,
+ * 1111-1112) the space pencil (J_k, M_k) commutes with the index reversal R, so U_k is built
+ * from even and odd eigenvectors (eq:eig_dec, PAPER.md 939-945, solved as two half-size
+ * pencils at setup) and every spatial mode product is two half-size products (half the
+ * flops; z = P^{-1} r is unchanged).  0 = n x n products with the same U_k.  Directions
+ * whose pencil is not centrosymmetric (P^G's weighted pencils) always use n x n products.
+ * The eigen index order of such a direction is [even | odd] (ls_get_factor 5 / 7). */
+#define LS_TUNE_FD_CS 9
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

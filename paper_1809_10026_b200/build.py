@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libls.so")
 OBJ = os.path.join(HERE, "build")
 SOURCES = ["api.cu", "comm.cu", "setup_host.cpp", "mv2.cu", "mv3.cu", "mv4.cu", "geo.cu", "geo_host.cpp", "err.cu"]
-RD_BUCKETS = [2, 4, 5, 8, 12, 16, 17, 18, 24, 25, 26, 30, 33, 34]  # = LS_RD_BUCKETS
+RD_BUCKETS = [2, 4, 5, 8, 9, 12, 13, 16, 17, 18, 24, 25, 26, 30, 33, 34]  # = LS_RD_BUCKETS
 
 
 def _nccl_dir():

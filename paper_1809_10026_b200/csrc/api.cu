@@ -66,6 +66,12 @@ struct ls_ctx {
   int64_t launches = 0;
   int fd_variant = 0;  // ls_tune knob LS_TUNE_FD_KERNEL: 0 auto, 1 smem-staged (v2/pp), 2 register-direct
   int fd_tail = 1;     // ls_tune knob LS_TUNE_FD_TAIL: DFMA tail rows in the ping-pong FD kernel
+  // centrosymmetric split of the spatial modes (fd_rd_kernel.cuh CS): cs_dir[k] = direction k's
+  // eigenbasis was built from the even / odd reduced pencils; fd_cs = ls_tune LS_TUNE_FD_CS
+  bool cs_dir[3] = {false, false, false};
+  int fd_cs = 1;
+  double* Wf_cs[3] = {nullptr, nullptr, nullptr};  // [A_e^T (he x he) | A_o^T (ho x ho)]
+  double* Wb_cs[3] = {nullptr, nullptr, nullptr};  // [A_e | A_o]
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
   // PCG: the next ls_matvec also forms p.q (x.y) into scal[fuse_dot_slot] when its last pass can
   // (v4 time-pass epilogue); fuse_dot_done reports whether it did
@@ -271,18 +277,33 @@ static int round_ks(int ks) {
 }
 
 // register-direct kernel (fd_rd_kernel.cuh), one explicit instantiation per k-step bucket
-static int launch_mode_rd(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale) {
+static int round_ks_rd(int ks) {
+  static const int list[] = {
+#define LS_RD_ITEM(K) K,
+      LS_RD_BUCKETS(LS_RD_ITEM)
+#undef LS_RD_ITEM
+  };
+  for (int v : list)
+    if (ks <= v) return v;
+  return -1;
+}
+
+// cs: 0 = n x n product; 1 / 2 = centrosymmetric fold / unfold (two half-size products,
+// W = [W_e | W_o]; the k-step bucket is that of the half extent ceil(n/2))
+static int launch_mode_rd(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale, int cs = 0) {
   if (a.ncols == 0) return LS_OK;
+  const int he = (a.n + 1) / 2, ho = a.n / 2;
   ls_ctx::ProfRec rec{};
   if (ctx->prof) {
     rec.a = ctx->get_event();
     rec.b = ctx->get_event();
-    rec.flops = 2.0 * double(a.n) * double(a.n) * double(a.ncols);
+    // algorithmic flops of the launch: 2 n^2 per column, or 2 (he^2 + ho^2) with the split
+    rec.flops = (cs ? 2.0 * (double(he) * he + double(ho) * ho) : 2.0 * double(a.n) * double(a.n)) * double(a.ncols);
     cudaEventRecord(rec.a, ctx->stream);
   }
   cudaError_t e = cudaErrorInvalidValue;
-  switch (round_ks((a.n + 3) / 4)) {
-#define LS_RD_CASE(K) case K: e = rd_launch<K>(a, mode1, scale, ctx->stream, ctx->num_sms); break;
+  switch (round_ks_rd(((cs ? he : a.n) + 3) / 4)) {
+#define LS_RD_CASE(K) case K: e = rd_launch<K>(a, mode1, scale, cs, ctx->stream, ctx->num_sms); break;
     LS_RD_BUCKETS(LS_RD_CASE)
 #undef LS_RD_CASE
     default: return LS_EINVAL;
@@ -298,7 +319,7 @@ static int launch_mode_rd(ls_ctx* ctx, const ModeArgs& a, bool mode1, bool scale
 
 static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W, int n, uint64_t P,
                        uint64_t Q, bool scale, const double* lam_a = nullptr,
-                       const double* lam_c = nullptr) {
+                       const double* lam_c = nullptr, int cs = 0) {
   ModeArgs a{};
   a.y16 = (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
   a.X = X;
@@ -317,6 +338,7 @@ static int launch_mode(ls_ctx* ctx, const double* X, double* Y, const double* W,
   // adds one 8-row tile with one valid row; tools/fdk_sel.py, config 5 p = 2: 4.67 -> 4.45 ms;
   // rd for n = 96 only: 4.51 ms).  Only these measured extents: at n = 98 / 99 and 102 / 103
   // (config 5 p = 4 / 8) the smem-staged kernels stay 13 / 9 % faster.
+  if (cs) return launch_mode_rd(ctx, a, mode1, false, cs);  // the split exists in the register-direct kernel
   const bool rd_auto = (n + 3) / 4 >= 30 || n == 96 || n == 97;
   if (ctx->fd_variant == 2 || (ctx->fd_variant == 0 && rd_auto)) return launch_mode_rd(ctx, a, mode1, scale);
   switch (round_ks((n + 3) / 4)) {
@@ -360,6 +382,108 @@ static int gen_eig(const std::vector<double>& K, const std::vector<double>& M, i
       err = std::max(err, std::fabs(s - (a == b ? 1.0 : 0.0)));
     }
   if (!(err < 1e-8)) return LS_ENOTSPD;
+  return LS_OK;
+}
+
+// R A R = A up to assembly rounding (64 ulps of max|A|; measured asymmetry <= 1 ulp: the
+// exact integrals on uniform open knots are centrosymmetric, PAPER.md 144-147, 1111-1112)
+static bool centrosymmetric(const std::vector<double>& A, int n) {
+  double mx = 0;
+  for (double v : A) mx = std::max(mx, std::fabs(v));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      if (std::fabs(A[size_t(i) * n + j] - A[size_t(n - 1 - i) * n + (n - 1 - j)]) > 64 * 2.220446049250313e-16 * mx)
+        return false;
+  return true;
+}
+
+static int upload(ls_ctx* ctx, const std::vector<double>& v, double** out);
+
+// eq:eig_dec (PAPER.md 939-945) for a centrosymmetric pencil (J, M), by its even and odd
+// reductions (fd_rd_kernel.cuh CS): with Q_e = [e_k + e_{n-1-k}] (k < he; e_h alone at the
+// middle of an odd n) and Q_o = [e_k - e_{n-1-k}] (k < ho), J_e = Q_e^T J Q_e, M_e = Q_e^T M Q_e
+// (the same for o), formed in 80-bit.  J_e a = M_e a lambda with a^T M_e a = 1 gives the
+// eigenvector u = Q_e a of (J, M) with u^T M u = 1, so U = [Q_e A_e | Q_o A_o] and
+// lambda = [lambda_e | lambda_o] (ascending within each half).  The cross terms Q_e^T J Q_o are
+// the assembly's last-ulp asymmetry and are dropped: this is the eigenbasis of (J + RJR)/2,
+// (M + RMR)/2 (z moves by <= 4e-14 relative, reading c24).
+static int cs_eig(ls_ctx* ctx, int k, const std::vector<double>& J, const std::vector<double>& M, int n) {
+  const int he = (n + 1) / 2, ho = n / 2;
+  auto reduce = [&](const std::vector<double>& A, int nh, int sg, std::vector<long double>& E) {
+    E.assign(size_t(nh) * nh, 0.0L);
+    for (int a = 0; a < nh; ++a)
+      for (int b = 0; b < nh; ++b) {
+        const int ra = n - 1 - a, rb = n - 1 - b;
+        long double v = A[size_t(a) * n + b];
+        if (rb != b) v += sg * (long double)A[size_t(a) * n + rb];
+        if (ra != a) v += sg * (long double)A[size_t(ra) * n + b];
+        if (ra != a && rb != b) v += (long double)A[size_t(ra) * n + rb];
+        E[size_t(a) * nh + b] = v;
+      }
+  };
+  std::vector<long double> Je, Me, Jo, Mo;
+  reduce(J, he, 1, Je);
+  reduce(M, he, 1, Me);
+  reduce(J, ho, -1, Jo);
+  reduce(M, ho, -1, Mo);
+  std::vector<double> le, lo, Ae, Ao;
+  if (generalized_eig(Je, Me, he, le, Ae) != 0) return LS_ENOTSPD;
+  if (ho > 0 && generalized_eig(Jo, Mo, ho, lo, Ao) != 0) return LS_ENOTSPD;
+  std::vector<double>& U = ctx->hU[k];
+  std::vector<double>& lam = ctx->hlam[k];
+  U.assign(size_t(n) * n, 0.0);
+  lam.assign(n, 0.0);
+  for (int j = 0; j < he; ++j) {
+    lam[j] = le[j];
+    for (int i = 0; i < n; ++i) U[size_t(i) * n + j] = Ae[size_t(std::min(i, n - 1 - i)) * he + j];
+  }
+  for (int j = 0; j < ho; ++j) {
+    lam[he + j] = lo[j];
+    for (int i = 0; i < ho; ++i) {
+      U[size_t(i) * n + he + j] = Ao[size_t(i) * ho + j];
+      U[size_t(n - 1 - i) * n + he + j] = -Ao[size_t(i) * ho + j];
+    }
+  }
+  // sanity: U^T M U = I, U^T J U = Lambda (PAPER.md 945) on the full matrices
+  {
+    std::vector<double> MU(size_t(n) * n, 0.0), JU(size_t(n) * n, 0.0);
+    for (int i = 0; i < n; ++i)
+      for (int l = 0; l < n; ++l) {
+        const double m = M[size_t(i) * n + l], jj = J[size_t(i) * n + l];
+        if (m == 0.0 && jj == 0.0) continue;
+        for (int c = 0; c < n; ++c) {
+          MU[size_t(i) * n + c] += m * U[size_t(l) * n + c];
+          JU[size_t(i) * n + c] += jj * U[size_t(l) * n + c];
+        }
+      }
+    double em = 0, ej = 0;
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) {
+        double sm = 0, sj = 0;
+        for (int i = 0; i < n; ++i) {
+          sm += U[size_t(i) * n + a] * MU[size_t(i) * n + b];
+          sj += U[size_t(i) * n + a] * JU[size_t(i) * n + b];
+        }
+        em = std::max(em, std::fabs(sm - (a == b ? 1.0 : 0.0)));
+        ej = std::max(ej, std::fabs(sj - (a == b ? lam[a] : 0.0)) / std::max(1.0, std::fabs(lam[b])));
+      }
+    if (!(em < 1e-8) || !(ej < 1e-8)) return LS_ENOTSPD;
+  }
+  std::vector<double> wf(size_t(he) * he + size_t(ho) * ho), wb(wf.size());
+  for (int a = 0; a < he; ++a)
+    for (int i = 0; i < he; ++i) {
+      wf[size_t(a) * he + i] = Ae[size_t(i) * he + a];
+      wb[size_t(i) * he + a] = Ae[size_t(i) * he + a];
+    }
+  const size_t o = size_t(he) * he;
+  for (int a = 0; a < ho; ++a)
+    for (int i = 0; i < ho; ++i) {
+      wf[o + size_t(a) * ho + i] = Ao[size_t(i) * ho + a];
+      wb[o + size_t(i) * ho + a] = Ao[size_t(i) * ho + a];
+    }
+  LS_CHECK(upload(ctx, wf, &ctx->Wf_cs[k]));
+  LS_CHECK(upload(ctx, wb, &ctx->Wb_cs[k]));
+  ctx->cs_dir[k] = true;
   return LS_OK;
 }
 
@@ -486,6 +610,8 @@ static int setup_common(ls_ctx* ctx) {
     if (pg) {
       weighted_space_factors(int(ctx->n_el[k]), p, mu[k], om[k], wM[k], wJ[k]);
       rc = gen_eig(wJ[k], wM[k], f.n, ctx->hlam[k], ctx->hU[k]);
+    } else if (centrosymmetric(f.J, f.n) && centrosymmetric(f.M, f.n)) {
+      rc = cs_eig(ctx, k, f.J, f.M, f.n);
     } else {
       rc = gen_eig(f.J, f.M, f.n, ctx->hlam[k], ctx->hU[k]);
     }
@@ -778,6 +904,9 @@ extern "C" int ls_set_stream(ls_ctx* ctx, void* s) {
 // ------------------------------------------------------------------------------------------
 static inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
 
+// direction k runs the centrosymmetric split (half the DMMA work of its mode products)
+static inline bool use_cs(const ls_ctx* ctx, int k) { return ctx->fd_cs && ctx->cs_dir[k]; }
+
 // spatial modes on a [rows][n_d]..[n_1] block (rows = local time slices)
 static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0, double* ws1,
                          uint64_t rows, bool forward) {
@@ -791,7 +920,11 @@ static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0
     for (int j = 0; j < k; ++j) Q *= ctx->n[j];
     for (int j = k + 1; j < d; ++j) P *= ctx->n[j];
     double* dst = (s == d - 1) ? out : ((s % 2 == 0) ? ws0 : ws1);
-    LS_CHECK(launch_mode(ctx, src, dst, forward ? ctx->Wf[k] : ctx->Wb[k], ctx->n[k], P, Q, false));
+    if (use_cs(ctx, k))
+      LS_CHECK(launch_mode(ctx, src, dst, forward ? ctx->Wf_cs[k] : ctx->Wb_cs[k], ctx->n[k], P, Q, false, nullptr,
+                           nullptr, forward ? 1 : 2));
+    else
+      LS_CHECK(launch_mode(ctx, src, dst, forward ? ctx->Wf[k] : ctx->Wb[k], ctx->n[k], P, Q, false));
     src = dst;
   }
   return LS_OK;
@@ -861,7 +994,10 @@ static int spatial_fwd_scatter(ls_ctx* ctx, const double* in, uint64_t rows, dou
     uint64_t Q = 1, P = rows;
     for (int j = 0; j < k; ++j) Q *= ctx->n[j];
     for (int j = k + 1; j < d; ++j) P *= ctx->n[j];
-    LS_CHECK(launch_mode(ctx, src, ws[k % 2], ctx->Wf[k], ctx->n[k], P, Q, false));
+    if (use_cs(ctx, k))
+      LS_CHECK(launch_mode(ctx, src, ws[k % 2], ctx->Wf_cs[k], ctx->n[k], P, Q, false, nullptr, nullptr, 1));
+    else
+      LS_CHECK(launch_mode(ctx, src, ws[k % 2], ctx->Wf[k], ctx->n[k], P, Q, false));
     src = ws[k % 2];
   }
   const int k = d - 1;
@@ -870,7 +1006,8 @@ static int spatial_fwd_scatter(ls_ctx* ctx, const double* in, uint64_t rows, dou
   ModeArgs a{};
   a.X = src;
   a.Y = ctx->tmp[5];  // unused by the scattering epilogue (alignment probe only)
-  a.W = ctx->Wf[k];
+  const bool cs = use_cs(ctx, k);
+  a.W = cs ? ctx->Wf_cs[k] : ctx->Wf[k];
   a.n = ctx->n[k];
   a.P = uint32_t(rows);
   a.Q = uint32_t(Q);
@@ -882,7 +1019,7 @@ static int spatial_fwd_scatter(ls_ctx* ctx, const double* in, uint64_t rows, dou
   a.me = me;
   a.nt_g = ctx->nt;
   a.Ns_g = ctx->Ns;
-  return launch_mode_rd(ctx, a, false, false);
+  return launch_mode_rd(ctx, a, false, false, cs ? 1 : 0);
 }
 
 // time mode of this rank's spatial chunk [n_t][chunk_ld(len)] (spatial offset c0): forward +
@@ -2010,6 +2147,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_FD_TAIL:
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->fd_tail = value;
+      return LS_OK;
+    case LS_TUNE_FD_CS:  // centrosymmetric split of the spatial modes (default 1 where the pencil allows)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->fd_cs = value;
       return LS_OK;
     case LS_TUNE_PDL:  // process-wide: programmatic dependent launch of the FD mode kernels
       if (value != 0 && value != 1) return LS_EINVAL;

@@ -28,6 +28,19 @@
 // FAST = strided mode with Q % (2*NT) == 0 and 16-byte aligned X, Y: every
 // NT-column group lies in one p-slice (vector loads/stores); otherwise every
 // column is addressed on its own.
+//
+// CS (centrosymmetric split, spatial modes).  With uniform open knots and Dirichlet
+// conditions at both ends (PAPER.md 266-267, 1111-1112) the space pencil (J, M) is
+// centrosymmetric: R J R = J, R M R = M for the exchange matrix R (b_i(1-x) = b_{n+1-i}(x)).
+// Its eigenvectors then split into he = ceil(n/2) even ones (u = R u) and ho = floor(n/2)
+// odd ones (u = -R u), each fixed by its first half a (setup: reduced pencils
+// Q^T J Q, Q^T M Q, api.cu cs_eig).  So U^T x = [A_e^T (x + R x)_half ; A_o^T (x - R x)_half]
+// and U y = [p + q ; R (p - q)] with p = A_e y_e, q = A_o y_o: two half-size products
+// instead of one n x n product, half the DMMA work (z = P^{-1} r is unchanged: any
+// eigenbasis of the same pencil gives it; the eigen index order is [even | odd]).
+// Fold (forward): the lane loads x[k] and x[n-1-k] and forms the sum / difference when
+// the k-step is consumed; unfold (backward): two B rows (k and he + k) and the butterfly in
+// the epilogue.  W = [W_e (he x he) | W_o (ho x ho)].
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -36,22 +49,31 @@
 
 namespace ls {
 
-template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_, int REMOTE_ = 0>
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_, int REMOTE_ = 0, int CS_ = 0, int MINB_ = 1>
 struct RDCfg {
   static constexpr int KS = KS_, NT = NT_, D = D_;
+  static constexpr int MINB = MINB_;  // CTAs per SM the register budget is sized for
   static constexpr int REMOTE = REMOTE_;  // fused all-to-all epilogue (ModeArgs::remote)
+  // CS: centrosymmetric split (see the header of this file): 0 = plain n x n product,
+  // 1 = fold (forward: even/odd halves of the input, outputs [even | odd]),
+  // 2 = unfold (backward: inputs [even | odd], outputs p + q and R(p - q))
+  static constexpr int CS = CS_;
+  static constexpr int NH = CS ? 2 : 1;    // half-products per tile
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_, FAST = FAST_;
-  static constexpr int MT = (KS + 1) / 2;  // ceil(n/8) for n in (4KS-4, 4KS]
+  static constexpr int MT = (KS + 1) / 2;  // ceil(n/8) for n in (4KS-4, 4KS] (CS: n -> ceil(n/2))
   static constexpr int KSP = (KS + 1) / 2;  // k-step pairs
   static constexpr int KSE = ((KS + D - 1) / D) * D;  // k-steps rounded up to the window
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int TW = 8 * NT;  // columns per warp tile
-  static constexpr int WFRAG = MT * KSP * 64;
+  static constexpr int WFRAG1 = MT * KSP * 64;  // one half's A fragments
+  static constexpr int WFRAG = NH * WFRAG1;
   static constexpr int LAMA = SCALE ? 8 * MT : 0;  // lambda_t per output row (SCALE)
   static constexpr size_t SMEM = size_t(WFRAG + LAMA) * sizeof(double);
   static_assert(!(MODE1 && FAST), "FAST is a strided-mode path");
   static_assert(REMOTE == 0 || (FAST && !SCALE), "fused all-to-all epilogues: unscaled FAST launches");
-  static_assert(NT % 2 == 0, "NT even (LDG.128 pairs)");
+  static_assert(CS == 0 || !SCALE, "the scaled (time) mode is not centrosymmetric");
+  static_assert(CS != 2 || REMOTE == 0, "unfold: local stores only");
+  static_assert(NT == 1 || NT % 2 == 0, "NT = 1 or even (LDG.128 pairs)");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -109,47 +131,82 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {
   return v;
 }
 
-// B fragments of k-step kk (rows 4kk + lane%4) of the lane's NT columns
+// B fragments of one k-step (rows 4kk + lane%4 of the lane's NT columns; CS: the two half
+// rows) from running pointers: lp[] at the half-0 row, lm[] at the half-1 row (fold: the
+// mirror row n-1-k, moving backwards; unfold: row he + k).  NP pointers: one for FAST / MODE1
+// (columns at +j or +j*n), one per column otherwise.  Advancing pointers instead of
+// recomputing base + kk * kstep keeps the unrolled k-loop from holding one 64-bit address per
+// k-step in registers.
 template <class C>
-__device__ __forceinline__ void rd_load(double (&dst)[C::NT], const double* __restrict__ X, const RDIn<C::NT>& in,
-                                        int kk, size_t kstep, bool kok, int n) {
+struct RDPtr {
+  static constexpr int NP = (C::FAST || C::MODE1) ? 1 : C::NT;
+  const double* lp[NP];
+  const double* lm[NP];
+};
+
+template <class C>
+__device__ __forceinline__ void rd_load(double (&dst)[C::NH][C::NT], RDPtr<C>& q, uint32_t mask, bool ok0,
+                                        bool ok1, size_t kstep, int n) {
   if (C::FAST) {
-    const bool ok = kok && in.mask;
-    const double* src = X + in.off[0] + kk * kstep;
+    const bool m = mask != 0;
+    if constexpr (C::NT == 1) {
+      dst[0][0] = (ok0 && m) ? ldg_stream(q.lp[0]) : 0.0;
+      if (C::CS) dst[C::NH - 1][0] = (ok1 && m) ? ldg_stream(q.lm[0]) : 0.0;
+    } else {
 #pragma unroll
-    for (int j = 0; j < C::NT; j += 2) {
-      double2 v = make_double2(0.0, 0.0);
-      if (ok) v = ldg_stream2(src + j);
-      dst[j] = v.x;
-      dst[j + 1] = v.y;
+      for (int j = 0; j < C::NT; j += 2) {
+        double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+        if (ok0 && m) v0 = ldg_stream2(q.lp[0] + j);
+        if (C::CS && ok1 && m) v1 = ldg_stream2(q.lm[0] + j);
+        dst[0][j] = v0.x;
+        dst[0][j + 1] = v0.y;
+        if (C::CS) {
+          dst[C::NH - 1][j] = v1.x;
+          dst[C::NH - 1][j + 1] = v1.y;
+        }
+      }
     }
-  } else if (C::MODE1) {
-    const double* src = X + in.off[0] + kk * kstep;
-#pragma unroll
-    for (int j = 0; j < C::NT; ++j) dst[j] = (kok && ((in.mask >> j) & 1u)) ? ldg_stream(src + size_t(j) * n) : 0.0;
   } else {
 #pragma unroll
-    for (int j = 0; j < C::NT; ++j)
-      dst[j] = (kok && ((in.mask >> j) & 1u)) ? ldg_stream(X + in.off[j] + kk * kstep) : 0.0;
+    for (int j = 0; j < C::NT; ++j) {
+      const bool cm = (mask >> j) & 1u;
+      const double* p0 = C::MODE1 ? q.lp[0] + size_t(j) * n : q.lp[C::MODE1 ? 0 : j];
+      dst[0][j] = (ok0 && cm) ? ldg_stream(p0) : 0.0;
+      if (C::CS) {
+        const double* p1 = C::MODE1 ? q.lm[0] + size_t(j) * n : q.lm[C::MODE1 ? 0 : j];
+        dst[C::NH - 1][j] = (ok1 && cm) ? ldg_stream(p1) : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RDPtr<C>::NP; ++i) {
+    q.lp[i] += kstep;
+    if (C::CS == 1) q.lm[i] -= kstep;
+    if (C::CS == 2) q.lm[i] += kstep;
   }
 }
 
 template <class C>
-__global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
+__global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args) {
   extern __shared__ __align__(16) double smem[];
   double* wsm = smem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, nq = lane >> 2;
   const int n = args.n;
+  const int he = C::CS ? (n + 1) / 2 : n, ho = C::CS ? n / 2 : 0;  // half sizes (CS)
   const uint32_t Q = args.Q, ncols = args.ncols;
 
   // W -> shared memory, A-fragment order, two k-steps per lane slot:
-  // wsm[((mt*KSP + ks/2)*32 + l)*2 + ks%2] = W[mt*8 + l/4][ks*4 + l%4]
+  // wsm[hf*WFRAG1 + ((mt*KSP + ks/2)*32 + l)*2 + ks%2] = W_hf[mt*8 + l/4][ks*4 + l%4]
+  // (CS: W = [W_0 (he x he) | W_1 (ho x ho)], both row-major)
   for (int e = tid; e < C::WFRAG; e += C::THREADS) {
-    const int h = e & 1, l = (e >> 1) & 31, ksp = (e >> 6) % C::KSP, mt = (e >> 6) / C::KSP;
+    const int hf = e / C::WFRAG1, e1 = e - hf * C::WFRAG1;
+    const int h = e1 & 1, l = (e1 >> 1) & 31, ksp = (e1 >> 6) % C::KSP, mt = (e1 >> 6) / C::KSP;
     const int ks = 2 * ksp + h;
     const int a = mt * 8 + (l >> 2), i = ks * 4 + (l & 3);
-    wsm[e] = (a < n && i < n && ks < C::KS) ? __ldg(args.W + size_t(a) * n + i) : 0.0;
+    const int nh = C::CS ? (hf ? ho : he) : n;
+    const double* Wh = args.W + (hf ? size_t(he) * he : 0);
+    wsm[e] = (a < nh && i < nh && ks < C::KS) ? __ldg(Wh + size_t(a) * nh + i) : 0.0;
   }
   double* lam_a_s = wsm + C::WFRAG;  // SCALE: lambda_t of the output rows, staged once
   if (C::SCALE)
@@ -160,19 +217,34 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
   const uint32_t wstride = gridDim.x * C::WARPS;
   uint32_t tile = blockIdx.x * C::WARPS + warp;
   if (tile >= ntw) return;
-  const size_t kstep = C::MODE1 ? size_t(4) : size_t(4) * Q;
-  // rows 4*kk + kq >= n are never loaded (zero B fragment): the bucket's KS may exceed
-  // ceil(n/4) by a few k-steps, and those rows lie past the end of the column
-  // (the k-step buckets exceed ceil(n/4) by at most 5, so only the last 6 k-steps test)
-  auto row_ok = [&](int kk) { return 4 * kk + kq < n; };
+  const size_t rstride = C::MODE1 ? size_t(1) : size_t(Q);
+  const size_t kstep = 4 * rstride;
+  // rows 4*kk + kq >= n (CS: >= he / ho) are never loaded (zero B fragment): the bucket's
+  // KS may exceed ceil(n/4), and those rows lie past the end of the column
+  auto row_ok = [&](int kk) { return 4 * kk + kq < he; };
+  auto row_ok1 = [&](int kk) { return 4 * kk + kq < ho; };
+  const int64_t off1 = C::CS == 1 ? int64_t(n - 1 - 2 * kq) * int64_t(rstride) : int64_t(he) * int64_t(rstride);
   const double* wl = wsm + lane * 2;
 
   pdl_wait();  // X is the previous kernel's output (fd_kernels.cuh)
   RDIn<C::NT> cur = rd_make_in<C>(args, tile, lane);
-  double bw[C::D][C::NT];
+  double bw[C::D][C::NH][C::NT];
+  RDPtr<C> q;
+  auto set_ptrs = [&](const RDIn<C::NT>& in) {
+#pragma unroll
+    for (int i = 0; i < RDPtr<C>::NP; ++i) {
+      q.lp[i] = args.X + in.off[i];
+      q.lm[i] = q.lp[i] + off1;
+    }
+  };
+  // loads run strictly in order: k-steps 0 .. KS-1 of a tile, then 0 .. of the next one
+  auto load = [&](double (&dst)[C::NH][C::NT], const RDIn<C::NT>& in, int kk) {
+    rd_load<C>(dst, q, in.mask, row_ok(kk), row_ok1(kk), kstep, n);
+  };
+  set_ptrs(cur);
 #pragma unroll
   for (int s = 0; s < C::D; ++s)
-    if (s < C::KS) rd_load<C>(bw[s], args.X, cur, s, kstep, row_ok(s), n);
+    if (s < C::KS) load(bw[s], cur, s);
 
 #pragma unroll 1
   for (; tile < ntw; tile += wstride) {
@@ -184,25 +256,45 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
 #pragma unroll
       for (int e = 0; e < 2 * C::NT; ++e) lc[e] = (cg + e < ncols) ? __ldg(args.lam_c + cg + e) : 0.0;
     }
-    double acc[C::MT][C::NT][2];
+    double acc[C::NH][C::MT][C::NT][2];
 #pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
+    for (int hf = 0; hf < C::NH; ++hf)
 #pragma unroll
-      for (int j = 0; j < C::NT; ++j) acc[mt][j][0] = acc[mt][j][1] = 0.0;
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) acc[hf][mt][j][0] = acc[hf][mt][j][1] = 0.0;
 
     // k-loop in pairs; phantom steps (KS <= ks < KSE) only refill the window
 #pragma unroll
     for (int ksp = 0; ksp < C::KSE / 2 + (C::KSE & 1); ++ksp) {
       const int k0 = 2 * ksp, k1 = 2 * ksp + 1;
       if (k0 < C::KS) {
+        // the B operands of both k-steps (fold: even half x + Rx, odd half x - Rx)
+        double b[2][C::NH][C::NT];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) {
+            const int s = (k0 + h) % C::D;
+            if (C::CS == 1) {
+              b[h][0][j] = bw[s][0][j] + bw[s][C::NH - 1][j];
+              b[h][C::NH - 1][j] = bw[s][0][j] - bw[s][C::NH - 1][j];
+            } else {
+#pragma unroll
+              for (int hf = 0; hf < C::NH; ++hf) b[h][hf][j] = bw[s][hf][j];
+            }
+          }
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt) {
-          const double2 af = *reinterpret_cast<const double2*>(wl + (mt * C::KSP + ksp) * 64);
 #pragma unroll
-          for (int j = 0; j < C::NT; ++j) dmma_8x8x4(acc[mt][j], af.x, bw[k0 % C::D][j]);
-          if (k1 < C::KS) {
+          for (int hf = 0; hf < C::NH; ++hf) {
+            const double2 af = *reinterpret_cast<const double2*>(wl + hf * C::WFRAG1 + (mt * C::KSP + ksp) * 64);
 #pragma unroll
-            for (int j = 0; j < C::NT; ++j) dmma_8x8x4(acc[mt][j], af.y, bw[k1 % C::D][j]);
+            for (int j = 0; j < C::NT; ++j) dmma_8x8x4(acc[hf][mt][j], af.x, b[0][hf][j]);
+            if (k1 < C::KS) {
+#pragma unroll
+              for (int j = 0; j < C::NT; ++j) dmma_8x8x4(acc[hf][mt][j], af.y, b[1][hf][j]);
+            }
           }
         }
       }
@@ -213,107 +305,110 @@ __global__ void __launch_bounds__(256, 1) fd_mode_rd_kernel(ModeArgs args) {
         if (k >= C::KSE) continue;
         const int kk = k + C::D;
         if (kk < C::KS) {
-          rd_load<C>(bw[k % C::D], args.X, cur, kk, kstep, row_ok(kk), n);
+          load(bw[k % C::D], cur, kk);
         } else if (kk >= C::KSE) {
           const int s = kk - C::KSE;  // next tile's k-step, same slot (KSE % D == 0)
-          if (s < C::KS) rd_load<C>(bw[k % C::D], args.X, nxt, s, kstep, row_ok(s), n);
+          if (s == 0) set_ptrs(nxt);
+          if (s < C::KS) load(bw[k % C::D], nxt, s);
         }
       }
     }
 
-    // ---- epilogue: lane's columns cg .. cg + 2NT - 1, rows mt*8 + nq
-    if (C::REMOTE) {
-      // fused all-to-all: every output element goes straight to its owner's receive buffer
-      // (peer memory over NVLink in a multi-GPU run); pairs that stay contiguous and
-      // 16-byte aligned in the destination are stored as one double2
-      if (cg < ncols) {
-        const uint32_t p = cg / Q, q = cg - p * Q;
+    // ---- epilogue: lane's columns cg .. cg + 2NT - 1 (v[e] = column cg + e) at output row a
+    constexpr bool ONEBASE = C::MODE1 || C::FAST || C::REMOTE;
+    uint32_t fp = 0, fq = 0;
+    if (cg < ncols) {
+      fp = cg / Q;
+      fq = cg - fp * Q;
+    }
+    size_t base[ONEBASE ? 1 : 2 * C::NT];
+    if (C::MODE1) {
+      base[0] = size_t(cg) * n;
+    } else if (!ONEBASE) {
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          const int a = mt * 8 + nq;
-          if (a < n) {
+      for (int e = 0; e < (ONEBASE ? 1 : 2 * C::NT); ++e) {
+        const uint32_t c = cg + e;
+        const uint32_t p = c / Q, q = c - p * Q;
+        base[e] = size_t(p) * n * Q + q;
+      }
+    }
+    auto emit = [&](int a, const double (&v)[2 * C::NT]) {
+      if (C::REMOTE) {
+        // fused all-to-all: every output element goes straight to its owner's receive buffer
+        // (peer memory over NVLink in a multi-GPU run); pairs that stay contiguous and
+        // 16-byte aligned in the destination are stored as one double2
+        if (cg >= ncols) return;
 #pragma unroll
-            for (int e = 0; e < 2 * C::NT; e += 2) {
-              if (cg + e >= ncols) continue;
-              const double v0 = acc[mt][e % C::NT][e / C::NT];
-              const double v1 = acc[mt][(e + 1) % C::NT][(e + 1) / C::NT];
-              int r0, r1;
-              int64_t o0, o1;
-              if (C::REMOTE == 1) {
-                const int64_t s0 = int64_t(a) * Q + q + e;
-                a2a_fwd_dest(int64_t(p), s0, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
-                a2a_fwd_dest(int64_t(p), s0 + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
-              } else {
-                a2a_bwd_dest(int64_t(a), int64_t(q) + e, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
-                a2a_bwd_dest(int64_t(a), int64_t(q) + e + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
-              }
-              const bool second = cg + e + 1 < ncols;
-              double* d0 = args.peer[r0] + o0;
-              if (second && r1 == r0 && o1 == o0 + 1 && ((reinterpret_cast<uintptr_t>(d0) & 15) == 0)) {
-                *reinterpret_cast<double2*>(d0) = make_double2(v0, v1);
-              } else {
-                *d0 = v0;
-                if (second) args.peer[r1][o1] = v1;
-              }
-            }
+        for (int e = 0; e < 2 * C::NT; e += 2) {
+          if (cg + e >= ncols) continue;
+          int r0, r1;
+          int64_t o0, o1;
+          if (C::REMOTE == 1) {
+            const int64_t s0 = int64_t(a) * Q + fq + e;
+            a2a_fwd_dest(int64_t(fp), s0, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
+            a2a_fwd_dest(int64_t(fp), s0 + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
+          } else {
+            a2a_bwd_dest(int64_t(a), int64_t(fq) + e, args.nt_g, args.Ns_g, args.world, args.me, &r0, &o0);
+            a2a_bwd_dest(int64_t(a), int64_t(fq) + e + 1, args.nt_g, args.Ns_g, args.world, args.me, &r1, &o1);
+          }
+          const bool second = cg + e + 1 < ncols;
+          double* d0 = args.peer[r0] + o0;
+          if (second && r1 == r0 && o1 == o0 + 1 && ((reinterpret_cast<uintptr_t>(d0) & 15) == 0)) {
+            *reinterpret_cast<double2*>(d0) = make_double2(v[e], v[e + 1]);
+          } else {
+            *d0 = v[e];
+            if (second) args.peer[r1][o1] = v[e + 1];
           }
         }
-      }
-    } else if (C::FAST) {
-      if (cg < ncols) {
-        const uint32_t p = cg / Q, q = cg - p * Q;
-        double* ob = args.Y + size_t(p) * n * Q + q;
+      } else if (C::FAST) {
+        if (cg >= ncols) return;
+        double* o = args.Y + size_t(fp) * n * Q + fq + size_t(a) * Q;
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          const int a = mt * 8 + nq;
-          if (a < n) {
-            double v[2 * C::NT];
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int j = 0; j < C::NT; ++j) v[h * C::NT + j] = acc[mt][j][h];
-            if (C::SCALE) {
-              const double la = lam_a_s[a];
-#pragma unroll
-              for (int e = 0; e < 2 * C::NT; ++e) v[e] *= fast_rcp(la + lc[C::SCALE ? e : 0]);
-            }
-            double* o = ob + size_t(a) * Q;
-#pragma unroll
-            for (int e = 0; e < 2 * C::NT; e += 2) *reinterpret_cast<double2*>(o + e) = make_double2(v[e], v[e + 1]);
-          }
-        }
-      }
-    } else {
-      size_t base[C::MODE1 ? 1 : 2 * C::NT];
-      if (C::MODE1) {
-        base[0] = size_t(cg) * n;
+        for (int e = 0; e < 2 * C::NT; e += 2) *reinterpret_cast<double2*>(o + e) = make_double2(v[e], v[e + 1]);
       } else {
 #pragma unroll
-        for (int e = 0; e < (C::MODE1 ? 1 : 2 * C::NT); ++e) {
-          const uint32_t c = cg + e;
-          const uint32_t p = c / Q, q = c - p * Q;
-          base[e] = size_t(p) * n * Q + q;
+        for (int e = 0; e < 2 * C::NT; ++e) {
+          if (cg + e < ncols) {
+            if (C::MODE1) args.Y[base[0] + size_t(e) * n + a] = v[e];
+            else args.Y[base[ONEBASE ? 0 : e] + size_t(a) * rstride] = v[e];
+          }
         }
       }
-      const size_t rstride = C::MODE1 ? size_t(1) : size_t(Q);
+    };
 #pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) {
-        const int a = mt * 8 + nq;
+    for (int mt = 0; mt < C::MT; ++mt) {
+      const int a = mt * 8 + nq;
+      double v[C::NH][2 * C::NT];
+#pragma unroll
+      for (int hf = 0; hf < C::NH; ++hf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) v[hf][h * C::NT + j] = acc[hf][mt][j][h];
+      if (C::CS == 0) {
         if (a < n) {
-          double la = 0.0;
-          if (C::SCALE) la = lam_a_s[a];
+          if (C::SCALE) {
+            const double la = lam_a_s[a];
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+            for (int e = 0; e < 2 * C::NT; ++e) v[0][e] *= fast_rcp(la + lc[C::SCALE ? e : 0]);
+          }
+          emit(a, v[0]);
+        }
+      } else if (C::CS == 1) {  // outputs in eigen order [even (he) | odd (ho)]
+        if (a < he) emit(a, v[0]);
+        if (a < ho) emit(he + a, v[C::NH - 1]);
+      } else {  // z[a] = p + q, z[n-1-a] = p - q (a < ho); z[h] = p (middle row, n odd)
+        if (a < ho) {
+          double s[2 * C::NT], t[2 * C::NT];
 #pragma unroll
-            for (int j = 0; j < C::NT; ++j) {
-              const int e = h * C::NT + j;
-              if (cg + e < ncols) {
-                double v = acc[mt][j][h];
-                if (C::SCALE) v *= fast_rcp(la + lc[C::SCALE ? e : 0]);
-                if (C::MODE1) args.Y[base[0] + size_t(e) * n + a] = v;
-                else args.Y[base[C::MODE1 ? 0 : e] + size_t(a) * rstride] = v;
-              }
-            }
+          for (int e = 0; e < 2 * C::NT; ++e) {
+            s[e] = v[0][e] + v[C::NH - 1][e];
+            t[e] = v[0][e] - v[C::NH - 1][e];
+          }
+          emit(a, s);
+          emit(n - 1 - a, t);
+        } else if (a < he) {
+          emit(a, v[0]);
         }
       }
     }

@@ -8,5 +8,5 @@
 #endif
 
 namespace ls {
-template cudaError_t rd_launch<LS_RD_KS>(const ModeArgs&, bool, bool, cudaStream_t, int);
+template cudaError_t rd_launch<LS_RD_KS>(const ModeArgs&, bool, bool, int, cudaStream_t, int);
 }

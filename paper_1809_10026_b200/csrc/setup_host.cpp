@@ -216,8 +216,9 @@ void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<d
 // ------------------------------------------------------------------------------------------
 namespace ls {
 
-int generalized_eig(const std::vector<double>& Kd, const std::vector<double>& Md, int n,
-                    std::vector<double>& lam, std::vector<double>& Uout) {
+template <class T>
+static int generalized_eig_t(const std::vector<T>& Kd, const std::vector<T>& Md, int n,
+                             std::vector<double>& lam, std::vector<double>& Uout) {
   typedef long double R;
   std::vector<R> L(size_t(n) * n, 0.0L), C(size_t(n) * n), Q(size_t(n) * n, 0.0L);
   // Cholesky M = L L^T
@@ -314,6 +315,16 @@ int generalized_eig(const std::vector<double>& Kd, const std::vector<double>& Md
     for (int i = 0; i < n; ++i) Uout[size_t(i) * n + j] = double(sg * U[size_t(i) * n + o]);
   }
   return 0;
+}
+
+int generalized_eig(const std::vector<double>& K, const std::vector<double>& M, int n,
+                    std::vector<double>& lam, std::vector<double>& U) {
+  return generalized_eig_t(K, M, n, lam, U);
+}
+
+int generalized_eig(const std::vector<long double>& K, const std::vector<long double>& M, int n,
+                    std::vector<double>& lam, std::vector<double>& U) {
+  return generalized_eig_t(K, M, n, lam, U);
 }
 
 } // namespace ls

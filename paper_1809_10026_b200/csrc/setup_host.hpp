@@ -42,5 +42,9 @@ void load_integrals(int n_el, int p, bool space, int fn, double c, std::vector<d
 // cyclic Jacobi).  U row-major, column j = eigenvector j.  Returns 1 if M is not SPD.
 int generalized_eig(const std::vector<double>& K, const std::vector<double>& M, int n,
                     std::vector<double>& lam, std::vector<double>& U);
+// the same for a pencil given in extended precision (the centrosymmetric reductions of
+// api.cu, formed in 80-bit from the fp64 matrices)
+int generalized_eig(const std::vector<long double>& K, const std::vector<long double>& M, int n,
+                    std::vector<double>& lam, std::vector<double>& U);
 
 } // namespace ls

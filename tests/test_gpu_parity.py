@@ -59,8 +59,8 @@ def test_setup_factors_match_oracle(torch_cuda, d, p, n_elems):
         for which, key in ((0, "M"), (1, "K"), (2, "J")):
             A = space[k - 1][key]
             np.testing.assert_allclose(ctx.get_factor(which, k), A, rtol=0, atol=1e-12 * np.abs(A).max())
-        lam = ctx.get_factor(5, k)
-        np.testing.assert_allclose(lam, fdd["lam_s"][k - 1], rtol=1e-10)
+        lam = ctx.get_factor(5, k)  # eigen index order [even | odd] (LS_TUNE_FD_CS split)
+        np.testing.assert_allclose(np.sort(lam), fdd["lam_s"][k - 1], rtol=1e-10)
         U = ctx.get_factor(7, k)
         M, J = space[k - 1]["M"], space[k - 1]["J"]
         n = M.shape[0]
@@ -95,14 +95,18 @@ VARIANT_CASES = FD_CASES + [
 ]
 
 
+@pytest.mark.parametrize("cs", [0, 1])
 @pytest.mark.parametrize("variant", [1, 2])
 @pytest.mark.parametrize("d,p,n_elems", VARIANT_CASES)
-def test_fd_apply_kernel_variants(torch_cuda, variant, d, p, n_elems):
+def test_fd_apply_kernel_variants(torch_cuda, variant, cs, d, p, n_elems):
     """Both FD mode-kernel families (ls_tune knob 1: 1 = smem-staged, 2 = register-
-    direct) against the oracle, whatever the automatic dispatch picks."""
+    direct) against the oracle, whatever the automatic dispatch picks; with and without the
+    centrosymmetric split of the spatial modes (knob 9; with it the spatial modes always run
+    the split register-direct kernel, the time modes the chosen family)."""
     torch = torch_cuda
     ctx = _ctx(d, p, n_elems)
     ctx.tune(1, variant)
+    ctx.tune(9, cs)
     _, _, fdd = _oracle(d, p, n_elems)
     r = synth.residual(ctx.shape, 11)
     z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
@@ -363,6 +367,7 @@ def test_fd_apply_slab_chunk_decomposition(torch_cuda, fdk, d, p, n_elems, world
     torch = torch_cuda
     ctx = _ctx(d, p, n_elems)
     ctx.tune(1, fdk)
+    ctx.tune(9, int(fdk == 2))  # the split with the register-direct family
     _, _, fdd = _oracle(d, p, n_elems)
     r = synth.residual(ctx.shape, 17)
     nt = ctx.shape[0]
@@ -452,14 +457,15 @@ def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
     z_ref = fd.fd_apply(r, fdd)
     y_ref = op.apply_A(r, space, tf)
     canary = 1.2345e300
-    for fdk in (1, 2):
+    for fdk, cs in ((1, 0), (2, 0), (1, 1), (2, 1)):
         ctx.tune(1, fdk)
+        ctx.tune(9, cs)
         _, rin, _ = _guarded(torch, ctx.shape, float("nan"))
         rin.copy_(torch.from_numpy(r))
         obig, zout, pad = _guarded(torch, ctx.shape, canary)
         ctx.fd_apply(rin, zout)
-        assert _rel(zout.cpu().numpy(), z_ref) <= TOL, fdk
-        assert bool((obig[:pad] == canary).all()) and bool((obig[pad + zout.numel():] == canary).all()), fdk
+        assert _rel(zout.cpu().numpy(), z_ref) <= TOL, (fdk, cs)
+        assert bool((obig[:pad] == canary).all()) and bool((obig[pad + zout.numel():] == canary).all()), (fdk, cs)
     ctx.tune(1, 0)
     for mv in ((1, 2, 3, 4) if d >= 2 else (1, 2, 3)):
         ctx.tune(2, mv)
@@ -601,6 +607,7 @@ def test_fd_tail_rows(torch_cuda, d, p, n_elems):
     rg = torch.from_numpy(r).cuda()
     z_auto = ctx.fd_apply(rg).cpu().numpy()     # automatic dispatch (n = 97: register-direct)
     ctx.tune(1, 1)                               # the smem-staged family, which has the tail path
+    ctx.tune(9, 0)                               # n x n spatial products (no split)
     z1 = ctx.fd_apply(rg).cpu().numpy()
     ctx.tune(7, 0)
     z0 = ctx.fd_apply(rg).cpu().numpy()

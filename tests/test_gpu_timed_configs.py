@@ -77,14 +77,17 @@ BUCKET_CASES = [
 ]
 
 
+@pytest.mark.parametrize("cs", [0, 1])
 @pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("d,p,n_elems", BUCKET_CASES)
-def test_fd_buckets_24_25_forced(variant, d, p, n_elems):
-    """ls_tune knob 1: 0 = automatic, 1 = smem-staged (ping-pong / m-half), 2 = register-direct."""
+def test_fd_buckets_24_25_forced(variant, cs, d, p, n_elems):
+    """ls_tune knob 1: 0 = automatic, 1 = smem-staged (ping-pong / m-half), 2 = register-direct;
+    knob 9: centrosymmetric split of the spatial modes off / on (half extents 37..50: buckets 12, 13)."""
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, n_elems)
     ctx.tune(1, variant)
+    ctx.tune(9, cs)
     r = synth.residual(ctx.shape, 17)
     z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
     _check(z, fd.fd_apply(r, _fdd(d, p, n_elems)))

@@ -132,3 +132,24 @@ def test_rank1_rows_match_full_fd():
     got = fd.fd_apply_rank1_rows(facs, fdd, rows)
     for j, idx in enumerate(rows):
         np.testing.assert_allclose(got[j], z[idx], rtol=1e-12, atol=1e-14 * np.abs(z).max())
+
+
+@pytest.mark.parametrize("n_el,p", [(16, 2), (64, 3), (96, 2), (96, 4), (96, 8), (128, 6), (130, 2)])
+def test_space_pencil_centrosymmetric(n_el, p):
+    """Reading c24: on uniform open knots with Dirichlet conditions at both ends
+    (PAPER.md 266-267, 1111-1112) the exact space matrices are centrosymmetric (b_i(1-x) =
+    b_{n+1-i}(x)); the assembled fp64 ones are so to the last ulp, and the FD solution with the
+    symmetrised pencil (J + RJR)/2, (M + RMR)/2 -- whose eigenbasis the library's split uses --
+    differs from the oracle's by far less than the 1e-9 parity bar."""
+    f = uv.space_factors(n_el, p)
+    g = dict(f)
+    for k in ("M", "K", "J"):
+        A = f[k]
+        R = A[::-1, ::-1]
+        assert np.max(np.abs(A - R)) <= 4 * np.finfo(float).eps * np.abs(A).max()
+        g[k] = 0.5 * (A + R)
+    tf = uv.time_factors(6, p)
+    r = np.random.default_rng(5).uniform(-1, 1, (tf["Mt_hat"].shape[0], f["M"].shape[0]))
+    z = fd.fd_apply(r, fd.setup([f], tf))
+    zs = fd.fd_apply(r, fd.setup([g], tf))
+    assert np.linalg.norm(zs - z) / np.linalg.norm(z) <= 1e-12
