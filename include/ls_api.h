@@ -423,6 +423,11 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * whose pencil is not centrosymmetric (P^G's weighted pencils) always use n x n products.
  * The eigen index order of such a direction is [even | odd] (ls_get_factor 5 / 7). */
 #define LS_TUNE_FD_CS 9
+/* LS_TUNE_MV5: 1 = the v4 matvec (LS_TUNE_MATVEC 4, the automatic choice for d >= 2, p >= 3)
+ * runs its direction-3 and time passes as ONE kernel (d = 3, p_s = p_t): the direction-3 results
+ * stay on chip and the time band product is a register scatter; 0 = two DMMA passes through
+ * HBM; 2 = automatic (default): the fused pass for p <= 4, where it measured faster. */
+#define LS_TUNE_MV5 10
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

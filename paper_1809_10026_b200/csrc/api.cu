@@ -19,6 +19,7 @@
 #include "matvec2_kernels.cuh"
 #include "matvec3_kernels.cuh"
 #include "mv4_kernels.cuh"
+#include "mv5_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 #include "geo.hpp"
@@ -73,6 +74,8 @@ struct ls_ctx {
   double* Wf_cs[3] = {nullptr, nullptr, nullptr};  // [A_e^T (he x he) | A_o^T (ho x ho)]
   double* Wb_cs[3] = {nullptr, nullptr, nullptr};  // [A_e | A_o]
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
+  int mv5 = 2;         // ls_tune knob LS_TUNE_MV5: v4's direction-3 and time passes fused (mv5_kernels.cuh):
+                       // 0 off, 1 on, 2 automatic (p <= 4: measured faster there, slower above)
   // PCG: the next ls_matvec also forms p.q (x.y) into scal[fuse_dot_slot] when its last pass can
   // (v4 time-pass epilogue); fuse_dot_done reports whether it did
   int fuse_dot_slot = -1;
@@ -97,6 +100,7 @@ struct ls_ctx {
   cudaEvent_t hev[17] = {};
   double** scatter_stage = nullptr;  // pinned host staging of that table
   double* xT_pad = nullptr;    // v3: the last time slice of x in the padded layout
+  double* tcol = nullptr;      // v5: column bands of K_t, M_t per time slice [nt][32]
 
   // host copies (introspection)
   std::vector<double> hM[3], hK[3], hJ[3], hMt, hKt, hlam[4], hU[4];
@@ -666,6 +670,18 @@ static int setup_common(ls_ctx* ctx) {
     const std::vector<double>* mats[2] = {&ctx->hKt, &ctx->hMt};
     const double scale[2] = {1.0, 1.0};
     LS_CHECK(make_frags(ctx, mats, scale, 2, ctx->nt, pt, &ctx->frag_time));
+  }
+  if (pt <= 8) {  // v5 time scatter: tcol[t'][k] = K_t[t' - p_t + k][t'], tcol[t'][20 + k] = M_t[..][t']
+    const int nt = ctx->nt;
+    std::vector<double> tc(size_t(nt) * 40, 0.0);
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k <= 2 * pt; ++k) {
+        const int r = t - pt + k;
+        if (r < 0 || r >= nt) continue;
+        tc[size_t(t) * 40 + k] = ctx->hKt[size_t(r) * nt + t];
+        tc[size_t(t) * 40 + 20 + k] = ctx->hMt[size_t(r) * nt + t];
+      }
+    LS_CHECK(upload(ctx, tc, &ctx->tcol));
   }
   // workspaces (halo rows for the distributed matvec: p slices each side)
   const size_t halo = size_t(2 * pt) * ctx->Ns;  // time halo of the banded time factors
@@ -1489,6 +1505,44 @@ static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     LS_CUDA(mv4_plane_run(a, P, ctx->num_sms, ctx->stream));
     ctx->launches++;
   }
+  // v5 measured (tools/ab_mv.py, r02): config 3 (p = 3) 0.720 -> 0.610 ms, config 5 p = 4 2.945 ->
+  // 2.924 ms; slower at p = 6 (config 4 10.08 -> 13.04 ms) and 8 (3.69 -> 5.18 ms): 255 registers
+  // (the 2p+1-row ring) and 8 warps per SM leave its latency exposed
+  const bool mv5 = ctx->mv5 == 1 || (ctx->mv5 == 2 && P <= 4);
+  if (d == 3 && mv5 && mv5_supported(P, PT) && ctx->tcol) {
+    // v5: direction 3 and time in one pass (mv5_kernels.cuh), v1 / v2 stay on chip
+    MV5Args a{};
+    a.in[0] = PM;
+    a.in[1] = PK;
+    a.in[2] = PJ;
+    a.y = y;
+    a.frag3 = ctx->frag_dir[2];
+    a.tcol = ctx->tcol;
+    a.n3 = ctx->n[2];
+    a.mt3 = mv3_mt(P, a.n3);
+    a.nt = ctx->nt;
+    a.Q = uint32_t(int64_t(n1) * n2);
+    a.s_first = int(s_first);
+    a.rows = int(rows);
+    a.t_first = int(t_first);
+    a.nout = int(nout);
+    if (ctx->fuse_dot_slot >= 0) {  // p.q in the epilogue: p = the own rows of x
+      a.dotp = x + (t_first - s_first) * ctx->Ns;
+      a.dot_part = ctx->partials;
+    }
+    unsigned grid = 0;
+    LS_CUDA(mv5_run(a, P, PT, ctx->num_sms, ctx->stream, &grid));
+    ctx->launches++;
+    if (ctx->fuse_dot_slot >= 0) {
+      LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(grid), ctx->scal,
+                         ctx->fuse_dot_slot));
+      ctx->launches++;
+      LS_CUDA(cudaGetLastError());
+      if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + ctx->fuse_dot_slot));
+      ctx->fuse_dot_done = true;
+    }
+    return LS_OK;
+  }
   const int64_t tT = (ctx->nt - 1) - s_first;  // the last time slice among the stored rows
   const bool have_last = tT >= 0 && tT < rows;
   const double *v1 = PM, *v2 = PJ, *v3 = have_last ? PK + tT * ctx->Ns : nullptr;
@@ -2147,6 +2201,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_FD_TAIL:
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->fd_tail = value;
+      return LS_OK;
+    case LS_TUNE_MV5:  // v4: direction 3 + time fused into one pass (d = 3, p_s = p_t); 2 = automatic
+      if (value < 0 || value > 2) return LS_EINVAL;
+      ctx->mv5 = value;
       return LS_OK;
     case LS_TUNE_FD_CS:  // centrosymmetric split of the spatial modes (default 1 where the pencil allows)
       if (value != 0 && value != 1) return LS_EINVAL;

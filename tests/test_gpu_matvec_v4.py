@@ -1,6 +1,8 @@
 """ls_matvec v4 (ls_tune(LS_TUNE_MATVEC, 4): the plane pass of directions 1 + 2, then the
 direction-3 and time DMMA passes; mv4_kernels.cuh) against the oracle's A x (eq:A_kron,
-PAPER.md 686-703) and the dense original form, whole-vector and per-rank slab rows."""
+PAPER.md 686-703) and the dense original form, whole-vector and per-rank slab rows; with the
+direction-3 and time passes fused into one kernel (ls_tune(LS_TUNE_MV5 = 10, 1); the automatic
+choice (2) for p <= 4; mv5_kernels.cuh: d = 3, p_s = p_t) and as two passes (10, 0)."""
 import numpy as np
 import pytest
 
@@ -30,12 +32,14 @@ def _rel(a, b):
     return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
 
 
+@pytest.mark.parametrize("mv5", [1, 0])
 @pytest.mark.parametrize("d,p,ne", CASES)
-def test_matvec_v4_matches_oracle(d, p, ne):
+def test_matvec_v4_matches_oracle(d, p, ne, mv5):
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, ne)
     ctx.tune(2, 4)
+    ctx.tune(10, mv5)
     space = [uv.space_factors(n, p) for n in ne[:d]]
     tf = uv.time_factors(ne[d], p)
     x = synth.residual(ctx.shape, 9)
@@ -71,13 +75,16 @@ def test_matvec_v4_original_form_tiny():
     assert _rel(y, A @ x.ravel()) <= 1e-12
 
 
+@pytest.mark.parametrize("mv5", [1, 0])
 @pytest.mark.parametrize("d,p,ne,world", [(3, 6, [9, 8, 7, 40], 4), (3, 2, [6, 5, 7, 29], 3),
-                                          (2, 8, [20, 12, 37], 2), (3, 3, [12, 10, 8, 61], 8)])
-def test_matvec_v4_slab_decomposition(d, p, ne, world):
+                                          (2, 8, [20, 12, 37], 2), (3, 3, [12, 10, 8, 61], 8),
+                                          (3, 8, [5, 6, 4, 50], 5), (3, 4, [7, 5, 6, 23], 2)])
+def test_matvec_v4_slab_decomposition(d, p, ne, world, mv5):
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, ne)
     ctx.tune(2, 4)
+    ctx.tune(10, mv5)
     space = [uv.space_factors(n, p) for n in ne[:d]]
     tf = uv.time_factors(ne[d], p)
     x = synth.residual(ctx.shape, 13)
@@ -100,5 +107,9 @@ def test_matvec_v4_config4_sampled():
     ctx.tune(2, 3)
     y3 = ctx.matvec(x)
     ctx.tune(2, 4)
+    ctx.tune(10, 0)
     y4 = ctx.matvec(x)
     assert float(torch.linalg.norm(y4 - y3) / torch.linalg.norm(y3)) <= 1e-13
+    ctx.tune(10, 1)
+    y5 = ctx.matvec(x)
+    assert float(torch.linalg.norm(y5 - y3) / torch.linalg.norm(y3)) <= 1e-13

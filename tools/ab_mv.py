@@ -1,4 +1,4 @@
-"""A/B of libls.so builds for ls_matvec: python tools/ab_mv.py <lib.so> <config[:p]> [variant]"""
+"""A/B of libls.so builds for ls_matvec: python tools/ab_mv.py <lib.so> <config[:p]> [variant] [mv5 0|1]"""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,6 +10,8 @@ c = synth.CONFIGS[int(cid)]
 p = int(pp) if pp else c["p"]
 ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
 ctx.tune(2, int(sys.argv[3]) if len(sys.argv) > 3 else 3)
+if len(sys.argv) > 4:
+    ctx.tune(10, int(sys.argv[4]))
 x = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 y = torch.empty_like(x)
 for _ in range(3):
@@ -24,4 +26,4 @@ for rep in range(3):
     e1.record()
     e1.synchronize()
     best = min(best, e0.elapsed_time(e1) / 10)
-print(json.dumps({"lib": sys.argv[1], "config": sys.argv[2], "ms": round(best, 4), "chk": float(y.abs().sum())}))
+print(json.dumps({"lib": sys.argv[1], "config": sys.argv[2], "args": sys.argv[3:], "ms": round(best, 4), "chk": float(y.abs().sum())}))
