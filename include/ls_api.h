@@ -173,6 +173,17 @@ int ls_matvec(ls_ctx* ctx, const double* x, double* y);
  */
 int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first, int64_t s_rows, double* y,
                    int64_t t_first, int64_t nout);
+/*
+ * ls_matvec_slab3 -- ls_matvec_slab with the stored rows in three separate device buffers, as
+ * the distributed ls_matvec holds them (no copy of x into a halo-extended buffer): rows
+ * [s_first, s_first + lo) in x_lo ([lo][N_s]), the next `own` rows in x_own, the last `hi` rows
+ * in x_hi; s_rows = lo + own + hi, same requirements and outputs as ls_matvec_slab.  The v4
+ * path (d >= 2, 3 <= p <= 8) reads the three buffers directly (own rows first: in the
+ * distributed ls_matvec the halo exchange overlaps that plane pass); other paths gather the
+ * rows into a workspace first.  A buffer may be null when its row count is 0.
+ */
+int ls_matvec_slab3(ls_ctx* ctx, const double* x_lo, int64_t lo, const double* x_own, int64_t own,
+                    const double* x_hi, int64_t hi, int64_t s_first, double* y, int64_t t_first, int64_t nout);
 
 /*
  * ls_rhs -- b_i = F(B_i) = int int f (d_t B_i - Lap B_i) (PAPER.md 409) for a
@@ -351,6 +362,13 @@ int ls_partition(int64_t total, int world, int part, int64_t* off, int64_t* len)
 int ls_a2a_plan(int64_t n_t, int64_t N_s, int world, int rank, int64_t* send_off,
                 int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt);
 int ls_pack_map(int64_t ntl, int64_t N_s, int world, int64_t* pos);
+/* ls_a2a_piece_plan -- piece `piece` of the pipelined slab -> chunk all-to-all of `rank`
+ * (the default NCCL path of the distributed fd_apply: every slab is cut into *pieces =
+ * min(4, floor(n_t / world)) runs of consecutive time slices; the spatial modes of piece c + 1
+ * run while piece c is exchanged).  Arrays of length world as ls_a2a_plan; the union over the
+ * pieces is ls_a2a_plan's exchange.  piece < 0 only returns *pieces. */
+int ls_a2a_piece_plan(int64_t n_t, int64_t N_s, int world, int rank, int piece, int* pieces, int64_t* send_off,
+                      int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt);
 int ls_halo_plan(int64_t n_t, int world, int rank, int p, int64_t* t0, int64_t* ntl,
                  int64_t* lo, int64_t* hi);
 /* ls_a2a_dest -- destination of one element in the fused all-to-all (the addressing of

@@ -28,9 +28,9 @@ LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_E
 
 # Every symbol include/ls_api.h declares (checked by tests/test_abi.py).
 EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
-            "fd_apply", "ls_matvec", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
+            "fd_apply", "ls_matvec", "ls_matvec_slab3", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
-            "ls_partition", "ls_a2a_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
+            "ls_partition", "ls_a2a_plan", "ls_a2a_piece_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
             "ls_setup_dist_deg", "ls_energy_error", "ls_error_norms", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist", "ls_pg_factors"]
 
@@ -107,9 +107,13 @@ def load_library(path=LIB_PATH):
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
         "ls_matvec_slab": (ctypes.c_int, [vp, dp, ctypes.c_int64, ctypes.c_int64, dp, ctypes.c_int64,
                                           ctypes.c_int64]),
+        "ls_matvec_slab3": (ctypes.c_int, [vp, dp, ctypes.c_int64, dp, ctypes.c_int64, dp, ctypes.c_int64,
+                                           ctypes.c_int64, dp, ctypes.c_int64, ctypes.c_int64]),
         "ls_partition": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i64p]),
         "ls_a2a_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                        i64p, i64p, i64p, i64p]),
+        "ls_a2a_piece_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(ctypes.c_int), i64p, i64p, i64p, i64p]),
         "ls_pack_map": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, i64p]),
         "ls_halo_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         i64p, i64p, i64p, i64p]),
@@ -156,6 +160,18 @@ def a2a_plan(n_t, N_s, world, rank):
     ptrs = [a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)) for a in arrs]
     _check(load_library().ls_a2a_plan(int(n_t), int(N_s), int(world), int(rank), *ptrs), "ls_a2a_plan")
     return dict(zip(("send_off", "send_cnt", "recv_off", "recv_cnt"), arrs))
+
+
+def a2a_piece_plan(n_t, N_s, world, rank, piece):
+    """ls_a2a_piece_plan: (pieces, [(send_off, send_cnt, recv_off, recv_cnt) per peer]) of one piece
+    of the pipelined slab -> chunk all-to-all (piece < 0: only the number of pieces)."""
+    np_ = ctypes.c_int(0)
+    arrs = [(ctypes.c_int64 * max(world, 1))() for _ in range(4)]
+    _check(load_library().ls_a2a_piece_plan(int(n_t), int(N_s), int(world), int(rank), int(piece),
+                                            ctypes.byref(np_), *arrs), "ls_a2a_piece_plan")
+    if piece < 0:
+        return np_.value, []
+    return np_.value, [tuple(int(a[h]) for a in arrs) for h in range(world)]
 
 
 def pack_map(ntl, N_s, world):
@@ -343,6 +359,31 @@ class Context:
         self._chk(y, "y", int(nout) * Ns)
         _check(self._lib.ls_matvec_slab(self._h, ctypes.c_void_p(x_ext.data_ptr()), int(s_first), int(s_rows),
                                         ctypes.c_void_p(y.data_ptr()), int(t_first), int(nout)), "ls_matvec_slab")
+        return y
+
+    def matvec_slab3(self, x_lo, x_own, x_hi, s_first, t_first, nout, y=None):
+        """ls_matvec_slab3: as matvec_slab with the stored rows in three buffers (lower halo rows,
+        own rows, upper halo rows; a halo may be None for zero rows)."""
+        torch = self._torch
+        Ns = int(np.prod(self.n_s))
+        parts = []
+        for t, name in ((x_lo, "x_lo"), (x_own, "x_own"), (x_hi, "x_hi")):
+            if t is None:
+                parts.append((None, 0))
+                continue
+            self._chk(t, name, 1)
+            if t.numel() % Ns:
+                raise ValueError(f"{name} has {t.numel()} elements, not a whole number of time slices of {Ns}")
+            parts.append((t, t.numel() // Ns))
+        if parts[1][0] is None:
+            raise ValueError("x_own is required")
+        if y is None:
+            y = torch.empty((nout,) + tuple(self.shape[1:]), dtype=torch.float64, device="cuda")
+        self._chk(y, "y", int(nout) * Ns)
+        ptr = [ctypes.c_void_p(t.data_ptr() if t is not None else 0) for t, _ in parts]
+        _check(self._lib.ls_matvec_slab3(self._h, ptr[0], parts[0][1], ptr[1], parts[1][1], ptr[2], parts[2][1],
+                                         int(s_first), ctypes.c_void_p(y.data_ptr()), int(t_first), int(nout)),
+               "ls_matvec_slab3")
         return y
 
     def rhs(self, kind, b=None):

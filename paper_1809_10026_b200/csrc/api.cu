@@ -97,6 +97,9 @@ struct ls_ctx {
   double** scatter_tab = nullptr;  // fd_apply_scatter: device copy of the caller's table
   // fd_apply_host pipeline: copy stream + events (H2D / D2H per time-slice chunk)
   cudaStream_t copy_stream = nullptr;
+  // distributed path: NCCL stream of the pipelined all-to-all / halo exchange and its events
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t cev[12] = {};
   cudaEvent_t hev[17] = {};
   double** scatter_stage = nullptr;  // pinned host staging of that table
   double* xT_pad = nullptr;    // v3: the last time slice of x in the padded layout
@@ -161,6 +164,9 @@ struct ls_ctx {
     for (auto e : hev)
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto e : cev)
+      if (e) cudaEventDestroy(e);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (pcg_exec) cudaGraphExecDestroy(pcg_exec);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_stream2) cudaStreamDestroy(cap_stream2);
@@ -816,6 +822,9 @@ extern "C" int ls_setup_geo_dist(int d, int p_s, int p_t, const int64_t* n_elems
   if (rc == LS_OK && world > 1) {
     ctx->comm.reset(new Comm());
     rc = ctx->comm->init(nccl_unique_id, rank, world, ctx->nt, ctx->Ns);
+    if (rc == LS_OK && cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess) rc = LS_ECUDA;
+    for (auto& e : ctx->cev)
+      if (rc == LS_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = LS_ECUDA;
   }
   if (rc != LS_OK) {
     delete ctx;
@@ -883,6 +892,9 @@ extern "C" int ls_setup_dist_deg(int d, int p_s, int p_t, const int64_t* n_elems
   if (rc == LS_OK && world > 1) {
     ctx->comm.reset(new Comm());
     rc = ctx->comm->init(nccl_unique_id, rank, world, ctx->nt, ctx->Ns);
+    if (rc == LS_OK && cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess) rc = LS_ECUDA;
+    for (auto& e : ctx->cev)
+      if (rc == LS_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) rc = LS_ECUDA;
   }
   if (rc != LS_OK) {
     delete ctx;
@@ -1124,17 +1136,52 @@ int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
     LS_CHECK(cm.barrier());
     return spatial_modes(ctx, A, z, C, ctx->tmp[3], ctx->ntl, false);
   }
-  LS_CHECK(spatial_modes(ctx, r, A, B, C, ctx->ntl, true));
-  // A: [ntl][Ns] slab -> B: [nt][chunk] (send order = destination chunks)
-  LS_CHECK(cm.slab_to_chunk(A, B, C, ctx->launches));
+  // NCCL path, pipelined over pieces of consecutive time slices (plan.hpp a2a_piece_plan): the
+  // exchange of piece c (comm stream) overlaps the spatial modes of piece c + 1 (compute stream),
+  // and on the way back the unpack + backward spatial modes of piece c overlap the exchange of
+  // piece c + 1.  A = slab [ntl][Ns], B = chunk [nt][chunk], C = packed staging; the spatial
+  // modes of a piece use tmp[3], tmp[4].
+  cudaStream_t cs = ctx->comm_stream;
+  cudaEvent_t* ev = ctx->cev;  // 0: entry, 1: forward done, 2: time modes done, 3..6 forward pieces, 7..10 backward
+  const int P = cm.pieces();
+  const int64_t Ns = ctx->Ns, ntl = ctx->ntl;
+  double* W0 = ctx->tmp[3];
+  double* W1 = ctx->tmp[4];
+  LS_CUDA(cudaEventRecord(ev[0], ctx->stream));  // the workspaces' previous users are done
+  LS_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+  for (int c = 0; c < P; ++c) {
+    int64_t a, l;
+    split_part(ntl, P, c, &a, &l);
+    if (l > 0) {
+      LS_CHECK(spatial_modes(ctx, r + a * Ns, A + a * Ns, W0, W1, uint64_t(l), true));
+      LS_CHECK(cm.pack_piece(true, A, C, c, ctx->stream, ctx->launches));
+    }
+    LS_CUDA(cudaEventRecord(ev[3 + c], ctx->stream));
+    LS_CUDA(cudaStreamWaitEvent(cs, ev[3 + c], 0));
+    LS_CHECK(cm.exchange_piece(true, C, B, c, cs));
+  }
+  LS_CUDA(cudaEventRecord(ev[1], cs));
+  LS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[1], 0));
   const int64_t chunk = cm.chunk_len[ctx->rank];
   const int64_t c0 = cm.chunk_off[ctx->rank];
   if (chunk > 0) {
     LS_CHECK(launch_mode(ctx, B, C, ctx->Wf[3], ctx->nt, 1, chunk, true, ctx->lam[3], ctx->lam_s + c0));
     LS_CHECK(launch_mode(ctx, C, B, ctx->Wb[3], ctx->nt, 1, chunk, false));
   }
-  LS_CHECK(cm.chunk_to_slab(B, A, C, ctx->launches));
-  LS_CHECK(spatial_modes(ctx, A, z, B, C, ctx->ntl, false));
+  LS_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  LS_CUDA(cudaStreamWaitEvent(cs, ev[2], 0));
+  for (int c = 0; c < P; ++c) {
+    LS_CHECK(cm.exchange_piece(false, B, C, c, cs));
+    LS_CUDA(cudaEventRecord(ev[7 + c], cs));
+  }
+  for (int c = 0; c < P; ++c) {
+    int64_t a, l;
+    split_part(ntl, P, c, &a, &l);
+    LS_CUDA(cudaStreamWaitEvent(ctx->stream, ev[7 + c], 0));
+    if (l == 0) continue;
+    LS_CHECK(cm.pack_piece(false, C, A, c, ctx->stream, ctx->launches));
+    LS_CHECK(spatial_modes(ctx, A + a * Ns, z + a * Ns, W0, W1, uint64_t(l), false));
+  }
   return LS_OK;
 }
 
@@ -1483,27 +1530,50 @@ static int mv3_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
 }
 
 // ---- matvec v4 (mv4_kernels.cuh): plane pass (directions 1 + 2) -> direction 3 -> time ------
+// MV4Split: the input rows in three pieces (distributed ls_matvec without the copy into the
+// halo-extended buffer): own rows [lo, lo + own) from `x`, halo rows [0, lo) from x_lo and
+// [lo + own, rows) from x_hi; the plane pass of the own rows runs first, the halo rows after
+// halo_ready (the exchange overlaps it)
+struct MV4Split {
+  const double* x_lo = nullptr;
+  const double* x_hi = nullptr;
+  int64_t lo = 0, own = 0, hi = 0;
+  cudaEvent_t halo_ready = nullptr;
+};
+
 static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int64_t s_first,
-                      int64_t t_first, int64_t nout) {
+                      int64_t t_first, int64_t nout, const MV4Split* split = nullptr) {
   const int d = ctx->d, P = ctx->p, PT = ctx->pt;
   if (d < 2 || P < 2 || P > 8 || PT < 2 || PT > 8) return LS_ENOTSUP;
   const int n1 = ctx->n[0], n2 = ctx->n[1];
   double *PM = ctx->tmp[0], *PK = ctx->tmp[1], *PJ = ctx->tmp[2];
-  {
+  auto plane = [&](const double* src, int64_t row0, int64_t nrows) -> int {
+    if (nrows <= 0) return LS_OK;
     MV4PlaneArgs a{};
-    a.x = x;
-    a.out[0] = PM;
-    a.out[1] = PK;
-    a.out[2] = PJ;
+    a.x = src;
+    a.out[0] = PM + row0 * ctx->Ns;
+    a.out[1] = PK + row0 * ctx->Ns;
+    a.out[2] = PJ + row0 * ctx->Ns;
     a.frag1 = ctx->frag_dir[0];
     a.frag2 = ctx->frag_dir[1];
     a.n1 = n1;
     a.n2 = n2;
     a.mt1 = mv3_mt(P, n1);
     a.mt2 = mv3_mt(P, n2);
-    a.nplanes = rows * (d == 3 ? ctx->n[2] : 1);
+    a.nplanes = nrows * (d == 3 ? ctx->n[2] : 1);
     LS_CUDA(mv4_plane_run(a, P, ctx->num_sms, ctx->stream));
     ctx->launches++;
+    return LS_OK;
+  };
+  // p.q (fused dot): p = the own rows of x
+  const double* xown = split ? x : x + (t_first - s_first) * ctx->Ns;
+  if (!split) {
+    LS_CHECK(plane(x, 0, rows));
+  } else {
+    LS_CHECK(plane(x, split->lo, split->own));
+    if (split->halo_ready) LS_CUDA(cudaStreamWaitEvent(ctx->stream, split->halo_ready, 0));
+    LS_CHECK(plane(split->x_lo, 0, split->lo));
+    LS_CHECK(plane(split->x_hi, split->lo + split->own, split->hi));
   }
   // v5 measured (tools/ab_mv.py, r02): config 3 (p = 3) 0.720 -> 0.610 ms, config 5 p = 4 2.945 ->
   // 2.924 ms; slower at p = 6 (config 4 10.08 -> 13.04 ms) and 8 (3.69 -> 5.18 ms): 255 registers
@@ -1527,7 +1597,7 @@ static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.t_first = int(t_first);
     a.nout = int(nout);
     if (ctx->fuse_dot_slot >= 0) {  // p.q in the epilogue: p = the own rows of x
-      a.dotp = x + (t_first - s_first) * ctx->Ns;
+      a.dotp = xown;
       a.dot_part = ctx->partials;
     }
     unsigned grid = 0;
@@ -1598,7 +1668,7 @@ static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     a.mt0 = int((t_first - S0) / 8);
     a.mt1 = int((t_first + nout - S0 + 7) / 8);
     if (ctx->fuse_dot_slot >= 0) {  // p.q in the epilogue: p = the own rows of x
-      a.dotp = x + (t_first - s_first) * ctx->Ns;
+      a.dotp = xown;
       a.dot_part = ctx->partials;
     }
   }
@@ -1650,6 +1720,24 @@ extern "C" int ls_matvec(ls_ctx* ctx, const double* x, double* y) {
   int64_t lo, hi;
   ext_geom(ctx, &lo, &hi);
   double* own = ctx->pp + lo * ctx->Ns;  // extended buffer [lo | own | hi]
+  const bool v4 = !ctx->geo && (ctx->mv_variant == 4 || (ctx->mv_variant == 0 && ctx->d >= 2 && ctx->p >= 3 &&
+                                                          ctx->pt >= 2 && ctx->p <= 8 && ctx->pt <= 8));
+  if (v4) {
+    // no copy of x: the halos arrive in pp's halo rows (comm stream) while the plane pass of the
+    // own rows runs; the halo rows' plane pass waits for them
+    LS_CUDA(cudaEventRecord(ctx->cev[0], ctx->stream));
+    LS_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->cev[0], 0));
+    LS_CHECK(ctx->comm->halo_exchange_from(x, ctx->pp, ctx->pt, ctx->comm_stream));
+    LS_CUDA(cudaEventRecord(ctx->cev[11], ctx->comm_stream));
+    MV4Split sp;
+    sp.x_lo = ctx->pp;
+    sp.x_hi = own + ctx->ntl * ctx->Ns;
+    sp.lo = lo;
+    sp.own = ctx->ntl;
+    sp.hi = hi;
+    sp.halo_ready = ctx->cev[11];
+    return mv4_launch(ctx, x, y, lo + ctx->ntl + hi, ctx->t0 - lo, ctx->t0, ctx->ntl, &sp);
+  }
   if (x != own)
     LS_CUDA(cudaMemcpyAsync(own, x, size_t(ctx->Nl) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   LS_CHECK(ctx->comm->halo_exchange(ctx->pp, ctx->pt));
@@ -1674,6 +1762,37 @@ extern "C" int ls_matvec_slab(ls_ctx* ctx, const double* x_ext, int64_t s_first,
     return geo_matvec(*ctx->geo, ctx->bKt, ctx->bMt, int(nt), x_ext, int(s_first), int(t_first), int(nout), y,
                       ctx->tmp[3], ctx->tmp[4], ctx->stream, &ctx->launches);
   return matvec_any(ctx, x_ext, y, s_rows, s_first, t_first, nout);
+}
+
+extern "C" int ls_matvec_slab3(ls_ctx* ctx, const double* x_lo, int64_t lo, const double* x_own, int64_t own,
+                               const double* x_hi, int64_t hi, int64_t s_first, double* y, int64_t t_first,
+                               int64_t nout) {
+  if (!ctx || !x_own || !y || lo < 0 || hi < 0 || own < 1 || (lo > 0 && !x_lo) || (hi > 0 && !x_hi)) return LS_EINVAL;
+  if (!aligned8(x_own) || !aligned8(y) || (x_lo && !aligned8(x_lo)) || (x_hi && !aligned8(x_hi))) return LS_EINVAL;
+  const int64_t nt = ctx->nt, p = ctx->pt, rows = lo + own + hi;
+  if (nout < 0 || t_first < 0 || t_first + nout > nt) return LS_EINVAL;
+  if (nout > ctx->ntl || rows > ctx->ntl + 2 * p) return LS_EINVAL;
+  const int64_t need_lo = std::max<int64_t>(0, t_first - p), need_hi = std::min<int64_t>(nt, t_first + nout + p);
+  if (nout > 0 && (s_first > need_lo || s_first + rows < need_hi)) return LS_EINVAL;
+  if (nout == 0) return LS_OK;
+  const bool v4 = !ctx->geo && (ctx->mv_variant == 4 || (ctx->mv_variant == 0 && ctx->d >= 2 && ctx->p >= 3 &&
+                                                          ctx->pt >= 2 && ctx->p <= 8 && ctx->pt <= 8));
+  if (v4) {
+    MV4Split sp;
+    sp.x_lo = x_lo;
+    sp.x_hi = x_hi;
+    sp.lo = lo;
+    sp.own = own;
+    sp.hi = hi;
+    return mv4_launch(ctx, x_own, y, rows, s_first, t_first, nout, &sp);
+  }
+  // other paths read one contiguous [rows][N_s] block: gather it into pp
+  const size_t rb = size_t(ctx->Ns) * sizeof(double);
+  double* ext = ctx->pp;
+  if (lo > 0) LS_CUDA(cudaMemcpyAsync(ext, x_lo, lo * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  LS_CUDA(cudaMemcpyAsync(ext + lo * ctx->Ns, x_own, own * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (hi > 0) LS_CUDA(cudaMemcpyAsync(ext + (lo + own) * ctx->Ns, x_hi, hi * rb, cudaMemcpyDeviceToDevice, ctx->stream));
+  return ls_matvec_slab(ctx, ext, s_first, rows, y, t_first, nout);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2140,6 +2259,17 @@ extern "C" int ls_a2a_plan(int64_t nt, int64_t Ns, int world, int rank, int64_t*
     return LS_EINVAL;
   for (int h = 0; h < world; ++h)
     a2a_plan(nt, Ns, world, rank, h, send_off + h, send_cnt + h, recv_off + h, recv_cnt + h);
+  return LS_OK;
+}
+
+extern "C" int ls_a2a_piece_plan(int64_t nt, int64_t Ns, int world, int rank, int piece, int* pieces,
+                                 int64_t* send_off, int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt) {
+  if (world < 1 || rank < 0 || rank >= world || nt < 1 || !pieces) return LS_EINVAL;
+  *pieces = a2a_pieces(nt, world);
+  if (piece < 0) return LS_OK;
+  if (piece >= *pieces || !send_off || !send_cnt || !recv_off || !recv_cnt) return LS_EINVAL;
+  for (int h = 0; h < world; ++h)
+    a2a_piece_plan(nt, Ns, world, rank, h, piece, *pieces, send_off + h, send_cnt + h, recv_off + h, recv_cnt + h);
   return LS_OK;
 }
 

@@ -140,9 +140,9 @@ int Comm::init(const void* uid, int rank_, int world_, int64_t nt_, int64_t Ns_)
 // pack (PACK) / unpack: slab element e <-> packed all-to-all position (plan.hpp pack_pos)
 template <bool PACK>
 __global__ void pack_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t ntl,
-                            int64_t Ns, int world) {
-  const int64_t total = ntl * Ns;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+                            int64_t Ns, int world, int64_t e0 = 0, int64_t e1 = -1) {
+  const int64_t total = e1 < 0 ? ntl * Ns : e1;  // elements [e0, total) of the slab
+  for (int64_t e = e0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t pe = pack_pos(e, ntl, Ns, world);
     if (PACK)
@@ -181,6 +181,61 @@ int Comm::chunk_to_slab(const double* B, double* A, double* tmp, int64_t& launch
   pack_kernel<false><<<1184, 256, 0, stream>>>(tmp, A, ntl, Ns, world);
   ++launches;
   if (cudaGetLastError() != cudaSuccess) return LS_ECUDA;
+  return LS_OK;
+}
+
+// ---- pipelined exchange (plan.hpp a2a_piece_plan) ------------------------------------------
+int Comm::pieces() const { return a2a_pieces(nt, world); }
+
+// pack (PACK) / unpack the slab rows of piece c: elements [a_c Ns, (a_c + l_c) Ns)
+int Comm::pack_piece(bool pack, const double* src, double* dst, int c, cudaStream_t s, int64_t& launches) {
+  const int64_t ntl = slab_len[rank];
+  int64_t a, l;
+  split_part(ntl, pieces(), c, &a, &l);
+  if (l == 0) return LS_OK;
+  if (pack)
+    pack_kernel<true><<<1184, 256, 0, s>>>(src, dst, ntl, Ns, world, a * Ns, (a + l) * Ns);
+  else
+    pack_kernel<false><<<1184, 256, 0, s>>>(src, dst, ntl, Ns, world, a * Ns, (a + l) * Ns);
+  ++launches;
+  return cudaGetLastError() == cudaSuccess ? LS_OK : LS_ECUDA;
+}
+
+// piece c of the all-to-all on stream s: fwd = packed slab (src) -> chunk tensor (dst); bwd = chunk
+// tensor (src) -> packed slab (dst), the transpose
+int Comm::exchange_piece(bool fwd, const double* src, double* dst, int c, cudaStream_t s) {
+  const int P = pieces();
+  NCCL_OK(ncclGroupStart());
+  for (int h = 0; h < world; ++h) {
+    int64_t so, sc, ro, rc;
+    a2a_piece_plan(nt, Ns, world, rank, h, c, P, &so, &sc, &ro, &rc);
+    if (fwd) {
+      NCCL_OK(ncclSend(src + so, size_t(sc), ncclDouble, h, C(nccl), s));
+      NCCL_OK(ncclRecv(dst + ro, size_t(rc), ncclDouble, h, C(nccl), s));
+    } else {
+      NCCL_OK(ncclSend(src + ro, size_t(rc), ncclDouble, h, C(nccl), s));
+      NCCL_OK(ncclRecv(dst + so, size_t(sc), ncclDouble, h, C(nccl), s));
+    }
+  }
+  NCCL_OK(ncclGroupEnd());
+  return LS_OK;
+}
+
+// halos of x_ext = [lo | own | hi] filled from the neighbours, the own boundary slices sent from
+// `own` (the caller's vector: no copy into x_ext), on stream s
+int Comm::halo_exchange_from(const double* own, double* x_ext, int p, cudaStream_t s) {
+  int64_t t0, ntl, lo, hi;
+  halo_plan(nt, world, rank, p, &t0, &ntl, &lo, &hi);
+  NCCL_OK(ncclGroupStart());
+  if (lo > 0) {
+    NCCL_OK(ncclRecv(x_ext, size_t(lo * Ns), ncclDouble, rank - 1, C(nccl), s));
+    NCCL_OK(ncclSend(own, size_t(lo * Ns), ncclDouble, rank - 1, C(nccl), s));
+  }
+  if (hi > 0) {
+    NCCL_OK(ncclRecv(x_ext + (lo + ntl) * Ns, size_t(hi * Ns), ncclDouble, rank + 1, C(nccl), s));
+    NCCL_OK(ncclSend(own + (ntl - hi) * Ns, size_t(hi * Ns), ncclDouble, rank + 1, C(nccl), s));
+  }
+  NCCL_OK(ncclGroupEnd());
   return LS_OK;
 }
 

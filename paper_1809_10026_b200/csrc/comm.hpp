@@ -38,6 +38,14 @@ struct Comm {
   // x_ext = [lo halo | own ntl slices | hi halo] (plan.hpp halo_plan): fill the halos
   int halo_exchange(double* x_ext, int p);
   int allreduce_scalar(double* dev_ptr);
+  // pipelined all-to-all (the default NCCL path of comm_fd_apply): pieces of consecutive time
+  // slices of every slab (plan.hpp a2a_piece_plan), packed / exchanged one by one so that the
+  // exchange of piece c overlaps the spatial modes of piece c + 1 (second stream)
+  int pieces() const;
+  int pack_piece(bool pack, const double* src, double* dst, int c, cudaStream_t s, int64_t& launches);
+  int exchange_piece(bool fwd, const double* src, double* dst, int c, cudaStream_t s);
+  // halos of x_ext filled from the neighbours, own boundary slices sent from `own` (no copy)
+  int halo_exchange_from(const double* own, double* x_ext, int p, cudaStream_t s);
 
   // ---- fused all-to-all over peer memory (ls_tune LS_TUNE_A2A = 1) -----------------
   // chunk_buf: this rank's [n_t][chunk_ld(len)] receive buffer of the forward exchange,

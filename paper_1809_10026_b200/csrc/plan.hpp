@@ -54,6 +54,35 @@ LS_HD void a2a_plan(int64_t nt, int64_t Ns, int world, int r, int h, int64_t* se
   *recv_cnt = ntlh * lenr;
 }
 
+// ---- pipelined NCCL all-to-all (comm.cu, comm_fd_apply) --------------------------------
+// Every slab is cut into the same number of pieces (consecutive time slices), so that the
+// spatial modes of piece c + 1 run while piece c is in flight.  Pieces per exchange: at most 4,
+// at most the thinnest slab (every rank derives the same number).
+LS_HD int a2a_pieces(int64_t nt, int world) {
+  const int64_t thin = nt / world;
+  return int(thin < 4 ? (thin < 1 ? 1 : thin) : 4);
+}
+
+// piece c of the slab -> chunk all-to-all of rank r with peer h (counts in doubles): piece c of
+// rank g's slab = its rows [a_gc, a_gc + l_gc) = split_part(ntl_g, pieces, c);
+//   send to h : packed buffer [ntl_r c0_h + a_rc len_h, + l_rc len_h)
+//   recv from h: chunk tensor rows [t0_h + a_hc, + l_hc): [(t0_h + a_hc) len_r, + l_hc len_r)
+// The union over the pieces is a2a_plan's exchange; chunk -> slab is the transpose.
+LS_HD void a2a_piece_plan(int64_t nt, int64_t Ns, int world, int r, int h, int c, int pieces, int64_t* send_off,
+                          int64_t* send_cnt, int64_t* recv_off, int64_t* recv_cnt) {
+  int64_t t0r, ntlr, t0h, ntlh, c0h, lenh, c0r, lenr, ar, lr, ah, lh;
+  split_part(nt, world, r, &t0r, &ntlr);
+  split_part(nt, world, h, &t0h, &ntlh);
+  split_part(Ns, world, h, &c0h, &lenh);
+  split_part(Ns, world, r, &c0r, &lenr);
+  split_part(ntlr, pieces, c, &ar, &lr);
+  split_part(ntlh, pieces, c, &ah, &lh);
+  *send_off = ntlr * c0h + ar * lenh;
+  *send_cnt = lr * lenh;
+  *recv_off = (t0h + ah) * lenr;
+  *recv_cnt = lh * lenr;
+}
+
 // ---- fused all-to-all (peer-memory epilogues, comm.cu / fd_rd_kernel.cuh) ---------------
 // Receive layouts: rank h's chunk buffer is [n_t][ld_h] with ld_h = chunk_ld(len_h) (rows
 // padded to 4 doubles so the time-mode kernel's 2-column loads and 4-column stores stay

@@ -72,6 +72,64 @@ def _fd_rank(rank, world, d, p, ne):
     return float(np.linalg.norm(z - ref) / np.linalg.norm(ref))
 
 
+def _fd_rank_pieces(rank, world, d, p, ne):
+    """The pipelined NCCL schedule of comm_fd_apply: per piece of consecutive time slices
+    (ls_a2a_piece_plan), F1 on the piece, pack the piece, exchange it; time mode on the chunk;
+    per piece, the transposed exchange, unpack, F3 on the piece."""
+    import paper_1809_10026_b200 as ls
+    space, tf, fdd = _setup(d, p, ne)
+    nt = tf["Mt"].shape[0]
+    gshape = (nt,) + tuple(f["M"].shape[0] for f in reversed(space))
+    Ns = int(np.prod(gshape[1:]))
+    r = synth.residual(gshape, 0)
+    t0, ntl = ls.partition(nt, world, rank)
+    c0, clen = ls.partition(Ns, world, rank)
+    P, _ = ls.a2a_piece_plan(nt, Ns, world, rank, -1)
+    pos = ls.pack_map(ntl, Ns, world)
+    packed = np.empty(ntl * Ns)
+    chunk = np.full(nt * clen, np.nan)
+    for c in range(P):
+        a, ln = ls.partition(ntl, P, c)
+        x = r[t0 + a:t0 + a + ln].copy()
+        for k in range(1, d + 1):                  # F1 on the piece
+            x = fd.mode_apply(x, fdd["U_s"][k - 1].T, d + 1 - k)
+        packed[pos[a * Ns:(a + ln) * Ns]] = x.ravel()  # pack_kernel<true> over the piece's elements
+        _, plan = ls.a2a_piece_plan(nt, Ns, world, rank, c)
+        send = np.concatenate([packed[so:so + sc] for (so, sc, _, _) in plan])
+        recv = torch.empty(sum(rc for (_, _, _, rc) in plan), dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(send), output_split_sizes=[rc for (_, _, _, rc) in plan],
+                               input_split_sizes=[sc for (_, sc, _, _) in plan])
+        off = 0
+        for (_, _, ro, rc) in plan:
+            chunk[ro:ro + rc] = recv.numpy()[off:off + rc]
+            off += rc
+    assert np.isfinite(chunk).all()
+    chunk = chunk.reshape(nt, clen)
+    lam_s = (fd.divisor(fdd) - fdd["lam_t"].reshape((-1,) + (1,) * d))[0].ravel()
+    y = fdd["U_t"].T @ chunk
+    y = y / (fdd["lam_t"][:, None] + lam_s[None, c0:c0 + clen])
+    y = np.ascontiguousarray(fdd["U_t"] @ y).ravel()
+    back = np.full(ntl * Ns, np.nan)
+    z = np.empty((ntl,) + gshape[1:])
+    for c in range(P):                             # transposed exchange, unpack, F3 per piece
+        a, ln = ls.partition(ntl, P, c)
+        _, plan = ls.a2a_piece_plan(nt, Ns, world, rank, c)
+        send = np.concatenate([y[ro:ro + rc] for (_, _, ro, rc) in plan])
+        recv = torch.empty(sum(sc for (_, sc, _, _) in plan), dtype=torch.float64)
+        dist.all_to_all_single(recv, torch.from_numpy(send), output_split_sizes=[sc for (_, sc, _, _) in plan],
+                               input_split_sizes=[rc for (_, _, _, rc) in plan])
+        off = 0
+        for (so, sc, _, _) in plan:
+            back[so:so + sc] = recv.numpy()[off:off + sc]
+            off += sc
+        zz = back[pos[a * Ns:(a + ln) * Ns]].reshape((ln,) + gshape[1:])  # pack_kernel<false>
+        for k in range(d, 0, -1):
+            zz = fd.mode_apply(zz, fdd["U_s"][k - 1], d + 1 - k)
+        z[a:a + ln] = zz
+    ref = fd.fd_apply(r, fdd)[t0:t0 + ntl]
+    return float(np.linalg.norm(z - ref) / np.linalg.norm(ref))
+
+
 def _matvec_rank(rank, world, d, p, ne):
     import paper_1809_10026_b200 as ls
     space, tf, _ = _setup(d, p, ne)
@@ -306,6 +364,38 @@ def _run(world, fn_name, args):
 def test_distributed_fd_schedule(world, d, p, ne):
     errs = _run(world, "_fd_rank", (d, p, ne))
     assert max(errs) <= 1e-12, errs
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("d,p,ne", [(2, 2, [5, 4, 7]), (3, 3, [3, 4, 2, 12])])
+def test_distributed_fd_schedule_pieces(world, d, p, ne):
+    errs = _run(world, "_fd_rank_pieces", (d, p, ne))
+    assert max(errs) <= 1e-12, errs
+
+
+def test_piece_plans_cover_the_exchange():
+    """The pieces of the pipelined all-to-all partition each rank's slab rows and reproduce
+    ls_a2a_plan's exchange segment by segment (what r sends to h in piece c is what h receives
+    from r in piece c)."""
+    import paper_1809_10026_b200 as ls
+    for nt, Ns, world in ((133, 1000, 8), (133, 2299968, 8), (13, 30, 2), (17, 45, 3), (9, 23, 4), (5, 64, 5), (7, 11, 1)):
+        P, _ = ls.a2a_piece_plan(nt, Ns, world, 0, -1)
+        assert P == min(4, max(1, nt // world))
+        for r in range(world):
+            full = ls.a2a_plan(nt, Ns, world, r)
+            pieces = [ls.a2a_piece_plan(nt, Ns, world, r, c)[1] for c in range(P)]
+            for h in range(world):
+                segs = [pc[h] for pc in pieces]
+                # send: consecutive sub-ranges of the packed block for h, in piece order
+                assert segs[0][0] == full["send_off"][h]
+                assert sum(sg[1] for sg in segs) == full["send_cnt"][h]
+                assert all(segs[c][0] + segs[c][1] == segs[c + 1][0] for c in range(P - 1))
+                # recv: consecutive row ranges of the chunk tensor from h
+                assert segs[0][2] == full["recv_off"][h]
+                assert sum(sg[3] for sg in segs) == full["recv_cnt"][h]
+                assert all(segs[c][2] + segs[c][3] == segs[c + 1][2] for c in range(P - 1))
+                for c in range(P):   # matching counts across the pair (r -> h) in piece c
+                    assert pieces[c][h][1] == ls.a2a_piece_plan(nt, Ns, world, h, c)[1][r][3]
 
 
 @pytest.mark.parametrize("world", [2, 3])
