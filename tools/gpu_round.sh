@@ -27,12 +27,12 @@ timeout 600 $G > gpurun_out/plain_pcg_$tag.log 2>&1 && \
 echo "pcg_launch_rc=$?"
 P="python tools/profile_fd.py --config 4 --reps 1"
 timeout 300 $P > gpurun_out/plain_prof_$tag.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fd_mode -c 3 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fd_mode -c 8 \
     -o gpurun_out/prof_c4_$tag -f $P > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu_full_rc=$?"
 M="python tools/profile_fd.py --config 4 --reps 1 --matvec"
 timeout 300 $M > gpurun_out/plain_mv_$tag.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k 'regex:band|mv4_plane' -c 4 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k 'regex:band|mv4_plane|mv5' -c 4 \
     -o gpurun_out/prof_mv_$tag -f $M > gpurun_out/ncu_mv_$tag.log 2>&1
 echo "ncu_mv_rc=$?"
 for r in gpurun_out/prof_c4_$tag gpurun_out/prof_mv_$tag; do
