@@ -446,6 +446,11 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * stay on chip and the time band product is a register scatter; 0 = two DMMA passes through
  * HBM; 2 = automatic (default): the fused pass for p <= 4, where it measured faster. */
 #define LS_TUNE_MV5 10
+/* LS_TUNE_FD_STAGED (process-wide): 1 = the split spatial mode products with an even extent
+ * (FAST strided or contiguous modes) run the cp.async-staged kernel (B operand ring in shared
+ * memory, 1 n-tile per warp, 2 CTAs per SM), 0 = the register-window kernel (default: the
+ * staged one measured 5 % slower at configs 4 and 5 p = 2, 2 % faster at p = 8). */
+#define LS_TUNE_FD_STAGED 11
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

@@ -31,6 +31,7 @@ extern int g_mv4_ctas;  // mv4.cu
 }
 
 int ls::g_ls_pdl = 1;  // programmatic dependent launch of the FD mode kernels (LS_TUNE_PDL)
+int ls::g_rd_staged = 0;  // staged split FD kernel (LS_TUNE_FD_STAGED; measured slower except p = 8, off)
 
 #define LS_CUDA(x)                                                                        \
   do {                                                                                    \
@@ -2335,6 +2336,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_MV5:  // v4: direction 3 + time fused into one pass (d = 3, p_s = p_t); 2 = automatic
       if (value < 0 || value > 2) return LS_EINVAL;
       ctx->mv5 = value;
+      return LS_OK;
+    case LS_TUNE_FD_STAGED:  // process-wide: the cp.async-staged split FD kernel where it applies
+      if (value != 0 && value != 1) return LS_EINVAL;
+      g_rd_staged = value;
       return LS_OK;
     case LS_TUNE_FD_CS:  // centrosymmetric split of the spatial modes (default 1 where the pencil allows)
       if (value != 0 && value != 1) return LS_EINVAL;

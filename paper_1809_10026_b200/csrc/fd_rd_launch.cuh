@@ -4,10 +4,12 @@
 #include <cuda_runtime.h>
 
 #include "fd_rd_kernel.cuh"
+#include "fd_rds_kernel.cuh"
 
 namespace ls {
 
 #define LS_RD_CS_MAXKS 17  // largest k-step bucket of the centrosymmetric split (n <= 136)
+extern int g_rd_staged;  // ls_tune LS_TUNE_FD_STAGED (process-wide), api.cu
 // tuning of the split kernels (variant builds: tools/rd_variant_libs.sh): n-tiles per warp,
 // CTAs per SM, prefetch window (0 = the per-bucket rule in rd_launch_cs)
 #ifndef LS_RD_CS_NT
@@ -47,12 +49,47 @@ static cudaError_t rd_launch_cfg(const ModeArgs& a, cudaStream_t s, int num_sms)
   return cudaGetLastError();
 }
 
+// staged split kernel (fd_rds_kernel.cuh): n even, FAST or contiguous, local stores
+template <class C>
+static cudaError_t rds_launch_cfg(const ModeArgs& a, cudaStream_t s, int num_sms) {
+  static bool ready = false;
+  if (!ready) {
+    cudaError_t e = cudaFuncSetAttribute(fd_mode_rds_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    ready = true;
+  }
+  const uint32_t ntw = (a.ncols + C::TW - 1) / C::TW;
+  if (ntw == 0) return cudaSuccess;
+  const unsigned grid = std::min<unsigned>((ntw + C::WARPS - 1) / C::WARPS, unsigned(num_sms * 2));
+  const cudaError_t e = launch_pdl(fd_mode_rds_kernel<C>, grid, C::THREADS, C::SMEM, s, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+#ifndef LS_RD_STAGED
+#define LS_RD_STAGED 1  // the staged split kernel where it applies (n even, FAST / contiguous)
+#endif
+
 // centrosymmetric split (cs = 1 fold / 2 unfold; KS = k-steps of the half extent ceil(n/2))
 template <int KS>
 cudaError_t rd_launch_cs(const ModeArgs& a, bool mode1, int cs, cudaStream_t s, int num_sms) {
   if constexpr (KS > LS_RD_CS_MAXKS) {
     return cudaErrorInvalidValue;
   } else {
+    if (LS_RD_STAGED && g_rd_staged && a.n % 2 == 0 && !a.remote) {
+      const bool fast16 = !mode1 && (a.Q % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
+                          ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
+      constexpr int DS = KS >= 16 ? 6 : 8;  // ring depth: 2 CTAs per SM within 227 KB
+      if (mode1) {
+        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, true, 1, DS>>(a, s, num_sms);
+        return rds_launch_cfg<RDSCfg<KS, true, 2, DS>>(a, s, num_sms);
+      }
+      if (fast16) {
+        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, false, 1, DS>>(a, s, num_sms);
+        return rds_launch_cfg<RDSCfg<KS, false, 2, DS>>(a, s, num_sms);
+      }
+    }
     // measured (tools/rd_variant_libs.sh + tools/ab_fd.py): half extents up to 52
     // (configs 3, 5) run 1 n-tile per warp, 2 CTAs per SM, window 4; above (config 4, he = 66) 2
     // n-tiles per warp, 1 CTA per SM, window 6

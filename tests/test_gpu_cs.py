@@ -80,11 +80,15 @@ FD_CASES = [
 ]
 
 
+@pytest.mark.parametrize("staged", [0, 1])
 @pytest.mark.parametrize("d,p,n_elems", FD_CASES)
-def test_cs_fd_apply(d, p, n_elems):
+def test_cs_fd_apply(d, p, n_elems, staged):
+    """staged = ls_tune LS_TUNE_FD_STAGED (11): the cp.async-staged split kernel for even
+    extents (fd_rds_kernel.cuh), process-wide, restored to the default afterwards."""
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, n_elems)
+    ctx.tune(11, staged)
     r = synth.residual(ctx.shape, 29)
     rg = torch.from_numpy(r).cuda()
     z_ref = fd.fd_apply(r, _fdd(d, p, n_elems))
@@ -94,6 +98,7 @@ def test_cs_fd_apply(d, p, n_elems):
     assert np.max(np.abs(z1 - z_ref)) <= TOL * np.abs(z_ref).max()
     ctx.tune(9, 0)
     z0 = ctx.fd_apply(rg).cpu().numpy()
+    ctx.tune(11, 0)
     assert _rel(z0, z_ref) <= TOL
     assert _rel(z1, z0) <= 1e-12
 
