@@ -61,12 +61,18 @@ static cudaError_t rds_launch_cfg(const ModeArgs& a, cudaStream_t s, int num_sms
   }
   const uint32_t ntw = (a.ncols + C::TW - 1) / C::TW;
   if (ntw == 0) return cudaSuccess;
-  const unsigned grid = std::min<unsigned>((ntw + C::WARPS - 1) / C::WARPS, unsigned(num_sms * 2));
+  const unsigned grid = std::min<unsigned>((ntw + C::WARPS - 1) / C::WARPS, unsigned(num_sms * C::MINB));
   const cudaError_t e = launch_pdl(fd_mode_rds_kernel<C>, grid, C::THREADS, C::SMEM, s, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
+#ifndef LS_RDS_NT
+#define LS_RDS_NT 1  // staged split kernel: n-tiles per warp (1: 2 CTAs per SM; 2: 1 CTA per SM, measured slower)
+#endif
+#ifndef LS_RDS_D
+#define LS_RDS_D 0   // staged split kernel: ring depth (0: 12 at NT = 2, 6 / 8 at NT = 1)
+#endif
 #ifndef LS_RD_STAGED
 #define LS_RD_STAGED 1  // the staged split kernel where it applies (n even, FAST / contiguous)
 #endif
@@ -80,14 +86,16 @@ cudaError_t rd_launch_cs(const ModeArgs& a, bool mode1, int cs, cudaStream_t s, 
     if (LS_RD_STAGED && g_rd_staged && a.n % 2 == 0 && !a.remote) {
       const bool fast16 = !mode1 && (a.Q % 2 == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
                           ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
-      constexpr int DS = KS >= 16 ? 6 : 8;  // ring depth: 2 CTAs per SM within 227 KB
+      // NT n-tiles per warp, MINB CTAs per SM, ring depth DS (within 227 KB of shared memory)
+      constexpr int NTS = LS_RDS_NT, MBS = NTS == 2 ? 1 : 2;
+      constexpr int DS = LS_RDS_D > 0 ? LS_RDS_D : (NTS == 2 ? 12 : (KS >= 16 ? 6 : 8));
       if (mode1) {
-        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, true, 1, DS>>(a, s, num_sms);
-        return rds_launch_cfg<RDSCfg<KS, true, 2, DS>>(a, s, num_sms);
+        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, true, 1, DS, NTS, MBS>>(a, s, num_sms);
+        return rds_launch_cfg<RDSCfg<KS, true, 2, DS, NTS, MBS>>(a, s, num_sms);
       }
-      if (fast16) {
-        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, false, 1, DS>>(a, s, num_sms);
-        return rds_launch_cfg<RDSCfg<KS, false, 2, DS>>(a, s, num_sms);
+      if (fast16 && a.Q % (2 * NTS) == 0) {
+        if (cs == 1) return rds_launch_cfg<RDSCfg<KS, false, 1, DS, NTS, MBS>>(a, s, num_sms);
+        return rds_launch_cfg<RDSCfg<KS, false, 2, DS, NTS, MBS>>(a, s, num_sms);
       }
     }
     // measured (tools/rd_variant_libs.sh + tools/ab_fd.py): half extents up to 52

@@ -12,6 +12,9 @@ ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
 ctx.tune(2, int(sys.argv[3]) if len(sys.argv) > 3 else 3)
 if len(sys.argv) > 4:
     ctx.tune(10, int(sys.argv[4]))
+for kv in filter(None, os.environ.get("LS_AB_TUNE", "").split(",")):  # knob=value,...
+    k, v = kv.split("=")
+    ctx.tune(int(k), int(v))
 x = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 y = torch.empty_like(x)
 for _ in range(3):
@@ -26,4 +29,4 @@ for rep in range(3):
     e1.record()
     e1.synchronize()
     best = min(best, e0.elapsed_time(e1) / 10)
-print(json.dumps({"lib": sys.argv[1], "config": sys.argv[2], "args": sys.argv[3:], "ms": round(best, 4), "chk": float(y.abs().sum())}))
+print(json.dumps({"lib": sys.argv[1], "config": sys.argv[2], "args": sys.argv[3:], "tune": os.environ.get("LS_AB_TUNE", ""), "ms": round(best, 4), "chk": float(y.abs().sum())}))
