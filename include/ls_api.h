@@ -451,6 +451,9 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * memory, 1 n-tile per warp, 2 CTAs per SM), 0 = the register-window kernel (default: the
  * staged one measured 5 % slower at configs 4 and 5 p = 2, 2 % faster at p = 8). */
 #define LS_TUNE_FD_STAGED 11
+/* LS_TUNE_PQ_FUSE: 1 = pcg_solve forms p.q in the epilogue of ls_matvec's last pass (v4 / v5
+ * paths; default), 0 = a separate dot pass. */
+#define LS_TUNE_PQ_FUSE 12
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

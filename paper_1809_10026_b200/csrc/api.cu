@@ -75,6 +75,7 @@ struct ls_ctx {
   double* Wf_cs[3] = {nullptr, nullptr, nullptr};  // [A_e^T (he x he) | A_o^T (ho x ho)]
   double* Wb_cs[3] = {nullptr, nullptr, nullptr};  // [A_e | A_o]
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
+  int pq_fuse = 1;     // ls_tune LS_TUNE_PQ_FUSE: p.q in the matvec's last-pass epilogue
   int mv5 = 2;         // ls_tune knob LS_TUNE_MV5: v4's direction-3 and time passes fused (mv5_kernels.cuh):
                        // 0 off, 1 on, 2 automatic (p <= 4: measured faster there, slower above)
   // PCG: the next ls_matvec also forms p.q (x.y) into scal[fuse_dot_slot] when its last pass can
@@ -1883,7 +1884,7 @@ static int dot(ls_ctx* ctx, const double* a, const double* b, int slot) {
 // q = A p and scal[slot] = p.q: fused into the matvec's last pass when the v4 path runs,
 // otherwise ls_matvec + dot
 static int matvec_dot(ls_ctx* ctx, const double* p, double* q, int slot) {
-  ctx->fuse_dot_slot = ctx->geo ? -1 : slot;
+  ctx->fuse_dot_slot = (ctx->geo || !ctx->pq_fuse) ? -1 : slot;
   ctx->fuse_dot_done = false;
   const int rc = ls_matvec(ctx, p, q);
   ctx->fuse_dot_slot = -1;
@@ -2336,6 +2337,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_MV5:  // v4: direction 3 + time fused into one pass (d = 3, p_s = p_t); 2 = automatic
       if (value < 0 || value > 2) return LS_EINVAL;
       ctx->mv5 = value;
+      return LS_OK;
+    case LS_TUNE_PQ_FUSE:  // PCG: p.q fused into the matvec's last pass (1) or a separate dot (0)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->pq_fuse = value;
       return LS_OK;
     case LS_TUNE_FD_STAGED:  // process-wide: the cp.async-staged split FD kernel where it applies
       if (value != 0 && value != 1) return LS_EINVAL;

@@ -149,8 +149,17 @@ __global__ void __launch_bounds__(256, 1) mv5_d3t_kernel(const __grid_constant__
     const uint32_t cy = strip * 8 + 2 * kq;  // its output columns cy, cy + 1
     const bool lane_ok = i3 >= 0 && i3 < n3 && cy < Q;
     const bool two = cy + 1 < Q;
+    // p of the row emitted at this slice (fused p.q), loaded before the slice's DMMAs
+    auto pload = [&](int t, double (&pv)[2]) {
+      pv[0] = pv[1] = 0.0;
+      if (a.dotp && t >= o_lo && t < o_hi && t < nt && lane_ok) {
+        const double* pp = a.dotp + int64_t(t - o_lo) * plane + int64_t(i3) * Q + cy;
+        pv[0] = __ldg(pp);
+        if (two) pv[1] = __ldg(pp + 1);
+      }
+    };
     // store row t (global) from a ring slot, then clear the slot
-    auto emit = [&](double (&yk)[2], int t) {
+    auto emit = [&](double (&yk)[2], int t, const double (&pv)[2]) {
       if (t >= o_lo && t < o_hi && t < nt && lane_ok) {
         double y0 = yk[0], y1 = yk[1];
         if (t == nt - 1) {
@@ -164,11 +173,7 @@ __global__ void __launch_bounds__(256, 1) mv5_d3t_kernel(const __grid_constant__
           o[0] = y0;
           if (two) o[1] = y1;
         }
-        if (a.dotp) {
-          const double* pp = a.dotp + (o - a.y);
-          dacc = fma(y0, __ldg(pp), dacc);
-          if (two) dacc = fma(y1, __ldg(pp + 1), dacc);
-        }
+        if (a.dotp) dacc = fma(y0, pv[0], fma(y1, pv[1], dacc));  // pv[1] = 0 when !two
       }
       yk[0] = yk[1] = 0.0;
     };
@@ -180,6 +185,8 @@ __global__ void __launch_bounds__(256, 1) mv5_d3t_kernel(const __grid_constant__
       for (int s = 0; s < R; ++s) {
         const int tp = t0 + s;  // global slice
         if (tp >= a.s_first && tp < t_end) {
+          double pv[2];
+          pload(tp - PT, pv);
           issue();  // slice tp + DEPTH - 1
           cp_async_wait<DEPTH - 1>();
           __syncwarp();
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(256, 1) mv5_d3t_kernel(const __grid_constant__
             yk[1] = fma(kt, v1[1], fma(mtc, v2[1], yk[1]));
           }
           // 3. row tp - PT is complete
-          emit(yr[(s - PT + 2 * R) % R], tp - PT);
+          emit(yr[(s - PT + 2 * R) % R], tp - PT, pv);
         }
       }
     }
@@ -226,7 +233,11 @@ __global__ void __launch_bounds__(256, 1) mv5_d3t_kernel(const __grid_constant__
     for (int k = 0; k < R; ++k) {
       const int te = t_end - PT;
       const int t = te + ((k - te) % R + R) % R;  // the row in slot k among [te, te + R)
-      if (t < t_end) emit(yr[k], t);
+      if (t < t_end) {
+        double pv[2];
+        pload(t, pv);
+        emit(yr[k], t, pv);
+      }
     }
     cp_async_wait<0>();
     __syncwarp();  // the ring is reused by the warp's next unit

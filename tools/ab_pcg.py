@@ -11,6 +11,9 @@ for spec in sys.argv[2:] or ["5:2", "4:6"]:
     c = synth.CONFIGS[int(cfg)]
     p = int(pp) if pp else c["p"]
     ctx = ls.Context(c["d"], p, [c["n_el"]] * (c["d"] + 1))
+    for kv in filter(None, os.environ.get("LS_AB_TUNE", "").split(",")):  # knob=value,...
+        k, v = kv.split("=")
+        ctx.tune(int(k), int(v))
     b = ctx.rhs(1)
     ctx.pcg(b, tol=1e-8)
     best = 1e9
@@ -20,7 +23,7 @@ for spec in sys.argv[2:] or ["5:2", "4:6"]:
         x, st = ctx.pcg(b, tol=1e-8)
         torch.cuda.synchronize()
         best = min(best, time.perf_counter() - t0)
-    print(json.dumps({"lib": os.path.basename(sys.argv[1]), "case": spec, "iters": st["iters"],
+    print(json.dumps({"lib": os.path.basename(sys.argv[1]), "tune": os.environ.get("LS_AB_TUNE", ""), "case": spec, "iters": st["iters"],
                       "solve_ms": round(best * 1e3, 2), "true_rel_res": st["true_rel_res"]}), flush=True)
     ctx.close()
     del b, x

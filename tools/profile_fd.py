@@ -23,6 +23,7 @@ ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--mv", type=int, default=0, help="ls_tune matvec variant")
 ap.add_argument("--fdk", type=int, default=0, help="ls_tune FD kernel variant")
 ap.add_argument("--pad", type=int, default=0, help="ls_tune v3 matvec padding")
+ap.add_argument("--nograph", action="store_true", help="PCG as the host-driven loop (profilers see every kernel)")
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = a.p if a.p is not None else (c["p"] if isinstance(c["p"], int) else c["p"][0])
@@ -31,6 +32,8 @@ ctx.tune(2, a.mv)
 ctx.tune(1, a.fdk)
 if a.pad:
     ctx.tune(3, a.pad)
+if a.nograph:
+    ctx.tune(5, 0)
 r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 z = torch.empty_like(r)
 if a.pcg:
