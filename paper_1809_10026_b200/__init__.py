@@ -35,6 +35,9 @@ EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_se
             "ls_setup_dist_deg", "ls_energy_error", "ls_error_norms", "ls_setup_geo", "ls_geo_info", "ls_setup_geo_dist", "ls_pg_factors"]
 
 LS_PRECOND_P, LS_PRECOND_PG = 0, 1
+# ls_tune knobs (include/ls_api.h)
+LS_TUNE_FD_KERNEL, LS_TUNE_MATVEC, LS_TUNE_MV3_PAD, LS_TUNE_A2A, LS_TUNE_PCG_GRAPH, LS_TUNE_PDL = 1, 2, 3, 4, 5, 6
+LS_TUNE_FD_TAIL, LS_TUNE_MV4_CTAS, LS_TUNE_FD_CS, LS_TUNE_MV5, LS_TUNE_FD_STAGED, LS_TUNE_PQ_FUSE = 7, 8, 9, 10, 11, 12
 
 
 class Geometry(ctypes.Structure):
@@ -458,8 +461,8 @@ class Context:
         return out[0], int(out[1])
 
     def tune(self, knob, value):
-        """ls_tune: select an equivalent implementation (knob 1 = FD mode kernel:
-        0 auto, 1 shared-memory staged, 2 register-direct)."""
+        """ls_tune: select an equivalent implementation (knobs LS_TUNE_*, include/ls_api.h;
+        e.g. LS_TUNE_FD_KERNEL: 0 auto, 1 shared-memory staged, 2 register-direct)."""
         _check(self._lib.ls_tune(self._h, int(knob), int(value)), "ls_tune")
 
     def profile(self, enable):

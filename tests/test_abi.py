@@ -58,3 +58,14 @@ def test_null_arguments(lib):
     assert lib.ls_matvec(None, None, None) == ls.LS_EINVAL
     assert lib.pcg_solve(None, None, None, 1e-8, 10, None) == ls.LS_EINVAL
     assert lib.ls_layout(None, None, None, None, None) == ls.LS_EINVAL
+
+
+def test_tune_constants_match_header():
+    """The binding's LS_TUNE_* constants are the header's (include/ls_api.h)."""
+    import re
+    import paper_1809_10026_b200 as ls
+    h = open(os.path.join(ROOT, "include", "ls_api.h")).read()
+    knobs = dict((k, int(v)) for k, v in re.findall(r"#define (LS_TUNE_\w+) (\d+)", h))
+    assert len(knobs) >= 12
+    for k, v in knobs.items():
+        assert getattr(ls, k) == v, k
