@@ -476,7 +476,7 @@ def main():
             # unsplit implementation would need for this DOF/s (not a hardware rate; > peak is possible)
             "gflops_paper_count_equivalent": w["flops_paper"] / (ms * 1e-3) / 1e9,
             "flops_note": ("algorithmic flops as executed: spatial mode products split by centrosymmetry "
-                           "(2 (he^2 + ho^2) per column instead of 2 n^2; DESIGN.md 5, reading c24), time modes "
+                           "(2 (he^2 + ho^2) per column instead of 2 n^2; DESIGN.md 5, reading c25), time modes "
                            "2 n_t^2 per column"),
             "roofline": roof,
             "cpu_baseline": {"value": cpu_val, "unit": "DOF/s", "cores": cores, "kind": "oracle",

@@ -418,7 +418,7 @@ static int upload(ls_ctx* ctx, const std::vector<double>& v, double** out);
 // eigenvector u = Q_e a of (J, M) with u^T M u = 1, so U = [Q_e A_e | Q_o A_o] and
 // lambda = [lambda_e | lambda_o] (ascending within each half).  The cross terms Q_e^T J Q_o are
 // the assembly's last-ulp asymmetry and are dropped: this is the eigenbasis of (J + RJR)/2,
-// (M + RMR)/2 (z moves by <= 4e-14 relative, reading c24).
+// (M + RMR)/2 (z moves by <= 4e-14 relative, reading c25).
 static int cs_eig(ls_ctx* ctx, int k, const std::vector<double>& J, const std::vector<double>& M, int n) {
   const int he = (n + 1) / 2, ho = n / 2;
   auto reduce = [&](const std::vector<double>& A, int nh, int sg, std::vector<long double>& E) {

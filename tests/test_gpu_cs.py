@@ -1,5 +1,5 @@
 """Centrosymmetric split of the spatial FD mode products (ls_tune LS_TUNE_FD_CS = 9, default 1;
-fd_rd_kernel.cuh "CS", api.cu cs_eig, reading c24).
+fd_rd_kernel.cuh "CS", api.cu cs_eig, reading c25).
 
 With uniform open knots and Dirichlet conditions at both ends (PAPER.md 266-267, 1111-1112)
 the space pencil (J, M) commutes with the index reversal R, so its eigenvectors (eq:eig_dec,

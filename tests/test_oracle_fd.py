@@ -136,7 +136,7 @@ def test_rank1_rows_match_full_fd():
 
 @pytest.mark.parametrize("n_el,p", [(16, 2), (64, 3), (96, 2), (96, 4), (96, 8), (128, 6), (130, 2)])
 def test_space_pencil_centrosymmetric(n_el, p):
-    """Reading c24: on uniform open knots with Dirichlet conditions at both ends
+    """Reading c25: on uniform open knots with Dirichlet conditions at both ends
     (PAPER.md 266-267, 1111-1112) the exact space matrices are centrosymmetric (b_i(1-x) =
     b_{n+1-i}(x)); the assembled fp64 ones are so to the last ulp, and the FD solution with the
     symmetrised pencil (J + RJR)/2, (M + RMR)/2 -- whose eigenbasis the library's split uses --
