@@ -454,6 +454,16 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
 /* LS_TUNE_PQ_FUSE: 1 = pcg_solve forms p.q in the epilogue of ls_matvec's last pass (v4 / v5
  * paths; default), 0 = a separate dot pass. */
 #define LS_TUNE_PQ_FUSE 12
+/* LS_TUNE_FD_TIME: 1 = fd_apply's time mode (U_t^T, the division by lambda_t + Lambda_s of
+ * Algorithm 1 step 3, U_t; PAPER.md 947-962) runs as ONE kernel whose intermediate stays in
+ * registers, where n_t <= 104 (default); 0 = two launches (the scaled forward product into a
+ * workspace, then the backward product).  n_t > 104 always uses two launches. */
+#define LS_TUNE_FD_TIME 13
+/* LS_TUNE_FD_PLANE: 1 = fd_apply's spatial mode products of directions 1 and 2 run as ONE
+ * kernel per (i_3, .., t) plane whose intermediate stays in registers, where both directions
+ * use the centrosymmetric split (LS_TUNE_FD_CS) with n_1 = n_2 <= 104; 0 = one launch per
+ * direction (default: the plane kernel measured 5-10 % slower at BASELINE configs 3 and 5). */
+#define LS_TUNE_FD_PLANE 14
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

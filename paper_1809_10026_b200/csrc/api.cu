@@ -15,6 +15,10 @@
 #include "plan.hpp"
 #include "fd_kernels.cuh"
 #include "fd_rd_launch.cuh"
+#include "fd_time_kernel.cuh"
+#include "ft.hpp"
+#include "fd_plane_kernel.cuh"
+#include "pl.hpp"
 #include "matvec_kernels.cuh"
 #include "matvec2_kernels.cuh"
 #include "matvec3_kernels.cuh"
@@ -72,6 +76,9 @@ struct ls_ctx {
   // eigenbasis was built from the even / odd reduced pencils; fd_cs = ls_tune LS_TUNE_FD_CS
   bool cs_dir[3] = {false, false, false};
   int fd_cs = 1;
+  int fd_time = 1;
+  int fd_plane = 0;  // ls_tune LS_TUNE_FD_PLANE: spatial modes 1 + 2 in one launch (fd_plane_kernel.cuh;
+                     // opt-in: measured slower than the per-direction split kernels)  // ls_tune LS_TUNE_FD_TIME: fused time mode (fd_time_kernel.cuh) where n_t <= 104
   double* Wf_cs[3] = {nullptr, nullptr, nullptr};  // [A_e^T (he x he) | A_o^T (ho x ho)]
   double* Wb_cs[3] = {nullptr, nullptr, nullptr};  // [A_e | A_o]
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
@@ -937,19 +944,68 @@ static inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>
 // direction k runs the centrosymmetric split (half the DMMA work of its mode products)
 static inline bool use_cs(const ls_ctx* ctx, int k) { return ctx->fd_cs && ctx->cs_dir[k]; }
 
+// directions 1 and 2 run as one plane launch (fd_plane_kernel.cuh): both split, n_1 = n_2
+static bool use_plane(const ls_ctx* ctx) {
+  return ctx->fd_plane && ctx->d >= 2 && use_cs(ctx, 0) && use_cs(ctx, 1) && ctx->n[0] == ctx->n[1] &&
+         pl_supported(ctx->n[0]);
+}
+
+static int launch_plane(ls_ctx* ctx, const double* X, double* Y, uint64_t planes, bool forward) {
+  if (planes == 0) return LS_OK;
+  PLArgs a{};
+  a.X = X;
+  a.Y = Y;
+  a.W2 = forward ? ctx->Wf_cs[1] : ctx->Wb_cs[1];
+  a.W1 = forward ? ctx->Wf_cs[0] : ctx->Wb_cs[0];
+  a.n = ctx->n[0];
+  a.planes = uint32_t(planes);
+  ls_ctx::ProfRec rec{};
+  if (ctx->prof) {
+    rec.a = ctx->get_event();
+    rec.b = ctx->get_event();
+    const double he = (a.n + 1) / 2, ho = a.n / 2;
+    rec.flops = 2.0 * 2.0 * (he * he + ho * ho) * double(a.n) * double(planes);  // two split products per plane
+    cudaEventRecord(rec.a, ctx->stream);
+  }
+  const cudaError_t e = pl_launch(a, forward, ctx->stream, ctx->num_sms);
+  ctx->launches++;
+  if (ctx->prof) {
+    cudaEventRecord(rec.b, ctx->stream);
+    ctx->prof_recs.push_back(rec);
+  }
+  LS_CUDA(e);
+  return LS_OK;
+}
+
 // spatial modes on a [rows][n_d]..[n_1] block (rows = local time slices)
 static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0, double* ws1,
                          uint64_t rows, bool forward) {
   const int d = ctx->d;
-  // forward: modes 1..d ; backward: modes d..1.  Ping-pong ws0/ws1, first reads `in`,
-  // last writes `out`.
+  // steps: direction k (0-based), or -1 = the plane launch of directions 1 + 2.  forward:
+  // 1..d, backward: d..1.  Ping-pong ws0/ws1, the first step reads `in`, the last writes `out`.
+  int steps[3], ns = 0;
+  const bool plane = use_plane(ctx);
+  if (forward) {
+    if (plane) steps[ns++] = -1;
+    for (int k = plane ? 2 : 0; k < d; ++k) steps[ns++] = k;
+  } else {
+    for (int k = d - 1; k >= (plane ? 2 : 0); --k) steps[ns++] = k;
+    if (plane) steps[ns++] = -1;
+  }
   const double* src = in;
-  for (int s = 0; s < d; ++s) {
-    const int k = forward ? s : d - 1 - s;  // 0-based direction
+  for (int s = 0; s < ns; ++s) {
+    double* dst = (s == ns - 1) ? out : ((s % 2 == 0) ? ws0 : ws1);
+    const int k = steps[s];
+    if (k < 0) {
+      uint64_t P = rows;
+      for (int j = 2; j < d; ++j) P *= ctx->n[j];
+      LS_CHECK(launch_plane(ctx, src, dst, P, forward));
+      src = dst;
+      continue;
+    }
     uint64_t Q = 1, P = rows;
     for (int j = 0; j < k; ++j) Q *= ctx->n[j];
     for (int j = k + 1; j < d; ++j) P *= ctx->n[j];
-    double* dst = (s == d - 1) ? out : ((s % 2 == 0) ? ws0 : ws1);
     if (use_cs(ctx, k))
       LS_CHECK(launch_mode(ctx, src, dst, forward ? ctx->Wf_cs[k] : ctx->Wb_cs[k], ctx->n[k], P, Q, false, nullptr,
                            nullptr, forward ? 1 : 2));
@@ -958,6 +1014,42 @@ static int spatial_modes(ls_ctx* ctx, const double* in, double* out, double* ws0
     src = dst;
   }
   return LS_OK;
+}
+
+// F2: the time mode on columns [n_t][ld] (ncols used; Lambda_s of column 0 at lam_c):
+// U_t^T, /(lambda_t + Lambda_s), U_t.  One fused launch (fd_time_kernel.cuh: the intermediate
+// stays in registers) where n_t <= 104, else the scaled forward launch into `mid` and the
+// backward launch.  X -> Z; Z may equal X on the fused path only.
+static int time_modes(ls_ctx* ctx, const double* X, double* mid, double* Z, uint64_t ncols, const double* lam_c) {
+  if (ncols == 0) return LS_OK;
+  if (ctx->fd_time && ft_bucket(ctx->nt) > 0) {
+    FTArgs a{};
+    a.X = X;
+    a.Z = Z;
+    a.U = ctx->Wb[3];
+    a.lam_t = ctx->lam[3];
+    a.lam_s = lam_c;
+    a.nt = ctx->nt;
+    a.ncols = uint32_t(ncols);
+    a.ld = ncols;
+    ls_ctx::ProfRec rec{};
+    if (ctx->prof) {
+      rec.a = ctx->get_event();
+      rec.b = ctx->get_event();
+      rec.flops = 4.0 * double(ctx->nt) * double(ctx->nt) * double(ncols);  // two n_t x n_t products
+      cudaEventRecord(rec.a, ctx->stream);
+    }
+    const cudaError_t e = ft_launch(a, ctx->stream, ctx->num_sms);
+    ctx->launches++;
+    if (ctx->prof) {
+      cudaEventRecord(rec.b, ctx->stream);
+      ctx->prof_recs.push_back(rec);
+    }
+    LS_CUDA(e);
+    return LS_OK;
+  }
+  LS_CHECK(launch_mode(ctx, X, mid, ctx->Wf[3], ctx->nt, 1, ncols, true, ctx->lam[3], lam_c));
+  return launch_mode(ctx, mid, Z, ctx->Wb[3], ctx->nt, 1, ncols, false);
 }
 
 static int fd_core(ls_ctx* ctx, const double* r, double* z);
@@ -981,8 +1073,7 @@ static int fd_core(ls_ctx* ctx, const double* r, double* z) {
   if (ctx->world == 1) {
     // F1: forward spatial modes r -> A ; F2: time fwd + scale (A -> B), time bwd (B -> C)
     LS_CHECK(spatial_modes(ctx, r, A, B, C, ctx->nt, true));
-    LS_CHECK(launch_mode(ctx, A, B, ctx->Wf[3], ctx->nt, 1, ctx->Ns, true, ctx->lam[3], ctx->lam_s));
-    LS_CHECK(launch_mode(ctx, B, C, ctx->Wb[3], ctx->nt, 1, ctx->Ns, false));
+    LS_CHECK(time_modes(ctx, A, B, C, ctx->Ns, ctx->lam_s));
     // F3: backward spatial modes C -> z
     LS_CHECK(spatial_modes(ctx, C, z, A, B, ctx->nt, false));
     return LS_OK;
@@ -1003,9 +1094,7 @@ extern "C" int fd_apply_stage(ls_ctx* ctx, int stage, const double* in, double* 
     }
     case 1: {  // time mode U_t^T, /(lambda_t + Lambda_s), U_t on a chunk [n_t][b] at spatial offset a
       if (a < 0 || b < 1 || a + b > ctx->Ns || int64_t(ctx->nt) * b > (ctx->Nl + 2 * ctx->pt * ctx->Ns)) return LS_EINVAL;
-      double* mid = ctx->tmp[3];
-      LS_CHECK(launch_mode(ctx, in, mid, ctx->Wf[3], ctx->nt, 1, uint64_t(b), true, ctx->lam[3], ctx->lam_s + a));
-      return launch_mode(ctx, mid, out, ctx->Wb[3], ctx->nt, 1, uint64_t(b), false);
+      return time_modes(ctx, in, ctx->tmp[3], out, uint64_t(b), ctx->lam_s + a);
     }
     default: return LS_EINVAL;
   }
@@ -1167,8 +1256,7 @@ int comm_fd_apply(ls_ctx* ctx, const double* r, double* z) {
   const int64_t chunk = cm.chunk_len[ctx->rank];
   const int64_t c0 = cm.chunk_off[ctx->rank];
   if (chunk > 0) {
-    LS_CHECK(launch_mode(ctx, B, C, ctx->Wf[3], ctx->nt, 1, chunk, true, ctx->lam[3], ctx->lam_s + c0));
-    LS_CHECK(launch_mode(ctx, C, B, ctx->Wb[3], ctx->nt, 1, chunk, false));
+    LS_CHECK(time_modes(ctx, B, C, B, uint64_t(chunk), ctx->lam_s + c0));
   }
   LS_CUDA(cudaEventRecord(ev[2], ctx->stream));
   LS_CUDA(cudaStreamWaitEvent(cs, ev[2], 0));
@@ -2179,8 +2267,7 @@ extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) 
       LS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->hev[k], 0));
       LS_CHECK(spatial_modes(ctx, R + off * Ns, A + off * Ns, B + off * Ns, C + off * Ns, uint64_t(rows), true));
     }
-    LS_CHECK(launch_mode(ctx, A, B, ctx->Wf[3], ctx->nt, 1, Ns, true, ctx->lam[3], ctx->lam_s));
-    LS_CHECK(launch_mode(ctx, B, C, ctx->Wb[3], ctx->nt, 1, Ns, false));
+    LS_CHECK(time_modes(ctx, A, B, C, uint64_t(Ns), ctx->lam_s));
     for (int k = 0; k < NCH; ++k) {
       int64_t off, rows;
       split_part(ctx->ntl, NCH, k, &off, &rows);
@@ -2345,6 +2432,14 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_FD_STAGED:  // process-wide: the cp.async-staged split FD kernel where it applies
       if (value != 0 && value != 1) return LS_EINVAL;
       g_rd_staged = value;
+      return LS_OK;
+    case LS_TUNE_FD_TIME:  // fused time mode (one launch) where n_t <= 104 (1, default) or two launches (0)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->fd_time = value;
+      return LS_OK;
+    case LS_TUNE_FD_PLANE:  // spatial modes 1 + 2 as one plane launch where supported (1) or per direction (0, default)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->fd_plane = value;
       return LS_OK;
     case LS_TUNE_FD_CS:  // centrosymmetric split of the spatial modes (default 1 where the pencil allows)
       if (value != 0 && value != 1) return LS_EINVAL;

@@ -1,0 +1,234 @@
+// Fused time mode of fd_apply (Algorithm 1 steps 2-4 for the time direction, PAPER.md
+// 959-962; SURVEY.md 3 "k_time_fused"): for every spatial column s of X[t][s]
+//     Y[j][s] = sum_t U_t[t][j] X[t][s]                       (U_t^T, forward time mode)
+//     Y[j][s] /= (lambda_t[j] + Lambda_s[s])                    (step 3, reading c3)
+//     Z[t'][s] = sum_j U_t[t'][j] Y[j][s]                      (U_t, backward time mode)
+// in ONE kernel: Y never leaves the registers (one HBM round trip, 16 B/DOF, instead of two).
+//
+// Operand roles (m8n8k4, FP64 DMMA; fd_kernels.cuh): the streamed X is the A operand of
+// the first product, A[m = s][k = t] (Y^T = X^T U_t), so its accumulators (C fragments:
+// lane (r = l/4, c = l%4) holds rows m = r, columns n = 2c, 2c+1 of every n-tile) are,
+// register for register, the A fragments of the second product Z^T = Y^T U_t^T
+// (A[m = r][k = c] of k-step (jt, h) is column 2c + h of n-tile jt).  The k order of a
+// contraction is free, so the eigen index j of column n = 2c + h of n-tile jt is chosen as
+// j = 8 jt + 4 h + c: k-step (jt, h) of the second product then covers j = 8jt+4h .. +3,
+// and the k-steps past 4 KS (all-zero columns) are skipped.
+// M mapping: a warp owns 16 consecutive columns s0 .. s0+15; row r of m-tile ms is column
+// s = s0 + 2 r + ms, so a lane's two m-tile elements are one 16-byte pair (LDG.128 / STG.128
+// when the row stride is even: VEC).
+// Both U_t operands sit in shared memory in B-fragment order, two k-steps per LDS.128:
+//   B1 (first product):  b1[((jt*KSP + ks/2)*32 + l)*2 + ks%2] = U_t[4ks + l%4][8jt + 4((l/4)%2) + l/8]
+//   B2 (second product): b2[((tt*NJ + jt)*32 + l)*2 + h]      = U_t[8tt + l/4][8jt + 4h + l%4]
+// (zero outside n_t x n_t).  Each LDS.128 feeds 4 DMMAs (2 k-steps x 2 m-tiles).
+// X loads stream through a rolling register window D k-steps ahead that crosses into the
+// warp's next tile, so the second product of one tile overlaps the first loads of the next.
+// Sizes: n_t <= 4 KS, KS <= 26 (n_t <= 104: both fragment sets fit in shared memory).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fd_rd_kernel.cuh"  // ldg_stream, dmma_8x8x4, fast_rcp
+
+namespace ls {
+
+struct FTArgs {
+  const double* X;       // [n_t][ld] (columns 0 .. ncols-1 used)
+  double* Z;             // [n_t][ld]; may equal X (a warp reads its columns before writing them)
+  const double* U;       // U_t, n_t x n_t row-major (row = time index t, column = eigen index j)
+  const double* lam_t;   // lambda_t [n_t]
+  const double* lam_s;   // Lambda_s per column [ncols]
+  int nt;
+  uint32_t ncols;
+  uint64_t ld;           // row stride (elements)
+};
+
+template <int KS_, bool VEC_, int D_, int MINB_>
+struct FTCfg {
+  static constexpr int KS = KS_, D = D_, MINB = MINB_;
+  static constexpr bool VEC = VEC_;
+  static constexpr int NJ = (KS + 1) / 2;      // 8-wide n-tiles of j (and of t' in the output)
+  static constexpr int KSP = NJ;               // k-step pairs of the first product
+  static constexpr int WARPS = 8, THREADS = 32 * WARPS;
+  static constexpr int TW = 16;                // columns per warp tile (2 m-tiles)
+  static constexpr int B1N = NJ * KSP * 64;    // doubles
+  static constexpr int B2N = NJ * NJ * 64;
+  static constexpr int LAMN = 8 * NJ;
+  static constexpr int KSE = ((KS + D - 1) / D) * D;  // k-steps rounded up to the window
+  static constexpr size_t SMEM = size_t(B1N + B2N + LAMN) * sizeof(double);
+  static_assert(KS <= 26, "n_t <= 104");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <class C>
+__global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  double* b1 = smem;
+  double* b2 = smem + C::B1N;
+  double* lam = b2 + C::B2N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = lane & 3, r = lane >> 2;
+  const int nt = a.nt;
+
+  // U_t -> B-fragment order (see the header); lambda_t padded with 1 (the padded
+  // accumulator columns are 0, a finite divisor keeps them 0)
+  for (int e = tid; e < C::B1N; e += C::THREADS) {
+    const int h = e & 1, l = (e >> 1) & 31, ksp = (e >> 6) % C::KSP, jt = (e >> 6) / C::KSP;
+    const int t = 4 * (2 * ksp + h) + (l & 3);
+    const int j = 8 * jt + 4 * ((l >> 2) & 1) + (l >> 3);
+    b1[e] = (t < nt && j < nt) ? __ldg(a.U + size_t(t) * nt + j) : 0.0;
+  }
+  for (int e = tid; e < C::B2N; e += C::THREADS) {
+    const int h = e & 1, l = (e >> 1) & 31, jt = (e >> 6) % C::NJ, tt = (e >> 6) / C::NJ;
+    const int t = 8 * tt + (l >> 2);
+    const int j = 8 * jt + 4 * h + (l & 3);
+    b2[e] = (t < nt && j < nt) ? __ldg(a.U + size_t(t) * nt + j) : 0.0;
+  }
+  for (int e = tid; e < C::LAMN; e += C::THREADS) lam[e] = e < nt ? __ldg(a.lam_t + e) : 1.0;
+  __syncthreads();
+
+  const uint32_t ncols = a.ncols;
+  const uint32_t ntw = (ncols + C::TW - 1) / C::TW;
+  const uint32_t wstride = gridDim.x * C::WARPS;
+  uint32_t tile = blockIdx.x * C::WARPS + warp;
+  if (tile >= ntw) return;
+  const size_t ld = a.ld;
+  const size_t kstep = 4 * ld;
+
+  pdl_wait();  // X is the previous kernel's output
+
+  // lane's A elements of k-step ks: X[4ks + c][s0 + 2r + {0, 1}]
+  const double* lp;
+  uint32_t cnt = 0;  // valid columns of the lane's pair (0, 1, 2)
+  auto set_ptr = [&](uint32_t tl) {
+    const uint32_t s = tl * C::TW + 2 * r;
+    lp = a.X + size_t(c) * ld + s;
+    cnt = s >= ncols ? 0u : (s + 1 >= ncols ? 1u : 2u);
+  };
+  auto load = [&](double2& dst, int ks) {
+    const bool ok = 4 * ks + c < nt;
+    if (C::VEC) {
+      dst = (ok && cnt == 2) ? ldg_stream2(lp) : make_double2(0.0, 0.0);
+    } else {
+      dst.x = (ok && cnt >= 1) ? ldg_stream(lp) : 0.0;
+      dst.y = (ok && cnt == 2) ? ldg_stream(lp + 1) : 0.0;
+    }
+    lp += kstep;
+  };
+  double2 win[C::D];
+  set_ptr(tile);
+#pragma unroll
+  for (int s = 0; s < C::D; ++s)
+    if (s < C::KS) load(win[s], s);
+
+  const double* b1l = b1 + 2 * lane;
+  const double* b2l = b2 + 2 * lane;
+
+#pragma unroll 1
+  for (; tile < ntw; tile += wstride) {
+    const uint32_t nxt = tile + wstride;
+    const uint32_t s0 = tile * C::TW + 2 * r;  // the lane's column pair
+    double ls0 = 1.0, ls1 = 1.0;                // Lambda_s of the pair (loaded ahead of use)
+    if (s0 < ncols) ls0 = __ldg(a.lam_s + s0);
+    if (s0 + 1 < ncols) ls1 = __ldg(a.lam_s + s0 + 1);
+
+    // ---- first product: acc[ms][jt] = (X^T U_t) rows s0 + ms, columns of n-tile jt
+    double acc[2][C::NJ][2];
+#pragma unroll
+    for (int ms = 0; ms < 2; ++ms)
+#pragma unroll
+      for (int jt = 0; jt < C::NJ; ++jt) acc[ms][jt][0] = acc[ms][jt][1] = 0.0;
+#pragma unroll
+    for (int ksp = 0; ksp < C::KSE / 2 + (C::KSE & 1); ++ksp) {
+      const int k0 = 2 * ksp, k1 = 2 * ksp + 1;
+      if (k0 < C::KS) {
+        const double2 x0 = win[k0 % C::D];
+        const double2 x1 = (k1 < C::KS) ? win[k1 % C::D] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int jt = 0; jt < C::NJ; ++jt) {
+          const double2 bf = *reinterpret_cast<const double2*>(b1l + (jt * C::KSP + ksp) * 64);
+          dmma_8x8x4(acc[0][jt], x0.x, bf.x);
+          dmma_8x8x4(acc[1][jt], x0.y, bf.x);
+          if (k1 < C::KS) {
+            dmma_8x8x4(acc[0][jt], x1.x, bf.y);
+            dmma_8x8x4(acc[1][jt], x1.y, bf.y);
+          }
+        }
+      }
+      // refill the consumed slots: k + D of this tile, or the next tile's first k-steps
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = k0 + h;
+        if (k >= C::KSE) continue;
+        const int kk = k + C::D;
+        if (kk < C::KS) {
+          load(win[k % C::D], kk);
+        } else if (kk >= C::KSE) {
+          const int s = kk - C::KSE;  // the next tile's k-step s, same slot (KSE % D == 0)
+          if (s == 0) set_ptr(nxt);
+          if (s < C::KS) load(win[k % C::D], s);
+        }
+      }
+    }
+
+    // ---- step 3: acc[ms][jt][h] is Y^T[s0 + ms][j = 8jt + 4h + c]
+#pragma unroll
+    for (int jt = 0; jt < C::NJ; ++jt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double lt = lam[8 * jt + 4 * h + c];
+        acc[0][jt][h] *= fast_rcp(lt + ls0);
+        acc[1][jt][h] *= fast_rcp(lt + ls1);
+      }
+
+    // ---- second product, two output n-tiles (t' = 8tt + 2c + {0,1}) at a time
+    double* zp = a.Z + s0;
+#pragma unroll 1
+    for (int tt = 0; tt < C::NJ; tt += 2) {
+      const bool two = tt + 1 < C::NJ;
+      double o[2][2][2];  // [tile of the pair][ms][column half]
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int ms = 0; ms < 2; ++ms) o[u][ms][0] = o[u][ms][1] = 0.0;
+#pragma unroll
+      for (int jt = 0; jt < C::NJ; ++jt) {
+        const bool h1 = 2 * jt + 1 < C::KS;  // k-step (jt, 1) has valid columns
+        const double2 f0 = *reinterpret_cast<const double2*>(b2l + (tt * C::NJ + jt) * 64);
+        dmma_8x8x4(o[0][0], acc[0][jt][0], f0.x);
+        dmma_8x8x4(o[0][1], acc[1][jt][0], f0.x);
+        if (h1) {
+          dmma_8x8x4(o[0][0], acc[0][jt][1], f0.y);
+          dmma_8x8x4(o[0][1], acc[1][jt][1], f0.y);
+        }
+        if (two) {
+          const double2 f1 = *reinterpret_cast<const double2*>(b2l + ((tt + 1) * C::NJ + jt) * 64);
+          dmma_8x8x4(o[1][0], acc[0][jt][0], f1.x);
+          dmma_8x8x4(o[1][1], acc[1][jt][0], f1.x);
+          if (h1) {
+            dmma_8x8x4(o[1][0], acc[0][jt][1], f1.y);
+            dmma_8x8x4(o[1][1], acc[1][jt][1], f1.y);
+          }
+        }
+      }
+      // store: o[u][ms][h] = Z[t' = 8(tt+u) + 2c + h][s0 + ms]
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int t = 8 * (tt + u) + 2 * c + h;
+          if (t >= nt || s0 >= ncols) continue;
+          double* dst = zp + size_t(t) * ld;
+          if (C::VEC) {
+            *reinterpret_cast<double2*>(dst) = make_double2(o[u][0][h], o[u][1][h]);
+          } else {
+            dst[0] = o[u][0][h];
+            if (s0 + 1 < ncols) dst[1] = o[u][1][h];
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace ls
