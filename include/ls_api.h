@@ -464,6 +464,11 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * use the centrosymmetric split (LS_TUNE_FD_CS) with n_1 = n_2 <= 104; 0 = one launch per
  * direction (default: the plane kernel measured 5-10 % slower at BASELINE configs 3 and 5). */
 #define LS_TUNE_FD_PLANE 14
+/* LS_TUNE_MV6: the v4 matvec's direction-3 and time passes (after its DMMA plane pass) as
+ * streaming DFMA Toeplitz-stencil passes (exactly 2p + 1 multiply-adds per banded output, no
+ * band-tile padding) instead of DMMA band tiles: 0 = off (default: latency-bound, measured
+ * slower at configs 4 and 5), 1 = on (the v5 fused pass, where it applies, takes precedence). */
+#define LS_TUNE_MV6 15
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

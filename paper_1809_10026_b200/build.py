@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libls.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["api.cu", "comm.cu", "setup_host.cpp", "mv2.cu", "mv3.cu", "mv4.cu", "mv5.cu", "geo.cu", "geo_host.cpp", "err.cu", "ft.cu", "pl.cu"]
+SOURCES = ["api.cu", "comm.cu", "setup_host.cpp", "mv2.cu", "mv3.cu", "mv4.cu", "mv5.cu", "geo.cu", "geo_host.cpp", "err.cu", "ft.cu", "pl.cu", "mv6.cu"]
 RD_BUCKETS = [2, 4, 5, 8, 9, 12, 13, 16, 17, 18, 24, 25, 26, 30, 33, 34]  # = LS_RD_BUCKETS
 
 

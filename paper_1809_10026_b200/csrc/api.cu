@@ -24,6 +24,7 @@
 #include "matvec3_kernels.cuh"
 #include "mv4_kernels.cuh"
 #include "mv5_kernels.cuh"
+#include "matvec6_kernels.cuh"
 #include "pcg_kernels.cuh"
 #include "setup_host.hpp"
 #include "geo.hpp"
@@ -82,6 +83,8 @@ struct ls_ctx {
   double* Wf_cs[3] = {nullptr, nullptr, nullptr};  // [A_e^T (he x he) | A_o^T (ho x ho)]
   double* Wb_cs[3] = {nullptr, nullptr, nullptr};  // [A_e | A_o]
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
+  int mv6 = 0;         // ls_tune LS_TUNE_MV6: v4's direction-3 and time passes as DFMA stencil passes
+                       // (matvec6_kernels.cuh): 0 off (default: measured slower), 1 on
   int pq_fuse = 1;     // ls_tune LS_TUNE_PQ_FUSE: p.q in the matvec's last-pass epilogue
   int mv5 = 2;         // ls_tune knob LS_TUNE_MV5: v4's direction-3 and time passes fused (mv5_kernels.cuh):
                        // 0 off, 1 on, 2 automatic (p <= 4: measured faster there, slower above)
@@ -1706,6 +1709,65 @@ static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   const int64_t tT = (ctx->nt - 1) - s_first;  // the last time slice among the stored rows
   const bool have_last = tT >= 0 && tT < rows;
   const double *v1 = PM, *v2 = PJ, *v3 = have_last ? PK + tT * ctx->Ns : nullptr;
+  if (ctx->mv6 == 1) {
+    // v6: the same two passes as DFMA Toeplitz stencils (matvec6_kernels.cuh)
+    if (d == 3) {
+      MV6Args a{};
+      const auto& sp = ctx->dsplit[2];
+      mv_set(a.m, 0, sp.M);
+      mv_set(a.m, 1, sp.J);
+      mv_set(a.m, 2, sp.K);
+      mv_set(a.m, 3, sp.K2);
+      a.m.r_lo = sp.lo;
+      a.m.r_hi = sp.hi;
+      a.m.in[0] = PM;
+      a.m.in[1] = PK;
+      a.m.in[2] = PJ;
+      a.m.out[0] = ctx->tmp[3];
+      a.m.out[1] = ctx->tmp[4];
+      a.m.n = ctx->n[2];
+      a.Q = uint32_t(int64_t(n1) * n2);
+      a.rows = int(rows);
+      a.tT = have_last ? int(tT) : -1;
+      a.L = ctx->xT_pad;
+      LS_CUDA(mv6_run_d3(a, P, ctx->num_sms, ctx->stream));
+      ctx->launches++;
+      v1 = ctx->tmp[3];
+      v2 = ctx->tmp[4];
+      v3 = have_last ? ctx->xT_pad : nullptr;
+    }
+    MV6Args b{};
+    mv_set(b.m, 0, ctx->tsplit.K);
+    mv_set(b.m, 1, ctx->tsplit.M);
+    b.m.r_lo = ctx->tsplit.lo;
+    b.m.r_hi = ctx->tsplit.hi;
+    b.m.in[0] = v1;
+    b.m.in[1] = v2;
+    b.m.xT = v3;
+    b.m.out[0] = y;
+    b.m.n = ctx->nt;
+    b.m.t_first = int(t_first);
+    b.m.s_first = int(s_first);
+    b.m.s_rows = int(rows);
+    b.m.nout = int(nout);
+    b.Q = uint32_t(ctx->Ns);
+    if (ctx->fuse_dot_slot >= 0) {  // p.q in the epilogue: p = the own rows of x
+      b.dotp = xown;
+      b.dot_part = ctx->partials;
+    }
+    unsigned grid = 0;
+    LS_CUDA(mv6_run_time(b, PT, ctx->num_sms, ctx->stream, &grid));
+    ctx->launches++;
+    if (ctx->fuse_dot_slot >= 0) {
+      LS_CUDA(launch_pdl(reduce_final_kernel, 1, RED_THREADS, 0, ctx->stream, ctx->partials, int(grid), ctx->scal,
+                         ctx->fuse_dot_slot));
+      ctx->launches++;
+      LS_CUDA(cudaGetLastError());
+      if (ctx->world > 1) LS_CHECK(ctx->comm->allreduce_scalar(ctx->scal + ctx->fuse_dot_slot));
+      ctx->fuse_dot_done = true;
+    }
+    return LS_OK;
+  }
   MV3Pass ps[2];
   int np = 0;
   if (d == 3) {  // direction 3: (P_M, P_K, P_J) -> v1, v2 (+ v3 on the last slice)
@@ -2436,6 +2498,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_FD_TIME:  // fused time mode (one launch) where n_t <= 104 (1, default) or two launches (0)
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->fd_time = value;
+      return LS_OK;
+    case LS_TUNE_MV6:  // v4's direction-3 + time passes as DFMA stencils: 0 off (default), 1 on
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->mv6 = value;
       return LS_OK;
     case LS_TUNE_FD_PLANE:  // spatial modes 1 + 2 as one plane launch where supported (1) or per direction (0, default)
       if (value != 0 && value != 1) return LS_EINVAL;

@@ -2,7 +2,9 @@
 direction-3 and time DMMA passes; mv4_kernels.cuh) against the oracle's A x (eq:A_kron,
 PAPER.md 686-703) and the dense original form, whole-vector and per-rank slab rows; with the
 direction-3 and time passes fused into one kernel (ls_tune(LS_TUNE_MV5 = 10, 1); the automatic
-choice (2) for p <= 4; mv5_kernels.cuh: d = 3, p_s = p_t) and as two passes (10, 0)."""
+choice (2) for p <= 4; mv5_kernels.cuh: d = 3, p_s = p_t) and as two passes (10, 0): DMMA band
+passes (LS_TUNE_MV6 = 15, 0, the default) or DFMA Toeplitz-stencil passes (15, 1;
+matvec6_kernels.cuh, opt-in)."""
 import numpy as np
 import pytest
 
@@ -32,14 +34,19 @@ def _rel(a, b):
     return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
 
 
-@pytest.mark.parametrize("mv5", [1, 0])
+# second-stage variants: (LS_TUNE_MV5, LS_TUNE_MV6)
+STAGES = {"v5": (1, 0), "dmma": (0, 0), "dfma": (0, 1)}
+
+
+@pytest.mark.parametrize("stage", list(STAGES))
 @pytest.mark.parametrize("d,p,ne", CASES)
-def test_matvec_v4_matches_oracle(d, p, ne, mv5):
+def test_matvec_v4_matches_oracle(d, p, ne, stage):
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, ne)
     ctx.tune(2, 4)
-    ctx.tune(10, mv5)
+    ctx.tune(10, STAGES[stage][0])
+    ctx.tune(15, STAGES[stage][1])
     space = [uv.space_factors(n, p) for n in ne[:d]]
     tf = uv.time_factors(ne[d], p)
     x = synth.residual(ctx.shape, 9)
@@ -47,14 +54,16 @@ def test_matvec_v4_matches_oracle(d, p, ne, mv5):
     assert _rel(y, op.apply_A(x, space, tf)) <= 1e-12
 
 
+@pytest.mark.parametrize("mv6", [0, 1])
 @pytest.mark.parametrize("d,pp,ne", [(2, (3, 2), [8, 7, 9]), (3, (4, 3), [6, 5, 7, 8]), (2, (8, 6), [20, 5, 30]),
-                                     (3, (6, 5), [10, 9, 8, 12]), (2, (2, 5), [9, 8, 11])])
-def test_matvec_v4_degrees(d, pp, ne):
+                                     (3, (6, 5), [10, 9, 8, 12]), (2, (2, 5), [9, 8, 11]), (3, (5, 7), [9, 8, 10, 13])])
+def test_matvec_v4_degrees(d, pp, ne, mv6):
     import torch
     import paper_1809_10026_b200 as ls
     ps, pt = pp
     ctx = ls.Context(d, pp, ne)
     ctx.tune(2, 4)
+    ctx.tune(15, mv6)
     space = [uv.space_factors(n, ps) for n in ne[:d]]
     tf = uv.time_factors(ne[d], pt)
     x = synth.residual(ctx.shape, 29)
@@ -75,16 +84,17 @@ def test_matvec_v4_original_form_tiny():
     assert _rel(y, A @ x.ravel()) <= 1e-12
 
 
-@pytest.mark.parametrize("mv5", [1, 0])
+@pytest.mark.parametrize("stage", list(STAGES))
 @pytest.mark.parametrize("d,p,ne,world", [(3, 6, [9, 8, 7, 40], 4), (3, 2, [6, 5, 7, 29], 3),
                                           (2, 8, [20, 12, 37], 2), (3, 3, [12, 10, 8, 61], 8),
                                           (3, 8, [5, 6, 4, 50], 5), (3, 4, [7, 5, 6, 23], 2)])
-def test_matvec_v4_slab_decomposition(d, p, ne, world, mv5):
+def test_matvec_v4_slab_decomposition(d, p, ne, world, stage):
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, ne)
     ctx.tune(2, 4)
-    ctx.tune(10, mv5)
+    ctx.tune(10, STAGES[stage][0])
+    ctx.tune(15, STAGES[stage][1])
     space = [uv.space_factors(n, p) for n in ne[:d]]
     tf = uv.time_factors(ne[d], p)
     x = synth.residual(ctx.shape, 13)
@@ -108,14 +118,18 @@ def test_matvec_v4_config4_sampled():
     y3 = ctx.matvec(x)
     ctx.tune(2, 4)
     ctx.tune(10, 0)
+    ctx.tune(15, 0)
     y4 = ctx.matvec(x)
     assert float(torch.linalg.norm(y4 - y3) / torch.linalg.norm(y3)) <= 1e-13
+    ctx.tune(15, 1)
+    y6 = ctx.matvec(x)
+    assert float(torch.linalg.norm(y6 - y3) / torch.linalg.norm(y3)) <= 1e-13
     ctx.tune(10, 1)
     y5 = ctx.matvec(x)
     assert float(torch.linalg.norm(y5 - y3) / torch.linalg.norm(y3)) <= 1e-13
 
 
-@pytest.mark.parametrize("mv", [4, 1, 2])
+@pytest.mark.parametrize("mv", [4, 1, 2, 6])
 @pytest.mark.parametrize("d,p,ne,world", [(3, 6, [9, 8, 7, 40], 4), (3, 3, [12, 10, 8, 61], 8), (2, 4, [20, 12, 37], 3),
                                           (3, 2, [6, 5, 7, 29], 3)])
 def test_matvec_slab3_decomposition(d, p, ne, world, mv):
@@ -125,7 +139,10 @@ def test_matvec_slab3_decomposition(d, p, ne, world, mv):
     import torch
     import paper_1809_10026_b200 as ls
     ctx = ls.Context(d, p, ne)
-    ctx.tune(2, mv)
+    ctx.tune(2, 4 if mv == 6 else mv)
+    ctx.tune(15, 1 if mv == 6 else 0)  # 6: v4 with the DFMA stencil passes
+    if mv == 6:
+        ctx.tune(10, 0)
     space = [uv.space_factors(n, p) for n in ne[:d]]
     tf = uv.time_factors(ne[d], p)
     x = synth.residual(ctx.shape, 37)

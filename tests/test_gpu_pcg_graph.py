@@ -19,7 +19,8 @@ def _solve(ctx, b, graph, **kw):
     return x.cpu().numpy(), st
 
 
-@pytest.mark.parametrize("d,p,n_el,kind", [(2, 3, 16, 0), (3, 2, 8, 1), (3, 3, [5, 6, 7, 9], None)])
+@pytest.mark.parametrize("d,p,n_el,kind", [(2, 3, 16, 0), (3, 2, 8, 1), (3, 3, [5, 6, 7, 9], None),
+                                           (3, 6, [8, 7, 9, 10], None), (2, 8, [20, 18, 22], 0)])
 def test_graph_loop_equals_host_loop(d, p, n_el, kind):
     import torch
     import paper_1809_10026_b200 as ls
