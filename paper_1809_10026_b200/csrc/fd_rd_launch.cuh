@@ -99,12 +99,12 @@ cudaError_t rd_launch_cs(const ModeArgs& a, bool mode1, int cs, cudaStream_t s, 
       }
     }
     // measured (tools/rd_variant_libs.sh + tools/ab_fd.py): half extents up to 52
-    // (configs 3, 5) run 1 n-tile per warp, 2 CTAs per SM, window 4; above (config 4, he = 66) 2
-    // n-tiles per warp, 1 CTA per SM, window 6
+    // (configs 3, 5) run 1 n-tile per warp, 2 CTAs per SM, (window 4 until r02); above (config 4, he = 66) 2
+    // n-tiles per warp, 1 CTA per SM; window 6 for both
     constexpr bool SMALL = KS <= 13;
     constexpr int NT = LS_RD_CS_NT > 0 ? LS_RD_CS_NT : (SMALL ? 1 : 2);
     constexpr int MB = LS_RD_CS_MINB > 0 ? LS_RD_CS_MINB : (SMALL ? 2 : 1);
-    constexpr int D = LS_RD_CS_D > 0 ? LS_RD_CS_D : (SMALL ? 4 : 6);
+    constexpr int D = LS_RD_CS_D > 0 ? LS_RD_CS_D : 6;  // r02: window 6 also for SMALL (4 -> 6: config 3 -0.6 %, config 5 -0.2..-0.9 %)
     const bool fast = !mode1 && (a.Q % (2 * NT) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
                       ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
     if (cs == 1) {
