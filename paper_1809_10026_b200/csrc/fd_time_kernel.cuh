@@ -42,11 +42,18 @@ struct FTArgs {
   uint64_t ld;           // row stride (elements)
 };
 
-template <int KS_, bool VEC_, int D_, int MINB_>
+template <int KS_, bool VEC_, int D_, int MINB_, bool TAIL_ = false>
 struct FTCfg {
   static constexpr int KS = KS_, D = D_, MINB = MINB_;
   static constexpr bool VEC = VEC_;
   static constexpr int NJ = (KS + 1) / 2;      // 8-wide n-tiles of j (and of t' in the output)
+  // TAIL (n_t = 8 (NJ - 1) + 1 or + 2): the last n-tile of j and the last output tile of t' hold
+  // one or two valid indices; they are computed with DFMAs instead of 7/8- or 3/4-padded DMMA
+  // tiles (the eigen columns j0 + v and output rows j0 + w, j0 = 8 (NJ - 1), v, w < 2)
+  static constexpr bool TAIL = TAIL_;
+  static constexpr int NJD = TAIL ? NJ - 1 : NJ;  // DMMA n-tiles / output tiles
+  static constexpr int UTN = TAIL ? 2 * 8 * NJ : 0;  // ut[t][v] = U_t[t][j0 + v]
+  static constexpr int UON = TAIL ? 2 * 8 * NJ : 0;  // uo[j][w] = U_t[j0 + w][j]
   static constexpr int KSP = NJ;               // k-step pairs of the first product
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int TW = 16;                // columns per warp tile (2 m-tiles)
@@ -54,7 +61,7 @@ struct FTCfg {
   static constexpr int B2N = NJ * NJ * 64;
   static constexpr int LAMN = 8 * NJ;
   static constexpr int KSE = ((KS + D - 1) / D) * D;  // k-steps rounded up to the window
-  static constexpr size_t SMEM = size_t(B1N + B2N + LAMN) * sizeof(double);
+  static constexpr size_t SMEM = size_t(B1N + B2N + LAMN + UTN + UON) * sizeof(double);
   static_assert(KS <= 26, "n_t <= 104");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
@@ -65,6 +72,8 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
   double* b1 = smem;
   double* b2 = smem + C::B1N;
   double* lam = b2 + C::B2N;
+  double* ut = lam + C::LAMN;  // TAIL tables (16-byte aligned: all offsets are multiples of 8 doubles)
+  double* uo = ut + C::UTN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = lane & 3, r = lane >> 2;
   const int nt = a.nt;
@@ -84,6 +93,14 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     b2[e] = (t < nt && j < nt) ? __ldg(a.U + size_t(t) * nt + j) : 0.0;
   }
   for (int e = tid; e < C::LAMN; e += C::THREADS) lam[e] = e < nt ? __ldg(a.lam_t + e) : 1.0;
+  constexpr int J0 = 8 * (C::NJ - 1);
+  if (C::TAIL) {
+    for (int e = tid; e < C::UTN; e += C::THREADS) {
+      const int t = e >> 1, v = e & 1;
+      ut[e] = (t < nt && J0 + v < nt) ? __ldg(a.U + size_t(t) * nt + J0 + v) : 0.0;
+      uo[e] = (t < nt && J0 + v < nt) ? __ldg(a.U + size_t(J0 + v) * nt + t) : 0.0;  // uo[j][w], j = t
+    }
+  }
   __syncthreads();
 
   const uint32_t ncols = a.ncols;
@@ -137,14 +154,29 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     for (int ms = 0; ms < 2; ++ms)
 #pragma unroll
       for (int jt = 0; jt < C::NJ; ++jt) acc[ms][jt][0] = acc[ms][jt][1] = 0.0;
+    double py[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // TAIL: lane-partial Y^T[s0 + ms][J0 + v] (t = c mod 4)
 #pragma unroll
     for (int ksp = 0; ksp < C::KSE / 2 + (C::KSE & 1); ++ksp) {
       const int k0 = 2 * ksp, k1 = 2 * ksp + 1;
       if (k0 < C::KS) {
         const double2 x0 = win[k0 % C::D];
         const double2 x1 = (k1 < C::KS) ? win[k1 % C::D] : make_double2(0.0, 0.0);
+        if (C::TAIL) {
+          const double2 u0 = *reinterpret_cast<const double2*>(ut + 2 * (4 * k0 + c));
+          py[0][0] = fma(x0.x, u0.x, py[0][0]);
+          py[0][1] = fma(x0.x, u0.y, py[0][1]);
+          py[1][0] = fma(x0.y, u0.x, py[1][0]);
+          py[1][1] = fma(x0.y, u0.y, py[1][1]);
+          if (k1 < C::KS) {
+            const double2 u1 = *reinterpret_cast<const double2*>(ut + 2 * (4 * k1 + c));
+            py[0][0] = fma(x1.x, u1.x, py[0][0]);
+            py[0][1] = fma(x1.x, u1.y, py[0][1]);
+            py[1][0] = fma(x1.y, u1.x, py[1][0]);
+            py[1][1] = fma(x1.y, u1.y, py[1][1]);
+          }
+        }
 #pragma unroll
-        for (int jt = 0; jt < C::NJ; ++jt) {
+        for (int jt = 0; jt < C::NJD; ++jt) {
           const double2 bf = *reinterpret_cast<const double2*>(b1l + (jt * C::KSP + ksp) * 64);
           dmma_8x8x4(acc[0][jt], x0.x, bf.x);
           dmma_8x8x4(acc[1][jt], x0.y, bf.x);
@@ -171,8 +203,19 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     }
 
     // ---- step 3: acc[ms][jt][h] is Y^T[s0 + ms][j = 8jt + 4h + c]
+    if (C::TAIL) {  // quad sum of the tail partials (t = c mod 4), then the same division
 #pragma unroll
-    for (int jt = 0; jt < C::NJ; ++jt)
+      for (int ms = 0; ms < 2; ++ms)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          double y = py[ms][v];
+          y += __shfl_xor_sync(0xffffffffu, y, 1);
+          y += __shfl_xor_sync(0xffffffffu, y, 2);
+          py[ms][v] = y * fast_rcp(lam[J0 + v] + (ms ? ls1 : ls0));
+        }
+    }
+#pragma unroll
+    for (int jt = 0; jt < C::NJD; ++jt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double lt = lam[8 * jt + 4 * h + c];
@@ -183,15 +226,25 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     // ---- second product, two output n-tiles (t' = 8tt + 2c + {0,1}) at a time
     double* zp = a.Z + s0;
 #pragma unroll 1
-    for (int tt = 0; tt < C::NJ; tt += 2) {
-      const bool two = tt + 1 < C::NJ;
+    for (int tt = 0; tt < C::NJD; tt += 2) {
+      const bool two = tt + 1 < C::NJD;
       double o[2][2][2];  // [tile of the pair][ms][column half]
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int ms = 0; ms < 2; ++ms) o[u][ms][0] = o[u][ms][1] = 0.0;
+      if (C::TAIL) {  // the tail columns' rank-2 update: o += Y^T[., J0 + v] U_t[t'][J0 + v]
 #pragma unroll
-      for (int jt = 0; jt < C::NJ; ++jt) {
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double2 w = *reinterpret_cast<const double2*>(ut + 2 * (8 * (tt + u) + 2 * c + h));
+#pragma unroll
+            for (int ms = 0; ms < 2; ++ms) o[u][ms][h] = fma(py[ms][1], w.y, fma(py[ms][0], w.x, o[u][ms][h]));
+          }
+      }
+#pragma unroll
+      for (int jt = 0; jt < C::NJD; ++jt) {
         const bool h1 = 2 * jt + 1 < C::KS;  // k-step (jt, 1) has valid columns
         const double2 f0 = *reinterpret_cast<const double2*>(b2l + (tt * C::NJ + jt) * 64);
         dmma_8x8x4(o[0][0], acc[0][jt][0], f0.x);
@@ -225,6 +278,50 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
             dst[0] = o[u][0][h];
             if (s0 + 1 < ncols) dst[1] = o[u][1][h];
           }
+        }
+      }
+    }
+    if (C::TAIL) {  // output rows J0 + w: Z^T[s][J0 + w] = sum_j Y^T[s][j] U_t[J0 + w][j]
+      double pz[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int jt = 0; jt < C::NJD; ++jt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 w = *reinterpret_cast<const double2*>(uo + 2 * (8 * jt + 4 * h + c));
+#pragma unroll
+          for (int ms = 0; ms < 2; ++ms) {
+            pz[ms][0] = fma(acc[ms][jt][h], w.x, pz[ms][0]);
+            pz[ms][1] = fma(acc[ms][jt][h], w.y, pz[ms][1]);
+          }
+        }
+      if (c == 0) {  // the tail-tail block (quad-uniform py): once per quad
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const double2 w = *reinterpret_cast<const double2*>(uo + 2 * (J0 + v));
+#pragma unroll
+          for (int ms = 0; ms < 2; ++ms) {
+            pz[ms][0] = fma(py[ms][v], w.x, pz[ms][0]);
+            pz[ms][1] = fma(py[ms][v], w.y, pz[ms][1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int ms = 0; ms < 2; ++ms)
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+          pz[ms][w] += __shfl_xor_sync(0xffffffffu, pz[ms][w], 1);
+          pz[ms][w] += __shfl_xor_sync(0xffffffffu, pz[ms][w], 2);
+        }
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const int t = J0 + w;
+        if (c != w || t >= nt || s0 >= ncols) continue;  // lanes c = 0, 1 store rows J0, J0 + 1
+        double* dst = zp + size_t(t) * ld;
+        if (C::VEC) {
+          *reinterpret_cast<double2*>(dst) = make_double2(pz[0][w], pz[1][w]);
+        } else {
+          dst[0] = pz[0][w];
+          if (s0 + 1 < ncols) dst[1] = pz[1][w];
         }
       }
     }
