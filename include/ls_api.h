@@ -333,6 +333,17 @@ int ls_geo_info(const ls_ctx* ctx, double* out2);
 int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host);
 
 /*
+ * fd_apply_host_batch -- z_k = P^{-1} r_k (Algorithm 1, PAPER.md 955-964) for count HOST vector
+ * pairs (r_host[k], z_host[k]; each the rank's local slab, pinned host memory recommended),
+ * pipelined across the vectors: the host->device copy of r_{k+1} and the device->host copy of
+ * z_{k-1} overlap the application to r_k (two device buffer pairs, allocated on the first call:
+ * + 2 N doubles; separate copy streams).  Synchronous: returns when every z_k is on the host.
+ * r_host[k] may alias r_host[j]; z_host[k] must not alias any r_host[j].
+ * Errors: LS_EINVAL (null table or entry, count < 0), LS_ENOMEM, LS_ECUDA.
+ */
+int fd_apply_host_batch(ls_ctx* ctx, const double* const* r_host, double* const* z_host, int64_t count);
+
+/*
  * ls_get_factor -- copy a setup quantity to host memory (introspection for
  * tests).  which: 0 = M_k, 1 = K_k, 2 = J_k (dense n_k x n_k, row-major; dir
  * = k in 1..d), 3 = M_t^ , 4 = K_t^ (n_t x n_t, dir ignored), 5 = lambda_k

@@ -28,7 +28,7 @@ LS_OK, LS_EINVAL, LS_ENOTSPD, LS_ENOCONV, LS_ENUMERIC, LS_ENOMEM, LS_ECUDA, LS_E
 
 # Every symbol include/ls_api.h declares (checked by tests/test_abi.py).
 EXPORTED = ["ls_setup", "ls_setup_dist", "ls_get_unique_id", "ls_layout", "ls_set_stream",
-            "fd_apply", "ls_matvec", "ls_matvec_slab3", "ls_rhs", "pcg_solve", "fd_apply_host", "ls_get_factor",
+            "fd_apply", "ls_matvec", "ls_matvec_slab3", "ls_rhs", "pcg_solve", "fd_apply_host", "fd_apply_host_batch", "ls_get_factor",
             "ls_kernel_launches", "ls_profile", "ls_profile_read", "ls_destroy", "ls_strerror",
             "ls_partition", "ls_a2a_plan", "ls_a2a_piece_plan", "ls_pack_map", "ls_halo_plan", "ls_tune",
             "ls_matvec_slab", "fd_apply_stage", "fd_apply_scatter", "ls_a2a_dest", "ls_setup_deg",
@@ -89,6 +89,7 @@ def load_library(path=LIB_PATH):
         "ls_rhs": (ctypes.c_int, [vp, ctypes.c_int, dp]),
         "pcg_solve": (ctypes.c_int, [vp, dp, dp, ctypes.c_double, ctypes.c_int, ctypes.POINTER(PCGStats)]),
         "fd_apply_host": (ctypes.c_int, [vp, dp, dp]),
+        "fd_apply_host_batch": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64]),
         "ls_get_factor": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, dp]),
         "ls_kernel_launches": (ctypes.c_int64, [vp]),
         "ls_profile": (ctypes.c_int, [vp, ctypes.c_int]),
@@ -436,6 +437,32 @@ class Context:
             return ctypes.c_void_p(a.ctypes.data)
         _check(self._lib.fd_apply_host(self._h, ptr(r_host, "r"), ptr(z_host, "z")), "fd_apply_host")
         return z_host
+
+    def fd_apply_host_batch(self, rs, zs):
+        """fd_apply_host over lists of host vectors, copies of neighbouring vectors overlapped
+        with the application (pinned memory recommended); synchronous."""
+        if len(rs) != len(zs):
+            raise ValueError("rs and zs must have the same length")
+        need = self.N
+
+        def ptr(a, name):
+            if hasattr(a, "data_ptr"):
+                if a.is_cuda or a.dtype != self._torch.float64 or not a.is_contiguous():
+                    raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
+                n, p = a.numel(), a.data_ptr()
+            else:
+                if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+                    raise TypeError(f"{name} must be a C-contiguous float64 array")
+                n, p = a.size, a.ctypes.data
+            if n != need:
+                raise ValueError(f"{name} has {n} elements, expected {need}")
+            return p
+        k = len(rs)
+        rp = (ctypes.c_void_p * max(k, 1))(*[ptr(a, "r") for a in rs])
+        zp = (ctypes.c_void_p * max(k, 1))(*[ptr(a, "z") for a in zs])
+        _check(self._lib.fd_apply_host_batch(self._h, ctypes.cast(rp, ctypes.c_void_p),
+                                             ctypes.cast(zp, ctypes.c_void_p), k), "fd_apply_host_batch")
+        return zs
 
     def get_factor(self, which, direction=0):
         """Setup quantities (see ls_get_factor): returns a numpy array."""

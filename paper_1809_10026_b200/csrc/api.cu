@@ -109,6 +109,11 @@ struct ls_ctx {
   double** scatter_tab = nullptr;  // fd_apply_scatter: device copy of the caller's table
   // fd_apply_host pipeline: copy stream + events (H2D / D2H per time-slice chunk)
   cudaStream_t copy_stream = nullptr;
+  // fd_apply_host_batch: the second device buffer pair, the H2D / D2H streams and their events
+  double* hb_r = nullptr;
+  double* hb_z = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t bev[7] = {};
   // distributed path: NCCL stream of the pipelined all-to-all / halo exchange and its events
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t cev[12] = {};
@@ -176,6 +181,10 @@ struct ls_ctx {
     for (auto e : hev)
       if (e) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (auto e : bev)
+      if (e) cudaEventDestroy(e);
+    if (h2d_stream) cudaStreamDestroy(h2d_stream);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     for (auto e : cev)
       if (e) cudaEventDestroy(e);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -2347,6 +2356,49 @@ extern "C" int fd_apply_host(ls_ctx* ctx, const double* r_host, double* z_host) 
   LS_CHECK(fd_apply(ctx, ctx->pr, ctx->pz));
   LS_CUDA(cudaMemcpyAsync(z_host, ctx->pz, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LS_OK;
+}
+
+// count fd_apply calls on host vectors, pipelined across vectors: two device buffer pairs, the
+// H2D copy of vector k + 1 (H2D stream) and the D2H copy of vector k - 1 (D2H stream) run while
+// vector k is applied on the context stream (PCIe is full duplex, so both directions overlap).
+extern "C" int fd_apply_host_batch(ls_ctx* ctx, const double* const* r_host, double* const* z_host, int64_t count) {
+  if (!ctx || count < 0 || (count > 0 && (!r_host || !z_host))) return LS_EINVAL;
+  for (int64_t k = 0; k < count; ++k)
+    if (!r_host[k] || !z_host[k]) return LS_EINVAL;
+  if (count == 0) return LS_OK;
+  if (!ctx->hb_r) {
+    LS_CHECK(ctx->alloc(&ctx->hb_r, ctx->Nl));
+    LS_CHECK(ctx->alloc(&ctx->hb_z, ctx->Nl));
+    LS_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+    LS_CUDA(cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->bev) LS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const size_t bytes = size_t(ctx->Nl) * sizeof(double);
+  double* R[2] = {ctx->pr, ctx->hb_r};
+  double* Z[2] = {ctx->pz, ctx->hb_z};
+  cudaEvent_t* h2d_done = ctx->bev;      // [2]
+  cudaEvent_t* comp_done = ctx->bev + 2;  // [2]
+  cudaEvent_t* d2h_done = ctx->bev + 4;   // [2]
+  LS_CUDA(cudaEventRecord(ctx->bev[6], ctx->stream));  // earlier work on the context stream
+  LS_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ctx->bev[6], 0));
+  LS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, ctx->bev[6], 0));
+  for (int64_t k = 0; k < count; ++k) {
+    const int b = int(k & 1);
+    if (k >= 2) LS_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, comp_done[b], 0));  // R[b] read by vector k - 2
+    LS_CUDA(cudaMemcpyAsync(R[b], r_host[k], bytes, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    LS_CUDA(cudaEventRecord(h2d_done[b], ctx->h2d_stream));
+    LS_CUDA(cudaStreamWaitEvent(ctx->stream, h2d_done[b], 0));
+    if (k >= 2) LS_CUDA(cudaStreamWaitEvent(ctx->stream, d2h_done[b], 0));  // Z[b] copied out
+    LS_CHECK(fd_apply(ctx, R[b], Z[b]));
+    LS_CUDA(cudaEventRecord(comp_done[b], ctx->stream));
+    LS_CUDA(cudaStreamWaitEvent(ctx->d2h_stream, comp_done[b], 0));
+    LS_CUDA(cudaMemcpyAsync(z_host[k], Z[b], bytes, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    LS_CUDA(cudaEventRecord(d2h_done[b], ctx->d2h_stream));
+  }
+  LS_CUDA(cudaStreamSynchronize(ctx->h2d_stream));
+  LS_CUDA(cudaStreamSynchronize(ctx->stream));
+  LS_CUDA(cudaStreamSynchronize(ctx->d2h_stream));
   return LS_OK;
 }
 
