@@ -444,7 +444,9 @@ def test_fd_apply_fused_a2a_emulated(torch_cuda, d, p, n_elems, world):
 
 
 GUARD_CASES = [(3, 3, [6, 7, 5, 9]), (2, 6, [29, 3, 11]), (1, 2, [121, 125]), (3, 2, [3, 4, 2, 6]),
-               (2, 8, [130, 1, 14]), (3, 6, [128, 2, 3, 11])]
+               (2, 8, [130, 1, 14]), (3, 6, [128, 2, 3, 11]),
+               (2, 3, [9, 9, 64]),        # n_t = 66: fused time mode with DFMA tail tiles; n_1 = n_2 (plane kernel)
+               (3, 2, [5, 5, 6, 96])]     # n_t = 97 (tail, bucket 25), odd n_1 = n_2 = 5
 
 
 def _guarded(torch, shape, fill, pad=4096):
@@ -468,9 +470,12 @@ def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
     z_ref = fd.fd_apply(r, fdd)
     y_ref = op.apply_A(r, space, tf)
     canary = 1.2345e300
-    for fdk, cs in ((1, 0), (2, 0), (1, 1), (2, 1)):
+    # (FD kernel family, centrosymmetric split, fused time mode (knob 13), plane kernel (knob 14))
+    for fdk, cs, ft, pl in ((1, 0, 1, 0), (2, 0, 1, 0), (1, 1, 1, 0), (2, 1, 1, 0), (2, 1, 0, 0), (2, 1, 1, 1)):
         ctx.tune(1, fdk)
         ctx.tune(9, cs)
+        ctx.tune(13, ft)
+        ctx.tune(14, pl)
         _, rin, _ = _guarded(torch, ctx.shape, float("nan"))
         rin.copy_(torch.from_numpy(r))
         obig, zout, pad = _guarded(torch, ctx.shape, canary)
@@ -478,8 +483,11 @@ def test_guarded_buffers_all_variants(torch_cuda, d, p, n_elems):
         assert _rel(zout.cpu().numpy(), z_ref) <= TOL, (fdk, cs)
         assert bool((obig[:pad] == canary).all()) and bool((obig[pad + zout.numel():] == canary).all()), (fdk, cs)
     ctx.tune(1, 0)
-    for mv in ((1, 2, 3, 4) if d >= 2 else (1, 2, 3)):
-        ctx.tune(2, mv)
+    ctx.tune(13, 1)
+    ctx.tune(14, 0)
+    for mv in ((1, 2, 3, 4, 6) if d >= 2 else (1, 2, 3)):
+        ctx.tune(2, 4 if mv == 6 else mv)  # 6: v4 with the DFMA stencil passes (knob 15)
+        ctx.tune(15, 1 if mv == 6 else 0)
         _, xin, _ = _guarded(torch, ctx.shape, float("nan"))
         xin.copy_(torch.from_numpy(r))
         obig, yout, pad = _guarded(torch, ctx.shape, canary)
