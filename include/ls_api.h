@@ -480,6 +480,10 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * band-tile padding) instead of DMMA band tiles: 0 = off (default: latency-bound, measured
  * slower at configs 4 and 5), 1 = on (the v5 fused pass, where it applies, takes precedence). */
 #define LS_TUNE_MV6 15
+/* LS_TUNE_MV2_SWEEP: the v2 matvec's (p_s = 2) d = 3 plane pass of directions 2 + 1 as a
+ * register sweep (one warp per plane, no shared memory or barriers; n_1 <= 128; default 1) or
+ * as the shared-memory two-phase kernel (0). */
+#define LS_TUNE_MV2_SWEEP 16
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

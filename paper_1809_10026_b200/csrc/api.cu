@@ -85,6 +85,7 @@ struct ls_ctx {
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
   int mv6 = 0;         // ls_tune LS_TUNE_MV6: v4's direction-3 and time passes as DFMA stencil passes
                        // (matvec6_kernels.cuh): 0 off (default: measured slower), 1 on
+  int mv2_sweep = 1;   // ls_tune LS_TUNE_MV2_SWEEP: v2's d = 3 plane pass as the register sweep (p = 2)
   int pq_fuse = 1;     // ls_tune LS_TUNE_PQ_FUSE: p.q in the matvec's last-pass epilogue
   int mv5 = 2;         // ls_tune knob LS_TUNE_MV5: v4's direction-3 and time passes fused (mv5_kernels.cuh):
                        // 0 off, 1 on, 2 automatic (p <= 4: measured faster there, slower above)
@@ -1507,6 +1508,13 @@ static int mv2_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
     pl.smem_plane = size_t(3) * MV_PLANE_ROWS * mv_plane_pitch(ctx->n[0], P) * sizeof(double);
     const int per_sm = int(std::max<size_t>(1, std::min<size_t>(mv_plane_ctas(P), (227 * 1024) / pl.smem_plane)));
     pl.grid_plane = unsigned(std::min<uint64_t>(items, uint64_t(ctx->num_sms) * per_sm));
+    // the register sweep (one warp per plane, CW columns per lane; P = 2 only)
+    const int cw = std::max(2, (ctx->n[0] + 31) / 32);
+    pl.sweep_cw = 0;
+    if (d == 3 && P == 2 && ctx->mv2_sweep && cw <= 4) {
+      pl.sweep_cw = cw;
+      pl.grid_plane = unsigned(std::min<uint64_t>((uint64_t(a.ncols) + 7) / 8, uint64_t(ctx->num_sms)));
+    }
   }
   LS_CUDA(mv2_run(P, ctx->pt, pl, &ctx->launches));
   return LS_OK;
@@ -2550,6 +2558,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_FD_TIME:  // fused time mode (one launch) where n_t <= 104 (1, default) or two launches (0)
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->fd_time = value;
+      return LS_OK;
+    case LS_TUNE_MV2_SWEEP:  // v2 (p = 2): the d = 3 plane pass as the register sweep (1, default) or staged (0)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->mv2_sweep = value;
       return LS_OK;
     case LS_TUNE_MV6:  // v4's direction-3 + time passes as DFMA stencils: 0 off (default), 1 on
       if (value != 0 && value != 1) return LS_EINVAL;

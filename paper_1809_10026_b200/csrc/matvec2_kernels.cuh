@@ -345,12 +345,121 @@ __global__ void __launch_bounds__(MV_PLANE_THREADS, mv_plane_ctas(P)) mv_plane_k
   }
 }
 
+// --------------------------------------------------------------------------------------
+// sweep variant of the d = 3 plane pass (r02, LS_TUNE_MV2_SWEEP): the same algebra as
+// mv_plane_kernel (A2 = M2 A + J2 B + K2 C, B2 = M2 B, C2 = 2K2 B + M2 C along direction 2,
+// then y = M1 A2 + J1 B2 + K1 C2 along direction 1, stencils + boundary corrections), but
+// without shared memory or barriers: one warp owns a whole (t, i3) plane, lane l holds the CW
+// direction-1 columns CW l .. CW l + CW - 1 (32 CW >= n1), and the warp sweeps direction 2
+// row by row with a register ring of the 2P + 1 + D input rows of A, B, C (rows are loaded D
+// steps ahead).  Direction 1's P neighbours of a lane's columns come from the adjacent lanes
+// (shuffles).  Each input is read once, y written once: 32 B/DOF, streamed.
+// Why (ncu of mv_plane_kernel, config 5 p = 2): 2.6 TB/s, barrier and long-scoreboard stalls —
+// its two phases do not overlap inside a CTA.
+// --------------------------------------------------------------------------------------
+template <int P, int CW, int D>
+__global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant__ MVArgs a) {
+  static_assert(CW >= P, "direction-1 neighbours come from the adjacent lanes only");
+  constexpr int W = 2 * P + 1, R = W + D;  // stencil width, ring rows
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n1 = a.n1, n2 = a.n;
+  const int c0 = lane * CW;  // the lane's first column
+  const uint32_t planes = a.ncols;
+  for (uint32_t pl = blockIdx.x * 8u + warp; pl < planes; pl += gridDim.x * 8u) {
+    const size_t base = size_t(pl) * n2 * n1 + c0;
+    double w[3][R][CW];  // ring slot (r + P) % R holds input row r
+    auto load = [&](int slot, int row) {
+      const bool rv = row >= 0 && row < n2;
+#pragma unroll
+      for (int f = 0; f < 3; ++f)
+#pragma unroll
+        for (int m = 0; m < CW; ++m)
+          w[f][slot][m] = (rv && c0 + m < n1) ? mv_ld(a.in[f] + base + size_t(row) * n1 + m) : 0.0;
+    };
+#pragma unroll
+    for (int j = 0; j < R - 1; ++j) load(j, j - P);
+#pragma unroll 1
+    for (int i2b = 0; i2b < n2; i2b += R) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int i2 = i2b + u;
+        if (i2 >= n2) break;
+        load((u + R - 1) % R, i2 + P + D);  // D rows ahead: the slot of row i2 - P - 1
+        // ---- direction 2 at row i2 (ring slots (u + j) % R hold rows i2 - P + j)
+        double A2[CW], B2[CW], C2[CW];
+#pragma unroll
+        for (int m = 0; m < CW; ++m) A2[m] = B2[m] = C2[m] = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int sl = (u + j) % R;
+#pragma unroll
+          for (int m = 0; m < CW; ++m) {
+            A2[m] = fma(a.st[0][j], w[0][sl][m], fma(a.st[1][j], w[1][sl][m], fma(a.st[2][j], w[2][sl][m], A2[m])));
+            B2[m] = fma(a.st[0][j], w[1][sl][m], B2[m]);
+            C2[m] = fma(a.st[3][j], w[1][sl][m], fma(a.st[0][j], w[2][sl][m], C2[m]));
+          }
+        }
+        if (i2 < a.r_lo || i2 >= a.r_hi) {  // boundary row of direction 2 (warp-uniform)
+          const int er = (i2 < a.r_lo ? i2 : a.r_lo + (i2 - a.r_hi)) * W;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            const int sl = (u + j) % R;
+            const double eM = __ldg(a.E[0] + er + j), eJ = __ldg(a.E[1] + er + j), eK = __ldg(a.E[2] + er + j),
+                         e2K = __ldg(a.E[3] + er + j);
+#pragma unroll
+            for (int m = 0; m < CW; ++m) {
+              A2[m] = fma(eM, w[0][sl][m], fma(eJ, w[1][sl][m], fma(eK, w[2][sl][m], A2[m])));
+              B2[m] = fma(eM, w[1][sl][m], B2[m]);
+              C2[m] = fma(e2K, w[1][sl][m], fma(eM, w[2][sl][m], C2[m]));
+            }
+          }
+        }
+        // ---- direction 1: columns c0 - P .. c0 + CW - 1 + P (neighbours from lanes l -+ 1;
+        //      columns outside [0, n1) are zero: invalid columns hold 0 from the zero inputs)
+        double x[3][CW + 2 * P];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double* v = f == 0 ? A2 : (f == 1 ? B2 : C2);
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            const double lft = __shfl_up_sync(0xffffffffu, v[CW - P + k], 1);
+            const double rgt = __shfl_down_sync(0xffffffffu, v[k], 1);
+            x[f][k] = lane == 0 ? 0.0 : lft;
+            x[f][P + CW + k] = lane == 31 ? 0.0 : rgt;
+          }
+#pragma unroll
+          for (int m = 0; m < CW; ++m) x[f][P + m] = v[m];
+        }
+        double* yrow = a.out[0] + base + size_t(i2) * n1;
+#pragma unroll
+        for (int m = 0; m < CW; ++m) {
+          const int c = c0 + m;
+          double y = 0.0;
+#pragma unroll
+          for (int j = 0; j < W; ++j)
+            y = fma(a.st[4][j], x[0][m + j], fma(a.st[5][j], x[1][m + j], fma(a.st[6][j], x[2][m + j], y)));
+          if (c < n1 && (c < a.r_lo1 || c >= a.r_hi1)) {  // boundary column of direction 1
+            const int er = (c < a.r_lo1 ? c : a.r_lo1 + (c - a.r_hi1)) * W;
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+              y = fma(__ldg(a.E[4] + er + j), x[0][m + j],
+                      fma(__ldg(a.E[5] + er + j), x[1][m + j], fma(__ldg(a.E[6] + er + j), x[2][m + j], y)));
+          }
+          if (c < n1) yrow[m] = y;
+        }
+      }
+    }
+  }
+}
+
 // launch plan built by the host (api.cu) and executed by mv2.cu (own translation unit)
 struct MV2Plan {
   MVArgs time, dir, plane;
   int d;
   unsigned grid_time, grid_dir, grid_plane;
   size_t smem_plane;
+  int sweep_cw;  // > 0: the d = 3 plane pass runs mv_sweep_kernel with CW columns per lane
   cudaStream_t stream;
   int num_sms;
 };

@@ -3,6 +3,10 @@
 
 namespace ls {
 
+#ifndef LS_MV2_SWEEP_D
+#define LS_MV2_SWEEP_D 2  // rows loaded ahead by the sweep plane pass (A/B: 2 best of 2, 4, 6)
+#endif
+
 template <int P>
 static cudaError_t run_time(const MV2Plan& pl, int64_t* launches) {
   constexpr int R = 8;
@@ -27,6 +31,20 @@ static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
     if (e != cudaSuccess) return e;
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (pl.d == 3 && pl.sweep_cw > 0 && pl.grid_plane) {
+    e = cudaErrorInvalidValue;
+    if constexpr (P == 2) {
+      switch (pl.sweep_cw) {
+        case 2: e = launch_pdl(mv_sweep_kernel<P, 2, LS_MV2_SWEEP_D>, pl.grid_plane, 256, 0, pl.stream, pl.plane); break;
+        case 3: e = launch_pdl(mv_sweep_kernel<P, 3, LS_MV2_SWEEP_D>, pl.grid_plane, 256, 0, pl.stream, pl.plane); break;
+        case 4: e = launch_pdl(mv_sweep_kernel<P, 4, LS_MV2_SWEEP_D>, pl.grid_plane, 256, 0, pl.stream, pl.plane); break;
+        default: break;
+      }
+    }
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    return cudaGetLastError();
   }
   if (pl.d >= 2 && pl.grid_plane) {
     static bool attr[2] = {false, false};
