@@ -484,6 +484,10 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
  * register sweep (one warp per plane, no shared memory or barriers; n_1 <= 128; default 1) or
  * as the shared-memory two-phase kernel (0). */
 #define LS_TUNE_MV2_SWEEP 16
+/* LS_TUNE_MV4_SWEEP: the v4 matvec's plane pass (directions 1 + 2) as a DFMA register sweep
+ * (one warp per plane, Toeplitz stencils; d = 3, p_s = 3 or 4, n_1 <= 128) (1) or as the DMMA
+ * band-tile kernel (0, default: the sweep measured 2.2x slower at config 5 p = 4). */
+#define LS_TUNE_MV4_SWEEP 17
 int ls_tune(ls_ctx* ctx, int knob, int value);
 
 void ls_destroy(ls_ctx* ctx);

@@ -38,7 +38,7 @@ LS_PRECOND_P, LS_PRECOND_PG = 0, 1
 # ls_tune knobs (include/ls_api.h)
 LS_TUNE_FD_KERNEL, LS_TUNE_MATVEC, LS_TUNE_MV3_PAD, LS_TUNE_A2A, LS_TUNE_PCG_GRAPH, LS_TUNE_PDL = 1, 2, 3, 4, 5, 6
 LS_TUNE_FD_TAIL, LS_TUNE_MV4_CTAS, LS_TUNE_FD_CS, LS_TUNE_MV5, LS_TUNE_FD_STAGED, LS_TUNE_PQ_FUSE = 7, 8, 9, 10, 11, 12
-LS_TUNE_FD_TIME, LS_TUNE_FD_PLANE, LS_TUNE_MV6, LS_TUNE_MV2_SWEEP = 13, 14, 15, 16
+LS_TUNE_FD_TIME, LS_TUNE_FD_PLANE, LS_TUNE_MV6, LS_TUNE_MV2_SWEEP, LS_TUNE_MV4_SWEEP = 13, 14, 15, 16, 17
 
 
 class Geometry(ctypes.Structure):

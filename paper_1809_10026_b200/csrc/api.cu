@@ -85,7 +85,9 @@ struct ls_ctx {
   int mv_variant = 0;  // ls_tune knob LS_TUNE_MATVEC: 0 auto, 1 four passes (v1), 2 three fused passes (v2)
   int mv6 = 0;         // ls_tune LS_TUNE_MV6: v4's direction-3 and time passes as DFMA stencil passes
                        // (matvec6_kernels.cuh): 0 off (default: measured slower), 1 on
-  int mv2_sweep = 1;   // ls_tune LS_TUNE_MV2_SWEEP: v2's d = 3 plane pass as the register sweep (p = 2)
+  int mv2_sweep = 1;
+  int mv4_sweep = 0;   // ls_tune LS_TUNE_MV4_SWEEP: v4's plane pass as the DFMA register sweep (d = 3, p <= 4;
+                       // opt-in: measured 2.2x slower than the DMMA plane pass at config 5 p = 4)   // ls_tune LS_TUNE_MV2_SWEEP: v2's d = 3 plane pass as the register sweep (p = 2)
   int pq_fuse = 1;     // ls_tune LS_TUNE_PQ_FUSE: p.q in the matvec's last-pass epilogue
   int mv5 = 2;         // ls_tune knob LS_TUNE_MV5: v4's direction-3 and time passes fused (mv5_kernels.cuh):
                        // 0 off, 1 on, 2 automatic (p <= 4: measured faster there, slower above)
@@ -1657,8 +1659,35 @@ static int mv4_launch(ls_ctx* ctx, const double* x, double* y, int64_t rows, int
   if (d < 2 || P < 2 || P > 8 || PT < 2 || PT > 8) return LS_ENOTSUP;
   const int n1 = ctx->n[0], n2 = ctx->n[1];
   double *PM = ctx->tmp[0], *PK = ctx->tmp[1], *PJ = ctx->tmp[2];
+  const int cw4 = std::max(P, (n1 + 31) / 32);
+  const bool sweep = ctx->mv4_sweep && d == 3 && (P == 3 || P == 4) && cw4 <= 4;
   auto plane = [&](const double* src, int64_t row0, int64_t nrows) -> int {
     if (nrows <= 0) return LS_OK;
+    if (sweep) {  // DFMA register sweep (matvec2_kernels.cuh mv4_sweep_kernel)
+      MVArgs s{};
+      const auto& s2 = ctx->dsplit[1];
+      const auto& s1 = ctx->dsplit[0];
+      mv_set(s, 0, s2.M);
+      mv_set(s, 1, s2.J);
+      mv_set(s, 2, s2.K);
+      mv_set(s, 4, s1.M);
+      mv_set(s, 5, s1.J);
+      mv_set(s, 6, s1.K);
+      s.r_lo = s2.lo;
+      s.r_hi = s2.hi;
+      s.r_lo1 = s1.lo;
+      s.r_hi1 = s1.hi;
+      s.in[0] = src;
+      s.out[0] = PM + row0 * ctx->Ns;
+      s.out[1] = PK + row0 * ctx->Ns;
+      s.out[2] = PJ + row0 * ctx->Ns;
+      s.n = n2;
+      s.n1 = n1;
+      s.ncols = uint32_t(nrows * ctx->n[2]);
+      LS_CUDA(mv4_sweep_run(s, P, cw4, ctx->num_sms, ctx->stream));
+      ctx->launches++;
+      return LS_OK;
+    }
     MV4PlaneArgs a{};
     a.x = src;
     a.out[0] = PM + row0 * ctx->Ns;
@@ -2562,6 +2591,10 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
     case LS_TUNE_MV2_SWEEP:  // v2 (p = 2): the d = 3 plane pass as the register sweep (1, default) or staged (0)
       if (value != 0 && value != 1) return LS_EINVAL;
       ctx->mv2_sweep = value;
+      return LS_OK;
+    case LS_TUNE_MV4_SWEEP:  // v4's plane pass as the DFMA register sweep (d = 3, p = 3, 4; opt-in)
+      if (value != 0 && value != 1) return LS_EINVAL;
+      ctx->mv4_sweep = value;
       return LS_OK;
     case LS_TUNE_MV6:  // v4's direction-3 + time passes as DFMA stencils: 0 off (default), 1 on
       if (value != 0 && value != 1) return LS_EINVAL;

@@ -453,6 +453,121 @@ __global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant_
   }
 }
 
+// --------------------------------------------------------------------------------------
+// the v4 plane pass (mv4_kernels.cuh: P_M = M2 M1 x, P_K = (K2 M1 + M2 K1) x,
+// P_J = (J2 M1 + M2 J1 + 2 K2 K1) x) as the same register sweep (r02, LS_TUNE_MV4_SWEEP; p <= 4):
+// direction 2 first on the single input x (ring of the 2P + 1 + D rows of x),
+//     v_M = M2 x, v_K = K2 x, v_J = J2 x,
+// then direction 1 across the lanes,
+//     P_M = M1 v_M,  P_K = M1 v_K + K1 v_M,  P_J = M1 v_J + J1 v_M + 2 K1 v_K
+// (the Kronecker factors of different directions commute).  Exactly 2P + 1 DFMAs per banded
+// output (9 products: 81 DFMA / DOF at p = 4) instead of the DMMA band tiles' parallelogram
+// (8-row tiles over 8 + 2P columns: 56 % useful at p = 4); x read once, P_* written once.
+// Stencil slots: 0 M2, 1 J2, 2 K2, 4 M1, 5 J1, 6 K1 (+ boundary corrections E[.]).
+// --------------------------------------------------------------------------------------
+template <int P, int CW, int D>
+__global__ void __launch_bounds__(256, 1) mv4_sweep_kernel(const __grid_constant__ MVArgs a) {
+  static_assert(CW >= P, "direction-1 neighbours come from the adjacent lanes only");
+  constexpr int W = 2 * P + 1, R = W + D;
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n1 = a.n1, n2 = a.n;
+  const int c0 = lane * CW;
+  const uint32_t planes = a.ncols;
+  for (uint32_t pl = blockIdx.x * 8u + warp; pl < planes; pl += gridDim.x * 8u) {
+    const size_t base = size_t(pl) * n2 * n1 + c0;
+    double w[R][CW];  // ring slot (r + P) % R holds row r of x
+    auto load = [&](int slot, int row) {
+      const bool rv = row >= 0 && row < n2;
+#pragma unroll
+      for (int m = 0; m < CW; ++m) w[slot][m] = (rv && c0 + m < n1) ? mv_ld(a.in[0] + base + size_t(row) * n1 + m) : 0.0;
+    };
+#pragma unroll
+    for (int j = 0; j < R - 1; ++j) load(j, j - P);
+#pragma unroll 1
+    for (int i2b = 0; i2b < n2; i2b += R) {
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        const int i2 = i2b + u;
+        if (i2 >= n2) break;
+        load((u + R - 1) % R, i2 + P + D);
+        // ---- direction 2 at row i2: v_M, v_J, v_K
+        double v[3][CW];  // 0 M, 1 J, 2 K
+#pragma unroll
+        for (int m = 0; m < CW; ++m) v[0][m] = v[1][m] = v[2][m] = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int sl = (u + j) % R;
+#pragma unroll
+          for (int m = 0; m < CW; ++m) {
+            v[0][m] = fma(a.st[0][j], w[sl][m], v[0][m]);
+            v[1][m] = fma(a.st[1][j], w[sl][m], v[1][m]);
+            v[2][m] = fma(a.st[2][j], w[sl][m], v[2][m]);
+          }
+        }
+        if (i2 < a.r_lo || i2 >= a.r_hi) {  // boundary row of direction 2 (warp-uniform)
+          const int er = (i2 < a.r_lo ? i2 : a.r_lo + (i2 - a.r_hi)) * W;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            const int sl = (u + j) % R;
+            const double eM = __ldg(a.E[0] + er + j), eJ = __ldg(a.E[1] + er + j), eK = __ldg(a.E[2] + er + j);
+#pragma unroll
+            for (int m = 0; m < CW; ++m) {
+              v[0][m] = fma(eM, w[sl][m], v[0][m]);
+              v[1][m] = fma(eJ, w[sl][m], v[1][m]);
+              v[2][m] = fma(eK, w[sl][m], v[2][m]);
+            }
+          }
+        }
+        // ---- direction 1: columns c0 - P .. c0 + CW - 1 + P of v_M, v_J, v_K
+        double x[3][CW + 2 * P];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            const double lft = __shfl_up_sync(0xffffffffu, v[f][CW - P + k], 1);
+            const double rgt = __shfl_down_sync(0xffffffffu, v[f][k], 1);
+            x[f][k] = lane == 0 ? 0.0 : lft;
+            x[f][P + CW + k] = lane == 31 ? 0.0 : rgt;
+          }
+#pragma unroll
+          for (int m = 0; m < CW; ++m) x[f][P + m] = v[f][m];
+        }
+        const size_t ro = base + size_t(i2) * n1;
+#pragma unroll
+        for (int m = 0; m < CW; ++m) {
+          const int c = c0 + m;
+          double pm = 0.0, pk = 0.0, pj = 0.0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            const double xm = x[0][m + j], xj = x[1][m + j], xk = x[2][m + j];
+            pm = fma(a.st[4][j], xm, pm);
+            pk = fma(a.st[4][j], xk, fma(a.st[6][j], xm, pk));
+            pj = fma(a.st[4][j], xj, fma(a.st[5][j], xm, fma(2.0 * a.st[6][j], xk, pj)));
+          }
+          if (c < n1 && (c < a.r_lo1 || c >= a.r_hi1)) {  // boundary column of direction 1
+            const int er = (c < a.r_lo1 ? c : a.r_lo1 + (c - a.r_hi1)) * W;
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+              const double eM = __ldg(a.E[4] + er + j), eJ = __ldg(a.E[5] + er + j), eK = __ldg(a.E[6] + er + j);
+              const double xm = x[0][m + j], xj = x[1][m + j], xk = x[2][m + j];
+              pm = fma(eM, xm, pm);
+              pk = fma(eM, xk, fma(eK, xm, pk));
+              pj = fma(eM, xj, fma(eJ, xm, fma(2.0 * eK, xk, pj)));
+            }
+          }
+          if (c < n1) {
+            a.out[0][ro + m] = pm;
+            a.out[1][ro + m] = pk;
+            a.out[2][ro + m] = pj;
+          }
+        }
+      }
+    }
+  }
+}
+cudaError_t mv4_sweep_run(const MVArgs& a, int p, int cw, int num_sms, cudaStream_t s);
+
 // launch plan built by the host (api.cu) and executed by mv2.cu (own translation unit)
 struct MV2Plan {
   MVArgs time, dir, plane;

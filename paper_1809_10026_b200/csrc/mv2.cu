@@ -1,6 +1,8 @@
 // ls_matvec v2 launches (matvec2_kernels.cuh), one translation unit of their own.
 #include "matvec2_kernels.cuh"
 
+#include <algorithm>
+
 namespace ls {
 
 #ifndef LS_MV2_SWEEP_D
@@ -62,6 +64,25 @@ static cudaError_t run_p(const MV2Plan& pl, int64_t* launches) {
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+#ifndef LS_MV4_SWEEP_D
+#define LS_MV4_SWEEP_D 2  // rows of x loaded ahead by the v4 sweep plane pass
+#endif
+
+template <int P, int CW>
+static cudaError_t sweep4(const MVArgs& a, int num_sms, cudaStream_t s) {
+  if (a.ncols == 0) return cudaSuccess;
+  const unsigned grid = unsigned(std::min<uint64_t>((uint64_t(a.ncols) + 7) / 8, uint64_t(num_sms)));
+  const cudaError_t e = launch_pdl(mv4_sweep_kernel<P, CW, LS_MV4_SWEEP_D>, grid, 256, 0, s, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t mv4_sweep_run(const MVArgs& a, int p, int cw, int num_sms, cudaStream_t s) {
+  if (p == 3 && cw == 3) return sweep4<3, 3>(a, num_sms, s);
+  if (p == 3 && cw == 4) return sweep4<3, 4>(a, num_sms, s);
+  if (p == 4 && cw == 4) return sweep4<4, 4>(a, num_sms, s);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t mv2_run(int p, int pt, const MV2Plan& plan, int64_t* launches) {

@@ -154,3 +154,29 @@ def test_matvec_slab3_decomposition(d, p, ne, world, mv):
         x_hi = xg[t0 + ntl:t0 + ntl + hi].clone() if hi else None
         y = ctx.matvec_slab3(x_lo, xg[t0:t0 + ntl].clone(), x_hi, t0 - lo, t0, ntl).cpu().numpy()
         assert _rel(y, y_ref[t0:t0 + ntl]) <= 1e-12, (r, t0, ntl)
+
+
+@pytest.mark.parametrize("p,ne", [(3, [7, 6, 9, 8]), (3, [64, 5, 6, 7]), (3, [60, 70, 3, 4]), (4, [94, 9, 5, 4]),
+                                  (4, [30, 3, 2, 5]), (3, [95, 4, 6, 3]), (4, [124, 2, 3, 3]), (3, [2, 40, 3, 5])])
+def test_matvec_v4_sweep_plane(p, ne):
+    """The plane pass as the DFMA register sweep (LS_TUNE_MV4_SWEEP = 17, opt-in for d = 3,
+    p = 3, 4; matvec2_kernels.cuh mv4_sweep_kernel) against the oracle and the DMMA plane pass
+    (17 = 0, default), with the fused (v5) and the two-pass second stage."""
+    import torch
+    import paper_1809_10026_b200 as ls
+    d = 3
+    ctx = ls.Context(d, p, ne)
+    ctx.tune(2, 4)
+    space = [uv.space_factors(n, p) for n in ne[:d]]
+    tf = uv.time_factors(ne[d], p)
+    x = synth.residual(ctx.shape, 41)
+    xg = torch.from_numpy(x).cuda()
+    y_ref = op.apply_A(x, space, tf)
+    for mv5 in (1, 0):
+        ctx.tune(10, mv5)
+        ctx.tune(17, 1)
+        y = ctx.matvec(xg).cpu().numpy()
+        ctx.tune(17, 0)
+        y0 = ctx.matvec(xg).cpu().numpy()
+        assert _rel(y, y_ref) <= 1e-12, mv5
+        assert _rel(y, y0) <= 1e-13, mv5
