@@ -42,18 +42,20 @@ struct FTArgs {
   uint64_t ld;           // row stride (elements)
 };
 
-template <int KS_, bool VEC_, int D_, int MINB_, bool TAIL_ = false>
+template <int KS_, bool VEC_, int D_, int MINB_, int TV_ = 0>
 struct FTCfg {
   static constexpr int KS = KS_, D = D_, MINB = MINB_;
   static constexpr bool VEC = VEC_;
   static constexpr int NJ = (KS + 1) / 2;      // 8-wide n-tiles of j (and of t' in the output)
-  // TAIL (n_t = 8 (NJ - 1) + 1 or + 2): the last n-tile of j and the last output tile of t' hold
-  // one or two valid indices; they are computed with DFMAs instead of 7/8- or 3/4-padded DMMA
-  // tiles (the eigen columns j0 + v and output rows j0 + w, j0 = 8 (NJ - 1), v, w < 2)
-  static constexpr bool TAIL = TAIL_;
+  // TAIL (n_t = 8 (NJ - 1) + 1 .. + TV, TV = 2 or 4): the last n-tile of j and the last output
+  // tile of t' hold at most TV valid indices; they are computed with DFMAs instead of mostly
+  // padded DMMA tiles (the eigen columns j0 + v and output rows j0 + w, j0 = 8 (NJ - 1), v, w < TV)
+  static constexpr int TV = TV_;
+  static constexpr bool TAIL = TV > 0;
   static constexpr int NJD = TAIL ? NJ - 1 : NJ;  // DMMA n-tiles / output tiles
-  static constexpr int UTN = TAIL ? 2 * 8 * NJ : 0;  // ut[t][v] = U_t[t][j0 + v]
-  static constexpr int UON = TAIL ? 2 * 8 * NJ : 0;  // uo[j][w] = U_t[j0 + w][j]
+  static constexpr int UTN = TV * 8 * NJ;  // ut[t][v] = U_t[t][j0 + v]
+  static constexpr int UON = TV * 8 * NJ;  // uo[j][w] = U_t[j0 + w][j]
+  static_assert(TV == 0 || TV == 2 || TV == 4, "tail width");
   static constexpr int KSP = NJ;               // k-step pairs of the first product
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int TW = 16;                // columns per warp tile (2 m-tiles)
@@ -94,9 +96,9 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
   }
   for (int e = tid; e < C::LAMN; e += C::THREADS) lam[e] = e < nt ? __ldg(a.lam_t + e) : 1.0;
   constexpr int J0 = 8 * (C::NJ - 1);
-  if (C::TAIL) {
+  if constexpr (C::TAIL) {
     for (int e = tid; e < C::UTN; e += C::THREADS) {
-      const int t = e >> 1, v = e & 1;
+      const int t = e / C::TV, v = e % C::TV;
       ut[e] = (t < nt && J0 + v < nt) ? __ldg(a.U + size_t(t) * nt + J0 + v) : 0.0;
       uo[e] = (t < nt && J0 + v < nt) ? __ldg(a.U + size_t(J0 + v) * nt + t) : 0.0;  // uo[j][w], j = t
     }
@@ -154,7 +156,9 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     for (int ms = 0; ms < 2; ++ms)
 #pragma unroll
       for (int jt = 0; jt < C::NJ; ++jt) acc[ms][jt][0] = acc[ms][jt][1] = 0.0;
-    double py[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // TAIL: lane-partial Y^T[s0 + ms][J0 + v] (t = c mod 4)
+    double py[2][C::TV > 0 ? C::TV : 1];  // TAIL: lane-partial Y^T[s0 + ms][J0 + v] (t = c mod 4)
+#pragma unroll
+    for (int v = 0; v < C::TV; ++v) py[0][v] = py[1][v] = 0.0;
 #pragma unroll
     for (int ksp = 0; ksp < C::KSE / 2 + (C::KSE & 1); ++ksp) {
       const int k0 = 2 * ksp, k1 = 2 * ksp + 1;
@@ -162,17 +166,20 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
         const double2 x0 = win[k0 % C::D];
         const double2 x1 = (k1 < C::KS) ? win[k1 % C::D] : make_double2(0.0, 0.0);
         if (C::TAIL) {
-          const double2 u0 = *reinterpret_cast<const double2*>(ut + 2 * (4 * k0 + c));
-          py[0][0] = fma(x0.x, u0.x, py[0][0]);
-          py[0][1] = fma(x0.x, u0.y, py[0][1]);
-          py[1][0] = fma(x0.y, u0.x, py[1][0]);
-          py[1][1] = fma(x0.y, u0.y, py[1][1]);
-          if (k1 < C::KS) {
-            const double2 u1 = *reinterpret_cast<const double2*>(ut + 2 * (4 * k1 + c));
-            py[0][0] = fma(x1.x, u1.x, py[0][0]);
-            py[0][1] = fma(x1.x, u1.y, py[0][1]);
-            py[1][0] = fma(x1.y, u1.x, py[1][0]);
-            py[1][1] = fma(x1.y, u1.y, py[1][1]);
+#pragma unroll
+          for (int v = 0; v < C::TV; v += 2) {
+            const double2 u0 = *reinterpret_cast<const double2*>(ut + C::TV * (4 * k0 + c) + v);
+            py[0][v] = fma(x0.x, u0.x, py[0][v]);
+            py[0][v + 1] = fma(x0.x, u0.y, py[0][v + 1]);
+            py[1][v] = fma(x0.y, u0.x, py[1][v]);
+            py[1][v + 1] = fma(x0.y, u0.y, py[1][v + 1]);
+            if (k1 < C::KS) {
+              const double2 u1 = *reinterpret_cast<const double2*>(ut + C::TV * (4 * k1 + c) + v);
+              py[0][v] = fma(x1.x, u1.x, py[0][v]);
+              py[0][v + 1] = fma(x1.x, u1.y, py[0][v + 1]);
+              py[1][v] = fma(x1.y, u1.x, py[1][v]);
+              py[1][v + 1] = fma(x1.y, u1.y, py[1][v + 1]);
+            }
           }
         }
 #pragma unroll
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
 #pragma unroll
       for (int ms = 0; ms < 2; ++ms)
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
+        for (int v = 0; v < C::TV; ++v) {
           double y = py[ms][v];
           y += __shfl_xor_sync(0xffffffffu, y, 1);
           y += __shfl_xor_sync(0xffffffffu, y, 2);
@@ -233,15 +240,18 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int ms = 0; ms < 2; ++ms) o[u][ms][0] = o[u][ms][1] = 0.0;
-      if (C::TAIL) {  // the tail columns' rank-2 update: o += Y^T[., J0 + v] U_t[t'][J0 + v]
+      if (C::TAIL) {  // the tail columns' rank-TV update: o += Y^T[., J0 + v] U_t[t'][J0 + v]
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double2 w = *reinterpret_cast<const double2*>(ut + 2 * (8 * (tt + u) + 2 * c + h));
+          for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int ms = 0; ms < 2; ++ms) o[u][ms][h] = fma(py[ms][1], w.y, fma(py[ms][0], w.x, o[u][ms][h]));
-          }
+            for (int v = 0; v < C::TV; v += 2) {
+              const double2 w = *reinterpret_cast<const double2*>(ut + C::TV * (8 * (tt + u) + 2 * c + h) + v);
+#pragma unroll
+              for (int ms = 0; ms < 2; ++ms)
+                o[u][ms][h] = fma(py[ms][v + 1], w.y, fma(py[ms][v], w.x, o[u][ms][h]));
+            }
       }
 #pragma unroll
       for (int jt = 0; jt < C::NJD; ++jt) {
@@ -282,40 +292,46 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
       }
     }
     if (C::TAIL) {  // output rows J0 + w: Z^T[s][J0 + w] = sum_j Y^T[s][j] U_t[J0 + w][j]
-      double pz[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      double pz[2][C::TV > 0 ? C::TV : 1];
+#pragma unroll
+      for (int w = 0; w < C::TV; ++w) pz[0][w] = pz[1][w] = 0.0;
 #pragma unroll
       for (int jt = 0; jt < C::NJD; ++jt)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double2 w = *reinterpret_cast<const double2*>(uo + 2 * (8 * jt + 4 * h + c));
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int ms = 0; ms < 2; ++ms) {
-            pz[ms][0] = fma(acc[ms][jt][h], w.x, pz[ms][0]);
-            pz[ms][1] = fma(acc[ms][jt][h], w.y, pz[ms][1]);
+          for (int w = 0; w < C::TV; w += 2) {
+            const double2 uw = *reinterpret_cast<const double2*>(uo + C::TV * (8 * jt + 4 * h + c) + w);
+#pragma unroll
+            for (int ms = 0; ms < 2; ++ms) {
+              pz[ms][w] = fma(acc[ms][jt][h], uw.x, pz[ms][w]);
+              pz[ms][w + 1] = fma(acc[ms][jt][h], uw.y, pz[ms][w + 1]);
+            }
           }
-        }
       if (c == 0) {  // the tail-tail block (quad-uniform py): once per quad
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const double2 w = *reinterpret_cast<const double2*>(uo + 2 * (J0 + v));
+        for (int v = 0; v < C::TV; ++v)
 #pragma unroll
-          for (int ms = 0; ms < 2; ++ms) {
-            pz[ms][0] = fma(py[ms][v], w.x, pz[ms][0]);
-            pz[ms][1] = fma(py[ms][v], w.y, pz[ms][1]);
+          for (int w = 0; w < C::TV; w += 2) {
+            const double2 uw = *reinterpret_cast<const double2*>(uo + C::TV * (J0 + v) + w);
+#pragma unroll
+            for (int ms = 0; ms < 2; ++ms) {
+              pz[ms][w] = fma(py[ms][v], uw.x, pz[ms][w]);
+              pz[ms][w + 1] = fma(py[ms][v], uw.y, pz[ms][w + 1]);
+            }
           }
-        }
       }
 #pragma unroll
       for (int ms = 0; ms < 2; ++ms)
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
+        for (int w = 0; w < C::TV; ++w) {
           pz[ms][w] += __shfl_xor_sync(0xffffffffu, pz[ms][w], 1);
           pz[ms][w] += __shfl_xor_sync(0xffffffffu, pz[ms][w], 2);
         }
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
+      for (int w = 0; w < C::TV; ++w) {
         const int t = J0 + w;
-        if (c != w || t >= nt || s0 >= ncols) continue;  // lanes c = 0, 1 store rows J0, J0 + 1
+        if (c != w || t >= nt || s0 >= ncols) continue;  // lane c = w of each quad stores row J0 + w
         double* dst = zp + size_t(t) * ld;
         if (C::VEC) {
           *reinterpret_cast<double2*>(dst) = make_double2(pz[0][w], pz[1][w]);

@@ -29,6 +29,9 @@ static cudaError_t ft_launch_cfg(const FTArgs& a, cudaStream_t s, int num_sms) {
 #ifndef LS_FT_TAIL
 #define LS_FT_TAIL 1  // DFMA tail tiles (FTCfg TAIL) where they apply
 #endif
+#ifndef LS_FT_TAIL_MAXV
+#define LS_FT_TAIL_MAXV 4  // largest number of valid indices in a DFMA tail tile
+#endif
 #ifndef LS_FT_MINB2_MAXKS
 #define LS_FT_MINB2_MAXKS 18  // buckets up to this KS run 2 CTAs per SM (<= 128 registers)
 #endif
@@ -37,13 +40,20 @@ template <int KS>
 static cudaError_t ft_launch_ks(const FTArgs& a, bool vec, cudaStream_t s, int num_sms) {
   // two CTAs per SM while both fragment sets and the accumulators fit (n_t <= 72)
   constexpr int MINB = KS <= LS_FT_MINB2_MAXKS ? 2 : 1;
-  // DFMA tail when the last 8-wide tile of j / t' holds one or two valid indices
+  // DFMA tail when the last 8-wide tile of j / t' holds at most 4 valid indices
   constexpr int J0 = 8 * ((KS + 1) / 2 - 1);
-  const bool tail = LS_FT_TAIL && J0 > 0 && a.nt > J0 && a.nt <= J0 + 2;
-  if (tail) {  // the tail accumulators do not fit 128 registers above n_t = 36: 1 CTA per SM there
+  const int tv = a.nt - J0;  // valid indices in the last tile
+  if (LS_FT_TAIL && J0 > 0 && tv >= 1 && tv <= LS_FT_TAIL_MAXV) {
+    // the tail accumulators do not fit 128 registers above n_t = 36: 1 CTA per SM there
     constexpr int MINBT = KS <= 9 ? 2 : 1;
-    if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D, MINBT, true>>(a, s, num_sms);
-    return ft_launch_cfg<FTCfg<KS, false, LS_FT_D, MINBT, true>>(a, s, num_sms);
+    if (tv <= 2) {
+      if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D, MINBT, 2>>(a, s, num_sms);
+      return ft_launch_cfg<FTCfg<KS, false, LS_FT_D, MINBT, 2>>(a, s, num_sms);
+    }
+    if constexpr (LS_FT_TAIL_MAXV >= 3) {
+      if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D, MINBT, 4>>(a, s, num_sms);
+      return ft_launch_cfg<FTCfg<KS, false, LS_FT_D, MINBT, 4>>(a, s, num_sms);
+    }
   }
   if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D, MINB>>(a, s, num_sms);
   return ft_launch_cfg<FTCfg<KS, false, LS_FT_D, MINB>>(a, s, num_sms);
