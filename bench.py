@@ -454,7 +454,8 @@ def main():
     achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
     hbm, hbm_src = _hbm_peak()
     traffic, traffic_src = _traffic(args.config)
-    roof = {"kernel": "fd_mode_kernel (all mode products of fd_apply)", "bound": "tensor",
+    roof = {"kernel": ("FD mode-product kernels (all mode products of fd_apply: fd_mode_rd_kernel spatial "
+                       "launches + fd_time_fused_kernel)"), "bound": "tensor",
             "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
             "traffic_unit": "bytes per launch (mean over the captured launches)", "traffic_source": traffic_src,

@@ -467,8 +467,8 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
 #define LS_TUNE_PQ_FUSE 12
 /* LS_TUNE_FD_TIME: 1 = fd_apply's time mode (U_t^T, the division by lambda_t + Lambda_s of
  * Algorithm 1 step 3, U_t; PAPER.md 947-962) runs as ONE kernel whose intermediate stays in
- * registers, where n_t <= 104 (default); 0 = two launches (the scaled forward product into a
- * workspace, then the backward product).  n_t > 104 always uses two launches. */
+ * registers (default; every supported n_t <= 136); 0 = two launches (the scaled forward product
+ * into a workspace, then the backward product). */
 #define LS_TUNE_FD_TIME 13
 /* LS_TUNE_FD_PLANE: 1 = fd_apply's spatial mode products of directions 1 and 2 run as ONE
  * kernel per (i_3, .., t) plane whose intermediate stays in registers, where both directions

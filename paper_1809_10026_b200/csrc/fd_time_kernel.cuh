@@ -42,7 +42,7 @@ struct FTArgs {
   uint64_t ld;           // row stride (elements)
 };
 
-template <int KS_, bool VEC_, int D_, int MINB_, int TV_ = 0>
+template <int KS_, bool VEC_, int D_, int MINB_, int TV_ = 0, bool SC_ = false>
 struct FTCfg {
   static constexpr int KS = KS_, D = D_, MINB = MINB_;
   static constexpr bool VEC = VEC_;
@@ -59,12 +59,19 @@ struct FTCfg {
   static constexpr int KSP = NJ;               // k-step pairs of the first product
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
   static constexpr int TW = 16;                // columns per warp tile (2 m-tiles)
-  static constexpr int B1N = NJ * KSP * 64;    // doubles
-  static constexpr int B2N = NJ * NJ * 64;
+  // SC (single copy, n_t up to 136): ONE copy of U_t in 8 x 8 blocks, element (a, b) of block
+  // (T, J) at 8a + (b ^ m(a)), m(a) = 6 if a & 2 else 0 -- an XOR swizzle under which both
+  // fragment patterns (first product: 4 rows x 8 columns of a block, second: 8 rows x 4 columns)
+  // are bank-conflict free (one LDS.64 per fragment instead of one LDS.128 per two); 148 KB at
+  // n_t = 133 where the two fragment-ordered copies would need 296 KB
+  static constexpr bool SC = SC_;
+  static constexpr int B1N = SC ? 0 : NJ * KSP * 64;    // doubles
+  static constexpr int B2N = SC ? 0 : NJ * NJ * 64;
+  static constexpr int UBN = SC ? NJ * NJ * 64 : 0;
   static constexpr int LAMN = 8 * NJ;
   static constexpr int KSE = ((KS + D - 1) / D) * D;  // k-steps rounded up to the window
-  static constexpr size_t SMEM = size_t(B1N + B2N + LAMN + UTN + UON) * sizeof(double);
-  static_assert(KS <= 26, "n_t <= 104");
+  static constexpr size_t SMEM = size_t(B1N + B2N + UBN + LAMN + UTN + UON) * sizeof(double);
+  static_assert(SC ? KS <= 34 : KS <= 26, "n_t <= 104 (two fragment copies) / 136 (single copy)");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -73,7 +80,8 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
   extern __shared__ __align__(16) double smem[];
   double* b1 = smem;
   double* b2 = smem + C::B1N;
-  double* lam = b2 + C::B2N;
+  double* ub = b2 + C::B2N;  // SC: the swizzled single copy
+  double* lam = ub + C::UBN;
   double* ut = lam + C::LAMN;  // TAIL tables (16-byte aligned: all offsets are multiples of 8 doubles)
   double* uo = ut + C::UTN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -93,6 +101,12 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
     const int t = 8 * tt + (l >> 2);
     const int j = 8 * jt + 4 * h + (l & 3);
     b2[e] = (t < nt && j < nt) ? __ldg(a.U + size_t(t) * nt + j) : 0.0;
+  }
+  for (int e = tid; e < C::UBN; e += C::THREADS) {
+    const int blk = e >> 6, pos = e & 63, ra = pos >> 3;
+    const int t = 8 * (blk / C::NJ) + ra;
+    const int j = 8 * (blk % C::NJ) + ((pos & 7) ^ ((ra & 2) ? 6 : 0));
+    ub[e] = (t < nt && j < nt) ? __ldg(a.U + size_t(t) * nt + j) : 0.0;
   }
   for (int e = tid; e < C::LAMN; e += C::THREADS) lam[e] = e < nt ? __ldg(a.lam_t + e) : 1.0;
   constexpr int J0 = 8 * (C::NJ - 1);
@@ -141,6 +155,11 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
 
   const double* b1l = b1 + 2 * lane;
   const double* b2l = b2 + 2 * lane;
+  // SC lane offsets inside a block: first product (row 4 (ks & 1) + c, column pi(r)),
+  // second product (row r, column 4h + c)
+  const int l1 = 8 * c + ((4 * (r & 1) + (r >> 1)) ^ ((c & 2) ? 6 : 0));
+  const int l20 = 8 * r + (c ^ ((r & 2) ? 6 : 0));
+  const int l21 = 8 * r + ((4 + c) ^ ((r & 2) ? 6 : 0));
 
 #pragma unroll 1
   for (; tile < ntw; tile += wstride) {
@@ -184,7 +203,14 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
         }
 #pragma unroll
         for (int jt = 0; jt < C::NJD; ++jt) {
-          const double2 bf = *reinterpret_cast<const double2*>(b1l + (jt * C::KSP + ksp) * 64);
+          double2 bf;
+          if constexpr (C::SC) {
+            const double* blk = ub + (ksp * C::NJ + jt) * 64;
+            bf.x = blk[l1];
+            bf.y = blk[l1 + 32];
+          } else {
+            bf = *reinterpret_cast<const double2*>(b1l + (jt * C::KSP + ksp) * 64);
+          }
           dmma_8x8x4(acc[0][jt], x0.x, bf.x);
           dmma_8x8x4(acc[1][jt], x0.y, bf.x);
           if (k1 < C::KS) {
@@ -256,7 +282,13 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
 #pragma unroll
       for (int jt = 0; jt < C::NJD; ++jt) {
         const bool h1 = 2 * jt + 1 < C::KS;  // k-step (jt, 1) has valid columns
-        const double2 f0 = *reinterpret_cast<const double2*>(b2l + (tt * C::NJ + jt) * 64);
+        double2 f0;
+        if constexpr (C::SC) {
+          const double* blk = ub + (tt * C::NJ + jt) * 64;
+          f0 = make_double2(blk[l20], blk[l21]);
+        } else {
+          f0 = *reinterpret_cast<const double2*>(b2l + (tt * C::NJ + jt) * 64);
+        }
         dmma_8x8x4(o[0][0], acc[0][jt][0], f0.x);
         dmma_8x8x4(o[0][1], acc[1][jt][0], f0.x);
         if (h1) {
@@ -264,7 +296,13 @@ __global__ void __launch_bounds__(256, C::MINB) fd_time_fused_kernel(FTArgs a) {
           dmma_8x8x4(o[0][1], acc[1][jt][1], f0.y);
         }
         if (two) {
-          const double2 f1 = *reinterpret_cast<const double2*>(b2l + ((tt + 1) * C::NJ + jt) * 64);
+          double2 f1;
+          if constexpr (C::SC) {
+            const double* blk = ub + ((tt + 1) * C::NJ + jt) * 64;
+            f1 = make_double2(blk[l20], blk[l21]);
+          } else {
+            f1 = *reinterpret_cast<const double2*>(b2l + ((tt + 1) * C::NJ + jt) * 64);
+          }
           dmma_8x8x4(o[1][0], acc[0][jt][0], f1.x);
           dmma_8x8x4(o[1][1], acc[1][jt][0], f1.x);
           if (h1) {

@@ -26,6 +26,9 @@ static cudaError_t ft_launch_cfg(const FTArgs& a, cudaStream_t s, int num_sms) {
 #ifndef LS_FT_D
 #define LS_FT_D 6  // prefetch window (k-steps)
 #endif
+#ifndef LS_FT_D_SC
+#define LS_FT_D_SC 8  // prefetch window of the single-copy buckets (config 4: 6 -> 8: 14.85 -> 14.79 ms)
+#endif
 #ifndef LS_FT_TAIL
 #define LS_FT_TAIL 1  // DFMA tail tiles (FTCfg TAIL) where they apply
 #endif
@@ -38,6 +41,10 @@ static cudaError_t ft_launch_cfg(const FTArgs& a, cudaStream_t s, int num_sms) {
 
 template <int KS>
 static cudaError_t ft_launch_ks(const FTArgs& a, bool vec, cudaStream_t s, int num_sms) {
+  if constexpr (KS > 26) {  // n_t > 104: the single swizzled copy of U_t (FTCfg SC), 1 CTA per SM
+    if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D_SC, 1, 0, true>>(a, s, num_sms);
+    return ft_launch_cfg<FTCfg<KS, false, LS_FT_D_SC, 1, 0, true>>(a, s, num_sms);
+  } else {
   // two CTAs per SM while both fragment sets and the accumulators fit (n_t <= 72)
   constexpr int MINB = KS <= LS_FT_MINB2_MAXKS ? 2 : 1;
   // DFMA tail when the last 8-wide tile of j / t' holds at most 4 valid indices
@@ -57,6 +64,7 @@ static cudaError_t ft_launch_ks(const FTArgs& a, bool vec, cudaStream_t s, int n
   }
   if (vec) return ft_launch_cfg<FTCfg<KS, true, LS_FT_D, MINB>>(a, s, num_sms);
   return ft_launch_cfg<FTCfg<KS, false, LS_FT_D, MINB>>(a, s, num_sms);
+  }
 }
 
 int ft_bucket(int nt) {
@@ -79,6 +87,9 @@ cudaError_t ft_launch(const FTArgs& a, cudaStream_t s, int num_sms) {
     case 21: return ft_launch_ks<21>(a, vec, s, num_sms);
     case 25: return ft_launch_ks<25>(a, vec, s, num_sms);
     case 26: return ft_launch_ks<26>(a, vec, s, num_sms);
+    case 30: return ft_launch_ks<30>(a, vec, s, num_sms);
+    case 33: return ft_launch_ks<33>(a, vec, s, num_sms);
+    case 34: return ft_launch_ks<34>(a, vec, s, num_sms);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -6,11 +6,11 @@ namespace ls {
 
 struct FTArgs;
 
-// k-step buckets (ceil(n_t / 4) rounded up to one of these); n_t <= 104
-#define LS_FT_BUCKETS 3, 5, 9, 13, 17, 21, 25, 26
-#define LS_FT_NT_MAX 104
+// k-step buckets (ceil(n_t / 4) rounded up to one of these); n_t <= 136
+#define LS_FT_BUCKETS 3, 5, 9, 13, 17, 21, 25, 26, 30, 33, 34
+#define LS_FT_NT_MAX 136
 
-int ft_bucket(int nt);  // -1 if n_t > LS_FT_NT_MAX
+int ft_bucket(int nt);  // -1 if n_t > LS_FT_NT_MAX (buckets above 26: the single-copy layout)
 cudaError_t ft_launch(const FTArgs& a, cudaStream_t s, int num_sms);
 
 }  // namespace ls

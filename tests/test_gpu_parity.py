@@ -265,7 +265,7 @@ def test_fd_apply_host_roundtrip(torch_cuda, d, p, n_elems):
 
 def test_kernels_launched(torch_cuda):
     """The CUDA path is the one that runs: fd_apply launches 2d + 1 kernels (the two time modes
-    fused, n_t <= 104), or 2(d+1) with the fused time mode off (LS_TUNE_FD_TIME = 0) or n_t > 104."""
+    fused), or 2(d+1) with the fused time mode off (LS_TUNE_FD_TIME = 0)."""
     torch = torch_cuda
     import paper_1809_10026_b200 as ls
     ctx = _ctx(3, 3, [6, 6, 6, 6])
@@ -277,11 +277,11 @@ def test_kernels_launched(torch_cuda):
     n0 = ctx.launches
     ctx.fd_apply(r)
     assert ctx.launches - n0 == 8
-    ctx2 = _ctx(1, 2, [10, 110])
+    ctx2 = _ctx(1, 2, [10, 110])  # n_t = 111: the single-copy fused kernel
     r2 = torch.rand(ctx2.shape, dtype=torch.float64, device="cuda")
     n0 = ctx2.launches
     ctx2.fd_apply(r2)
-    assert ctx2.launches - n0 == 4
+    assert ctx2.launches - n0 == 3
 
 
 EDGE_CASES = [

@@ -2,7 +2,8 @@
 
 Algorithm 1 steps 2-4 restricted to the time direction (PAPER.md 947-962): U_t^T along time,
 the division by lambda_t[i_t] + Lambda_s[s] (reading c3), U_t along time -- one kernel whose
-intermediate never leaves the registers, for n_t <= 104.  z = P^{-1} r is unique,
+intermediate never leaves the registers (two fragment-ordered copies of U_t in shared memory up to
+n_t = 104, one XOR-swizzled copy up to n_t = 136).  z = P^{-1} r is unique,
 so the fused path must match the oracle at the parity bar and the two-launch path (knob 13 = 0)
 to rounding.  Covered: every k-step bucket (3, 5, 9, 13, 17, 21, 25, 26) with n_t at both ends,
 even row strides (16-byte vector path) and odd ones (scalar path), ragged last warp tiles,
@@ -43,8 +44,12 @@ CASES = [
     (2, 4, [20, 21, 96]),      # n_t = 99  (bucket 25), config 5 p = 4's n_t
     (2, 2, [24, 25, 96]),      # n_t = 97  (bucket 25), config 5 p = 2's n_t
     (2, 8, [10, 11, 96]),      # n_t = 103 (bucket 26), config 5 p = 8's n_t
-    (1, 2, [50, 103]),         # n_t = 104 (largest fused)
-    (1, 2, [50, 104]),         # n_t = 105 (two launches)
+    (1, 2, [50, 103]),         # n_t = 104 (largest two-copy bucket)
+    (1, 2, [50, 104]),         # n_t = 105 (single swizzled copy, bucket 30)
+    (2, 2, [30, 31, 119]),     # n_t = 120 (bucket 30, full)
+    (2, 6, [9, 10, 124]),      # n_t = 129 (bucket 33)
+    (3, 6, [4, 5, 6, 128]),    # n_t = 133 (bucket 34: config 4's n_t)
+    (1, 2, [40, 135]),         # n_t = 136 (the cap)
 ]
 
 

@@ -27,7 +27,7 @@ timeout 600 $G > gpurun_out/plain_pcg_$tag.log 2>&1 && \
 echo "pcg_launch_rc=$?"
 P="python tools/profile_fd.py --config 4 --reps 1"
 timeout 300 $P > gpurun_out/plain_prof_$tag.log 2>&1 && \
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:fd_mode -c 8 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k 'regex:fd_mode|fd_time' -c 7 \
     -o gpurun_out/prof_c4_$tag -f $P > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu_full_rc=$?"
 M="python tools/profile_fd.py --config 4 --reps 1 --matvec"

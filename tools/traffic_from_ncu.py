@@ -11,7 +11,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 path, cfg, src = sys.argv[1], sys.argv[2], sys.argv[3]
 rows = [json.loads(l) for l in open(path) if l.startswith("{")]
-rows = [r for r in rows if "fd_mode" in r["kernel"]]
+rows = [r for r in rows if "fd_mode" in r["kernel"] or "fd_time" in r["kernel"]]
 assert rows and rows[0]["dram_unit"] in ("byte", "B"), rows[:1]
 b = sum(r["dram_read"] + r["dram_write"] for r in rows) / len(rows)
 out_path = os.path.join(ROOT, "profiles", "traffic.json")
