@@ -70,7 +70,8 @@ def test_time_fused_vs_oracle(d, p, n_elems):
     assert _rel(z, z2) <= 1e-12
 
 
-@pytest.mark.parametrize("ps,pt,n_elems", [(3, 1, [20, 21, 40]), (2, 5, [18, 19, 60]), (4, 2, [9, 10, 11, 70])])
+@pytest.mark.parametrize("ps,pt,n_elems", [(3, 1, [20, 21, 40]), (2, 5, [18, 19, 60]), (4, 2, [9, 10, 11, 70]),
+                                          (2, 7, [12, 13, 120]), (5, 3, [6, 7, 8, 131])])
 def test_time_fused_separate_degrees(ps, pt, n_elems):
     import torch
     import paper_1809_10026_b200 as ls
@@ -139,3 +140,16 @@ def test_time_fused_nonfinite_guard():
     assert bad[:, 7].all()
     bad[:, 7] = False
     assert not bad.any()
+
+
+def test_time_fused_mapped_pg_long_time():
+    """The P^G preconditioner (PAPER.md 969-1045: D^{-1/2} scaling around the FD solve of the
+    weighted pencils) with n_t = 133 (the single swizzled U_t copy) against the two-launch path."""
+    import torch
+    import paper_1809_10026_b200 as ls
+    ctx = ls.Context(2, 3, [6, 6, 131], geometry=synth.quarter_annulus(), precond=ls.LS_PRECOND_PG)
+    r = torch.from_numpy(synth.residual(ctx.shape, 9)).cuda()
+    z = ctx.fd_apply(r).cpu().numpy()
+    ctx.tune(ls.LS_TUNE_FD_TIME, 0)
+    z0 = ctx.fd_apply(r).cpu().numpy()
+    assert _rel(z, z0) <= 1e-12
