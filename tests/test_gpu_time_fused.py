@@ -153,3 +153,15 @@ def test_time_fused_mapped_pg_long_time():
     ctx.tune(ls.LS_TUNE_FD_TIME, 0)
     z0 = ctx.fd_apply(r).cpu().numpy()
     assert _rel(z, z0) <= 1e-12
+
+
+@pytest.mark.parametrize("d,ps,pt,ne", [(1, 2, 1, [4, 1]), (2, 2, 1, [3, 4, 1]), (3, 2, 1, [2, 3, 2, 1]),
+                                        (1, 3, 1, [40, 2]), (2, 2, 2, [1, 1, 1])])
+def test_time_fused_edge_shapes(d, ps, pt, ne):
+    """n_t = 1 and 2 (a single, mostly padded k-step), N_s = 1: the fused kernel against the oracle."""
+    import torch
+    import paper_1809_10026_b200 as ls
+    ctx = ls.Context(d, (ps, pt), ne)
+    r = synth.residual(ctx.shape, 1)
+    z = ctx.fd_apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    assert _rel(z, _oracle(d, ps, pt, ne, r)) <= TOL
