@@ -59,6 +59,10 @@ struct RDCfg {
   // 2 = unfold (backward: inputs [even | odd], outputs p + q and R(p - q))
   static constexpr int CS = CS_;
   static constexpr int NH = CS ? 2 : 1;    // half-products per tile
+#ifndef LS_RD_PF64_MINKS
+#define LS_RD_PF64_MINKS 17
+#endif
+  static constexpr bool PF64 = CS && KS >= LS_RD_PF64_MINKS;  // .L2::64B streaming loads (see ldg_stream)
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_, FAST = FAST_;
   static constexpr int MT = (KS + 1) / 2;  // ceil(n/8) for n in (4KS-4, 4KS] (CS: n -> ceil(n/2))
   static constexpr int KSP = (KS + 1) / 2;  // k-step pairs
@@ -120,14 +124,27 @@ __device__ __forceinline__ RDIn<C::NT> rd_make_in(const ModeArgs& a, uint32_t ti
 
 // streaming loads kept in program order at the NVVM level (volatile): the compiler
 // otherwise hoists a whole tile of B loads ahead of the DMMAs and spills
+#ifndef LS_LDG_L2PF
+#define LS_LDG_L2PF ""  // L2 prefetch-size qualifier of the streaming loads (e.g. ".L2::128B")
+#endif
+// PF64: the .L2::64B prefetch-size hint (an L2 miss fills 64 bytes).  Measured (A/B of whole
+// builds): config 4 fd_apply 14.795 -> 14.728 ms with it on every streaming load, but config 3
+// +0.4 % and config 5 p = 8 +1.2 %; .L2::128B neutral, .L2::256B +1.1 % at config 4.  So it is
+// used by the config-4-sized split kernels only (RDCfg::PF64).
+template <bool PF64 = false>
 __device__ __forceinline__ double ldg_stream(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  if constexpr (PF64) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else asm volatile("ld.global.nc.L1::no_allocate" LS_LDG_L2PF ".f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+template <bool PF64 = false>
 __device__ __forceinline__ double2 ldg_stream2(const double* p) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  if constexpr (PF64)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate" LS_LDG_L2PF ".v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 
@@ -150,14 +167,14 @@ __device__ __forceinline__ void rd_load(double (&dst)[C::NH][C::NT], RDPtr<C>& q
   if (C::FAST) {
     const bool m = mask != 0;
     if constexpr (C::NT == 1) {
-      dst[0][0] = (ok0 && m) ? ldg_stream(q.lp[0]) : 0.0;
-      if (C::CS) dst[C::NH - 1][0] = (ok1 && m) ? ldg_stream(q.lm[0]) : 0.0;
+      dst[0][0] = (ok0 && m) ? ldg_stream<C::PF64>(q.lp[0]) : 0.0;
+      if (C::CS) dst[C::NH - 1][0] = (ok1 && m) ? ldg_stream<C::PF64>(q.lm[0]) : 0.0;
     } else {
 #pragma unroll
       for (int j = 0; j < C::NT; j += 2) {
         double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
-        if (ok0 && m) v0 = ldg_stream2(q.lp[0] + j);
-        if (C::CS && ok1 && m) v1 = ldg_stream2(q.lm[0] + j);
+        if (ok0 && m) v0 = ldg_stream2<C::PF64>(q.lp[0] + j);
+        if (C::CS && ok1 && m) v1 = ldg_stream2<C::PF64>(q.lm[0] + j);
         dst[0][j] = v0.x;
         dst[0][j + 1] = v0.y;
         if (C::CS) {
@@ -171,10 +188,10 @@ __device__ __forceinline__ void rd_load(double (&dst)[C::NH][C::NT], RDPtr<C>& q
     for (int j = 0; j < C::NT; ++j) {
       const bool cm = (mask >> j) & 1u;
       const double* p0 = C::MODE1 ? q.lp[0] + size_t(j) * n : q.lp[C::MODE1 ? 0 : j];
-      dst[0][j] = (ok0 && cm) ? ldg_stream(p0) : 0.0;
+      dst[0][j] = (ok0 && cm) ? ldg_stream<C::PF64>(p0) : 0.0;
       if (C::CS) {
         const double* p1 = C::MODE1 ? q.lm[0] + size_t(j) * n : q.lm[C::MODE1 ? 0 : j];
-        dst[C::NH - 1][j] = (ok1 && cm) ? ldg_stream(p1) : 0.0;
+        dst[C::NH - 1][j] = (ok1 && cm) ? ldg_stream<C::PF64>(p1) : 0.0;
       }
     }
   }
