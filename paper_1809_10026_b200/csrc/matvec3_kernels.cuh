@@ -111,14 +111,17 @@ struct MV3Geom {
   static constexpr int G = RING / 2;  // m-tiles per unrolled group
 };
 
+#ifndef LS_MV3_L2PF
+#define LS_MV3_L2PF ""  // L2 prefetch-size qualifier of the band-pass loads (experiment knob)
+#endif
 __device__ __forceinline__ double mv3_ld(const double* p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate" LS_MV3_L2PF ".f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ double2 mv3_ld2(const double* p) {
   double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate" LS_MV3_L2PF ".v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 

@@ -57,9 +57,12 @@ struct MV4Geom {
   static constexpr int JT0 = -((OFF + 1) / 2);    // first source row tile (k-step 2 JT0 <= -OFF)
 };
 
+#ifndef LS_MV4_L2PF
+#define LS_MV4_L2PF ""  // L2 prefetch-size qualifier of the plane-pass loads (experiment knob)
+#endif
 __device__ __forceinline__ double mv4_ld(const double* p) {
   double v;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc" LS_MV4_L2PF ".f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 
