@@ -142,6 +142,17 @@ struct MV3Occ {
                                                                                          : MV3_MID_CTAS;
 };
 
+// independent accumulator chains (MV3_SPLIT): the direction-3 pass' v2 = J P_M + M P_J + 2K P_K
+// and the time pass' y = K_t v1 + M_t v2 accumulate one product per chain, summed in a fixed
+// order before the store, instead of one dependent DMMA chain of 3 NKB / 2 NKB links
+#ifndef MV3_SPLIT
+#define MV3_SPLIT 0
+#endif
+template <int KIND>
+struct MV3Extra {
+  static constexpr int NX = !MV3_SPLIT ? 0 : KIND == MV3_D3 ? 2 : (KIND == MV3_T2 && MV3_SPLIT == 1) ? 1 : 0;
+};
+
 template <int P, int NT, int KIND, bool MODE1, bool FAST>
 __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const __grid_constant__ MV3Args a) {
   pdl_wait();
@@ -266,9 +277,10 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
               pv[e + 1] = t.y;
             }
           }
-          double acc[NOUT][NT][2];
+          constexpr int NX = MV3Extra<KIND>::NX;
+          double acc[NOUT + NX][NT][2];
 #pragma unroll
-          for (int o = 0; o < NOUT; ++o)
+          for (int o = 0; o < NOUT + NX; ++o)
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[o][j][0] = acc[o][j][1] = 0.0;
           double acc3[KIND == MV3_D3 ? NT : 1][2];  // MV3_D3: v3 of the last time slice
@@ -306,8 +318,8 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
             } else if (KIND == MV3_D3) {     // mats: 0 M, 1 J, 2 K, 3 2K; in: P_M, P_K, P_J
               mma(0, 0, 0);
               mma(1, 1, 0);
-              mma(1, 0, 2);
-              mma(1, 3, 1);
+              mma(NX ? NOUT : 1, 0, 2);
+              mma(NX ? NOUT + 1 : 1, 3, 1);
               if (warp_last) {
 #pragma unroll
                 for (int j = 0; j < NT; ++j) {
@@ -317,7 +329,7 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
               }
             } else if (KIND == MV3_T2) {     // mats: 0 K_t, 1 M_t; in: v1, v2
               mma(0, 0, 0);
-              mma(0, 1, 1);
+              mma(NX ? NOUT : 0, 1, 1);
             } else if (KIND == MV3_MID) {    // mats: 0 M, 1 J, 2 K, 3 2K; in: A, B, C
               mma(0, 0, 0);
               mma(0, 1, 1);
@@ -330,6 +342,16 @@ __global__ void __launch_bounds__(256, MV3Occ<KIND>::CTAS) mv3_band_kernel(const
               mma(0, 1, 1);
               mma(0, 2, 2);
             }
+          }
+          if (NX) {  // fold the extra chains: v2 = (J P_M + M P_J) + 2K P_K, y = K_t v1 + M_t v2
+            constexpr int o0 = KIND == MV3_D3 ? 1 : 0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                acc[o0][j][h] += acc[NOUT][j][h];
+                if (NX > 1) acc[o0][j][h] += acc[NOUT + (NX > 1 ? 1 : 0)][j][h];
+              }
           }
           // refill the two consumed slots with k-steps two m-tiles ahead
 #pragma unroll
