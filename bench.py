@@ -449,6 +449,29 @@ def main():
         t = torch.tensor([e2eb_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2eb_s = float(t.item())
+    # the e2e floor on this box: one vector in and one out over PCIe at once (torch copies of
+    # the same pinned buffers on two streams, no kernel; CUDA events, best of 2)
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    duplex_ms = 1e30
+    for _ in range(2):
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        s_in.wait_stream(stream)
+        s_out.wait_stream(stream)
+        with torch.cuda.stream(s_in):
+            r.copy_(pin_r, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            pin_z.copy_(z, non_blocking=True)
+        stream.wait_stream(s_in)
+        stream.wait_stream(s_out)
+        f1.record(stream)
+        f1.synchronize()
+        duplex_ms = min(duplex_ms, f0.elapsed_time(f1))
+    if world > 1:
+        t = torch.tensor([duplex_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        duplex_ms = float(t.item())
 
     # roofline of the dominant kernel (fd_mode_kernel): algorithmic flops / device time
     achieved = kflops / (kms * 1e-3) / 1e12 if kms > 0 else 0.0
@@ -498,6 +521,11 @@ def main():
                     "d2h_bytes_per_step": e2e_bytes, "steps": e2e_steps,
                     "api": "fd_apply_host_batch (pinned host buffers; every step copies its r in and its z "
                            "out, the copies of steps k+1 / k-1 overlap step k)",
+                    "pcie_floor": {"value": w["N"] / (duplex_ms * 1e-3), "unit": "DOF/s",
+                                   "frac": round((duplex_ms * 1e-3) / e2eb_s, 4),
+                                   "how": ("one step's H2D and D2H copies issued at once on two streams, "
+                                           "no kernel (torch copies of the same pinned buffers; CUDA events, "
+                                           "best of 2): the e2e rate if fd_apply were free")},
                     "single_call": {"value": w["N"] / e2e_s, "unit": "DOF/s",
                                     "api": "fd_apply_host (one synchronous call per step)"}},
             "gpu_launches": launches,

@@ -24,6 +24,19 @@
 //      stored at once.
 // u never leaves the registers; x is read once from HBM (neighbouring column tiles re-read it
 // from L1 / L2); P_* are written once.
+//
+// Packed direction 2 (LS_MV4_PACK): an 8-row band tile spans NKB k-steps, a 4-row one NKB - 1,
+// so two matrices on the SAME 4 output rows share one DMMA tile with one k-step less per row
+// (p = 6: 4 k-steps for 2 x 4 rows instead of 5 for 8).  With a = the tile's first output row,
+// b = a + 4, and "X_a" the rows a .. a+3 of X, the six chains per output m-tile are
+//     T1a = [M_a ; K_a] u_M    T2a = [2K_a ; M_a] u_K     (k-steps 0 .. NKB-2)
+//     T1b = [K_b ; M_b] u_M    T2b = [M_b ; 2K_b] u_K     (k-steps 1 .. NKB-1)
+//     Jt  = J u_M,  Mt = M u_J (plain 8-row tiles)
+// and a lane of row r (D rows 0-3: lanes 0-15, rows 4-7: lanes 16-31) finds its outputs in the
+// same registers in both halves: P_M(a + r) = T1a | T1b, P_J(a + r) = (T2a | T2b) + Jt + Mt,
+// P_K(a + r + 4 | a + r - 4) = T1b + T2b | T1a + T2a.  26 instead of 30 DMMAs per m-tile at
+// p = 6 (4 (NKB - 1) + 2 NKB vs 6 NKB).  The packed fragments are assembled in the prologue
+// from the plain ones (same lane for the matrix in its own half, lane -+ 16 for the other).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -57,6 +70,17 @@ struct MV4Geom {
   static constexpr int JT0 = -((OFF + 1) / 2);    // first source row tile (k-step 2 JT0 <= -OFF)
 };
 
+#ifndef LS_MV4_PACK
+#define LS_MV4_PACK 0
+#endif
+// shared memory of the plane kernel (doubles): plain [M, J, K, 2K] fragments, or packed:
+// [M, J] plain + [T1a, T2a, T1b, T2b] x (NKB - 1) k-steps
+template <int P, bool PACK>
+constexpr size_t mv4_smem_doubles(int mt2) {
+  return PACK ? size_t(mt2) * 32 * (2 * MV4Geom<P>::NKB + 4 * (MV4Geom<P>::NKB - 1))
+              : size_t(4) * mt2 * MV4Geom<P>::NKB * 32;
+}
+
 #ifndef LS_MV4_L2PF
 #define LS_MV4_L2PF ""  // L2 prefetch-size qualifier of the plane-pass loads (experiment knob)
 #endif
@@ -67,18 +91,39 @@ __device__ __forceinline__ double mv4_ld(const double* p) {
 }
 
 // CTAS = CTAs per SM the register budget is sized for (1: <= 255 registers, 2: <= 128)
-template <int P, int CTAS>
-__global__ void __launch_bounds__(256, CTAS) mv4_plane_kernel(const __grid_constant__ MV4PlaneArgs a) {
+// WARPS per CTA: 8, or 16 for the packed kernel in place of 2 CTAs of 8 (one shared copy of the
+// fragments, which no longer fit twice per SM at p = 6, n = 132)
+template <int P, int CTAS, bool PACK = false, int WARPS = 8>
+__global__ void __launch_bounds__(32 * WARPS, CTAS) mv4_plane_kernel(const __grid_constant__ MV4PlaneArgs a) {
   using Gm = MV4Geom<P>;
   constexpr int NKB = Gm::NKB, OFF = Gm::OFF, S0 = Gm::S0, LAG = Gm::LAG, G = Gm::G, RING = Gm::RING;
   constexpr int JT0 = Gm::JT0;
-  extern __shared__ __align__(16) double fsm[];  // frag2, all 4 matrices
+  constexpr int KP = NKB - 1;  // k-steps of a packed 4-row tile
+  extern __shared__ __align__(16) double fsm[];  // frag2: 4 plain matrices, or 2 plain + 4 packed
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane & 3, r = lane >> 2;
   const int MT1 = a.mt1, MT2 = a.mt2, n1 = a.n1, n2 = a.n2;
-  {
+  if (!PACK) {
     const int nf = 4 * MT2 * NKB * 32;
-    for (int e = tid; e < nf; e += 256) fsm[e] = __ldg(a.frag2 + e);
+    for (int e = tid; e < nf; e += 32 * WARPS) fsm[e] = __ldg(a.frag2 + e);
+  } else {
+    // plain M (mat 0) and J (mat 1) as they are, then the packed tiles [4][MT2][KP][32]
+    const int nf = 2 * MT2 * NKB * 32;
+    for (int e = tid; e < nf; e += 32 * WARPS) fsm[e] = __ldg(a.frag2 + e);
+    const int mstride = MT2 * NKB * 32;  // frag2 matrices: 0 M, 1 J, 2 K, 3 2K
+    const int np = 4 * MT2 * KP * 32;
+    for (int e = tid; e < np; e += 32 * WARPS) {
+      const int l = e & 31, jp = (e >> 5) % KP, mt = (e >> 5) / KP % MT2, t = (e >> 5) / (KP * MT2);
+      const bool top = l < 16;  // D rows 0-3 of the packed tile
+      int mat, src_l, jk;
+      switch (t) {
+        case 0: mat = top ? 0 : 2; src_l = top ? l : l - 16; jk = jp; break;      // T1a = [M_a ; K_a]
+        case 1: mat = top ? 3 : 0; src_l = top ? l : l - 16; jk = jp; break;      // T2a = [2K_a ; M_a]
+        case 2: mat = top ? 2 : 0; src_l = top ? l + 16 : l; jk = jp + 1; break;  // T1b = [K_b ; M_b]
+        default: mat = top ? 0 : 3; src_l = top ? l + 16 : l; jk = jp + 1; break; // T2b = [M_b ; 2K_b]
+      }
+      fsm[nf + e] = __ldg(a.frag2 + mat * mstride + (mt * NKB + jk) * 32 + src_l);
+    }
   }
   __syncthreads();
   pdl_wait();
@@ -86,7 +131,7 @@ __global__ void __launch_bounds__(256, CTAS) mv4_plane_kernel(const __grid_const
   const int64_t plane_sz = int64_t(n1) * n2;
   const int sh_lo = (lane & ~3) | (q >> 1), sh_hi = (lane & ~3) | (2 + (q >> 1));
   const bool odd = q & 1;
-  for (int64_t task = int64_t(blockIdx.x) * 8 + warp; task < ntasks; task += int64_t(gridDim.x) * 8) {
+  for (int64_t task = int64_t(blockIdx.x) * WARPS + warp; task < ntasks; task += int64_t(gridDim.x) * WARPS) {
     const int64_t plane = task / MT1;
     const int ct = int(task - plane * MT1);
     const double* X = a.x + plane * plane_sz;
@@ -141,7 +186,53 @@ __global__ void __launch_bounds__(256, CTAS) mv4_plane_kernel(const __grid_const
           // output m-tile of the PREVIOUS row tile (one extra step of lag): its DMMAs are
           // independent of this tile's direction-1 DMMAs, which stay in flight meanwhile
           const int mt2 = jt - 1 - LAG;
-          if (mt2 >= 0) {
+          if (PACK && mt2 >= 0) {
+            double t1a[2] = {0.0, 0.0}, t2a[2] = {0.0, 0.0}, t1b[2] = {0.0, 0.0}, t2b[2] = {0.0, 0.0};
+            double jt_[2] = {0.0, 0.0}, mt_[2] = {0.0, 0.0};
+            const double* fp = fsm + 2 * MT2 * NKB * 32 + mt2 * KP * 32 + lane;  // packed tile 0
+            constexpr int PS = 0;  // (packed tile stride MT2 * KP * 32 is run-time)
+            const int pst = MT2 * KP * 32;
+#pragma unroll
+            for (int jk = 0; jk < NKB; ++jk) {
+              constexpr int base = RING * 8;
+              const int slot = (base + 2 * u - 2 - 2 * LAG - OFF + jk) % RING;
+              const double* f = fsm + (mt2 * NKB + jk) * 32 + lane;
+              const double fM = f[0], fJ = f[MT2 * NKB * 32];
+              const double bM = ring[0][slot], bK = ring[1][slot], bJ = ring[2][slot];
+              dmma_8x8x4(jt_, fJ, bM);
+              dmma_8x8x4(mt_, fM, bJ);
+              if (jk < KP) {
+                dmma_8x8x4(t1a, fp[PS + jk * 32], bM);
+                dmma_8x8x4(t2a, fp[pst + jk * 32], bK);
+              }
+              if (jk >= 1) {
+                dmma_8x8x4(t1b, fp[2 * pst + (jk - 1) * 32], bM);
+                dmma_8x8x4(t2b, fp[3 * pst + (jk - 1) * 32], bK);
+              }
+            }
+            const bool lo = lane < 16;
+            const int i2 = 8 * mt2 + S0 + r;               // P_M, P_J row
+            const int i2k = lo ? i2 + 4 : i2 - 4;          // P_K row
+            double pm[2], pk[2], pj[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              pm[h] = lo ? t1a[h] : t1b[h];
+              pk[h] = lo ? t1b[h] + t2b[h] : t1a[h] + t2a[h];
+              pj[h] = (lo ? t2a[h] : t2b[h]) + jt_[h] + mt_[h];
+            }
+            const int64_t ob = plane * plane_sz + i1;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (i1 + h >= 0 && i1 + h < n1) {
+                if (i2 >= 0 && i2 < n2) {
+                  a.out[0][ob + int64_t(i2) * n1 + h] = pm[h];
+                  a.out[2][ob + int64_t(i2) * n1 + h] = pj[h];
+                }
+                if (i2k >= 0 && i2k < n2) a.out[1][ob + int64_t(i2k) * n1 + h] = pk[h];
+              }
+            }
+          }
+          if (!PACK && mt2 >= 0) {
             // six independent accumulator chains (P_K, P_J summed at the end)
             double pm[2] = {0.0, 0.0}, pk[2] = {0.0, 0.0}, pj[2] = {0.0, 0.0};
             double pk1[2] = {0.0, 0.0}, pj1[2] = {0.0, 0.0}, pj2[2] = {0.0, 0.0};
