@@ -100,8 +100,12 @@ struct MV3Geom {
 #ifndef MV3_AHEAD3_HI
 #define MV3_AHEAD3_HI 2
 #endif
+// v4 time pass (two ring inputs, 2 CTAs per SM): depth 2 (r02 end, tools/ab_mv.py, two A/B
+// pairs: config 4 matvec 10.18 -> 10.08 ms, config 5 p = 8 3.742 -> 3.701 ms against depth 3,
+// which spilled 48 B at 128 registers; 4 / 5 spill more; one CTA with depth 6 / 9: 10.57 /
+// 10.59 ms)
 #ifndef MV3_AHEAD_T2
-#define MV3_AHEAD_T2 3
+#define MV3_AHEAD_T2 2
 #endif
   static constexpr int AHEAD = KIND == MV3_T2 ? MV3_AHEAD_T2
                                : MV3IO<KIND>::NIN == 1 ? MV3_AHEAD1
