@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(MV_PLANE_THREADS, mv_plane_ctas(P)) mv_plane_k
 // Why (ncu of mv_plane_kernel, config 5 p = 2): 2.6 TB/s, barrier and long-scoreboard stalls —
 // its two phases do not overlap inside a CTA.
 // --------------------------------------------------------------------------------------
+#ifndef LS_MV2_SWEEP_SPLIT
+#define LS_MV2_SWEEP_SPLIT 0
+#endif
 template <int P, int CW, int D>
 __global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant__ MVArgs a) {
   static_assert(CW >= P, "direction-1 neighbours come from the adjacent lanes only");
@@ -390,6 +393,30 @@ __global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant_
         double A2[CW], B2[CW], C2[CW];
 #pragma unroll
         for (int m = 0; m < CW; ++m) A2[m] = B2[m] = C2[m] = 0.0;
+#if LS_MV2_SWEEP_SPLIT
+        // one accumulator chain per input field (W links each instead of 3W / 2W), summed at the end
+        double A2b[CW], A2c[CW], C2b[CW];
+#pragma unroll
+        for (int m = 0; m < CW; ++m) A2b[m] = A2c[m] = C2b[m] = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int sl = (u + j) % R;
+#pragma unroll
+          for (int m = 0; m < CW; ++m) {
+            A2[m] = fma(a.st[0][j], w[0][sl][m], A2[m]);
+            A2b[m] = fma(a.st[1][j], w[1][sl][m], A2b[m]);
+            A2c[m] = fma(a.st[2][j], w[2][sl][m], A2c[m]);
+            B2[m] = fma(a.st[0][j], w[1][sl][m], B2[m]);
+            C2[m] = fma(a.st[0][j], w[2][sl][m], C2[m]);
+            C2b[m] = fma(a.st[3][j], w[1][sl][m], C2b[m]);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < CW; ++m) {
+          A2[m] = (A2[m] + A2b[m]) + A2c[m];
+          C2[m] += C2b[m];
+        }
+#else
 #pragma unroll
         for (int j = 0; j < W; ++j) {
           const int sl = (u + j) % R;
@@ -400,6 +427,7 @@ __global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant_
             C2[m] = fma(a.st[3][j], w[1][sl][m], fma(a.st[0][j], w[2][sl][m], C2[m]));
           }
         }
+#endif
         if (i2 < a.r_lo || i2 >= a.r_hi) {  // boundary row of direction 2 (warp-uniform)
           const int er = (i2 < a.r_lo ? i2 : a.r_lo + (i2 - a.r_hi)) * W;
 #pragma unroll
@@ -436,9 +464,20 @@ __global__ void __launch_bounds__(256, 1) mv_sweep_kernel(const __grid_constant_
         for (int m = 0; m < CW; ++m) {
           const int c = c0 + m;
           double y = 0.0;
+#if LS_MV2_SWEEP_SPLIT
+          double yb = 0.0, yc = 0.0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) {
+            y = fma(a.st[4][j], x[0][m + j], y);
+            yb = fma(a.st[5][j], x[1][m + j], yb);
+            yc = fma(a.st[6][j], x[2][m + j], yc);
+          }
+          y = (y + yb) + yc;
+#else
 #pragma unroll
           for (int j = 0; j < W; ++j)
             y = fma(a.st[4][j], x[0][m + j], fma(a.st[5][j], x[1][m + j], fma(a.st[6][j], x[2][m + j], y)));
+#endif
           if (c < n1 && (c < a.r_lo1 || c >= a.r_hi1)) {  // boundary column of direction 1
             const int er = (c < a.r_lo1 ? c : a.r_lo1 + (c - a.r_hi1)) * W;
 #pragma unroll
