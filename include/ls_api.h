@@ -438,7 +438,9 @@ int ls_profile_read(ls_ctx* ctx, double* total_ms, double* total_flops, int64_t*
 #define LS_TUNE_PDL 6
 /* LS_TUNE_FD_TAIL: 1 = when n = 8 m + 1 or 8 m + 2 in an odd k-step bucket (e.g. n = 65, 66),
  * the shared-memory FD kernel computes the last one or two output rows with DFMAs instead of
- * a 7/8- or 3/4-padded DMMA m-tile (default), 0 = all rows on DMMAs. */
+ * a 7/8- or 3/4-padded DMMA m-tile (default), 0 = all rows on DMMAs, 2 = as 1 and also in the
+ * centrosymmetric split kernels (process-wide; half extents 8 m + 1 or 8 m + 2: n = 65, 66, 97,
+ * 98, 129 .. 132; opt-in: measured slower at config 4, 14.72 -> 16.25 ms). */
 #define LS_TUNE_FD_TAIL 7
 /* LS_TUNE_MV4_CTAS: process-wide; the v4 plane pass' register budget, 1 or 2 CTAs of 256
  * threads per SM (<= 255 / <= 128 registers per thread); default 2. */

@@ -36,6 +36,7 @@ extern int g_mv4_ctas;  // mv4.cu
 }
 
 int ls::g_ls_pdl = 1;  // programmatic dependent launch of the FD mode kernels (LS_TUNE_PDL)
+int ls::g_rd_tail = 0;    // DFMA tail rows in the split FD kernels (LS_TUNE_FD_TAIL = 2, RDCfg::TR; measured slower, off)
 int ls::g_rd_staged = 0;  // staged split FD kernel (LS_TUNE_FD_STAGED; measured slower except p = 8, off)
 
 #define LS_CUDA(x)                                                                        \
@@ -2569,8 +2570,9 @@ extern "C" int ls_tune(ls_ctx* ctx, int knob, int value) {
       g_mv4_ctas = value;
       return LS_OK;
     case LS_TUNE_FD_TAIL:
-      if (value != 0 && value != 1) return LS_EINVAL;
-      ctx->fd_tail = value;
+      if (value < 0 || value > 2) return LS_EINVAL;
+      ctx->fd_tail = value != 0;
+      g_rd_tail = value == 2;  // process-wide: the split register-direct kernels (RDCfg::TR)
       return LS_OK;
     case LS_TUNE_MV5:  // v4: direction 3 + time fused into one pass (d = 3, p_s = p_t); 2 = automatic
       if (value < 0 || value > 2) return LS_EINVAL;

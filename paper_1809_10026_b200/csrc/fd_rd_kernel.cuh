@@ -49,9 +49,16 @@
 
 namespace ls {
 
-template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_, int REMOTE_ = 0, int CS_ = 0, int MINB_ = 1>
+template <int KS_, int NT_, bool MODE1_, bool SCALE_, bool FAST_, int D_, int REMOTE_ = 0, int CS_ = 0, int MINB_ = 1,
+          int TR_ = 0>
 struct RDCfg {
   static constexpr int KS = KS_, NT = NT_, D = D_;
+  // TR: DFMA tail rows (split kernels, odd KS).  When the half extents are 8(MT - 1) + 1 or + 2
+  // (he = 66 at config 4, 33 at configs 2 / 3, 49 at config 5 p = 4) the last m-tile is 3/4 or
+  // 7/8 padding: its TR = 2 rows are computed by DFMAs on the B fragments the lane already
+  // holds (W rows from the same shared-memory fragments, a quad shuffle reduction at the end
+  // of the tile) and the DMMA m-tiles stop at MT - 1.
+  static constexpr int TR = TR_;
   static constexpr int MINB = MINB_;  // CTAs per SM the register budget is sized for
   static constexpr int REMOTE = REMOTE_;  // fused all-to-all epilogue (ModeArgs::remote)
   // CS: centrosymmetric split (see the header of this file): 0 = plain n x n product,
@@ -65,6 +72,7 @@ struct RDCfg {
   static constexpr bool PF64 = CS && KS >= LS_RD_PF64_MINKS;  // .L2::64B streaming loads (see ldg_stream)
   static constexpr bool MODE1 = MODE1_, SCALE = SCALE_, FAST = FAST_;
   static constexpr int MT = (KS + 1) / 2;  // ceil(n/8) for n in (4KS-4, 4KS] (CS: n -> ceil(n/2))
+  static constexpr int MTD = TR ? MT - 1 : MT;  // m-tiles computed by DMMAs
   static constexpr int KSP = (KS + 1) / 2;  // k-step pairs
   static constexpr int KSE = ((KS + D - 1) / D) * D;  // k-steps rounded up to the window
   static constexpr int WARPS = 8, THREADS = 32 * WARPS;
@@ -78,6 +86,7 @@ struct RDCfg {
   static_assert(CS == 0 || !SCALE, "the scaled (time) mode is not centrosymmetric");
   static_assert(CS != 2 || REMOTE == 0, "unfold: local stores only");
   static_assert(NT == 1 || NT % 2 == 0, "NT = 1 or even (LDG.128 pairs)");
+  static_assert(TR == 0 || (TR == 2 && CS != 0 && REMOTE == 0 && KS % 2 == 1), "tail rows: local split kernels, odd KS");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -273,13 +282,21 @@ __global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args)
 #pragma unroll
       for (int e = 0; e < 2 * C::NT; ++e) lc[e] = (cg + e < ncols) ? __ldg(args.lam_c + cg + e) : 0.0;
     }
-    double acc[C::NH][C::MT][C::NT][2];
+    double acc[C::NH][C::MTD][C::NT][2];
 #pragma unroll
     for (int hf = 0; hf < C::NH; ++hf)
 #pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt)
+      for (int mt = 0; mt < C::MTD; ++mt)
 #pragma unroll
         for (int j = 0; j < C::NT; ++j) acc[hf][mt][j][0] = acc[hf][mt][j][1] = 0.0;
+    // tail rows 8 MTD + i: this lane's partial sums over its k = 4 ks + kq
+    double tl[C::NH][C::TR ? C::TR : 1][C::NT];
+#pragma unroll
+    for (int hf = 0; hf < C::NH; ++hf)
+#pragma unroll
+      for (int i = 0; i < (C::TR ? C::TR : 1); ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) tl[hf][i][j] = 0.0;
 
     // k-loop in pairs; phantom steps (KS <= ks < KSE) only refill the window
 #pragma unroll
@@ -301,8 +318,23 @@ __global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args)
               for (int hf = 0; hf < C::NH; ++hf) b[h][hf][j] = bw[s][hf][j];
             }
           }
+        if constexpr (C::TR > 0) {
+          // W_hf[8 MTD + i][4 k + kq] of both k-steps: the A-fragment slot of lane 4 i + kq
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
+          for (int hf = 0; hf < C::NH; ++hf)
+#pragma unroll
+            for (int i = 0; i < C::TR; ++i) {
+              const double2 wt = *reinterpret_cast<const double2*>(
+                  wsm + hf * C::WFRAG1 + (C::MTD * C::KSP + ksp) * 64 + (4 * i + kq) * 2);
+#pragma unroll
+              for (int j = 0; j < C::NT; ++j) {
+                tl[hf][i][j] = fma(wt.x, b[0][hf][j], tl[hf][i][j]);
+                if (k1 < C::KS) tl[hf][i][j] = fma(wt.y, b[1][hf][j], tl[hf][i][j]);
+              }
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < C::MTD; ++mt) {
 #pragma unroll
           for (int hf = 0; hf < C::NH; ++hf) {
             const double2 af = *reinterpret_cast<const double2*>(wl + hf * C::WFRAG1 + (mt * C::KSP + ksp) * 64);
@@ -393,7 +425,7 @@ __global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args)
       }
     };
 #pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt) {
+    for (int mt = 0; mt < C::MTD; ++mt) {
       const int a = mt * 8 + nq;
       double v[C::NH][2 * C::NT];
 #pragma unroll
@@ -426,6 +458,72 @@ __global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args)
           emit(n - 1 - a, t);
         } else if (a < he) {
           emit(a, v[0]);
+        }
+      }
+    }
+    if constexpr (C::TR > 0) {
+      // quad reduction over kq: every lane of quad nq then holds rows 8 MTD + {0, 1} of both
+      // halves at the quad's NT columns c0 .. c0 + NT - 1 (the B-fragment columns); lane kq
+      // stores one (half / sign th, row ti) combination
+#pragma unroll
+      for (int hf = 0; hf < C::NH; ++hf)
+#pragma unroll
+        for (int i = 0; i < C::TR; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) {
+            double t = tl[hf][i][j];
+            t += __shfl_xor_sync(0xffffffffu, t, 1);
+            t += __shfl_xor_sync(0xffffffffu, t, 2);
+            tl[hf][i][j] = t;
+          }
+      const int ti = kq & 1, th = kq >> 1;
+      const int a = 8 * C::MTD + ti;
+      double tv[C::NT];
+      int row = a;
+      bool ok;
+      if (C::CS == 1) {  // [even (he) | odd (ho)]
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j)
+          tv[j] = th ? (ti ? tl[C::NH - 1][1][j] : tl[C::NH - 1][0][j]) : (ti ? tl[0][1][j] : tl[0][0][j]);
+        row = th ? he + a : a;
+        ok = a < (th ? ho : he);
+      } else {  // z[a] = p + q, z[n-1-a] = p - q (a < ho); z[a] = p (middle row, n odd)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+          const double pv = ti ? tl[0][1][j] : tl[0][0][j];
+          const double qv = ti ? tl[C::NH - 1][1][j] : tl[C::NH - 1][0][j];
+          tv[j] = th ? pv - qv : pv + qv;
+        }
+        row = th ? n - 1 - a : a;
+        ok = a < ho || (a < he && th == 0);
+      }
+      const uint32_t c0 = tile * C::TW + C::NT * nq;
+      if (ok) {
+        if (C::MODE1) {
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j)
+            if (c0 + j < ncols) args.Y[size_t(c0 + j) * n + row] = tv[j];
+        } else if (C::FAST) {
+          if (c0 < ncols) {
+            const uint32_t p = c0 / Q, qq = c0 - p * Q;
+            double* o = args.Y + (size_t(p) * n + row) * Q + qq;
+            if constexpr (C::NT == 1) {
+              o[0] = tv[0];
+            } else {
+#pragma unroll
+              for (int j = 0; j < C::NT; j += 2)
+                *reinterpret_cast<double2*>(o + j) = make_double2(tv[j], tv[j + 1 < C::NT ? j + 1 : j]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) {
+            const uint32_t c = c0 + j;
+            if (c < ncols) {
+              const uint32_t p = c / Q, qq = c - p * Q;
+              args.Y[(size_t(p) * n + row) * Q + qq] = tv[j];
+            }
+          }
         }
       }
     }

@@ -10,6 +10,7 @@ namespace ls {
 
 #define LS_RD_CS_MAXKS 17  // largest k-step bucket of the centrosymmetric split (n <= 136)
 extern int g_rd_staged;  // ls_tune LS_TUNE_FD_STAGED (process-wide), api.cu
+extern int g_rd_tail;    // ls_tune LS_TUNE_FD_TAIL (process-wide for the split kernels), api.cu
 // tuning of the split kernels (variant builds: tools/rd_variant_libs.sh): n-tiles per warp,
 // CTAs per SM, prefetch window (0 = the per-bucket rule in rd_launch_cs)
 #ifndef LS_RD_CS_NT
@@ -107,6 +108,21 @@ cudaError_t rd_launch_cs(const ModeArgs& a, bool mode1, int cs, cudaStream_t s, 
     constexpr int D = LS_RD_CS_D > 0 ? LS_RD_CS_D : 6;  // r02: window 6 also for SMALL (4 -> 6: config 3 -0.6 %, config 5 -0.2..-0.9 %)
     const bool fast = !mode1 && (a.Q % (2 * NT) == 0) && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) &&
                       ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
+    // DFMA tail rows (RDCfg::TR): half extents 8(MT - 1) + 1 or + 2 in an odd k-step bucket
+    // (he = 66: config 4; 33: configs 2, 3; 49: config 5 p = 4), local stores
+    if constexpr (KS % 2 == 1 && KS >= 5) {
+      const int he = (a.n + 1) / 2;
+      if (g_rd_tail && !a.remote && he - 8 * ((KS + 1) / 2 - 1) <= 2 && he > 8 * ((KS + 1) / 2 - 1)) {
+        if (cs == 1) {
+          if (mode1) return rd_launch_cfg<RDCfg<KS, NT, true, false, false, D, 0, 1, MB, 2>>(a, s, num_sms);
+          if (fast) return rd_launch_cfg<RDCfg<KS, NT, false, false, true, D, 0, 1, MB, 2>>(a, s, num_sms);
+          return rd_launch_cfg<RDCfg<KS, NT, false, false, false, D, 0, 1, MB, 2>>(a, s, num_sms);
+        }
+        if (mode1) return rd_launch_cfg<RDCfg<KS, NT, true, false, false, D, 0, 2, MB, 2>>(a, s, num_sms);
+        if (fast) return rd_launch_cfg<RDCfg<KS, NT, false, false, true, D, 0, 2, MB, 2>>(a, s, num_sms);
+        return rd_launch_cfg<RDCfg<KS, NT, false, false, false, D, 0, 2, MB, 2>>(a, s, num_sms);
+      }
+    }
     if (cs == 1) {
       if (a.remote == 1) {
         if (!fast) return cudaErrorInvalidValue;

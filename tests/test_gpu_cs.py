@@ -132,3 +132,48 @@ def test_cs_not_used_for_pg():
     ctx.tune(9, 0)
     z0 = ctx.fd_apply(r).cpu().numpy()
     assert np.array_equal(z1, z0)
+
+
+# DFMA tail rows of the split kernels (RDCfg::TR, fd_rd_kernel.cuh; ls_tune LS_TUNE_FD_TAIL = 7):
+# half extents he = ceil(n/2) = 8 m + 1 or 8 m + 2 in an odd k-step bucket (5, 9, 13, 17), every
+# mode position (contiguous / strided FAST / strided general), even and odd n
+TAIL_CASES = [
+    (1, 3, [64, 5]),            # n = 65 (he = 33, ho = 32), contiguous
+    (2, 3, [64, 64, 6]),        # config 2 extents: contiguous + strided general (Q = 65)
+    (2, 2, [66, 66, 3]),        # n = 66 (he = ho = 33): strided FAST, 1 n-tile per warp
+    (2, 2, [33, 34, 4]),        # n = 33 / 34 (he = 17, bucket 5)
+    (3, 4, [96, 2, 3, 4]),      # n_1 = 98 (he = 49, bucket 13): config 5 p = 4, contiguous
+    (3, 4, [4, 96, 3, 3]),      # n_2 = 98 strided FAST (Q = 6)
+    (3, 4, [3, 95, 3, 3]),      # n_2 = 97 (he = 49, ho = 48) strided general (Q = 5)
+    (3, 6, [128, 2, 3, 5]),     # n_1 = 132 (he = 66, bucket 17): config 4, contiguous, 2 n-tiles
+    (3, 6, [4, 128, 3, 3]),     # n_2 = 132 strided FAST (Q = 8)
+    (3, 6, [3, 128, 3, 3]),     # n_2 = 132 strided general (Q = 7)
+    (3, 6, [2, 2, 127, 4]),     # n_3 = 131 (he = 66, ho = 65), Q = 36
+    (2, 6, [125, 5, 4]),        # n_1 = 129 (he = 65 = 8 * 8 + 1, ho = 64)
+]
+
+
+@pytest.mark.parametrize("d,p,n_elems", TAIL_CASES)
+def test_cs_tail_rows(d, p, n_elems):
+    """The last one or two rows of each half product on DFMAs (opt-in, knob value 2) against all-DMMA
+    m-tiles and against the oracle (Algorithm 1, PAPER.md 955-964); two seeds so that a
+    column tile's tail is non-trivial in every warp."""
+    import torch
+    import paper_1809_10026_b200 as ls
+    ctx = ls.Context(d, p, n_elems)
+    fdd = _fdd(d, p, n_elems)
+    try:
+        for seed in (5, 6):
+            r = synth.residual(ctx.shape, seed)
+            rg = torch.from_numpy(r).cuda()
+            z_ref = fd.fd_apply(r, fdd)
+            ctx.tune(7, 2)
+            z1 = ctx.fd_apply(rg).cpu().numpy()
+            ctx.tune(7, 0)
+            z0 = ctx.fd_apply(rg).cpu().numpy()
+            assert _rel(z1, z_ref) <= TOL
+            assert np.max(np.abs(z1 - z_ref)) <= TOL * np.abs(z_ref).max()
+            assert _rel(z0, z_ref) <= TOL
+            assert _rel(z1, z0) <= 1e-12
+    finally:
+        ctx.tune(7, 1)
