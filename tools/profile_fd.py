@@ -24,6 +24,7 @@ ap.add_argument("--mv", type=int, default=0, help="ls_tune matvec variant")
 ap.add_argument("--fdk", type=int, default=0, help="ls_tune FD kernel variant")
 ap.add_argument("--pad", type=int, default=0, help="ls_tune v3 matvec padding")
 ap.add_argument("--nograph", action="store_true", help="PCG as the host-driven loop (profilers see every kernel)")
+ap.add_argument("--tune", default="", help="extra ls_tune knobs, 'knob=value,...'")
 a = ap.parse_args()
 c = synth.CONFIGS[a.config]
 p = a.p if a.p is not None else (c["p"] if isinstance(c["p"], int) else c["p"][0])
@@ -34,6 +35,9 @@ if a.pad:
     ctx.tune(3, a.pad)
 if a.nograph:
     ctx.tune(5, 0)
+for kv in filter(None, a.tune.split(",")):
+    k, v = kv.split("=")
+    ctx.tune(int(k), int(v))
 r = torch.from_numpy(synth.residual(ctx.shape, 0)).cuda()
 z = torch.empty_like(r)
 if a.pcg:
