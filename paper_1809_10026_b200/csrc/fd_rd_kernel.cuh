@@ -170,9 +170,34 @@ struct RDPtr {
   const double* lm[NP];
 };
 
+// LS_RD_PFA > 0 (experiment knob, split kernels): with every k-step's loads, an L2 prefetch of the
+// rows LS_RD_PFA k-steps further down the same columns.  Why: ptxas sinks the window's loads
+// towards their uses (255 registers: the SASS of the KS = 17 fold kernel issues a k-step pair's
+// LDGs about 45 DMMAs before the DADDs that read them, not the 6 k-steps = 216 DMMAs of the
+// source), and ncu attributes a quarter of the warp-stall samples to those DADDs' long
+// scoreboard; a prefetch has no destination registers, so it stays where it is written.
+#ifndef LS_RD_PFA
+#define LS_RD_PFA 0
+#endif
+__device__ __forceinline__ void prefetch_l2(const double* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <class C>
 __device__ __forceinline__ void rd_load(double (&dst)[C::NH][C::NT], RDPtr<C>& q, uint32_t mask, bool ok0,
-                                        bool ok1, size_t kstep, int n) {
+                                        bool ok1, size_t kstep, int n, bool pf0 = false, bool pf1 = false) {
+  if constexpr (LS_RD_PFA > 0 && C::CS != 0) {
+    // FAST: the lane's NT columns are contiguous (one address); MODE1: column j at + j n
+    const int64_t ahead = int64_t(LS_RD_PFA) * int64_t(kstep);
+#pragma unroll
+    for (int j = 0; j < ((C::FAST) ? 1 : C::NT); ++j) {
+      const bool cm = C::FAST ? mask != 0 : ((mask >> j) & 1u);
+      const double* p0 = C::MODE1 ? q.lp[0] + size_t(j) * n : q.lp[(C::MODE1 || C::FAST) ? 0 : j];
+      const double* p1 = C::MODE1 ? q.lm[0] + size_t(j) * n : q.lm[(C::MODE1 || C::FAST) ? 0 : j];
+      if (pf0 && cm) prefetch_l2(p0 + ahead);
+      if (pf1 && cm) prefetch_l2(C::CS == 1 ? p1 - ahead : p1 + ahead);
+    }
+  }
   if (C::FAST) {
     const bool m = mask != 0;
     if constexpr (C::NT == 1) {
@@ -265,7 +290,8 @@ __global__ void __launch_bounds__(256, C::MINB) fd_mode_rd_kernel(ModeArgs args)
   };
   // loads run strictly in order: k-steps 0 .. KS-1 of a tile, then 0 .. of the next one
   auto load = [&](double (&dst)[C::NH][C::NT], const RDIn<C::NT>& in, int kk) {
-    rd_load<C>(dst, q, in.mask, row_ok(kk), row_ok1(kk), kstep, n);
+    rd_load<C>(dst, q, in.mask, row_ok(kk), row_ok1(kk), kstep, n, kk + LS_RD_PFA < C::KS && row_ok(kk + LS_RD_PFA),
+               kk + LS_RD_PFA < C::KS && row_ok1(kk + LS_RD_PFA));
   };
   set_ptrs(cur);
 #pragma unroll
